@@ -1,0 +1,132 @@
+"""Mortar nodes and Gaussian mortar functions (oracle).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md §3.3 "Mortar nodes and mortar functions":
+  * placement: first two = farthest pair of F^{c_j}; then
+    x_{m_{i+1}} = argmin_{y in F} sum_{j<=i} 1/||y - x_{m_j}||   (eq:node_init,
+    P:137-141); then sweeps that move each node to the argmin of the potential
+    of all OTHER nodes until nothing changes;
+  * Gaussian mortars eta_{m_i gamma}^{(d)} = delta_{d gamma} alpha_i/sum_j alpha_j,
+    alpha_i(x) = exp(-||x-x_{m_i}||^2 / (beta min_j ||x_{m_i}-x_{m_j}||^2))
+    (eq:gauss), beta = 4.
+Readings: R9 (nu_c = min(n, |F_c|)), R10 (deterministic placement: integer d^2,
+IEEE 1/sqrt, sequential sums in chosen order, lowest id on ties, ascending
+sweep order, move only on a > 1e-12 relative improvement, <= 20 sweeps; nu=|F|
+=> all nodes ascending; nu=1 => node nearest the centroid), R11 (min over
+j != i; nu=1 => w == 1).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def _d2(a, b) -> int:
+    return int((a[0] - b[0]) ** 2 + (a[1] - b[1]) ** 2 + (a[2] - b[2]) ** 2)
+
+
+def _potential(y, X, skip=-1) -> float:
+    """sum_j 1/||y - x_j|| over X in order (j != skip), sequential fp64 sum."""
+    s = 0.0
+    for j, x in enumerate(X):
+        if j == skip:
+            continue
+        s += 1.0 / math.sqrt(float(_d2(y, x)))
+    return s
+
+
+def place_mortars(F: np.ndarray, ijk: np.ndarray, n: int, max_sweeps: int = 20):
+    """Mortar node ids (a list in placement order) on interface node set F
+    (ascending node ids) with lattice coords ijk[F]."""
+    F = [int(p) for p in F]
+    P = {p: tuple(int(v) for v in ijk[p]) for p in F}
+    nu = min(n, len(F))
+    if nu == len(F):
+        return list(F)
+    if nu == 1:
+        m = len(F)
+        S = [sum(P[p][a] for p in F) for a in range(3)]
+        best, bd = None, None
+        for p in F:                          # integer |F|^2 * d^2 to centroid
+            d = sum((m * P[p][a] - S[a]) ** 2 for a in range(3))
+            if bd is None or d < bd:
+                best, bd = p, d
+        return [best]
+    # farthest pair, lowest (id_a, id_b) lexicographic
+    best, bd = None, -1
+    for ia, a in enumerate(F):
+        for b in F[ia + 1:]:
+            d = _d2(P[a], P[b])
+            if d > bd:
+                best, bd = (a, b), d
+    X = [best[0], best[1]]
+    # greedy Coulomb argmin (eq:node_init)
+    while len(X) < nu:
+        chosen = set(X)
+        xs = [P[x] for x in X]
+        arg, val = None, None
+        for y in F:
+            if y in chosen:
+                continue
+            v = _potential(P[y], xs)
+            if val is None or v < val:
+                arg, val = y, v
+        X.append(arg)
+    # sweeps in ascending mortar index (R10)
+    for _ in range(max_sweeps):
+        moved = False
+        for i in range(nu):
+            others = set(X[:i] + X[i + 1:])
+            xs = [P[x] for x in X]
+            cur = _potential(P[X[i]], xs, skip=i)
+            arg, val = None, None
+            for y in F:
+                if y in others:
+                    continue
+                v = _potential(P[y], xs, skip=i)
+                if val is None or v < val:
+                    arg, val = y, v
+            if val < cur * (1.0 - 1e-12):
+                X[i] = arg
+                moved = True
+        if not moved:
+            break
+    return X
+
+
+def gaussian_weights(F: np.ndarray, ijk: np.ndarray, mortars, beta: float) -> np.ndarray:
+    """W[y, i] = eta_{m_i}(y) for y in F (eq:gauss with R11).  Evaluated with a
+    max-exponent shift (identical in exact arithmetic)."""
+    F = np.asarray(F)
+    nu = len(mortars)
+    if nu == 1:
+        return np.ones((F.size, 1))
+    xm = ijk[np.asarray(mortars)].astype(np.int64)
+    dmin2 = np.empty(nu)
+    for i in range(nu):
+        dmin2[i] = min(_d2(xm[i], xm[j]) for j in range(nu) if j != i)
+    y = ijk[F].astype(np.int64)
+    d2 = ((y[:, None, :] - xm[None, :, :]) ** 2).sum(-1).astype(np.float64)
+    e = -d2 / (beta * dmin2[None, :])
+    alpha = np.exp(e - e.max(axis=1, keepdims=True))
+    return alpha / alpha.sum(axis=1, keepdims=True)
+
+
+class Mortars:
+    """Mortar nodes + weights for every interface; coarse column ordering R13:
+    interface id -> mortar index (placement order) -> gamma in {x,y,z}."""
+
+    def __init__(self, decomp, node_ijk, n_mortar: int, beta: float):
+        self.nodes = []
+        self.weights = []
+        self.offset = [0]
+        for F in decomp.interfaces:
+            X = place_mortars(F, node_ijk, n_mortar)
+            self.nodes.append(X)
+            self.weights.append(gaussian_weights(F, node_ijk, X, beta))
+            self.offset.append(self.offset[-1] + len(X))
+        self.offset = np.array(self.offset, dtype=np.int64)
+        self.n_mortar_nodes = int(self.offset[-1])
+        self.n_mortar_dofs = 3 * self.n_mortar_nodes

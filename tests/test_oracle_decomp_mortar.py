@@ -1,0 +1,150 @@
+"""Pins for oracle/decomp.py and oracle/mortar.py.
+
+SURVEY §8(c) pins O4 (closed-form cfg1 decomposition), O5 (brute-force contact
+grids), O6 (brute-force global minimum of the Coulomb energy, eq:node_init),
+O7 (partition of unity, nu=1 reduction, two-node closed form; eq:gauss).
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+from oracle import decomp, mortar
+
+
+def test_cfg1_decomposition_closed_form(cfg1):
+    _, s, h = cfg1
+    d = h.dec
+    assert d.n_grains == 8
+    assert d.n_interfaces == 12
+    sizes = sorted(F.size for F in d.interfaces)
+    assert sizes == [64] * 10 + [72] * 2
+    big = [tuple(d.iface_pair[c]) for c, F in enumerate(d.interfaces) if F.size == 72]
+    assert big == [(0, 1), (4, 5)]
+    assert sum(F.size for F in d.interfaces) == 784
+    assert int((d.node_class == decomp.CLASS_D).sum()) == 289
+    assert max(g.size for g in d.grain_nodes) == 529
+    # every node is in exactly one of: some I_g, some interface
+    cover = np.zeros(s.mesh.n_nodes, int)
+    for g in d.grain_nodes:
+        cover[g] += 1
+    for F in d.interfaces:
+        cover[F] += 1
+    assert np.all(cover == 1)
+
+
+def _brute_components(nodes, adj):
+    """Union-find over an explicit adjacency (plain Python)."""
+    parent = {p: p for p in nodes}
+
+    def find(p):
+        while parent[p] != p:
+            parent[p] = parent[parent[p]]
+            p = parent[p]
+        return p
+    for p in nodes:
+        for q in adj(p):
+            if q in parent:
+                a, b = find(p), find(q)
+                if a != b:
+                    parent[max(a, b)] = min(a, b)
+    comps = {}
+    for p in nodes:
+        comps.setdefault(find(p), []).append(p)
+    return comps
+
+
+def test_porous_interfaces_and_contact_grids_brute_force(porous20):
+    p, s, h = porous20
+    d = h.dec
+    mesh = s.mesh
+    ijk = mesh.node_ijk
+    # R6: interface nodes = non-D nodes touching >= 2 grains, pair = 2 smallest
+    vox_of = {}
+    for v, nodes in enumerate(mesh.vox_nodes):
+        for q in nodes:
+            vox_of.setdefault(int(q), set()).add(int(mesh.vox_grain[v]))
+    for q in range(mesh.n_nodes):
+        gs = sorted(vox_of[q])
+        if mesh.dirichlet[q]:
+            assert d.node_class[q] == decomp.CLASS_D and d.owner[q] == gs[0]
+        elif len(gs) >= 2:
+            assert d.node_class[q] == decomp.CLASS_I and tuple(d.pair[q]) == tuple(gs[:2])
+        else:
+            assert d.node_class[q] == decomp.CLASS_G and d.owner[q] == gs[0]
+    # R7: components under "share a solid voxel", brute force
+    share = {}
+    for nodes in mesh.vox_nodes:
+        for a in nodes:
+            share.setdefault(int(a), set()).update(int(b) for b in nodes)
+    want = []
+    pairs = sorted({tuple(d.pair[q]) for q in range(mesh.n_nodes) if d.node_class[q] == decomp.CLASS_I})
+    for pr in pairs:
+        nodes = [q for q in range(mesh.n_nodes)
+                 if d.node_class[q] == decomp.CLASS_I and tuple(d.pair[q]) == pr]
+        comps = _brute_components(nodes, lambda q: share[q])
+        want += sorted((pr, min(c), sorted(c)) for c in comps.values())
+    got = [(tuple(d.iface_pair[c]), int(F[0]), list(map(int, F))) for c, F in enumerate(d.interfaces)]
+    assert got == [(pr, m, c) for pr, m, c in want]
+    # R8: contact grid = all non-D nodes within Chebyshev distance h (no bbox)
+    hh = d.contact_h
+    nonD = np.flatnonzero(~mesh.dirichlet)
+    for F, Z in zip(d.interfaces, d.contact_nodes):
+        dist = np.abs(ijk[nonD][:, None, :] - ijk[F][None, :, :]).max(-1).min(-1)
+        assert np.array_equal(np.sort(nonD[dist <= hh]), Z)
+
+
+def _coulomb(ijk, S):
+    return sum(1.0 / math.dist(ijk[a], ijk[b]) for a, b in itertools.combinations(S, 2))
+
+
+@pytest.mark.parametrize("shape", [(9, 8), (8, 8), (8, 7)])
+def test_rectangle_placement_is_global_minimum(shape):
+    """On cfg1's rectangular interface shapes the R10 placement equals the
+    brute-force global minimum of the Coulomb energy over all C(|F|,4) subsets
+    (unique minimum = the 4 corners)."""
+    a, b = shape
+    jj, ii = np.meshgrid(np.arange(b), np.arange(a), indexing="ij")
+    ijk = np.stack([ii.ravel(), jj.ravel(), np.zeros(a * b, int)], 1)
+    F = np.arange(a * b)
+    X = mortar.place_mortars(F, ijk, 4)
+    P = ijk.astype(float)
+    D = np.sqrt(((P[:, None] - P[None]) ** 2).sum(-1))
+    np.fill_diagonal(D, np.inf)
+    inv = 1.0 / D
+    # vectorised brute force over all 4-subsets
+    idx = np.array(list(itertools.combinations(range(a * b), 4)))
+    E = np.zeros(len(idx))
+    for x, y in itertools.combinations(range(4), 2):
+        E += inv[idx[:, x], idx[:, y]]
+    m = E.min()
+    winners = idx[E <= m * (1 + 1e-12)]
+    corners = sorted([0, a - 1, a * (b - 1), a * b - 1])
+    assert len(winners) == 1 and sorted(winners[0]) == corners
+    assert sorted(X) == corners
+
+
+def test_gaussian_two_node_closed_form():
+    # own-node weight with two mortars = 1/(1+e^{-1/4})
+    ijk = np.array([[0, 0, 0], [5, 0, 0], [2, 0, 0]])
+    W = mortar.gaussian_weights(np.array([0, 1, 2]), ijk, [0, 1], 4.0)
+    assert abs(W[0, 0] - 1.0 / (1.0 + math.exp(-0.25))) <= 1e-15
+    assert abs(W[0, 0] - 0.5621765008857981) <= 1e-15
+
+
+def test_mortar_partition_of_unity_and_nu1(porous20):
+    p, s, h = porous20
+    for F, W in zip(h.dec.interfaces, h.mor.weights):
+        assert np.abs(W.sum(1) - 1.0).max() <= 1e-15 * 4
+        assert np.all(W > 0)
+    d = h.dec
+    m1 = mortar.Mortars(d, s.mesh.node_ijk, 1, 4.0)
+    for W in m1.weights:
+        assert np.all(W == 1.0)           # PLMM reduction, bitwise
+
+
+def test_full_cap_places_every_node(cfg1):
+    _, s, h = cfg1
+    F = h.dec.interfaces[0]
+    assert mortar.place_mortars(F, s.mesh.node_ijk, 10 ** 6) == list(map(int, F))

@@ -1,0 +1,96 @@
+"""Pins for oracle/fem.py against closed forms / invariants (not against itself).
+
+SURVEY §8(c) pin table rows O1, O2, O3.
+"""
+import itertools
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+from oracle import fem
+from workloads import Problem, make_problem
+
+
+def test_cfg1_counts():
+    # BASELINE.json configs[0]: 14,739 DOF = 17^3 * 3; nnzb closed form
+    # (3*17-2)^3 = 117,649 before and 110,735 after Dirichlet removal.
+    s = fem.build_system(make_problem("cfg1"))
+    assert s.n_dof == 14739 == 17 ** 3 * 3
+    assert s.full.nnz // 9 == (3 * 17 - 2) ** 3 == 117649
+    assert s.nnzb == 110735
+    assert int(s.mesh.dirichlet.sum()) == 17 * 17
+
+
+@pytest.mark.parametrize("nu", [0.25, 0.3, 0.45])
+def test_K0_kernel_and_exactness(nu):
+    K = fem.element_K0(nu)
+    assert np.abs(K - K.T).max() <= 1e-15 * np.abs(K).max()
+    ev = np.linalg.eigvalsh(0.5 * (K + K.T))
+    tol = 1e-12 * ev.max()
+    assert np.sum(np.abs(ev) < tol) == 6          # 3 translations + 3 rotations
+    assert np.sum(ev > tol) == 18
+    # 2x2x2 Gauss is exact for constant-coefficient Q1 (equals 3x3x3)
+    assert np.abs(fem.element_K0(nu, 3) - K).max() <= 1e-14 * np.abs(K).max()
+
+
+def test_K0_constant_strain_closed_form():
+    """u = eps x (eps symmetric)  =>  K0 u = boundary integral of sigma.n N_a:
+    each corner gets, from each of its 3 faces, sigma.n * (1/4)."""
+    rng = np.random.default_rng(0)
+    nu = 0.3
+    e = rng.standard_normal((3, 3)); e = 0.5 * (e + e.T)
+    lam, mu = fem.lame(1.0, nu)
+    sig = lam * np.trace(e) * np.eye(3) + 2 * mu * e
+    u = np.zeros(24)
+    f = np.zeros(24)
+    for a in range(8):
+        x = np.array([a & 1, (a >> 1) & 1, (a >> 2) & 1], float)
+        u[3 * a:3 * a + 3] = e @ x
+        for d in range(3):
+            n = np.zeros(3); n[d] = 1.0 if x[d] == 1 else -1.0
+            f[3 * a:3 * a + 3] += sig @ n / 4.0
+    assert np.abs(fem.element_K0(nu) @ u - f).max() <= 1e-14 * np.abs(f).max()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "porous20"])
+def test_rigid_body_modes_and_symmetry(name):
+    s = fem.build_system(make_problem(name))
+    R = fem.rigid_body_modes(s.mesh.node_ijk)
+    assert np.linalg.norm(s.full @ R) <= 1e-14 * np.linalg.norm(R) * abs(s.full).max()
+    d = abs(s.A - s.A.T).max()
+    assert d <= 1e-15 * abs(s.A).max()
+
+
+def _patch_problem(L=4):
+    solid = np.ones((L, L, L), np.uint8)
+    lat = (L + 1,) * 3
+    k, j, i = np.meshgrid(*[np.arange(L + 1)] * 3, indexing="ij")
+    bnd = (i == 0) | (i == L) | (j == 0) | (j == L) | (k == 0) | (k == L)
+    a = np.array([0.1, -0.2, 0.3])
+    G = np.array([[0.01, 0.02, -0.03], [0.04, -0.05, 0.06], [0.07, 0.08, 0.02]])
+    X = np.stack([i, j, k], -1).astype(float)
+    u = a + X @ G.T
+    return Problem(name="patch", nx=L, ny=L, nz=L, solid=solid, E=np.ones((L, L, L)),
+                   nu=0.3, grain=np.zeros((L, L, L), np.int32), n_grains=1,
+                   node_dirichlet=bnd.astype(np.uint8), node_u=u, node_f=np.zeros(lat + (3,)),
+                   block=L), u
+
+
+def test_patch_test():
+    """Linear u prescribed on the whole boundary, f = 0 => the interior
+    reproduces u (Q1 exactness for linear fields)."""
+    p, u = _patch_problem()
+    s = fem.build_system(p)
+    x = spla.spsolve(s.A.tocsc(), s.b)
+    ue = u.reshape(-1, 3)[s.mesh.node_key].ravel()
+    assert np.abs(x - ue).max() <= 1e-12 * np.abs(ue).max()
+
+
+def test_cfg1_load_equilibrium():
+    s = fem.build_system(make_problem("cfg1"))
+    assert s.mesh.f[:, 2].sum() == -256.0
+    x = spla.spsolve(s.A.tocsc(), s.b)
+    reac = (s.full @ x).reshape(-1, 3)[s.mesh.dirichlet]
+    assert abs(reac[:, 2].sum() - 256.0) <= 1e-10 * 256.0
+    assert np.abs(reac[:, :2].sum(0)).max() <= 1e-9
