@@ -1,0 +1,217 @@
+/* hplmm.h -- C ABI of the B200-native hPLMM-preconditioned GMRES solver.
+ *
+ * Method: arXiv 2509.19777 (Khan & Mehmani), "High-order Multiscale
+ * Preconditioner for Elasticity of Arbitrary Structures".  Citations are
+ * PAPER.md line numbers (P:<line>) plus the LaTeX equation label.  Readings
+ * R1..R24 where the paper is silent are listed in DESIGN.md ("Readings").
+ *
+ * The library solves the fine Q1-hex FEM elasticity system
+ *     A^ x^ = b^                                   (eq:ls_all)
+ * with right-preconditioned GMRES(restart) (R22) whose preconditioner is
+ *     M^-1 = M_G^-1 + M_L^-1 (I - A^ M_G^-1)       (eq:multi_precond)
+ *     M_G^-1 = P^ (P^T A^ P^)^-1 P^T,  P^ = W Q P  (eq:mg_struct/eq:WQP)
+ *     M_L = M_CG = M_zeta^-1 + M_g^-1 (I - A^ M_zeta^-1)
+ *                                                  (eq:local_smoother_CG)
+ * on one CUDA device (sm_100a).  All arithmetic is fp64 (R1).
+ *
+ * Conventions (all entry points)
+ *  - Return value: hplmm_status; negative = error (message via
+ *    hplmm_last_error(), thread-local, valid until the next call on this
+ *    thread), 0 = OK, positive = a non-fatal outcome (NOT_CONVERGED).
+ *  - Pointers marked "host or device" are classified with
+ *    cudaPointerGetAttributes; device pointers must live on the handle's
+ *    device.  Every input is borrowed for the call only (copied if kept).
+ *    Outputs are caller-allocated with the stated length.
+ *  - A handle owns all device memory it allocates; hplmm_destroy frees it.
+ *    A handle is not thread-safe; distinct handles are independent.
+ *  - Streams: every GPU entry point takes a cudaStream_t (0 = legacy default
+ *    stream) passed as void* so this header needs no CUDA include.  Calls are
+ *    synchronous with respect to the host on return unless stated.
+ *  - There is no CPU fallback: GPU entry points fail with HPLMM_ERR_CUDA when
+ *    no device is usable.
+ */
+#ifndef HPLMM_H
+#define HPLMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HPLMM_OK = 0,
+  HPLMM_NOT_CONVERGED = 1,        /* solve hit max_iter; x and history written  */
+  HPLMM_ERR_ARG = -1,             /* bad argument / size / null pointer         */
+  HPLMM_ERR_CUDA = -2,            /* CUDA runtime error (incl. no device)       */
+  HPLMM_ERR_OOM = -3,             /* device allocation failed                   */
+  HPLMM_ERR_SINGULAR_LOCAL = -4,  /* non-positive pivot in a grain/contact-grid
+                                     factorisation; report.err_index = subdomain */
+  HPLMM_ERR_SINGULAR_COARSE = -5, /* non-positive pivot in the coarse matrix S  */
+  HPLMM_ERR_NONFINITE = -6,       /* NaN/Inf in the GMRES residual estimate     */
+  HPLMM_ERR_STATE = -7            /* call out of order (e.g. solve before setup) */
+} hplmm_status;
+
+/* Voxel problem (§2; Cartesian decomposition §3.1).
+ * All arrays are HOST arrays, x fastest: voxel arrays [nz][ny][nx], node
+ * (lattice) arrays [nz+1][ny+1][nx+1] (x3 for vectors, component fastest). */
+typedef struct {
+  int32_t nx, ny, nz;            /* voxels                                          */
+  const uint8_t *solid;          /* 1 = solid voxel (one Q1 hex element)      */
+  const double *E;               /* Young's modulus per voxel (read where solid)    */
+  double nu;                     /* uniform Poisson ratio (eq:stiff_iso via R2)     */
+  const int32_t *grain;          /* grain id per voxel in [0,n_grains), -1 = void   */
+  int32_t n_grains;
+  const uint8_t *node_dirichlet; /* 1 = all 3 components prescribed (R4)            */
+  const double *node_u;          /* prescribed displacement (used where dirichlet)  */
+  const double *node_f;          /* consistent external nodal force                 */
+} hplmm_problem;
+
+typedef struct {
+  int32_t n_mortar;   /* n: mortar nodes per interface (R9, default 4)             */
+  double beta;        /* Gaussian mortar spread (eq:gauss; default 4.0)      */
+  int32_t contact_h;  /* contact-grid Chebyshev dilation h in nodes (R8); <0 invalid */
+  int32_t restart;    /* GMRES restart m (R22, default 50; 1..512)                  */
+  int32_t max_iter;   /* total Arnoldi steps cap (default 300)               */
+  int32_t n_st;       /* smoother stages (eq:local_smoother); only 1 is supported   */
+  int32_t coarse_refine; /* 1 = one step of iterative refinement of the coarse
+                            solve y = S^-1 r with S kept resident (residual
+                            ~(kappa u)^2 instead of ~kappa u); default 0        */
+} hplmm_options;
+
+typedef struct {
+  /* sizes */
+  int32_t n_nodes;        /* FEM nodes (DOF = 3 n_nodes, R3)                        */
+  int64_t nnzb;           /* 3x3 blocks of A^ after Dirichlet removal               */
+  int32_t n_grains;       /* grain grids N^g                                        */
+  int32_t n_interfaces;   /* contact interfaces N^c = contact grids N^zeta          */
+  int32_t n_mortar_dofs;  /* N^o_m = 3 N^m                                          */
+  int32_t n_coarse;       /* N^o_m + number of correction columns (after set_rhs)   */
+  int64_t local_bytes;    /* bytes of the packed local inverse tiles                */
+  int64_t coarse_bytes;   /* bytes of the packed coarse inverse tiles               */
+  int64_t prolong_nnz;    /* stored entries of P^_B (grain blocks + Q^o)            */
+  /* solve outcome */
+  int32_t iterations;     /* total Arnoldi steps                                    */
+  int32_t converged;
+  int32_t hist_len;       /* entries written to hist                                */
+  int32_t err_index;      /* failing subdomain for SINGULAR_LOCAL, else -1          */
+  double final_true_relres; /* ||b - A x|| / ||b|| at exit                          */
+  /* timings (s), CUDA events on the call's stream                                 */
+  double t_host_setup_s;  /* integer setup (hplmm_create)                           */
+  double t_assemble_s;
+  double t_setup_local_s; /* ~T_ML: grain + contact-grid inversions                 */
+  double t_setup_coarse_s;/* ~T_MG: mortars, P^_B, S, coarse inversion              */
+  double t_rhs_s;         /* per-RHS correction columns (set_rhs)                   */
+  double t_solve_s;       /* GMRES (T_sol)                                          */
+  int64_t kernel_launches;/* kernels launched by the last solve                      */
+} hplmm_report;
+
+typedef struct hplmm_handle hplmm_handle;
+
+/* Default options: n=4, beta=4, h=1, restart=50, max_iter=300, n_st=1,
+ * coarse_refine=0. */
+void hplmm_default_options(hplmm_options *opt);
+
+/* Host-only integer setup (no GPU work; bit-exact vs the oracle):
+ * mesh numbering (R3), BSR pattern with Dirichlet couplings removed (R4),
+ * node classes (R6), interfaces (R7), grain-interior sets (R18), contact grids
+ * (R8), mortar placement (eq:node_init, R10), shape-vector column sets (R14).
+ * Copies everything it needs from `prob`. */
+hplmm_status hplmm_create(const hplmm_problem *prob, const hplmm_options *opt,
+                          hplmm_handle **out);
+
+/* GPU assembly of A^ values and b^ (R2, R4) into handle-owned device
+ * memory.  Selects device `device` for the handle (cudaSetDevice). */
+hplmm_status hplmm_assemble(hplmm_handle *h, int32_t device, void *stream);
+
+/* Replace the values of A^ (nnzb*9 doubles, row-major 3x3 blocks in the
+ * handle's pattern, host or device) -- used to parity-test later stages on an
+ * externally supplied matrix.  Must precede hplmm_setup. */
+hplmm_status hplmm_set_matrix(hplmm_handle *h, const double *val, void *stream);
+
+/* GPU numeric setup, timed separately from the solve (north_star (6)):
+ * Gaussian mortar weights (eq:gauss), inverses of every grain block
+ * A^{g}_{g} and contact-grid block A^[zeta,zeta] (T_ML), shape vectors
+ * B = -A_g^-1 Abar^g_m Q^o (eq:col_pk, R14), S = P_B^T A^ P_B (eq:mg_struct,
+ * R16) and its inverse (R17).  Errors: SINGULAR_LOCAL (report.err_index via
+ * hplmm_get_report), SINGULAR_COARSE, OOM. */
+hplmm_status hplmm_setup(hplmm_handle *h, void *stream);
+
+/* Per-RHS correction columns c^g = A_g^-1 b^g (eq:col_cg) for grains with
+ * b[I_g] != 0 (R15), D_c[g] = b^g . c^g (R16).  b: n_dof doubles, host or
+ * device.  hplmm_solve calls it itself; needed before hplmm_apply(MG/MINV). */
+hplmm_status hplmm_set_rhs(hplmm_handle *h, const double *b, void *stream);
+
+/* Solve A^ x = b to ||b - A^x||/||b|| < tol (R22).  b, x: n_dof doubles, host
+ * or device (x is overwritten, x0 = 0).  hist: host array of hist_cap doubles
+ * receiving the per-step Arnoldi estimates (may be NULL).  report may be NULL.
+ * Returns OK, NOT_CONVERGED (x = last iterate) or an error.  b = 0 => x = 0. */
+hplmm_status hplmm_solve(hplmm_handle *h, const double *b, double tol, double *x,
+                         hplmm_report *report, double *hist, int32_t hist_cap,
+                         void *stream);
+
+typedef enum {
+  HPLMM_OP_SPMV = 0,   /* out = A^ in                                           */
+  HPLMM_OP_MG = 1,     /* out = M_G^-1 in        (needs set_rhs)                */
+  HPLMM_OP_MZETA = 2,  /* out = M_zeta^-1 in     (eq:Mg_Mz)                      */
+  HPLMM_OP_MGRAIN = 3, /* out = M_g^-1 in        (eq:Mg_Mz, R18)                 */
+  HPLMM_OP_MCG = 4,    /* out = M_CG^-1 in       (eq:local_smoother_CG)          */
+  HPLMM_OP_MINV = 5,   /* out = M^-1 in          (eq:multi_precond; set_rhs)     */
+  HPLMM_OP_RESTRICT = 6,/* out[n_coarse] = P^T in                               */
+  HPLMM_OP_PROLONG = 7, /* out[n_dof] = P^ in, in has n_coarse entries          */
+  HPLMM_OP_COARSE = 8   /* out[N_m] = S^-1 in[N_m]: the coarse mortar-block solve  */
+} hplmm_op;
+
+/* One application of an operator (parity entry point).  in/out: host or
+ * device; lengths n_dof unless stated. */
+hplmm_status hplmm_apply(hplmm_handle *h, int32_t op, const double *in, double *out,
+                         void *stream);
+
+typedef enum {
+  HPLMM_ART_NODE_KEY = 0,     /* int64[n_nodes] lattice key of each node (R3)   */
+  HPLMM_ART_ROW_PTR = 1,      /* int32[n_nodes+1]                               */
+  HPLMM_ART_COL_IDX = 2,      /* int32[nnzb]                                    */
+  HPLMM_ART_NODE_CLASS = 3,   /* int32[n_nodes] 0=grain-interior 1=interface 2=Dirichlet */
+  HPLMM_ART_NODE_IFACE = 4,   /* int32[n_nodes] interface id or -1              */
+  HPLMM_ART_NODE_OWNER = 5,   /* int32[n_nodes] owning grain or -1 (interface)  */
+  HPLMM_ART_IFACE_PTR = 6,    /* int32[N^c+1] CSR over interface node lists     */
+  HPLMM_ART_IFACE_NODES = 7,  /* int32[...] ascending nodes of each interface   */
+  HPLMM_ART_CONTACT_PTR = 8,  /* int32[N^c+1]                                   */
+  HPLMM_ART_CONTACT_NODES = 9,/* int32[...] ascending nodes of each contact grid */
+  HPLMM_ART_MORTAR_PTR = 10,  /* int32[N^c+1] CSR over mortar nodes             */
+  HPLMM_ART_MORTAR_NODES = 11,/* int32[N^m] mortar node ids in placement order  */
+  HPLMM_ART_GRAIN_COLS_PTR = 12, /* int32[N^g+1] CSR over shape-vector columns  */
+  HPLMM_ART_GRAIN_COLS = 13,  /* int32[...] ascending mortar DOF columns (R14)  */
+  HPLMM_ART_VAL = 14,         /* double[nnzb*9] values of A^ (after assemble)   */
+  HPLMM_ART_RHS = 15,         /* double[n_dof] b^ (after assemble)              */
+  HPLMM_ART_S = 16,           /* double[N_m*N_m] coarse mortar block S (setup)  */
+  HPLMM_ART_MORTAR_W = 17     /* double[sum |F_c| nu_c] weights, row-major per interface */
+} hplmm_artifact;
+
+/* Copy an artifact to the host buffer `buf` of `cap` BYTES; *len receives the
+ * element count (call with buf=NULL to query).  ERR_STATE if not yet built. */
+hplmm_status hplmm_export(hplmm_handle *h, int32_t artifact, void *buf, int64_t cap,
+                          int64_t *len);
+
+/* Sizes / timings gathered so far. */
+hplmm_status hplmm_get_report(hplmm_handle *h, hplmm_report *report);
+
+/* Profiling of the dominant kernel (the packed symmetric tile product that
+ * applies every local and coarse inverse): when enabled, CUDA events are
+ * recorded around each launch on the launch stream.  reset != 0 clears the
+ * accumulated statistics. */
+hplmm_status hplmm_profile(hplmm_handle *h, int32_t enable, int32_t reset);
+
+/* Statistics of kernel class `kernel` (0 = grain SYMV tiles, 1 = contact-grid
+ * SYMV tiles, 2 = coarse SYMV tiles): total device ms and launch count since
+ * the last reset; tile_bytes = packed-tile bytes one launch streams. */
+hplmm_status hplmm_kernel_stats(hplmm_handle *h, int32_t kernel, double *total_ms,
+                                int64_t *launches, int64_t *tile_bytes);
+
+void hplmm_destroy(hplmm_handle *h);
+const char *hplmm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPLMM_H */

@@ -1,0 +1,1065 @@
+// libhplmm C ABI: handle, device state, setup / solve / apply orchestration.
+// See include/hplmm.h for the contract and DESIGN.md for the data layout.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hplmm_internal.h"
+#include "kernels.cuh"
+
+using namespace hplmm;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct HError {
+  hplmm_status st;
+  std::string msg;
+};
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw HError{e_ == cudaErrorMemoryAllocation ? HPLMM_ERR_OOM : HPLMM_ERR_CUDA,       \
+                   std::string(#call) + ": " + cudaGetErrorString(e_)};                   \
+  } while (0)
+
+enum KernelClass { KC_SYMV_GRAIN = 0, KC_SYMV_CONTACT = 1, KC_SYMV_COARSE = 2, KC_N = 3 };
+
+}  // namespace
+
+struct hplmm_handle {
+  HostSetup hs;
+  int device = -1;
+  cudaStream_t st = 0;
+  bool assembled = false, setup_done = false, rhs_set = false;
+  hplmm_report rep{};
+  std::vector<void*> allocs;
+  std::vector<void*> setup_allocs;
+
+  // mesh / matrix
+  int n_nodes = 0, n_dof = 0;
+  int64_t nnzb = 0;
+  int32_t *d_row_ptr = nullptr, *d_col = nullptr, *d_block_row = nullptr, *d_drow_ptr = nullptr,
+          *d_dcol = nullptr, *d_ijk = nullptr;
+  uint8_t *d_dir = nullptr, *d_solid = nullptr;
+  double *d_E = nullptr, *d_K0 = nullptr, *d_val = nullptr, *d_b = nullptr, *d_f = nullptr,
+         *d_uD = nullptr;
+
+  // subdomains
+  DevBatch gb, cb, sb, sS;  // grain, contact, coarse inverse, coarse S (refinement)
+  double* d_ym = nullptr;
+  int32_t *d_gnode_ptr = nullptr, *d_gnodes = nullptr, *d_cnode_ptr = nullptr,
+          *d_cnodes = nullptr;
+  int32_t *d_cptr = nullptr, *d_cidx = nullptr;
+  DevCoarse co;
+  std::vector<int32_t> h_corr;   // grains with a correction column (after set_rhs)
+  double* d_Sdense = nullptr;
+  int64_t lds = 0;
+  std::vector<int32_t> h_ld, h_nbg;
+
+  // work vectors
+  double *d_in = nullptr, *d_out = nullptr, *d_y = nullptr, *d_r1 = nullptr, *d_z1 = nullptr,
+         *d_t = nullptr, *d_rm = nullptr, *d_rc = nullptr, *d_yc = nullptr, *d_x = nullptr,
+         *d_u = nullptr, *d_bb = nullptr;
+  double *d_V = nullptr, *d_partial = nullptr, *d_hbuf = nullptr;
+  int64_t ldv = 0;
+  int Vcap = 0;
+
+  // profiling of the dominant kernel (packed SYMV tiles)
+  bool profile = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+  double kc_ms[KC_N] = {0, 0, 0};
+  int64_t kc_launches[KC_N] = {0, 0, 0};
+  int64_t launches = 0;
+
+  template <class T>
+  T* dalloc(size_t n, bool setup_only = false) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw HError{HPLMM_ERR_OOM, "cudaMalloc of " + std::to_string(n * sizeof(T)) + " bytes: " +
+                                      cudaGetErrorString(e)};
+    }
+    (setup_only ? setup_allocs : allocs).push_back(p);
+    return (T*)p;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = dalloc<T>(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return p;
+  }
+  void free_setup() {
+    for (void* p : setup_allocs) cudaFree(p);
+    setup_allocs.clear();
+  }
+  ~hplmm_handle() {
+    if (device >= 0) {
+      cudaSetDevice(device);
+      cudaDeviceSynchronize();
+      for (void* p : allocs) cudaFree(p);
+      free_setup();
+      for (auto e : ev_pool) cudaEventDestroy(e);
+      for (auto& e : ev_pending) {
+        cudaEventDestroy(e.second.first);
+        cudaEventDestroy(e.second.second);
+      }
+    }
+  }
+
+  // ---- profiled launches of the dominant kernel --------------------------
+  void symv(DevBatch& b, int kc) {
+    if (profile && b.ntiles > 0) {
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, st));
+      launch_symv_tiles(b, st);
+      CK(cudaEventRecord(e1, st));
+      ev_pending.push_back({kc, {e0, e1}});
+    } else {
+      launch_symv_tiles(b, st);
+    }
+    launch_symv_reduce(b, st);
+    launches += 2;
+  }
+  void flush_profile() {
+    for (auto& e : ev_pending) {
+      float ms = 0.f;
+      CK(cudaEventSynchronize(e.second.second));
+      CK(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+      kc_ms[e.first] += ms;
+      kc_launches[e.first] += 1;
+      cudaEventDestroy(e.second.first);
+      cudaEventDestroy(e.second.second);
+    }
+    ev_pending.clear();
+  }
+};
+
+namespace {
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+hplmm_status fail(const HError& e) {
+  g_last_error = e.msg;
+  return e.st;
+}
+
+// Build a packed-tile batch over subdomains given by node lists (DOFs 3n+c)
+// or, for the coarse block, one subdomain of `ndof_override` identity DOFs.
+void build_batch(hplmm_handle* h, DevBatch& b, const std::vector<int32_t>& ptr,
+                 const std::vector<int32_t>& nodes, int ndof_override, bool setup_buffers) {
+  int nsub = ndof_override >= 0 ? 1 : (int)ptr.size() - 1;
+  std::vector<int32_t> nb(nsub), ndof(nsub);
+  std::vector<int64_t> tile_base(nsub), row_base(nsub);
+  int64_t nt = 0, nr = 0;
+  int maxnb = 0;
+  for (int s = 0; s < nsub; ++s) {
+    ndof[s] = ndof_override >= 0 ? ndof_override : 3 * (ptr[s + 1] - ptr[s]);
+    nb[s] = (ndof[s] + TB - 1) / TB;
+    tile_base[s] = nt;
+    row_base[s] = nr;
+    nt += (int64_t)nb[s] * (nb[s] + 1) / 2;
+    nr += nb[s];
+    maxnb = std::max(maxnb, nb[s]);
+  }
+  std::vector<int32_t> tile_s(nt), tile_ij(nt), row_s(nr), row_k(nr), lmap(nr * TB, -1);
+  for (int s = 0; s < nsub; ++s) {
+    int64_t t = tile_base[s];
+    for (int I = 0; I < nb[s]; ++I) {
+      row_s[row_base[s] + I] = s;
+      row_k[row_base[s] + I] = I;
+      for (int J = 0; J <= I; ++J, ++t) {
+        tile_s[t] = s;
+        tile_ij[t] = (I << 16) | J;
+      }
+    }
+    for (int i = 0; i < ndof[s]; ++i)
+      lmap[row_base[s] * TB + i] =
+          ndof_override >= 0 ? i : 3 * nodes[ptr[s] + i / 3] + (i % 3);
+  }
+  b.nsub = nsub;
+  b.max_nb = maxnb;
+  b.ntiles = nt;
+  b.nrows = nr;
+  b.nloc = nr * TB;
+  b.nb = h->upload(nb);
+  b.ndof = h->upload(ndof);
+  b.tile_base = h->upload(tile_base);
+  b.row_base = h->upload(row_base);
+  b.tile_s = h->upload(tile_s);
+  b.tile_ij = h->upload(tile_ij);
+  b.row_s = h->upload(row_s);
+  b.row_k = h->upload(row_k);
+  b.lmap = h->upload(lmap);
+  b.tiles = h->dalloc<double>((size_t)nt * TILE);
+  b.part_row = h->dalloc<double>((size_t)nt * TB);
+  b.part_col = h->dalloc<double>((size_t)nt * TB);
+  b.xloc = h->dalloc<double>((size_t)b.nloc);
+  b.yloc = h->dalloc<double>((size_t)b.nloc);
+  b.err = h->dalloc<int32_t>(1);
+  if (setup_buffers) {
+    b.dinv = h->dalloc<double>((size_t)nsub * TILE, true);
+    b.cbuf = h->dalloc<double>((size_t)nr * TILE, true);
+    b.wbuf = h->dalloc<double>((size_t)nr * TILE, true);
+  }
+}
+
+void check_batch_err(hplmm_handle* h, DevBatch& b, int offset, bool coarse) {
+  int32_t e = INT_MAX;
+  CK(cudaMemcpyAsync(&e, b.err, sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (e != INT_MAX) {
+    h->rep.err_index = offset + e;
+    if (coarse) throw HError{HPLMM_ERR_SINGULAR_COARSE, "non-positive pivot in the coarse matrix S"};
+    throw HError{HPLMM_ERR_SINGULAR_LOCAL,
+                 "non-positive pivot in local subdomain " + std::to_string(offset + e)};
+  }
+}
+
+double elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(&ms, a, b);
+  return ms * 1e-3;
+}
+
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t st;
+  explicit Timer(cudaStream_t s) : st(s) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  double stop() {
+    cudaEventRecord(b, st);
+    return elapsed(a, b);
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+// copy `n` doubles from host-or-device `src` to device `dst`
+void to_device(hplmm_handle* h, double* dst, const double* src, int64_t n) {
+  CK(cudaMemcpyAsync(dst, src, n * sizeof(double),
+                     is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
+}
+void from_device(hplmm_handle* h, double* dst, const double* src, int64_t n) {
+  CK(cudaMemcpyAsync(dst, src, n * sizeof(double),
+                     is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+}
+
+void require_device(hplmm_handle* h) {
+  if (h->device < 0) throw HError{HPLMM_ERR_STATE, "no device bound: call hplmm_assemble first"};
+  CK(cudaSetDevice(h->device));
+}
+
+// ---------------------------------------------------------------------------
+// operator applications (all on device vectors of length n_dof)
+// ---------------------------------------------------------------------------
+void op_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
+  launch_spmv(h->n_nodes, h->d_row_ptr, h->d_col, h->d_val, x, v, y, h->st);
+  h->launches++;
+}
+
+void op_mzeta(hplmm_handle* h, const double* in, double* out) {
+  launch_gather(h->cb, in, h->st);
+  h->symv(h->cb, KC_SYMV_CONTACT);
+  launch_sum_contact(h->n_dof, h->d_cptr, h->d_cidx, h->cb.yloc, out, h->st);
+  h->launches += 2;
+}
+
+// out = a + b + M_g^-1 in
+void op_mgrain(hplmm_handle* h, const double* in, const double* a, const double* b, double* out) {
+  launch_gather(h->gb, in, h->st);
+  h->symv(h->gb, KC_SYMV_GRAIN);
+  launch_combine_grain(h->n_dof, h->co.gpos, h->gb.yloc, a, b, out, h->st);
+  h->launches += 2;
+}
+
+// y_m = S^-1 r_m by the packed inverse; optional refinement y += S^-1 (r - S y)
+const double* op_coarse(hplmm_handle* h, const double* rm) {
+  launch_gather(h->sb, rm, h->st);
+  h->symv(h->sb, KC_SYMV_COARSE);
+  h->launches += 1;
+  if (!h->hs.opt.coarse_refine || h->co.Nm == 0) return h->sb.yloc;
+  const int Nm = h->co.Nm;
+  CK(cudaMemcpyAsync(h->d_ym, h->sb.yloc, (size_t)Nm * 8, cudaMemcpyDeviceToDevice, h->st));
+  launch_gather(h->sS, h->d_ym, h->st);
+  h->symv(h->sS, KC_SYMV_COARSE);
+  launch_gather(h->sb, rm, h->st);
+  launch_axpy(h->sb.nloc, -1.0, h->sS.yloc, h->sb.xloc, h->st);
+  h->symv(h->sb, KC_SYMV_COARSE);
+  launch_axpy(Nm, 1.0, h->sb.yloc, h->d_ym, h->st);
+  h->launches += 4;
+  return h->d_ym;
+}
+
+void op_mg(hplmm_handle* h, const double* in, double* out) {
+  launch_restrict(h->co, in, h->d_rm, h->d_rc, h->st);
+  const double* ym = op_coarse(h, h->d_rm);
+  launch_coarse_diag(h->co.n_grains, h->d_rc, h->co.Dc, h->d_yc, h->st);
+  launch_prolong(h->co, ym, h->d_yc, out, h->st);
+  h->launches += 6;
+}
+
+// M_CG^-1: z1 = M_zeta^-1 in ; out = z1 + M_g^-1 (in - A z1)   (eq:local_smoother_CG)
+void op_mcg(hplmm_handle* h, const double* in, double* out) {
+  op_mzeta(h, in, h->d_z1);
+  op_spmv(h, h->d_z1, in, h->d_t);
+  op_mgrain(h, h->d_t, h->d_z1, nullptr, out);
+}
+
+// M^-1: y = M_G^-1 in ; r1 = in - A y ; out = y + M_CG^-1 r1     (eq:multi_precond)
+void op_minv(hplmm_handle* h, const double* in, double* out) {
+  op_mg(h, in, h->d_y);
+  op_spmv(h, h->d_y, in, h->d_r1);
+  op_mzeta(h, h->d_r1, h->d_z1);
+  op_spmv(h, h->d_z1, h->d_r1, h->d_t);
+  op_mgrain(h, h->d_t, h->d_y, h->d_z1, out);
+}
+
+void do_set_rhs(hplmm_handle* h, const double* b_dev) {
+  Timer t(h->st);
+  launch_gather(h->gb, b_dev, h->st);
+  h->symv(h->gb, KC_SYMV_GRAIN);
+  launch_set_correction(h->co, h->gb, h->st);
+  h->launches += 2;
+  std::vector<double> Dc(h->co.n_grains);
+  if (h->co.n_grains)
+    CK(cudaMemcpyAsync(Dc.data(), h->co.Dc, Dc.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       h->st));
+  CK(cudaStreamSynchronize(h->st));
+  h->h_corr.clear();
+  for (int g = 0; g < h->co.n_grains; ++g)
+    if (Dc[g] != 0.0) h->h_corr.push_back(g);
+  h->rep.n_coarse = h->co.Nm + (int)h->h_corr.size();
+  h->rhs_set = true;
+  h->rep.t_rhs_s = t.stop();
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+void hplmm_default_options(hplmm_options* o) {
+  if (!o) return;
+  o->n_mortar = 4;
+  o->beta = 4.0;
+  o->contact_h = 1;
+  o->restart = 50;
+  o->max_iter = 300;
+  o->n_st = 1;
+  o->coarse_refine = 0;
+}
+
+const char* hplmm_last_error(void) { return g_last_error.c_str(); }
+
+hplmm_status hplmm_create(const hplmm_problem* prob, const hplmm_options* opt,
+                          hplmm_handle** out) {
+  if (!out) { g_last_error = "hplmm_create: out is NULL"; return HPLMM_ERR_ARG; }
+  *out = nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  hplmm_handle* h = new hplmm_handle();
+  std::string err;
+  if (!host_setup(prob, opt, h->hs, err)) {
+    delete h;
+    g_last_error = err;
+    return HPLMM_ERR_ARG;
+  }
+  HostSetup& hs = h->hs;
+  h->n_nodes = hs.n_nodes;
+  h->n_dof = 3 * hs.n_nodes;
+  h->nnzb = (int64_t)hs.col_idx.size();
+  h->rep.n_nodes = hs.n_nodes;
+  h->rep.nnzb = h->nnzb;
+  h->rep.n_grains = hs.n_grains;
+  h->rep.n_interfaces = hs.n_ifaces();
+  h->rep.n_mortar_dofs = 3 * hs.n_mortar_nodes();
+  h->rep.n_coarse = h->rep.n_mortar_dofs;
+  h->rep.err_index = -1;
+  h->rep.t_host_setup_s =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = h;
+  return HPLMM_OK;
+}
+
+hplmm_status hplmm_assemble(hplmm_handle* h, int32_t device, void* stream) {
+  if (!h) { g_last_error = "null handle"; return HPLMM_ERR_ARG; }
+  try {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw HError{HPLMM_ERR_CUDA, "no CUDA device available (there is no CPU fallback)"};
+    }
+    if (h->device >= 0 && h->device != device)
+      throw HError{HPLMM_ERR_STATE, "handle already bound to another device"};
+    CK(cudaSetDevice(device));
+    h->device = device;
+    h->st = (cudaStream_t)stream;
+    HostSetup& hs = h->hs;
+    Timer t(h->st);
+    if (!h->d_val) {
+      std::vector<int32_t> brow(h->nnzb);
+      for (int p = 0; p < h->n_nodes; ++p)
+        for (int e2 = hs.row_ptr[p]; e2 < hs.row_ptr[p + 1]; ++e2) brow[e2] = p;
+      h->d_row_ptr = h->upload(hs.row_ptr);
+      h->d_col = h->upload(hs.col_idx);
+      h->d_block_row = h->upload(brow);
+      h->d_drow_ptr = h->upload(hs.drow_ptr);
+      h->d_dcol = h->upload(hs.dcol);
+      h->d_ijk = h->upload(hs.node_ijk);
+      h->d_dir = h->upload(hs.dir);
+      h->d_solid = h->upload(hs.solid);
+      h->d_E = h->upload(hs.E);
+      h->d_f = h->upload(hs.f);
+      h->d_uD = h->upload(hs.u_D);
+      h->d_K0 = h->dalloc<double>(576);
+      h->d_val = h->dalloc<double>((size_t)h->nnzb * 9);
+      h->d_b = h->dalloc<double>(h->n_dof);
+    }
+    launch_element_K0(h->d_K0, hs.nu, h->st);
+    launch_assemble((int)h->nnzb, h->d_block_row, h->d_col, h->d_ijk, h->d_dir, h->d_solid,
+                    h->d_E, hs.nx, hs.ny, hs.nz, h->d_K0, h->d_val, h->st);
+    launch_assemble_rhs(h->n_nodes, h->d_drow_ptr, h->d_dcol, h->d_ijk, h->d_dir, h->d_solid,
+                        h->d_E, hs.nx, hs.ny, hs.nz, h->d_K0, h->d_f, h->d_uD, h->d_b, h->st);
+    CK(cudaGetLastError());
+    h->rep.t_assemble_s = t.stop();
+    CK(cudaStreamSynchronize(h->st));
+    h->assembled = true;
+    return HPLMM_OK;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
+hplmm_status hplmm_set_matrix(hplmm_handle* h, const double* val, void* stream) {
+  if (!h || !val) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
+  try {
+    if (!h->assembled) throw HError{HPLMM_ERR_STATE, "hplmm_set_matrix before hplmm_assemble"};
+    if (h->setup_done) throw HError{HPLMM_ERR_STATE, "hplmm_set_matrix after hplmm_setup"};
+    require_device(h);
+    h->st = (cudaStream_t)stream;
+    to_device(h, h->d_val, val, h->nnzb * 9);
+    CK(cudaStreamSynchronize(h->st));
+    return HPLMM_OK;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
+hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
+  if (!h) { g_last_error = "null handle"; return HPLMM_ERR_ARG; }
+  try {
+    if (!h->assembled) throw HError{HPLMM_ERR_STATE, "hplmm_setup before hplmm_assemble"};
+    if (h->setup_done) throw HError{HPLMM_ERR_STATE, "hplmm_setup called twice"};
+    require_device(h);
+    h->st = (cudaStream_t)stream;
+    HostSetup& hs = h->hs;
+    const int G = hs.n_grains, C = hs.n_ifaces(), N = h->n_nodes;
+    const int Nm = 3 * hs.n_mortar_nodes();
+
+    // ---------------- host bookkeeping -----------------------------------
+    std::vector<int32_t> node_local(N, -1);
+    for (int g = 0; g < G; ++g)
+      for (int e = hs.grain_ptr[g]; e < hs.grain_ptr[g + 1]; ++e)
+        node_local[hs.grain_nodes[e]] = e - hs.grain_ptr[g];
+    for (int c = 0; c < C; ++c)
+      for (int e = hs.iface_ptr[c]; e < hs.iface_ptr[c + 1]; ++e)
+        node_local[hs.iface_nodes[e]] = e - hs.iface_ptr[c];
+
+    // ---------------- batches --------------------------------------------
+    build_batch(h, h->gb, hs.grain_ptr, hs.grain_nodes, -1, true);
+    build_batch(h, h->cb, hs.contact_ptr, hs.contact_nodes, -1, true);
+    build_batch(h, h->sb, {}, {}, Nm, true);
+    int64_t lb = (h->gb.ntiles + h->cb.ntiles) * (int64_t)TILE * 8;
+    h->rep.local_bytes = lb;
+    h->rep.coarse_bytes = h->sb.ntiles * (int64_t)TILE * 8 * (hs.opt.coarse_refine ? 2 : 1);
+
+    // grain positions and contact reverse map
+    std::vector<int32_t> nbg(G), gpos(h->n_dof, -1);
+    {
+      int64_t rb = 0;
+      for (int g = 0; g < G; ++g) {
+        int nd = 3 * (hs.grain_ptr[g + 1] - hs.grain_ptr[g]);
+        nbg[g] = (nd + TB - 1) / TB;
+        for (int i = 0; i < nd; ++i)
+          gpos[3 * hs.grain_nodes[hs.grain_ptr[g] + i / 3] + i % 3] = (int32_t)(rb * TB + i);
+        rb += nbg[g];
+      }
+    }
+    h->h_nbg = nbg;
+    {
+      std::vector<int32_t> cnt(h->n_dof + 1, 0);
+      int64_t rb = 0;
+      std::vector<int64_t> crb(C);
+      for (int c = 0; c < C; ++c) {
+        crb[c] = rb;
+        int nd = 3 * (hs.contact_ptr[c + 1] - hs.contact_ptr[c]);
+        for (int i = 0; i < nd; ++i) cnt[3 * hs.contact_nodes[hs.contact_ptr[c] + i / 3] + i % 3 + 1]++;
+        rb += (nd + TB - 1) / TB;
+      }
+      for (int d = 0; d < h->n_dof; ++d) cnt[d + 1] += cnt[d];
+      std::vector<int32_t> idx(cnt[h->n_dof]), fill(cnt.begin(), cnt.end() - 1);
+      for (int c = 0; c < C; ++c) {
+        int nd = 3 * (hs.contact_ptr[c + 1] - hs.contact_ptr[c]);
+        for (int i = 0; i < nd; ++i) {
+          int d = 3 * hs.contact_nodes[hs.contact_ptr[c] + i / 3] + i % 3;
+          idx[fill[d]++] = (int32_t)(crb[c] * TB + i);
+        }
+      }
+      h->d_cptr = h->upload(cnt);
+      h->d_cidx = h->upload(idx);
+    }
+
+    // coarse bookkeeping
+    DevCoarse& co = h->co;
+    co.n_grains = G;
+    co.n_ifaces = C;
+    co.Nm = Nm;
+    co.n_dof = h->n_dof;
+    std::vector<int32_t> ld(G), mortar_iface(hs.n_mortar_nodes());
+    std::vector<int64_t> b_off(G), wt_off(C), yext_off(G), cg_off(G), chunk_t(h->gb.nrows);
+    int64_t off = 0, yo = 0, co2 = 0, ct = 0;
+    int maxk = 0;
+    for (int g = 0; g < G; ++g) {
+      int k = hs.gcols_ptr[g + 1] - hs.gcols_ptr[g];
+      maxk = std::max(maxk, k);
+      ld[g] = k + 1;
+      b_off[g] = off;
+      off += (int64_t)TB * nbg[g] * ld[g];
+      yext_off[g] = yo;
+      yo += ld[g];
+      cg_off[g] = co2;
+      co2 += (int64_t)k * k;
+    }
+    {
+      int64_t rb = 0;
+      for (int g = 0; g < G; ++g)
+        for (int I = 0; I < nbg[g]; ++I, ++rb) {
+          chunk_t[rb] = ct;
+          ct += ld[g];
+        }
+    }
+    int64_t wo = 0;
+    for (int c = 0; c < C; ++c) {
+      wt_off[c] = wo;
+      int nu = hs.mortar_ptr[c + 1] - hs.mortar_ptr[c];
+      wo += (int64_t)(hs.iface_ptr[c + 1] - hs.iface_ptr[c]) * nu;
+      for (int m = hs.mortar_ptr[c]; m < hs.mortar_ptr[c + 1]; ++m) mortar_iface[m] = c;
+    }
+    std::vector<int32_t> mcol_ptr(Nm + 1, 0), mcol_g, mcol_j;
+    for (int g = 0; g < G; ++g)
+      for (int e = hs.gcols_ptr[g]; e < hs.gcols_ptr[g + 1]; ++e) mcol_ptr[hs.gcols[e] + 1]++;
+    for (int k = 0; k < Nm; ++k) mcol_ptr[k + 1] += mcol_ptr[k];
+    mcol_g.resize(mcol_ptr[Nm]);
+    mcol_j.resize(mcol_ptr[Nm]);
+    {
+      std::vector<int32_t> fill(mcol_ptr.begin(), mcol_ptr.end() - 1);
+      for (int g = 0; g < G; ++g)
+        for (int e = hs.gcols_ptr[g]; e < hs.gcols_ptr[g + 1]; ++e) {
+          int k = hs.gcols[e];
+          mcol_g[fill[k]] = g;
+          mcol_j[fill[k]++] = e - hs.gcols_ptr[g];
+        }
+    }
+    std::vector<int32_t> chunk_ptr(G + 1, 0);
+    for (int g = 0; g < G; ++g) chunk_ptr[g + 1] = chunk_ptr[g] + nbg[g];
+    h->h_ld = ld;
+    co.grain_node_ptr = h->upload(hs.grain_ptr);
+    co.grain_nodes = h->upload(hs.grain_nodes);
+    co.gcols_ptr = h->upload(hs.gcols_ptr);
+    co.gcols = h->upload(hs.gcols);
+    co.giface_ptr = h->upload(hs.giface_ptr);
+    co.giface = h->upload(hs.giface);
+    co.ld = h->upload(ld);
+    co.b_off = h->upload(b_off);
+    co.B = h->dalloc<double>(std::max<int64_t>(off, 1));
+    co.R = h->dalloc<double>(std::max<int64_t>(off, 1), true);
+    co.iface_ptr = h->upload(hs.iface_ptr);
+    co.iface_nodes = h->upload(hs.iface_nodes);
+    co.mortar_ptr = h->upload(hs.mortar_ptr);
+    co.wt_off = h->upload(wt_off);
+    co.W = h->dalloc<double>(std::max<int64_t>(wo, 1));
+    co.node_class = h->upload(hs.node_class);
+    co.node_owner = h->upload(hs.node_owner);
+    co.node_iface = h->upload(hs.node_iface);
+    co.node_local = h->upload(node_local);
+    co.n_chunks = h->gb.nrows;
+    co.chunk_g = h->gb.row_s;
+    {
+      std::vector<int32_t> r0(h->gb.nrows);
+      int64_t rb = 0;
+      for (int g = 0; g < G; ++g)
+        for (int I = 0; I < nbg[g]; ++I) r0[rb++] = TB * I;
+      co.chunk_r0 = h->upload(r0);
+    }
+    co.chunk_t = h->upload(chunk_t);
+    co.tpart = h->dalloc<double>(std::max<int64_t>(ct, 1));
+    co.chunk_ptr = h->upload(chunk_ptr);
+    co.mcol_ptr = h->upload(mcol_ptr);
+    co.mcol_g = h->upload(mcol_g);
+    co.mcol_j = h->upload(mcol_j);
+    co.yext = h->dalloc<double>(std::max<int64_t>(yo, 1));
+    co.yext_off = h->upload(yext_off);
+    co.Dc = h->dalloc<double>(std::max(G, 1));
+    co.Cg = h->dalloc<double>(std::max<int64_t>(co2, 1), true);
+    co.cg_off = h->upload(cg_off);
+    co.mortar_iface = h->upload(mortar_iface);
+    co.gpos = h->upload(gpos);
+    co.g_lmap = h->gb.lmap;
+    co.g_row_s = h->gb.row_s;
+    co.g_row_base = h->gb.row_base;
+    co.max_k = maxk;
+    h->rep.prolong_nnz = off + wo * 3;
+    CK(cudaMemsetAsync(co.B, 0, std::max<int64_t>(off, 1) * 8, h->st));
+    CK(cudaMemsetAsync(co.R, 0, std::max<int64_t>(off, 1) * 8, h->st));
+    CK(cudaMemsetAsync(co.Dc, 0, std::max(G, 1) * 8, h->st));
+
+    // node lists for extraction
+    h->d_gnode_ptr = h->upload(hs.grain_ptr);
+    h->d_gnodes = h->upload(hs.grain_nodes);
+    h->d_cnode_ptr = h->upload(hs.contact_ptr);
+    h->d_cnodes = h->upload(hs.contact_nodes);
+
+    // work vectors
+    int nd = h->n_dof;
+    for (double** p : {&h->d_in, &h->d_out, &h->d_y, &h->d_r1, &h->d_z1, &h->d_t, &h->d_x,
+                       &h->d_u, &h->d_bb})
+      *p = h->dalloc<double>(nd);
+    h->d_rm = h->dalloc<double>(std::max(Nm, 1));
+    h->d_ym = h->dalloc<double>(std::max(Nm, 1));
+    h->d_rc = h->dalloc<double>(std::max(G, 1));
+    h->d_yc = h->dalloc<double>(std::max(G, 1));
+    CK(cudaMemsetAsync(h->d_rm, 0, std::max(Nm, 1) * 8, h->st));
+
+    // ---------------- T_ML: local inversions ------------------------------
+    Timer tl(h->st);
+    int32_t big = INT_MAX;
+    for (DevBatch* b : {&h->gb, &h->cb, &h->sb}) {
+      CK(cudaMemsetAsync(b->tiles, 0, (size_t)b->ntiles * TILE * 8, h->st));
+      CK(cudaMemcpyAsync(b->err, &big, 4, cudaMemcpyHostToDevice, h->st));
+    }
+    launch_extract_local(h->gb, hs.grain_ptr.back(), h->d_gnode_ptr, h->d_gnodes, h->d_row_ptr,
+                         h->d_col, h->d_val, h->st);
+    launch_extract_local(h->cb, hs.contact_ptr.back(), h->d_cnode_ptr, h->d_cnodes, h->d_row_ptr,
+                         h->d_col, h->d_val, h->st);
+    launch_pad_identity(h->gb, h->st);
+    launch_pad_identity(h->cb, h->st);
+    launch_sweep_invert(h->gb, h->st);
+    launch_sweep_invert(h->cb, h->st);
+    CK(cudaGetLastError());
+    check_batch_err(h, h->gb, 0, false);
+    check_batch_err(h, h->cb, G, false);
+    h->rep.t_setup_local_s = tl.stop();
+
+    // ---------------- T_MG: mortars, P_B, S, S^-1 -------------------------
+    Timer tc(h->st);
+    {
+      std::vector<int32_t> iface_of(hs.iface_nodes.size());
+      for (int c = 0; c < C; ++c)
+        for (int e = hs.iface_ptr[c]; e < hs.iface_ptr[c + 1]; ++e) iface_of[e] = c;
+      int32_t* d_iface_of = h->upload(iface_of);
+      launch_mortar_weights((int)iface_of.size(), d_iface_of, co.iface_ptr, co.iface_nodes,
+                            co.mortar_ptr, h->upload(hs.mortar_nodes), co.wt_off, h->d_ijk,
+                            hs.opt.beta, co.W, h->st);
+    }
+    launch_build_R(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
+    {
+      std::vector<int32_t> kc(G);
+      for (int g = 0; g < G; ++g) kc[g] = ld[g] - 1;
+      launch_symm_neg(h->gb, co.b_off, co.ld, h->upload(kc), (maxk + TB - 1) / TB, co.R, co.B,
+                      h->st);
+    }
+    launch_grain_AB(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
+    launch_grain_BtY(co, h->gb, h->st);
+    int64_t npS = (int64_t)TB * h->sb.max_nb;
+    h->lds = npS;
+    bool keepS = (npS * npS * 8) <= (int64_t)512 << 20;
+    h->d_Sdense = h->dalloc<double>(std::max<int64_t>(npS * npS, 1), !keepS);
+    CK(cudaMemsetAsync(h->d_Sdense, 0, std::max<int64_t>(npS * npS, 1) * 8, h->st));
+    launch_S_iface(co, h->d_row_ptr, h->d_col, h->d_val, h->d_Sdense, npS, h->st);
+    launch_S_grain(co, h->d_Sdense, npS, h->st);
+    launch_pack_dense(h->sb, h->d_Sdense, npS, h->st);
+    launch_pad_identity(h->sb, h->st);
+    if (hs.opt.coarse_refine) {
+      h->sS = h->sb;
+      h->sS.tiles = h->dalloc<double>((size_t)h->sb.ntiles * TILE);
+      h->sS.xloc = h->dalloc<double>((size_t)h->sb.nloc);
+      h->sS.yloc = h->dalloc<double>((size_t)h->sb.nloc);
+      CK(cudaMemcpyAsync(h->sS.tiles, h->sb.tiles, (size_t)h->sb.ntiles * TILE * 8,
+                         cudaMemcpyDeviceToDevice, h->st));
+    }
+    launch_sweep_invert(h->sb, h->st);
+    CK(cudaGetLastError());
+    check_batch_err(h, h->sb, 0, true);
+    h->rep.t_setup_coarse_s = tc.stop();
+    CK(cudaStreamSynchronize(h->st));
+    if (!keepS) h->d_Sdense = nullptr;
+    h->free_setup();
+    h->gb.dinv = h->gb.cbuf = h->gb.wbuf = nullptr;
+    h->cb.dinv = h->cb.cbuf = h->cb.wbuf = nullptr;
+    h->sb.dinv = h->sb.cbuf = h->sb.wbuf = nullptr;
+    h->sS.dinv = h->sS.cbuf = h->sS.wbuf = nullptr;
+    co.R = nullptr;
+    co.Cg = nullptr;
+    h->setup_done = true;
+    return HPLMM_OK;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
+hplmm_status hplmm_set_rhs(hplmm_handle* h, const double* b, void* stream) {
+  if (!h || !b) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
+  try {
+    if (!h->setup_done) throw HError{HPLMM_ERR_STATE, "hplmm_set_rhs before hplmm_setup"};
+    require_device(h);
+    h->st = (cudaStream_t)stream;
+    to_device(h, h->d_bb, b, h->n_dof);
+    do_set_rhs(h, h->d_bb);
+    CK(cudaGetLastError());
+    return HPLMM_OK;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
+hplmm_status hplmm_apply(hplmm_handle* h, int32_t op, const double* in, double* out,
+                         void* stream) {
+  if (!h || !in || !out) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
+  try {
+    require_device(h);
+    h->st = (cudaStream_t)stream;
+    if (op == HPLMM_OP_SPMV) {
+      if (!h->assembled) throw HError{HPLMM_ERR_STATE, "apply(SPMV) before assemble"};
+    } else if (!h->setup_done) {
+      throw HError{HPLMM_ERR_STATE, "apply before hplmm_setup"};
+    }
+    if ((op == HPLMM_OP_MG || op == HPLMM_OP_MINV || op == HPLMM_OP_RESTRICT ||
+         op == HPLMM_OP_PROLONG) && !h->rhs_set)
+      throw HError{HPLMM_ERR_STATE, "apply(MG/MINV/RESTRICT/PROLONG) needs hplmm_set_rhs"};
+    int nd = h->n_dof;
+    double* din = h->d_in;
+    double* dout = h->d_out;
+    if (op == HPLMM_OP_SPMV && !din) {  // before setup: temporary buffers
+      din = h->dalloc<double>(nd);
+      dout = h->dalloc<double>(nd);
+      h->d_in = din;
+      h->d_out = dout;
+    }
+    int nin = (op == HPLMM_OP_PROLONG) ? h->rep.n_coarse : nd;
+    int nout = (op == HPLMM_OP_RESTRICT) ? h->rep.n_coarse : nd;
+    const int Nm = h->co.Nm;
+    if (op == HPLMM_OP_COARSE) {
+      to_device(h, h->d_rm, in, Nm);
+      const double* ym = op_coarse(h, h->d_rm);
+      from_device(h, out, ym, Nm);
+      CK(cudaStreamSynchronize(h->st));
+      h->flush_profile();
+      return HPLMM_OK;
+    }
+    if (op == HPLMM_OP_PROLONG) {
+      std::vector<double> hin(nin), yc(std::max(h->co.n_grains, 1), 0.0);
+      if (is_device_ptr(in)) CK(cudaMemcpy(hin.data(), in, nin * 8, cudaMemcpyDeviceToHost));
+      else std::memcpy(hin.data(), in, nin * 8);
+      for (size_t j = 0; j < h->h_corr.size(); ++j) yc[h->h_corr[j]] = hin[Nm + j];
+      CK(cudaMemcpyAsync(h->d_rm, hin.data(), std::max(Nm, 0) * 8, cudaMemcpyHostToDevice, h->st));
+      CK(cudaMemcpyAsync(h->d_yc, yc.data(), yc.size() * 8, cudaMemcpyHostToDevice, h->st));
+      launch_prolong(h->co, h->d_rm, h->d_yc, dout, h->st);
+    } else {
+      to_device(h, din, in, nin);
+      switch (op) {
+        case HPLMM_OP_SPMV: op_spmv(h, din, nullptr, dout); break;
+        case HPLMM_OP_MG: op_mg(h, din, dout); break;
+        case HPLMM_OP_MZETA: op_mzeta(h, din, dout); break;
+        case HPLMM_OP_MGRAIN: op_mgrain(h, din, nullptr, nullptr, dout); break;
+        case HPLMM_OP_MCG: op_mcg(h, din, dout); break;
+        case HPLMM_OP_MINV: op_minv(h, din, dout); break;
+        case HPLMM_OP_RESTRICT: {
+          launch_restrict(h->co, din, h->d_rm, h->d_rc, h->st);
+          std::vector<double> rm(std::max(Nm, 0)), rc(std::max(h->co.n_grains, 1));
+          CK(cudaMemcpyAsync(rm.data(), h->d_rm, Nm * 8, cudaMemcpyDeviceToHost, h->st));
+          CK(cudaMemcpyAsync(rc.data(), h->d_rc, h->co.n_grains * 8, cudaMemcpyDeviceToHost, h->st));
+          CK(cudaStreamSynchronize(h->st));
+          std::vector<double> o(nout);
+          std::copy(rm.begin(), rm.end(), o.begin());
+          for (size_t j = 0; j < h->h_corr.size(); ++j) o[Nm + j] = rc[h->h_corr[j]];
+          if (is_device_ptr(out)) CK(cudaMemcpy(out, o.data(), nout * 8, cudaMemcpyHostToDevice));
+          else std::memcpy(out, o.data(), nout * 8);
+          return HPLMM_OK;
+        }
+        default: throw HError{HPLMM_ERR_ARG, "unknown op"};
+      }
+    }
+    CK(cudaGetLastError());
+    from_device(h, out, dout, nout);
+    CK(cudaStreamSynchronize(h->st));
+    h->flush_profile();
+    return HPLMM_OK;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
+hplmm_status hplmm_solve(hplmm_handle* h, const double* b, double tol, double* x,
+                         hplmm_report* report, double* hist, int32_t hist_cap, void* stream) {
+  if (!h || !b || !x) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
+  try {
+    if (!h->setup_done) throw HError{HPLMM_ERR_STATE, "hplmm_solve before hplmm_setup"};
+    if (!(tol > 0)) throw HError{HPLMM_ERR_ARG, "tol must be > 0"};
+    require_device(h);
+    h->st = (cudaStream_t)stream;
+    cudaStream_t st = h->st;
+    const int n = h->n_dof;
+    const int m = h->hs.opt.restart;
+    const int maxit = h->hs.opt.max_iter;
+    h->launches = 0;
+    if (h->Vcap < m + 1) {
+      h->ldv = ((int64_t)n + 31) / 32 * 32;
+      h->d_V = h->dalloc<double>((size_t)(m + 1) * h->ldv);
+      h->d_partial = h->dalloc<double>((size_t)krylov_blocks(n) * (m + 1));
+      h->d_hbuf = h->dalloc<double>(2 * (m + 1) + 8);
+      h->Vcap = m + 1;
+    }
+    Timer tt(st);
+    double* dB = h->d_bb;
+    to_device(h, dB, b, n);
+    // ||b||
+    double* hb = h->d_hbuf;
+    launch_norm2(n, dB, h->d_partial, hb + 2 * (m + 1), st);
+    h->launches += 2;
+    double bn2 = 0;
+    CK(cudaMemcpyAsync(&bn2, hb + 2 * (m + 1), 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    double bnorm = std::sqrt(bn2);
+    double* dx = h->d_x;
+    CK(cudaMemsetAsync(dx, 0, (size_t)n * 8, st));
+    int total = 0, hl = 0;
+    bool conv = false;
+    double relres = 1.0;
+    hplmm_status status = HPLMM_OK;
+    if (bnorm == 0.0) {
+      conv = true;
+      relres = 0.0;
+    } else {
+      do_set_rhs(h, dB);   // correction columns for this RHS (R15)
+      // r = b (x0 = 0)
+      CK(cudaMemcpyAsync(h->d_r1, dB, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+      std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), hh(2 * (m + 1) + 1);
+      double beta2 = bn2;
+      while (true) {
+        double beta = std::sqrt(beta2);
+        // V0 = r / beta
+        double* V = h->d_V;
+        launch_scale(n, h->d_r1, hb + 2 * (m + 1), 1, V, st);
+        h->launches++;
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int k = 0;
+        for (int j = 0; j < m; ++j) {
+          double* vj = V + j * h->ldv;
+          double* w = V + (j + 1) * h->ldv;
+          op_minv(h, vj, h->d_u);
+          op_spmv(h, h->d_u, nullptr, w);
+          // CGS2
+          launch_multidot(n, j + 1, V, h->ldv, w, h->d_partial, hb, st);
+          launch_update(n, j + 1, V, h->ldv, hb, w, nullptr, nullptr, st);
+          launch_multidot(n, j + 1, V, h->ldv, w, h->d_partial, hb + (m + 1), st);
+          launch_update(n, j + 1, V, h->ldv, hb + (m + 1), w, h->d_partial, hb + 2 * (m + 1), st);
+          h->launches += 7;
+          CK(cudaMemcpyAsync(hh.data(), hb, (2 * (m + 1) + 1) * 8, cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          double hn = std::sqrt(hh[2 * (m + 1)]);
+          std::vector<double> col(j + 2);
+          for (int i = 0; i <= j; ++i) col[i] = hh[i] + hh[m + 1 + i];
+          col[j + 1] = hn;
+          for (int i = 0; i < j; ++i) {
+            double t = cs[i] * col[i] + sn[i] * col[i + 1];
+            col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+            col[i] = t;
+          }
+          double den = std::hypot(col[j], col[j + 1]);
+          cs[j] = col[j] / den;
+          sn[j] = col[j + 1] / den;
+          col[j] = den;
+          col[j + 1] = 0.0;
+          g[j + 1] = -sn[j] * g[j];
+          g[j] = cs[j] * g[j];
+          for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = col[i];
+          total++;
+          k = j + 1;
+          double est = std::fabs(g[j + 1]) / bnorm;
+          if (!std::isfinite(est)) throw HError{HPLMM_ERR_NONFINITE, "non-finite GMRES residual"};
+          if (hist && hl < hist_cap) hist[hl] = est;
+          hl++;
+          if (hn == 0.0 || est < tol || total >= maxit) break;
+          // v_{j+1} = w / hn
+          launch_scale(n, w, hb + 2 * (m + 1), 1, w, st);
+          h->launches++;
+        }
+        // y = H^-1 g ; x += M^-1 (V y)
+        std::vector<double> y(k);
+        for (int i = k - 1; i >= 0; --i) {
+          double s = g[i];
+          for (int l = i + 1; l < k; ++l) s -= H[(size_t)i * m + l] * y[l];
+          y[i] = s / H[(size_t)i * m + i];
+        }
+        CK(cudaMemcpyAsync(hb, y.data(), k * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(h->d_in, 0, (size_t)n * 8, st));
+        launch_combine_basis(n, k, V, h->ldv, hb, h->d_in, st);
+        op_minv(h, h->d_in, h->d_u);
+        launch_axpy(n, 1.0, h->d_u, dx, st);
+        op_spmv(h, dx, dB, h->d_r1);  // r = b - A x
+        launch_norm2(n, h->d_r1, h->d_partial, hb + 2 * (m + 1), st);
+        h->launches += 4;
+        CK(cudaMemcpyAsync(&beta2, hb + 2 * (m + 1), 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        relres = std::sqrt(beta2) / bnorm;
+        if (!std::isfinite(relres)) throw HError{HPLMM_ERR_NONFINITE, "non-finite true residual"};
+        if (relres < tol) { conv = true; break; }
+        if (total >= maxit) break;
+      }
+      if (!conv) status = HPLMM_NOT_CONVERGED;
+    }
+    from_device(h, x, dx, n);
+    CK(cudaGetLastError());
+    h->rep.t_solve_s = tt.stop();
+    CK(cudaStreamSynchronize(st));
+    h->flush_profile();
+    h->rep.iterations = total;
+    h->rep.converged = conv ? 1 : 0;
+    h->rep.hist_len = std::min(hl, hist_cap);
+    h->rep.final_true_relres = relres;
+    h->rep.kernel_launches = h->launches;
+    if (report) *report = h->rep;
+    return status;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
+hplmm_status hplmm_export(hplmm_handle* h, int32_t art, void* buf, int64_t cap, int64_t* len) {
+  if (!h || !len) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
+  try {
+    HostSetup& hs = h->hs;
+    const void* src = nullptr;
+    int64_t n = 0, esz = 4;
+    bool dev = false;
+    std::vector<int32_t> tmp;
+    switch (art) {
+      case HPLMM_ART_NODE_KEY: src = hs.node_key.data(); n = hs.node_key.size(); esz = 8; break;
+      case HPLMM_ART_ROW_PTR: src = hs.row_ptr.data(); n = hs.row_ptr.size(); break;
+      case HPLMM_ART_COL_IDX: src = hs.col_idx.data(); n = hs.col_idx.size(); break;
+      case HPLMM_ART_NODE_CLASS: src = hs.node_class.data(); n = hs.node_class.size(); break;
+      case HPLMM_ART_NODE_IFACE: src = hs.node_iface.data(); n = hs.node_iface.size(); break;
+      case HPLMM_ART_NODE_OWNER: src = hs.node_owner.data(); n = hs.node_owner.size(); break;
+      case HPLMM_ART_IFACE_PTR: src = hs.iface_ptr.data(); n = hs.iface_ptr.size(); break;
+      case HPLMM_ART_IFACE_NODES: src = hs.iface_nodes.data(); n = hs.iface_nodes.size(); break;
+      case HPLMM_ART_CONTACT_PTR: src = hs.contact_ptr.data(); n = hs.contact_ptr.size(); break;
+      case HPLMM_ART_CONTACT_NODES: src = hs.contact_nodes.data(); n = hs.contact_nodes.size(); break;
+      case HPLMM_ART_MORTAR_PTR: src = hs.mortar_ptr.data(); n = hs.mortar_ptr.size(); break;
+      case HPLMM_ART_MORTAR_NODES: src = hs.mortar_nodes.data(); n = hs.mortar_nodes.size(); break;
+      case HPLMM_ART_GRAIN_COLS_PTR: src = hs.gcols_ptr.data(); n = hs.gcols_ptr.size(); break;
+      case HPLMM_ART_GRAIN_COLS: src = hs.gcols.data(); n = hs.gcols.size(); break;
+      case HPLMM_ART_VAL:
+        if (!h->assembled) throw HError{HPLMM_ERR_STATE, "VAL before assemble"};
+        src = h->d_val; n = h->nnzb * 9; esz = 8; dev = true; break;
+      case HPLMM_ART_RHS:
+        if (!h->assembled) throw HError{HPLMM_ERR_STATE, "RHS before assemble"};
+        src = h->d_b; n = h->n_dof; esz = 8; dev = true; break;
+      case HPLMM_ART_S: {
+        if (!h->setup_done || !h->d_Sdense) throw HError{HPLMM_ERR_STATE, "S not available"};
+        int Nm = h->co.Nm;
+        n = (int64_t)Nm * Nm;
+        *len = n;
+        if (!buf) return HPLMM_OK;
+        if (cap < n * 8) throw HError{HPLMM_ERR_ARG, "buffer too small"};
+        require_device(h);
+        CK(cudaMemcpy2D(buf, Nm * 8, h->d_Sdense, h->lds * 8, Nm * 8, Nm, cudaMemcpyDeviceToHost));
+        return HPLMM_OK;
+      }
+      case HPLMM_ART_MORTAR_W: {
+        if (!h->setup_done) throw HError{HPLMM_ERR_STATE, "weights before setup"};
+        int64_t wo = 0;
+        for (int c = 0; c < hs.n_ifaces(); ++c)
+          wo += (int64_t)(hs.iface_ptr[c + 1] - hs.iface_ptr[c]) * (hs.mortar_ptr[c + 1] - hs.mortar_ptr[c]);
+        src = h->co.W; n = wo; esz = 8; dev = true; break;
+      }
+      default: throw HError{HPLMM_ERR_ARG, "unknown artifact"};
+    }
+    *len = n;
+    if (!buf) return HPLMM_OK;
+    if (cap < n * esz) throw HError{HPLMM_ERR_ARG, "buffer too small"};
+    if (dev) {
+      require_device(h);
+      CK(cudaMemcpy(buf, src, n * esz, cudaMemcpyDeviceToHost));
+    } else if (n) {
+      std::memcpy(buf, src, n * esz);
+    }
+    return HPLMM_OK;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
+hplmm_status hplmm_get_report(hplmm_handle* h, hplmm_report* r) {
+  if (!h || !r) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
+  *r = h->rep;
+  return HPLMM_OK;
+}
+
+// Profiling of the dominant kernel (packed SYMV tiles): CUDA events around
+// each launch on the launch stream; stats accumulate until reset.
+hplmm_status hplmm_profile(hplmm_handle* h, int32_t enable, int32_t reset) {
+  if (!h) { g_last_error = "null handle"; return HPLMM_ERR_ARG; }
+  h->profile = enable != 0;
+  if (reset)
+    for (int k = 0; k < KC_N; ++k) { h->kc_ms[k] = 0; h->kc_launches[k] = 0; }
+  return HPLMM_OK;
+}
+
+// kernel: 0 grain SYMV tiles, 1 contact SYMV tiles, 2 coarse SYMV tiles.
+// bytes = packed-tile bytes streamed per launch (32 KiB per tile).
+hplmm_status hplmm_kernel_stats(hplmm_handle* h, int32_t kernel, double* total_ms,
+                                int64_t* launches, int64_t* tile_bytes) {
+  if (!h || kernel < 0 || kernel >= KC_N) { g_last_error = "bad argument"; return HPLMM_ERR_ARG; }
+  if (total_ms) *total_ms = h->kc_ms[kernel];
+  if (launches) *launches = h->kc_launches[kernel];
+  DevBatch* b = kernel == 0 ? &h->gb : (kernel == 1 ? &h->cb : &h->sb);
+  if (tile_bytes) *tile_bytes = b->ntiles * (int64_t)TILE * 8;
+  return HPLMM_OK;
+}
+
+void hplmm_destroy(hplmm_handle* h) { delete h; }
+
+}  // extern "C"

@@ -1,0 +1,360 @@
+// Coarse space of hPLMM on the GPU (sm_100a, fp64).
+//
+// PAPER.md eq:mg_struct / eq:WQP, eq:reduced_defs (Q^o),
+// eq:all_prolong (P = [B C; I O]).  W is absorbed: P^ columns live
+// in the original DOF order.  Per grain g the non-zero rows of P^_B form the
+// dense block B_g (|I_g| x k_g, row-major, padded to 64-row blocks) over the
+// column set cols_g (R14, option B); the correction vector c^g is stored as the
+// extra last column of the same block so that restriction and prolongation
+// treat it uniformly (eq:col_cg, R15).  Interface rows of P^_B are the mortar
+// weights Q^o (R12).
+#include "kernels.cuh"
+
+namespace hplmm {
+
+__device__ __forceinline__ int grain_col_base(const DevCoarse& c, int g, int iface,
+                                              const int32_t* mortar_ptr) {
+  int base = 0;
+  for (int t = c.giface_ptr[g]; t < c.giface_ptr[g + 1]; ++t) {
+    int cc = c.giface[t];
+    if (cc == iface) return base;
+    base += 3 * (mortar_ptr[cc + 1] - mortar_ptr[cc]);
+  }
+  return -1;
+}
+
+// R_g = A^[I_g, iface] Q^o[:, cols_g]  (one thread per grain DOF row)
+__global__ void k_build_R(DevCoarse c, int64_t nloc, const int32_t* lmap, const int32_t* row_s,
+                          const int64_t* row_base, const int32_t* rp, const int32_t* col,
+                          const double* val) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nloc) return;
+  int d = lmap[i];
+  if (d < 0) return;
+  int g = row_s[i >> 6];
+  int64_t lr = i - 64 * row_base[g];
+  int p = d / 3, r = d - 3 * p;
+  int L = c.ld[g];
+  double* R = c.R + c.b_off[g] + lr * L;
+  for (int e = rp[p]; e < rp[p + 1]; ++e) {
+    int q = col[e];
+    int cf = c.node_iface[q];
+    if (cf < 0) continue;
+    int jb = grain_col_base(c, g, cf, c.mortar_ptr);
+    if (jb < 0) continue;
+    int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
+    const double* w = c.W + c.wt_off[cf] + (int64_t)c.node_local[q] * nu;
+    const double* a = val + 9 * (int64_t)e + 3 * r;
+    for (int m = 0; m < nu; ++m)
+      for (int gam = 0; gam < 3; ++gam) R[jb + 3 * m + gam] += a[gam] * w[m];
+  }
+}
+
+void launch_build_R(const DevCoarse& c, const DevBatch& gb, const int32_t* row_ptr,
+                    const int32_t* col, const double* val, cudaStream_t st) {
+  if (gb.nloc <= 0) return;
+  k_build_R<<<(unsigned)((gb.nloc + 127) / 128), 128, 0, st>>>(c, gb.nloc, gb.lmap, gb.row_s,
+                                                               gb.row_base, row_ptr, col, val);
+}
+
+// Y_g = A_g B_g + R_g  (overwrites R), one warp per grain DOF row
+__global__ void k_grain_AB(DevCoarse c, int64_t nloc, const int32_t* lmap, const int32_t* row_s,
+                           const int64_t* row_base, const int32_t* rp, const int32_t* col,
+                           const double* val) {
+  int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (i >= nloc) return;
+  int d = lmap[i];
+  if (d < 0) return;
+  int g = row_s[i >> 6];
+  int64_t lr = i - 64 * row_base[g];
+  int p = d / 3, r = d - 3 * p;
+  int L = c.ld[g];
+  int k = L - 1;
+  const double* Bg = c.B + c.b_off[g];
+  double* Y = c.R + c.b_off[g] + lr * L;
+  for (int j0 = 0; j0 < k; j0 += 32) {
+    int j = j0 + lane;
+    double acc = 0.0;
+    for (int e = rp[p]; e < rp[p + 1]; ++e) {
+      int q = col[e];
+      if (c.node_iface[q] >= 0 || c.node_owner[q] != g) continue;
+      int lq = c.node_local[q];
+      const double* a = val + 9 * (int64_t)e + 3 * r;
+      if (j < k)
+        for (int cc = 0; cc < 3; ++cc) acc += a[cc] * Bg[(int64_t)(3 * lq + cc) * L + j];
+    }
+    if (j < k) Y[j] += acc;
+  }
+}
+
+void launch_grain_AB(const DevCoarse& c, const DevBatch& gb, const int32_t* row_ptr,
+                     const int32_t* col, const double* val, cudaStream_t st) {
+  if (gb.nloc <= 0) return;
+  int64_t th = 32 * gb.nloc;
+  k_grain_AB<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(c, gb.nloc, gb.lmap, gb.row_s,
+                                                           gb.row_base, row_ptr, col, val);
+}
+
+// C_g = B_g^T Y_g (k_g x k_g); CTA per (grain, 8-row slab of C_g)
+__global__ void k_grain_BtY(DevCoarse c, const int32_t* nb) {
+  int g = blockIdx.x;
+  int j1 = blockIdx.y * 8;
+  int L = c.ld[g], k = L - 1;
+  if (j1 >= k) return;
+  int nrow = 64 * nb[g];
+  const double* Bg = c.B + c.b_off[g];
+  const double* Y = c.R + c.b_off[g];
+  double* C = c.Cg + c.cg_off[g];
+  for (int j2 = threadIdx.x; j2 < k; j2 += blockDim.x) {
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int row = 0; row < nrow; ++row) {
+      double y = Y[(int64_t)row * L + j2];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j1 + u < k) acc[u] += Bg[(int64_t)row * L + j1 + u] * y;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j1 + u < k) C[(int64_t)(j1 + u) * k + j2] = acc[u];
+  }
+}
+
+void launch_grain_BtY(const DevCoarse& c, const DevBatch& gb, cudaStream_t st) {
+  if (c.n_grains <= 0 || c.max_k <= 0) return;
+  dim3 grid(c.n_grains, (c.max_k + 7) / 8);
+  k_grain_BtY<<<grid, 128, 0, st>>>(c, gb.nb);
+}
+
+// Interface-row part of S = P_B^T (A^ P_B):  for every interface DOF d,
+//   S[k, :] += Q^o[d,k] * (A^[d,:] P_B)       (one CTA per interface; rows k
+// of S belong to exactly one interface, so CTAs never share an entry)
+__global__ void k_S_iface(DevCoarse c, const int32_t* rp, const int32_t* col, const double* val,
+                          double* S, int64_t lds) {
+  int cf = blockIdx.x;
+  int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
+  int kbase = 3 * c.mortar_ptr[cf];
+  for (int e0 = c.iface_ptr[cf]; e0 < c.iface_ptr[cf + 1]; ++e0) {
+    int y = c.iface_nodes[e0];
+    const double* wy = c.W + c.wt_off[cf] + (int64_t)(e0 - c.iface_ptr[cf]) * nu;
+    for (int gam = 0; gam < 3; ++gam) {
+      for (int e = rp[y]; e < rp[y + 1]; ++e) {
+        int q = col[e];
+        const double* a = val + 9 * (int64_t)e + 3 * gam;
+        int cq = c.node_iface[q];
+        for (int c3 = 0; c3 < 3; ++c3) {
+          double aa = a[c3];
+          if (cq < 0) {                      // grain row of P_B (class G)
+            int g = c.node_owner[q];
+            int L = c.ld[g], k = L - 1;
+            const double* Brow = c.B + c.b_off[g] + (int64_t)(3 * c.node_local[q] + c3) * L;
+            const int32_t* cols = c.gcols + c.gcols_ptr[g];
+            for (int t = threadIdx.x; t < nu * k; t += blockDim.x) {
+              int i = t / k, j = t - i * k;
+              S[(int64_t)(kbase + 3 * i + gam) * lds + cols[j]] += wy[i] * aa * Brow[j];
+            }
+          } else {                           // interface row of P_B (Q^o)
+            int nq = c.mortar_ptr[cq + 1] - c.mortar_ptr[cq];
+            const double* wq = c.W + c.wt_off[cq] + (int64_t)c.node_local[q] * nq;
+            int qbase = 3 * c.mortar_ptr[cq];
+            for (int t = threadIdx.x; t < nu * nq; t += blockDim.x) {
+              int i = t / nq, i2 = t - i * nq;
+              S[(int64_t)(kbase + 3 * i + gam) * lds + qbase + 3 * i2 + c3] += wy[i] * aa * wq[i2];
+            }
+          }
+          __syncthreads();
+        }
+      }
+    }
+  }
+}
+
+void launch_S_iface(const DevCoarse& c, const int32_t* row_ptr, const int32_t* col,
+                    const double* val, double* S, int64_t lds, cudaStream_t st) {
+  if (c.n_ifaces <= 0) return;
+  k_S_iface<<<c.n_ifaces, 256, 0, st>>>(c, row_ptr, col, val, S, lds);
+}
+
+// Grain-row part: S[k, cols_g] += C_g[j_k, :] for g in G(k) ascending
+__global__ void k_S_grain(DevCoarse c, double* S, int64_t lds) {
+  int kk = blockIdx.x;
+  if (kk >= c.Nm) return;
+  for (int e = c.mcol_ptr[kk]; e < c.mcol_ptr[kk + 1]; ++e) {
+    int g = c.mcol_g[e], jk = c.mcol_j[e];
+    int k = c.ld[g] - 1;
+    const double* C = c.Cg + c.cg_off[g] + (int64_t)jk * k;
+    const int32_t* cols = c.gcols + c.gcols_ptr[g];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) S[(int64_t)kk * lds + cols[j]] += C[j];
+    __syncthreads();
+  }
+}
+
+void launch_S_grain(const DevCoarse& c, double* S, int64_t lds, cudaStream_t st) {
+  if (c.Nm <= 0) return;
+  k_S_grain<<<c.Nm, 128, 0, st>>>(c, S, lds);
+}
+
+// ---------------------------------------------------------------------------
+// Restriction r_c = P^T r.  Pass 1: per (grain, 128-row chunk) partial
+// B_g^T r_g over all ld_g columns (coalesced row-major reads of B).  Pass 2:
+// per mortar column k, fixed-order sum over the grains/chunks touching k plus
+// the Q^o part; per grain the correction entry c_g^T r_g.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_restrict_chunks(DevCoarse c, const int32_t* lmap,
+                                                         const int64_t* row_base,
+                                                         const double* __restrict__ r) {
+  int64_t ch = blockIdx.x;                 // chunk = one 64-row block of a grain
+  if (ch >= c.n_chunks) return;
+  int g = c.chunk_g[ch];
+  int r0 = c.chunk_r0[ch];
+  int L = c.ld[g];
+  const double* Bg = c.B + c.b_off[g];
+  const int32_t* lm = lmap + 64 * row_base[g];
+  __shared__ double rv[64];
+  if (threadIdx.x < 64) {
+    int d = lm[r0 + threadIdx.x];
+    rv[threadIdx.x] = d >= 0 ? r[d] : 0.0;
+  }
+  __syncthreads();
+  double* out = c.tpart + c.chunk_t[ch];
+  for (int j = threadIdx.x; j < L; j += blockDim.x) {
+    double acc = 0.0;
+#pragma unroll 4
+    for (int rr = 0; rr < 64; ++rr) acc += __ldcs(Bg + (int64_t)(r0 + rr) * L + j) * rv[rr];
+    out[j] = acc;
+  }
+}
+
+__global__ void k_restrict_final(DevCoarse c, const int32_t* mortar_iface, const double* r,
+                                 double* rm, double* rc) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < c.Nm) {
+    double acc = 0.0;
+    for (int e = c.mcol_ptr[k]; e < c.mcol_ptr[k + 1]; ++e) {
+      int g = c.mcol_g[e], j = c.mcol_j[e];
+      for (int ch = c.chunk_ptr[g]; ch < c.chunk_ptr[g + 1]; ++ch) acc += c.tpart[c.chunk_t[ch] + j];
+    }
+    int m = k / 3, gam = k - 3 * m;
+    int cf = mortar_iface[m];
+    int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
+    int i = m - c.mortar_ptr[cf];
+    const double* w = c.W + c.wt_off[cf] + i;
+    for (int e = c.iface_ptr[cf]; e < c.iface_ptr[cf + 1]; ++e)
+      acc += w[(int64_t)(e - c.iface_ptr[cf]) * nu] * r[3 * (int64_t)c.iface_nodes[e] + gam];
+    rm[k] = acc;
+  } else if (k < c.Nm + c.n_grains) {
+    int g = k - c.Nm;
+    double acc = 0.0;
+    int j = c.ld[g] - 1;
+    if (c.Dc[g] != 0.0)
+      for (int ch = c.chunk_ptr[g]; ch < c.chunk_ptr[g + 1]; ++ch) acc += c.tpart[c.chunk_t[ch] + j];
+    rc[g] = acc;
+  }
+}
+
+void launch_restrict(const DevCoarse& c, const double* r, double* rm, double* rc,
+                     cudaStream_t st) {
+  if (c.n_chunks > 0)
+    k_restrict_chunks<<<(unsigned)c.n_chunks, 128, 0, st>>>(c, c.g_lmap, c.g_row_base, r);
+  int n = c.Nm + c.n_grains;
+  if (n > 0) k_restrict_final<<<(n + 127) / 128, 128, 0, st>>>(c, c.mortar_iface, r, rm, rc);
+}
+
+// ---------------------------------------------------------------------------
+// Prolongation x = P_B y_m + sum_g c^g y_c[g]
+// ---------------------------------------------------------------------------
+__global__ void k_yext(DevCoarse c, const double* ym, const double* yc) {
+  int g = blockIdx.x;
+  int L = c.ld[g];
+  const int32_t* cols = c.gcols + c.gcols_ptr[g];
+  double* out = c.yext + c.yext_off[g];
+  for (int j = threadIdx.x; j < L; j += blockDim.x)
+    out[j] = (j < L - 1) ? ym[cols[j]] : (c.Dc[g] != 0.0 ? yc[g] : 0.0);
+}
+
+__global__ void __launch_bounds__(256) k_prolong(DevCoarse c, const int32_t* gpos,
+                                                 const int32_t* row_s, const int64_t* row_base,
+                                                 const double* __restrict__ ym,
+                                                 double* __restrict__ x) {
+  int64_t d = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (d >= c.n_dof) return;
+  int gp = gpos[d];
+  if (gp >= 0) {
+    int g = row_s[gp >> 6];
+    int64_t lr = gp - 64 * row_base[g];
+    int L = c.ld[g];
+    const double* Brow = c.B + c.b_off[g] + lr * L;
+    const double* y = c.yext + c.yext_off[g];
+    double acc = 0.0;
+    for (int j = lane; j < L; j += 32) acc += __ldcs(Brow + j) * y[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) x[d] = acc;
+  } else if (lane == 0) {
+    int p = (int)(d / 3), gam = (int)(d - 3 * p);
+    int cf = c.node_iface[p];
+    int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
+    const double* w = c.W + c.wt_off[cf] + (int64_t)c.node_local[p] * nu;
+    int kb = 3 * c.mortar_ptr[cf] + gam;
+    double acc = 0.0;
+    for (int i = 0; i < nu; ++i) acc += w[i] * ym[kb + 3 * i];
+    x[d] = acc;
+  }
+}
+
+void launch_prolong(const DevCoarse& c, const double* ym, const double* yc, double* x,
+                    cudaStream_t st) {
+  if (c.n_grains > 0) k_yext<<<c.n_grains, 128, 0, st>>>(c, ym, yc);
+  int64_t th = 32 * (int64_t)c.n_dof;
+  k_prolong<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(c, c.gpos, c.g_row_s, c.g_row_base, ym,
+                                                          x);
+}
+
+__global__ void k_coarse_diag(int G, const double* rc, const double* Dc, double* yc) {
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  yc[g] = Dc[g] != 0.0 ? rc[g] / Dc[g] : 0.0;
+}
+
+void launch_coarse_diag(int G, const double* rc, const double* Dc, double* yc, cudaStream_t st) {
+  if (G <= 0) return;
+  k_coarse_diag<<<(G + 127) / 128, 128, 0, st>>>(G, rc, Dc, yc);
+}
+
+// c^g = A_g^-1 b^g is in the grain batch's yloc (b^g in xloc).  Keep it only if
+// b^g != 0 exactly (R15); D_c[g] = b^g . c^g (R16).
+__global__ void k_set_correction(DevCoarse c, const int32_t* nb, const int64_t* row_base,
+                                 const double* xloc, const double* yloc) {
+  int g = blockIdx.x;
+  int n = 64 * nb[g];
+  const double* b = xloc + 64 * row_base[g];
+  const double* y = yloc + 64 * row_base[g];
+  __shared__ double red[256];
+  __shared__ int anynz;
+  if (threadIdx.x == 0) anynz = 0;
+  __syncthreads();
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (b[i] != 0.0) anynz = 1;
+    acc += b[i] * y[i];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  int keep = anynz;
+  int L = c.ld[g];
+  double* Bg = c.B + c.b_off[g] + (L - 1);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) Bg[(int64_t)i * L] = keep ? y[i] : 0.0;
+  if (threadIdx.x == 0) c.Dc[g] = keep ? red[0] : 0.0;
+}
+
+void launch_set_correction(const DevCoarse& c, const DevBatch& gb, cudaStream_t st) {
+  if (c.n_grains <= 0) return;
+  k_set_correction<<<c.n_grains, 256, 0, st>>>(c, gb.nb, gb.row_base, gb.xloc, gb.yloc);
+}
+
+}  // namespace hplmm

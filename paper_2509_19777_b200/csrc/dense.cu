@@ -1,0 +1,522 @@
+// Batched dense subdomain operators on packed lower 64x64 tiles (sm_100a, fp64).
+//
+// Exact local solves of the additive-Schwarz smoothers M_zeta and M_g
+// (eq:Mg_Mz; local LU "precomputed" per P:739) and of the coarse
+// block S (eq:mg_struct with R16/R17).  Each SPD block is inverted once at
+// setup with the block sweep operator (symmetric Gauss-Jordan, no pivoting:
+// SPD) and stored as packed lower tiles; every apply is then a symmetric
+// matrix-vector product that streams the lower triangle ONCE (n^2/2 doubles),
+// i.e. half the bytes of a forward+backward triangular-solve pair over a
+// Cholesky factor, with no sequential dependency.
+#include <climits>
+
+#include "kernels.cuh"
+
+namespace hplmm {
+
+// ---------------------------------------------------------------------------
+// 64x64x64 fp64 tile product core (256 threads, 4x4 outputs each):
+//   acc[i][j] += sum_k As[k*64 + r0+i] * Bs[k*64 + c0+j]
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tile_mma(const double* __restrict__ As,
+                                         const double* __restrict__ Bs, double acc[4][4],
+                                         int r0, int c0) {
+#pragma unroll 8
+  for (int k = 0; k < TB; ++k) {
+    double2 a01 = *reinterpret_cast<const double2*>(As + k * TB + r0);
+    double2 a23 = *reinterpret_cast<const double2*>(As + k * TB + r0 + 2);
+    double2 b01 = *reinterpret_cast<const double2*>(Bs + k * TB + c0);
+    double2 b23 = *reinterpret_cast<const double2*>(Bs + k * TB + c0 + 2);
+    double a[4] = {a01.x, a01.y, a23.x, a23.y};
+    double b[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+  }
+}
+
+__device__ __forceinline__ void load_tile(double* dst, const double* __restrict__ src) {
+  for (int t = threadIdx.x; t < TILE / 2; t += blockDim.x)
+    reinterpret_cast<double2*>(dst)[t] = reinterpret_cast<const double2*>(src)[t];
+}
+// dst[k*64 + r] = src[r*64 + k]
+__device__ __forceinline__ void load_tile_T(double* dst, const double* __restrict__ src) {
+  for (int t = threadIdx.x; t < TILE; t += blockDim.x) {
+    int k = t >> 6, r = t & 63;
+    dst[k * TB + r] = src[r * TB + k];
+  }
+}
+
+__device__ __forceinline__ int64_t tidx(const int64_t* tile_base, int s, int I, int J) {
+  return tile_base[s] + (int64_t)I * (I + 1) / 2 + J;
+}
+
+// ---------------------------------------------------------------------------
+// extraction: tiles <- A^[sub, sub]  (one warp per subdomain node)
+// ---------------------------------------------------------------------------
+__global__ void k_extract(int total_nodes, int nsub, const int32_t* __restrict__ sub_node_ptr,
+                          const int32_t* __restrict__ sub_nodes, const int64_t* tile_base,
+                          const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                          const double* __restrict__ val, double* tiles) {
+  int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  int lane = threadIdx.x & 31;
+  if (w >= total_nodes) return;
+  // subdomain of entry w (binary search in sub_node_ptr)
+  int lo = 0, hi = nsub;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (sub_node_ptr[mid] <= w) lo = mid; else hi = mid;
+  }
+  int s = lo;
+  const int32_t* nodes = sub_nodes + sub_node_ptr[s];
+  int nn = sub_node_ptr[s + 1] - sub_node_ptr[s];
+  int lp = w - sub_node_ptr[s];
+  int p = nodes[lp];
+  for (int e = rp[p] + lane; e < rp[p + 1]; e += 32) {
+    int q = col[e];
+    int a = 0, b = nn;                       // lower_bound(q)
+    while (a < b) {
+      int m = (a + b) >> 1;
+      if (nodes[m] < q) a = m + 1; else b = m;
+    }
+    if (a >= nn || nodes[a] != q) continue;
+    int lq = a;
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        int R = 3 * lp + r, C = 3 * lq + c;
+        int I = R >> 6, J = C >> 6;
+        if (I < J) continue;
+        tiles[tidx(tile_base, s, I, J) * TILE + (C & 63) * TB + (R & 63)] = val[9 * (int64_t)e + 3 * r + c];
+      }
+  }
+}
+
+void launch_extract_local(const DevBatch& b, int total_nodes, const int32_t* sub_node_ptr,
+                          const int32_t* sub_nodes, const int32_t* row_ptr, const int32_t* col,
+                          const double* val, cudaStream_t st) {
+  if (total_nodes <= 0) return;
+  int64_t th = 32 * (int64_t)total_nodes;
+  k_extract<<<(int)((th + 255) / 256), 256, 0, st>>>(total_nodes, b.nsub, sub_node_ptr, sub_nodes,
+                                                     b.tile_base, row_ptr, col, val, b.tiles);
+}
+
+__global__ void k_pad_identity(int nsub, const int32_t* nb, const int32_t* ndof,
+                               const int64_t* tile_base, double* tiles) {
+  int s = blockIdx.x;
+  if (s >= nsub) return;
+  int np = TB * nb[s];
+  for (int R = ndof[s] + threadIdx.x; R < np; R += blockDim.x) {
+    int K = R >> 6;
+    tiles[tidx(tile_base, s, K, K) * TILE + (R & 63) * TB + (R & 63)] = 1.0;
+  }
+}
+
+void launch_pad_identity(const DevBatch& b, cudaStream_t st) {
+  if (b.nsub <= 0) return;
+  k_pad_identity<<<b.nsub, 64, 0, st>>>(b.nsub, b.nb, b.ndof, b.tile_base, b.tiles);
+}
+
+// ---------------------------------------------------------------------------
+// Block sweep operator (symmetric Gauss-Jordan) on packed lower tiles.
+// Sweeping pivot block p of a symmetric A with D = A_pp:
+//   A_pp <- -D^-1,  A_ip <- A_ip D^-1,  A_ij <- A_ij - A_ip D^-1 A_pj
+// keeps A symmetric; sweeping every block yields -A^-1 (negated at the end).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sweep_pivot(int p, int nsub, const int32_t* nb,
+                                                     const int64_t* tile_base,
+                                                     const double* tiles, double* dinv,
+                                                     int32_t* err) {
+  int s = blockIdx.x;
+  if (s >= nsub || nb[s] <= p) return;
+  extern __shared__ double sm[];
+  double* a = sm;              // 64x64 col-major
+  double* colk = sm + TILE;    // 64
+  __shared__ double dk;
+  load_tile(a, tiles + tidx(tile_base, s, p, p) * TILE);
+  bool bad = false;
+  for (int k = 0; k < TB; ++k) {
+    __syncthreads();
+    if (threadIdx.x < TB) colk[threadIdx.x] = a[k * TB + threadIdx.x];
+    if (threadIdx.x == 0) dk = a[k * TB + k];
+    __syncthreads();
+    double d = dk;
+    if (!(d > 0.0)) bad = true;
+    double inv = 1.0 / d;
+    for (int t = threadIdx.x; t < TILE; t += blockDim.x) {
+      int c = t >> 6, r = t & 63;
+      double v;
+      if (r == k && c == k) v = -inv;
+      else if (r == k) v = colk[c] * inv;
+      else if (c == k) v = colk[r] * inv;
+      else v = a[t] - colk[r] * colk[c] * inv;
+      a[t] = v;
+    }
+  }
+  __syncthreads();
+  if (bad && threadIdx.x == 0) atomicMin(err, s);
+  double* out = dinv + (int64_t)s * TILE;
+  for (int t = threadIdx.x; t < TILE; t += blockDim.x) out[t] = -a[t];
+}
+
+// C_i = A_ip (old), W_i = C_i D^-1 for every row block i != p
+__global__ void __launch_bounds__(256) k_sweep_panel(int p, int64_t nrows, const int32_t* row_s,
+                                                     const int32_t* row_k, const int32_t* nb,
+                                                     const int64_t* tile_base,
+                                                     const int64_t* row_base,
+                                                     const double* tiles, const double* dinv,
+                                                     double* cbuf, double* wbuf) {
+  int64_t rb = blockIdx.x;
+  if (rb >= nrows) return;
+  int s = row_s[rb], i = row_k[rb];
+  if (nb[s] <= p || i == p) return;
+  extern __shared__ double sm[];
+  double* As = sm;
+  double* Bs = sm + TILE;
+  if (i > p) load_tile(As, tiles + tidx(tile_base, s, i, p) * TILE);
+  else load_tile_T(As, tiles + tidx(tile_base, s, p, i) * TILE);
+  load_tile(Bs, dinv + (int64_t)s * TILE);   // (k,c) at c*64+k; D^-1 symmetric
+  __syncthreads();
+  int r0 = (threadIdx.x & 15) * 4, c0 = (threadIdx.x >> 4) * 4;
+  double acc[4][4] = {};
+  // Bs is used as Bs[k*64 + c] = D^-1[c][k] = D^-1[k][c]
+  tile_mma(As, Bs, acc, r0, c0);
+  double* W = wbuf + rb * TILE;
+  double* C = cbuf + rb * TILE;
+  for (int t = threadIdx.x; t < TILE / 2; t += blockDim.x)
+    reinterpret_cast<double2*>(C)[t] = reinterpret_cast<const double2*>(As)[t];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i2 = 0; i2 < 4; ++i2) W[(c0 + j) * TB + r0 + i2] = acc[i2][j];
+}
+
+__global__ void __launch_bounds__(256) k_sweep_update(int p, int64_t ntiles, const int32_t* tile_s,
+                                                      const int32_t* tile_ij, const int32_t* nb,
+                                                      const int64_t* row_base, double* tiles,
+                                                      const double* dinv, const double* cbuf,
+                                                      const double* wbuf) {
+  int64_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  int s = tile_s[t];
+  if (nb[s] <= p) return;
+  int I = tile_ij[t] >> 16, J = tile_ij[t] & 0xffff;
+  double* T = tiles + t * TILE;
+  if (I == p && J == p) {
+    const double* D = dinv + (int64_t)s * TILE;
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) T[e] = -D[e];
+    return;
+  }
+  if (J == p) {            // I > p:  A_ip <- W_i
+    const double* W = wbuf + (row_base[s] + I) * TILE;
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) T[e] = W[e];
+    return;
+  }
+  if (I == p) {            // J < p:  A_pj <- (W_j)^T
+    const double* W = wbuf + (row_base[s] + J) * TILE;
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+      int c = e >> 6, r = e & 63;
+      T[e] = W[r * TB + c];
+    }
+    return;
+  }
+  extern __shared__ double sm[];
+  double* As = sm;
+  double* Bs = sm + TILE;
+  load_tile(As, wbuf + (row_base[s] + I) * TILE);   // W_I (r,k) at k*64+r
+  load_tile(Bs, cbuf + (row_base[s] + J) * TILE);   // C_J (c,k) at k*64+c  == (C_J^T)(k,c)
+  __syncthreads();
+  int r0 = (threadIdx.x & 15) * 4, c0 = (threadIdx.x >> 4) * 4;
+  double acc[4][4] = {};
+  tile_mma(As, Bs, acc, r0, c0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double2* col = reinterpret_cast<double2*>(T + (c0 + j) * TB + r0);
+    double2 v0 = col[0], v1 = col[1];
+    v0.x -= acc[0][j]; v0.y -= acc[1][j]; v1.x -= acc[2][j]; v1.y -= acc[3][j];
+    col[0] = v0; col[1] = v1;
+  }
+}
+
+__global__ void k_negate(int64_t n, double* x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = -x[i];
+}
+
+void launch_sweep_invert(const DevBatch& b, cudaStream_t st) {
+  if (b.nsub <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    cudaFuncSetAttribute(k_sweep_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    cudaFuncSetAttribute(k_sweep_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    attr = true;
+  }
+  size_t sm1 = (TILE + TB) * sizeof(double);
+  size_t sm2 = 2 * TILE * sizeof(double);
+  for (int p = 0; p < b.max_nb; ++p) {
+    k_sweep_pivot<<<b.nsub, 256, sm1, st>>>(p, b.nsub, b.nb, b.tile_base, b.tiles, b.dinv, b.err);
+    k_sweep_panel<<<(unsigned)b.nrows, 256, sm2, st>>>(p, b.nrows, b.row_s, b.row_k, b.nb,
+                                                       b.tile_base, b.row_base, b.tiles, b.dinv,
+                                                       b.cbuf, b.wbuf);
+    k_sweep_update<<<(unsigned)b.ntiles, 256, sm2, st>>>(p, b.ntiles, b.tile_s, b.tile_ij, b.nb,
+                                                         b.row_base, b.tiles, b.dinv, b.cbuf,
+                                                         b.wbuf);
+  }
+  k_negate<<<148 * 8, 256, 0, st>>>(b.ntiles * TILE, b.tiles);
+}
+
+// ---------------------------------------------------------------------------
+// Packed symmetric matrix-vector product, one warp per lower tile (I,J):
+//   part_row[t] = A_IJ x_J        part_col[t] = A_IJ^T x_I   (I != J)
+// Lane l owns tile rows 2l, 2l+1: each column is one coalesced 512-byte load.
+// The 64 per-lane column partials are reduced by a 5-step recursive-halving
+// shuffle transpose (62 shuffles / tile), after which lane l holds columns
+// 2l, 2l+1.  No atomics: partials are summed in a fixed order by k_symv_reduce.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_symv_tiles(int64_t ntiles, const int32_t* __restrict__ tile_s,
+                                                    const int32_t* __restrict__ tile_ij,
+                                                    const int64_t* __restrict__ row_base,
+                                                    const double* __restrict__ tiles,
+                                                    const double* __restrict__ xloc,
+                                                    double* __restrict__ part_row,
+                                                    double* __restrict__ part_col) {
+  int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (t >= ntiles) return;
+  int s = __ldg(tile_s + t);
+  int ij = __ldg(tile_ij + t);
+  int I = ij >> 16, J = ij & 0xffff;
+  int64_t rb = __ldg(row_base + s);
+  const double* xJ = xloc + (rb + J) * TB;
+  double2 xI = *reinterpret_cast<const double2*>(xloc + (rb + I) * TB + 2 * lane);
+  const double2* A = reinterpret_cast<const double2*>(tiles + t * TILE) + lane;
+  double y0 = 0.0, y1 = 0.0;
+  double cp[64];
+#pragma unroll
+  for (int c0 = 0; c0 < TB; c0 += 16) {
+    double2 a[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) a[u] = __ldcs(A + (c0 + u) * (TB / 2));
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      double xj = __ldg(xJ + c0 + u);
+      y0 = fma(a[u].x, xj, y0);
+      y1 = fma(a[u].y, xj, y1);
+      cp[c0 + u] = fma(a[u].x, xI.x, a[u].y * xI.y);
+    }
+  }
+  reinterpret_cast<double2*>(part_row + t * TB)[lane] = make_double2(y0, y1);
+  if (I == J) return;
+  // recursive-halving transpose-reduce of cp[0..63] across the warp
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    bool up = lane & 16;
+    double send = up ? cp[k] : cp[32 + k];
+    double keep = up ? cp[32 + k] : cp[k];
+    cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    bool up = lane & 8;
+    double send = up ? cp[k] : cp[16 + k];
+    double keep = up ? cp[16 + k] : cp[k];
+    cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    bool up = lane & 4;
+    double send = up ? cp[k] : cp[8 + k];
+    double keep = up ? cp[8 + k] : cp[k];
+    cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    bool up = lane & 2;
+    double send = up ? cp[k] : cp[4 + k];
+    double keep = up ? cp[4 + k] : cp[k];
+    cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    bool up = lane & 1;
+    double send = up ? cp[k] : cp[2 + k];
+    double keep = up ? cp[2 + k] : cp[k];
+    cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+  reinterpret_cast<double2*>(part_col + t * TB)[lane] = make_double2(cp[0], cp[1]);
+}
+
+// y_K = sum_{J<=K} part_row(K,J) + sum_{I>K} part_col(I,K), fixed order
+__global__ void k_symv_reduce(int64_t nrows, const int32_t* __restrict__ row_s,
+                              const int32_t* __restrict__ row_k, const int32_t* __restrict__ nb,
+                              const int64_t* __restrict__ tile_base,
+                              const int64_t* __restrict__ row_base,
+                              const double* __restrict__ part_row,
+                              const double* __restrict__ part_col, double* __restrict__ yloc) {
+  int64_t rbi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (rbi >= nrows) return;
+  int s = row_s[rbi], K = row_k[rbi], n = nb[s];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int J = 0; J <= K; ++J) {
+    double2 v = reinterpret_cast<const double2*>(part_row + tidx(tile_base, s, K, J) * TB)[lane];
+    acc.x += v.x; acc.y += v.y;
+  }
+  for (int I = K + 1; I < n; ++I) {
+    double2 v = reinterpret_cast<const double2*>(part_col + tidx(tile_base, s, I, K) * TB)[lane];
+    acc.x += v.x; acc.y += v.y;
+  }
+  reinterpret_cast<double2*>(yloc + (row_base[s] + K) * TB)[lane] = acc;
+}
+
+__global__ void k_gather(int64_t n, const int32_t* __restrict__ lmap, const double* __restrict__ x,
+                         double* __restrict__ xloc) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int g = lmap[i];
+  xloc[i] = g >= 0 ? x[g] : 0.0;
+}
+
+void launch_gather(const DevBatch& b, const double* x, cudaStream_t st) {
+  if (b.nloc <= 0) return;
+  k_gather<<<(unsigned)((b.nloc + 255) / 256), 256, 0, st>>>(b.nloc, b.lmap, x, b.xloc);
+}
+
+void launch_symv_tiles(const DevBatch& b, cudaStream_t st) {
+  if (b.ntiles <= 0) return;
+  int64_t th = 32 * b.ntiles;
+  k_symv_tiles<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(b.ntiles, b.tile_s, b.tile_ij,
+                                                             b.row_base, b.tiles, b.xloc,
+                                                             b.part_row, b.part_col);
+}
+
+void launch_symv_reduce(const DevBatch& b, cudaStream_t st) {
+  if (b.nrows <= 0) return;
+  int64_t th2 = 32 * b.nrows;
+  k_symv_reduce<<<(unsigned)((th2 + 255) / 256), 256, 0, st>>>(b.nrows, b.row_s, b.row_k, b.nb,
+                                                               b.tile_base, b.row_base,
+                                                               b.part_row, b.part_col, b.yloc);
+}
+
+void launch_symv(const DevBatch& b, cudaStream_t st) {
+  launch_symv_tiles(b, st);
+  launch_symv_reduce(b, st);
+}
+
+// ---------------------------------------------------------------------------
+// B = -(A^-1 X) on the grain batch (shape vectors, eq:col_pk).  One CTA per
+// (row block I, 64-column chunk); loops over all tile columns J of the full
+// symmetric matrix (tile (J,I)^T above the diagonal).  X, B row-major [.. x ld].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_symm_neg(int64_t nrows, const int32_t* row_s,
+                                                  const int32_t* row_k, const int32_t* nb,
+                                                  const int64_t* tile_base,
+                                                  const double* tiles, const int64_t* x_off,
+                                                  const int32_t* ld, const int32_t* kcols,
+                                                  const double* X, double* B) {
+  int64_t rb = blockIdx.x;
+  int q = blockIdx.y;
+  int s = row_s[rb], I = row_k[rb], n = nb[s];
+  int kc = kcols[s], L = ld[s];
+  if (q * TB >= kc) return;
+  extern __shared__ double sm[];
+  double* As = sm;
+  double* Bs = sm + TILE;
+  const double* Xs = X + x_off[s];
+  int r0 = (threadIdx.x & 15) * 4, c0 = (threadIdx.x >> 4) * 4;
+  double acc[4][4] = {};
+  for (int J = 0; J < n; ++J) {
+    __syncthreads();
+    if (J <= I) load_tile(As, tiles + tidx(tile_base, s, I, J) * TILE);
+    else load_tile_T(As, tiles + tidx(tile_base, s, J, I) * TILE);
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+      int k = e >> 6, c = e & 63;
+      int col = q * TB + c;
+      Bs[e] = col < kc ? Xs[(int64_t)(J * TB + k) * L + col] : 0.0;
+    }
+    __syncthreads();
+    tile_mma(As, Bs, acc, r0, c0);
+  }
+  double* Bo = B + x_off[s];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int col = q * TB + c0 + j;
+      if (col < kc) Bo[(int64_t)(I * TB + r0 + i) * L + col] = -acc[i][j];
+    }
+}
+
+void launch_symm_neg(const DevBatch& b, const int64_t* x_off, const int32_t* ld,
+                     const int32_t* kcols, int max_kchunks, const double* X, double* B,
+                     cudaStream_t st) {
+  if (b.nrows <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_symm_neg, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    attr = true;
+  }
+  // grid.y = max column chunks; CTAs beyond a grain's k exit immediately
+  if (max_kchunks <= 0) return;
+  dim3 grid((unsigned)b.nrows, (unsigned)max_kchunks);
+  k_symm_neg<<<grid, 256, 2 * TILE * sizeof(double), st>>>(b.nrows, b.row_s, b.row_k, b.nb,
+                                                           b.tile_base, b.tiles, x_off, ld, kcols,
+                                                           X, B);
+}
+
+// S (dense row-major, leading dim lds) -> packed lower tiles, symmetrised
+// from its lower triangle (R16).
+__global__ void k_pack_dense(int64_t ntiles, const int32_t* tile_ij, const double* S, int64_t lds,
+                             double* tiles) {
+  int64_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  int I = tile_ij[t] >> 16, J = tile_ij[t] & 0xffff;
+  for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+    int c = e >> 6, r = e & 63;
+    int64_t R = I * TB + r, C = J * TB + c;
+    tiles[t * TILE + e] = (R >= C) ? S[R * lds + C] : S[C * lds + R];
+  }
+}
+
+void launch_pack_dense(const DevBatch& b, const double* S, int64_t lds, cudaStream_t st) {
+  if (b.ntiles <= 0) return;
+  k_pack_dense<<<(unsigned)b.ntiles, 256, 0, st>>>(b.ntiles, b.tile_ij, S, lds, b.tiles);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_combine_grain(int n, const int32_t* __restrict__ gpos,
+                                const double* __restrict__ yloc, const double* __restrict__ a,
+                                const double* __restrict__ b, double* __restrict__ out) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  double v = 0.0;
+  if (a) v += a[d];
+  if (b) v += b[d];
+  int g = gpos[d];
+  if (g >= 0) v += yloc[g];
+  out[d] = v;
+}
+
+void launch_combine_grain(int n_dof, const int32_t* gpos, const double* yloc, const double* a,
+                          const double* b, double* out, cudaStream_t st) {
+  k_combine_grain<<<(n_dof + 255) / 256, 256, 0, st>>>(n_dof, gpos, yloc, a, b, out);
+}
+
+__global__ void k_sum_contact(int n, const int32_t* __restrict__ cptr,
+                              const int32_t* __restrict__ cidx, const double* __restrict__ yloc,
+                              double* __restrict__ out) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  double v = 0.0;
+  for (int e = cptr[d]; e < cptr[d + 1]; ++e) v += yloc[cidx[e]];
+  out[d] = v;
+}
+
+void launch_sum_contact(int n_dof, const int32_t* cptr, const int32_t* cidx, const double* yloc,
+                        double* out, cudaStream_t st) {
+  k_sum_contact<<<(n_dof + 255) / 256, 256, 0, st>>>(n_dof, cptr, cidx, yloc, out);
+}
+
+}  // namespace hplmm

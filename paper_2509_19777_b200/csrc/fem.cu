@@ -1,0 +1,265 @@
+// FEM assembly, BSR SpMV and Gaussian mortar weights (sm_100a, fp64).
+//
+// PAPER.md P:74-78 (Galerkin Q1 FEM on the voxel grid -> eq:ls_all),
+// eq:stiff_iso, readings R2 (2x2x2 Gauss, unit voxel), R3
+// (node-major 3x3 blocks), R4 (Dirichlet identity rows, lifted RHS);
+// eq:gauss with R11 for the mortar weights.
+#include <cfloat>
+
+#include "kernels.cuh"
+
+namespace hplmm {
+
+// ---------------------------------------------------------------------------
+// K0 = int_[0,1]^3 B^T D(E=1,nu) B dV  (24x24, DOF 3a+c, a = dx+2dy+4dz)
+// ---------------------------------------------------------------------------
+__device__ void strain_col(int a, int r, const double xi[3], double e[6]) {
+  int c0 = a & 1, c1 = (a >> 1) & 1, c2 = (a >> 2) & 1;
+  double f0 = c0 ? xi[0] : 1.0 - xi[0], f1 = c1 ? xi[1] : 1.0 - xi[1], f2 = c2 ? xi[2] : 1.0 - xi[2];
+  double d0 = c0 ? 1.0 : -1.0, d1 = c1 ? 1.0 : -1.0, d2 = c2 ? 1.0 : -1.0;
+  double gx = d0 * f1 * f2, gy = f0 * d1 * f2, gz = f0 * f1 * d2;
+  e[0] = (r == 0) ? gx : 0.0;
+  e[1] = (r == 1) ? gy : 0.0;
+  e[2] = (r == 2) ? gz : 0.0;
+  e[3] = (r == 1) ? gz : (r == 2 ? gy : 0.0);   // gamma_yz
+  e[4] = (r == 0) ? gz : (r == 2 ? gx : 0.0);   // gamma_xz
+  e[5] = (r == 0) ? gy : (r == 1 ? gx : 0.0);   // gamma_xy
+}
+
+__global__ void k_element_K0(double* K0, double nu) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 576) return;
+  int i = t / 24, j = t % 24;
+  double lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+  double mu = 1.0 / (2.0 * (1.0 + nu));
+  const double g = 0.5 / sqrt(3.0);
+  double acc = 0.0;
+  for (int p = 0; p < 8; ++p) {
+    double xi[3] = {0.5 + ((p & 1) ? g : -g), 0.5 + ((p & 2) ? g : -g), 0.5 + ((p & 4) ? g : -g)};
+    double ei[6], ej[6];
+    strain_col(i / 3, i % 3, xi, ei);
+    strain_col(j / 3, j % 3, xi, ej);
+    double s = 0.0;
+    for (int m = 0; m < 3; ++m)
+      for (int n = 0; n < 3; ++n) s += ei[m] * (lam + (m == n ? 2.0 * mu : 0.0)) * ej[n];
+    for (int m = 3; m < 6; ++m) s += ei[m] * mu * ej[m];
+    acc += 0.125 * s;
+  }
+  K0[t] = acc;
+}
+
+void launch_element_K0(double* K0, double nu, cudaStream_t st) {
+  k_element_K0<<<9, 64, 0, st>>>(K0, nu);
+}
+
+// Block (p,q) of the unconstrained matrix: sum over voxels shared by p and q,
+// ascending local index a of p in the voxel (the oracle's accumulation order).
+__device__ void block_pq(const int32_t* ijk, int p, int q, const uint8_t* solid, const double* E,
+                         int nx, int ny, int nz, const double* K0, double out[9]) {
+  for (int t = 0; t < 9; ++t) out[t] = 0.0;
+  int px = ijk[3 * p], py = ijk[3 * p + 1], pz = ijk[3 * p + 2];
+  int qx = ijk[3 * q], qy = ijk[3 * q + 1], qz = ijk[3 * q + 2];
+  for (int a = 0; a < 8; ++a) {
+    int vx = px - (a & 1), vy = py - ((a >> 1) & 1), vz = pz - ((a >> 2) & 1);
+    if (vx < 0 || vy < 0 || vz < 0 || vx >= nx || vy >= ny || vz >= nz) continue;
+    int64_t v = vx + (int64_t)nx * (vy + (int64_t)ny * vz);
+    if (!solid[v]) continue;
+    int bx = qx - vx, by = qy - vy, bz = qz - vz;
+    if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+    int b = bx + 2 * by + 4 * bz;
+    double Ev = E[v];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c)
+        out[3 * r + c] = __dadd_rn(out[3 * r + c], __dmul_rn(Ev, K0[(3 * a + r) * 24 + 3 * b + c]));
+  }
+}
+
+__global__ void k_assemble(int nnzb, const int32_t* block_row, const int32_t* col,
+                           const int32_t* ijk, const uint8_t* dir, const uint8_t* solid,
+                           const double* E, int nx, int ny, int nz, const double* K0,
+                           double* val) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnzb) return;
+  int p = block_row[e], q = col[e];
+  double blk[9];
+  if (dir[p]) {
+    for (int t = 0; t < 9; ++t) blk[t] = (t % 4 == 0) ? 1.0 : 0.0;   // identity (R4)
+  } else {
+    block_pq(ijk, p, q, solid, E, nx, ny, nz, K0, blk);
+  }
+  for (int t = 0; t < 9; ++t) val[9 * (int64_t)e + t] = blk[t];
+}
+
+void launch_assemble(int nnzb, const int32_t* block_row, const int32_t* col,
+                     const int32_t* node_ijk, const uint8_t* dir, const uint8_t* solid,
+                     const double* E, int nx, int ny, int nz, const double* K0, double* val,
+                     cudaStream_t st) {
+  if (nnzb <= 0) return;
+  k_assemble<<<(nnzb + 255) / 256, 256, 0, st>>>(nnzb, block_row, col, node_ijk, dir, solid, E,
+                                                  nx, ny, nz, K0, val);
+}
+
+// b_free = f - sum_{q Dirichlet} K(p,q) u_q ;  b_D = u_D   (R4)
+__global__ void k_assemble_rhs(int n, const int32_t* drow_ptr, const int32_t* dcol,
+                               const int32_t* ijk, const uint8_t* dir, const uint8_t* solid,
+                               const double* E, int nx, int ny, int nz, const double* K0,
+                               const double* f, const double* uD, double* b) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  if (dir[p]) {
+    for (int r = 0; r < 3; ++r) b[3 * (int64_t)p + r] = uD[3 * (int64_t)p + r];
+    return;
+  }
+  double t[3] = {0.0, 0.0, 0.0};
+  for (int e = drow_ptr[p]; e < drow_ptr[p + 1]; ++e) {
+    int q = dcol[e];
+    double blk[9];
+    block_pq(ijk, p, q, solid, E, nx, ny, nz, K0, blk);
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) t[r] += blk[3 * r + c] * uD[3 * (int64_t)q + c];
+  }
+  for (int r = 0; r < 3; ++r) b[3 * (int64_t)p + r] = f[3 * (int64_t)p + r] - t[r];
+}
+
+void launch_assemble_rhs(int n_nodes, const int32_t* drow_ptr, const int32_t* dcol,
+                         const int32_t* node_ijk, const uint8_t* dir, const uint8_t* solid,
+                         const double* E, int nx, int ny, int nz, const double* K0,
+                         const double* f, const double* uD, double* b, cudaStream_t st) {
+  if (n_nodes <= 0) return;
+  k_assemble_rhs<<<(n_nodes + 255) / 256, 256, 0, st>>>(n_nodes, drow_ptr, dcol, node_ijk, dir,
+                                                         solid, E, nx, ny, nz, K0, f, uD, b);
+}
+
+// ---------------------------------------------------------------------------
+// BSR 3x3 SpMV: one warp per block row.  The warp streams the row's
+// contiguous 9*nnz_row values with 16-byte vector loads (lane-consecutive ->
+// fully coalesced), gathers x (L2-resident) and reduces the 3 row sums with
+// warp shuffles.  y = A x, or y = v - A x (fused residual, eq:multi_precond /
+// eq:local_smoother_CG residual updates).
+// ---------------------------------------------------------------------------
+template <bool RESID>
+__global__ void __launch_bounds__(256) k_spmv(int n, const int32_t* __restrict__ rp,
+                                              const int32_t* __restrict__ col,
+                                              const double* __restrict__ val,
+                                              const double* __restrict__ x,
+                                              const double* __restrict__ v,
+                                              double* __restrict__ y) {
+  int row = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  int s = __ldg(rp + row), e = __ldg(rp + row + 1);
+  int64_t v0 = 9 * (int64_t)s;          // first value of the row
+  int nv = 9 * (e - s);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  // Vector part: pairs of doubles at even global offsets.
+  int head = (int)(v0 & 1);             // one leading scalar if misaligned
+  if (head && lane == 0 && nv > 0) {
+    double prod = __ldg(val + v0) * __ldg(x + 3 * (int64_t)__ldg(col + s));
+    a0 += prod;                          // t = 0 -> r = 0, c = 0
+  }
+  const double2* vp = reinterpret_cast<const double2*>(val + v0 + head);
+  int npair = (nv - head) >> 1;
+  for (int t2 = lane; t2 < npair; t2 += 32) {
+    double2 pv = __ldg(vp + t2);
+    int t = head + 2 * t2;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int tt = t + u;
+      int b = tt / 9;
+      int rc = tt - 9 * b;
+      int r = rc / 3, c = rc - 3 * r;
+      double prod = (u ? pv.y : pv.x) * __ldg(x + 3 * (int64_t)__ldg(col + s + b) + c);
+      a0 += (r == 0) ? prod : 0.0;
+      a1 += (r == 1) ? prod : 0.0;
+      a2 += (r == 2) ? prod : 0.0;
+    }
+  }
+  if (((nv - head) & 1) && lane == 31) {  // trailing scalar
+    int tt = nv - 1;
+    int b = tt / 9;
+    int rc = tt - 9 * b;
+    int r = rc / 3, c = rc - 3 * r;
+    double prod = __ldg(val + v0 + tt) * __ldg(x + 3 * (int64_t)__ldg(col + s + b) + c);
+    a0 += (r == 0) ? prod : 0.0;
+    a1 += (r == 1) ? prod : 0.0;
+    a2 += (r == 2) ? prod : 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  if (lane < 3) {
+    double a = lane == 0 ? a0 : (lane == 1 ? a1 : a2);
+    int64_t d = 3 * (int64_t)row + lane;
+    y[d] = RESID ? (v[d] - a) : a;
+  }
+}
+
+void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const double* val,
+                 const double* x, const double* v, double* y, cudaStream_t st) {
+  if (n_nodes <= 0) return;
+  int64_t threads = 32 * (int64_t)n_nodes;
+  int grid = (int)((threads + 255) / 256);
+  if (v)
+    k_spmv<true><<<grid, 256, 0, st>>>(n_nodes, row_ptr, col, val, x, v, y);
+  else
+    k_spmv<false><<<grid, 256, 0, st>>>(n_nodes, row_ptr, col, val, x, v, y);
+}
+
+// ---------------------------------------------------------------------------
+// Gaussian mortar weights (eq:gauss, R11): W[y, i] = alpha_i(y) / sum_j alpha_j(y)
+// alpha_i(y) = exp(-|y-x_i|^2 / (beta min_{j!=i} |x_i-x_j|^2)), max-shifted.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t d2i(const int32_t* ijk, int a, int b) {
+  int64_t dx = ijk[3 * a] - ijk[3 * b], dy = ijk[3 * a + 1] - ijk[3 * b + 1],
+          dz = ijk[3 * a + 2] - ijk[3 * b + 2];
+  return dx * dx + dy * dy + dz * dz;
+}
+
+__device__ double gauss_exponent(const int32_t* ijk, const int32_t* X, int nu, int i, int y,
+                                 double beta) {
+  int64_t dmin = INT64_MAX;
+  for (int j = 0; j < nu; ++j)
+    if (j != i) {
+      int64_t d = d2i(ijk, X[i], X[j]);
+      dmin = d < dmin ? d : dmin;
+    }
+  return -(double)d2i(ijk, y, X[i]) / (beta * (double)dmin);
+}
+
+__global__ void k_mortar_weights(int n, const int32_t* iface_of, const int32_t* iface_ptr,
+                                 const int32_t* iface_nodes, const int32_t* mortar_ptr,
+                                 const int32_t* mortar_nodes, const int64_t* wt_off,
+                                 const int32_t* ijk, double beta, double* W) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  int c = iface_of[e];
+  int y = iface_nodes[e];
+  int yl = e - iface_ptr[c];
+  const int32_t* X = mortar_nodes + mortar_ptr[c];
+  int nu = mortar_ptr[c + 1] - mortar_ptr[c];
+  double* out = W + wt_off[c] + (int64_t)yl * nu;
+  if (nu == 1) {
+    out[0] = 1.0;
+    return;
+  }
+  double m = -DBL_MAX;
+  for (int i = 0; i < nu; ++i) m = fmax(m, gauss_exponent(ijk, X, nu, i, y, beta));
+  double s = 0.0;
+  for (int i = 0; i < nu; ++i) s += exp(gauss_exponent(ijk, X, nu, i, y, beta) - m);
+  for (int i = 0; i < nu; ++i) out[i] = exp(gauss_exponent(ijk, X, nu, i, y, beta) - m) / s;
+}
+
+void launch_mortar_weights(int n_iface_nodes, const int32_t* iface_of, const int32_t* iface_ptr,
+                           const int32_t* iface_nodes, const int32_t* mortar_ptr,
+                           const int32_t* mortar_nodes, const int64_t* wt_off,
+                           const int32_t* node_ijk, double beta, double* W, cudaStream_t st) {
+  if (n_iface_nodes <= 0) return;
+  k_mortar_weights<<<(n_iface_nodes + 127) / 128, 128, 0, st>>>(
+      n_iface_nodes, iface_of, iface_ptr, iface_nodes, mortar_ptr, mortar_nodes, wt_off, node_ijk,
+      beta, W);
+}
+
+}  // namespace hplmm

@@ -1,0 +1,152 @@
+// Arnoldi / GMRES vector kernels (sm_100a, fp64): fused multi-dot, multi-axpy
+// with an optional fused norm, all with deterministic two-stage reductions
+// (fixed block->range mapping, fixed-order final sums).  CGS2 (R22) uses
+// multidot + update twice per Arnoldi step.
+#include "kernels.cuh"
+
+namespace hplmm {
+
+constexpr int KT = 256;
+
+int krylov_blocks(int64_t n) {
+  int64_t b = (n + 4 * KT - 1) / (4 * KT);
+  if (b > 148 * 8) b = 148 * 8;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < KT / 32; ++i) s += red[i];
+  return s;  // valid in thread 0
+}
+
+// partial[b*m + j] = sum_{i in block b's range} V[j][i] w[i]
+__global__ void __launch_bounds__(KT) k_multidot(int64_t n, int m, const double* __restrict__ V,
+                                                 int64_t ldv, const double* __restrict__ w,
+                                                 double* __restrict__ partial) {
+  __shared__ double red[KT / 32];
+  int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  int64_t i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  for (int j = 0; j < m; ++j) {
+    const double* v = V + j * ldv;
+    double s = 0.0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) s = fma(v[i], w[i], s);
+    double t = block_sum(s, red);
+    if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * m + j] = t;
+  }
+}
+
+__global__ void k_final_sum(int nb, int m, const double* __restrict__ partial,
+                            double* __restrict__ out) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * m + j];
+  out[j] = s;
+}
+
+void launch_multidot(int64_t n, int m, const double* V, int64_t ldv, const double* w,
+                     double* partial, double* out, cudaStream_t st) {
+  int nb = krylov_blocks(n);
+  k_multidot<<<nb, KT, 0, st>>>(n, m, V, ldv, w, partial);
+  k_final_sum<<<(m + 63) / 64, 64, 0, st>>>(nb, m, partial, out);
+}
+
+// w -= sum_j V[j] h[j]   (+ partial ||w||^2 per block)
+__global__ void __launch_bounds__(KT) k_update(int64_t n, int m, const double* __restrict__ V,
+                                               int64_t ldv, const double* __restrict__ h,
+                                               double* __restrict__ w, double* __restrict__ partial) {
+  __shared__ double hs[513];
+  __shared__ double red[KT / 32];
+  for (int j = threadIdx.x; j < m; j += KT) hs[j] = h[j];
+  __syncthreads();
+  int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  int64_t i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  double s = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) {
+    double acc = w[i];
+    for (int j = 0; j < m; ++j) acc = fma(-V[j * ldv + i], hs[j], acc);
+    w[i] = acc;
+    s = fma(acc, acc, s);
+  }
+  if (partial) {
+    double t = block_sum(s, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  }
+}
+
+void launch_update(int64_t n, int m, const double* V, int64_t ldv, const double* h, double* w,
+                   double* partial, double* out_norm2, cudaStream_t st) {
+  int nb = krylov_blocks(n);
+  k_update<<<nb, KT, 0, st>>>(n, m, V, ldv, h, w, out_norm2 ? partial : nullptr);
+  if (out_norm2) k_final_sum<<<1, 64, 0, st>>>(nb, 1, partial, out_norm2);
+}
+
+__global__ void __launch_bounds__(KT) k_norm2(int64_t n, const double* __restrict__ x,
+                                              double* __restrict__ partial) {
+  __shared__ double red[KT / 32];
+  int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  int64_t i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  double s = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) s = fma(x[i], x[i], s);
+  double t = block_sum(s, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+void launch_norm2(int64_t n, const double* x, double* partial, double* out, cudaStream_t st) {
+  int nb = krylov_blocks(n);
+  k_norm2<<<nb, KT, 0, st>>>(n, x, partial);
+  k_final_sum<<<1, 64, 0, st>>>(nb, 1, partial, out);
+}
+
+// y = x * s  (invert: y = x / sqrt(s))
+__global__ void k_scale(int64_t n, const double* __restrict__ x, const double* __restrict__ s,
+                        int invert, double* __restrict__ y) {
+  double f = invert ? 1.0 / sqrt(s[0]) : s[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i] * f;
+}
+
+void launch_scale(int64_t n, const double* x, const double* s_dev, int invert, double* y,
+                  cudaStream_t st) {
+  k_scale<<<krylov_blocks(n), KT, 0, st>>>(n, x, s_dev, invert, y);
+}
+
+__global__ void k_combine_basis(int64_t n, int m, const double* __restrict__ V, int64_t ldv,
+                                const double* __restrict__ y, double* __restrict__ x) {
+  __shared__ double ys[513];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) ys[j] = y[j];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = x[i];
+    for (int j = 0; j < m; ++j) acc = fma(V[j * ldv + i], ys[j], acc);
+    x[i] = acc;
+  }
+}
+
+void launch_combine_basis(int64_t n, int m, const double* V, int64_t ldv, const double* y,
+                          double* x, cudaStream_t st) {
+  k_combine_basis<<<krylov_blocks(n), KT, 0, st>>>(n, m, V, ldv, y, x);
+}
+
+__global__ void k_axpy(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+
+void launch_axpy(int64_t n, double a, const double* x, double* y, cudaStream_t st) {
+  k_axpy<<<krylov_blocks(n), KT, 0, st>>>(n, a, x, y);
+}
+
+}  // namespace hplmm
