@@ -443,7 +443,7 @@ hplmm_status hplmm_assemble(hplmm_handle* h, int32_t device, void* stream) {
       h->d_f = h->upload(hs.f);
       h->d_uD = h->upload(hs.u_D);
       h->d_K0 = h->dalloc<double>(576);
-      h->d_val = h->dalloc<double>((size_t)h->nnzb * 9);
+      h->d_val = h->dalloc<double>((size_t)h->nnzb * 9 + 4);  // +pad: SpMV vector loads
       h->d_b = h->dalloc<double>(h->n_dof);
     }
     launch_element_K0(h->d_K0, hs.nu, h->st);

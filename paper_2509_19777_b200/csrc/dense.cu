@@ -8,7 +8,9 @@
 // matrix-vector product that streams the lower triangle ONCE (n^2/2 doubles),
 // i.e. half the bytes of a forward+backward triangular-solve pair over a
 // Cholesky factor, with no sequential dependency.
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -348,6 +350,157 @@ __global__ void __launch_bounds__(256) k_symv_tiles(int64_t ntiles, const int32_
   reinterpret_cast<double2*>(part_col + t * TB)[lane] = make_double2(cp[0], cp[1]);
 }
 
+// ---------------------------------------------------------------------------
+// TMA-pipelined persistent variant (the production kernel on sm_100a).
+// One CTA per SM streams a contiguous range of tiles through a ring of
+// SY_STAGES 32-KiB shared-memory stages with 1-D bulk async copies
+// (cp.async.bulk, completion via mbarrier transaction counts).  One producer
+// lane keeps up to SY_STAGES tiles in flight independently of register
+// pressure; SY_CONS consumer warps each take every SY_CONS-th tile and
+// compute the same two partial products as k_symv_tiles from shared memory.
+// ---------------------------------------------------------------------------
+constexpr int SY_STAGES = 6;
+constexpr int SY_CONS = 3;
+// Stage s is always consumed by warp s % SY_CONS (tile k -> stage k % STAGES,
+// warp k % CONS).  That keeps every consumer within one mbarrier phase of the
+// stage it waits on, which the parity wait requires.
+static_assert(SY_STAGES % SY_CONS == 0, "each stage must belong to one consumer warp");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
+    k_symv_tma(int64_t ntiles, const int32_t* __restrict__ tile_s,
+               const int32_t* __restrict__ tile_ij, const int64_t* __restrict__ row_base,
+               const double* __restrict__ tiles, const double* __restrict__ xloc,
+               double* __restrict__ part_row, double* __restrict__ part_col) {
+  extern __shared__ __align__(1024) double sm_tiles[];
+  __shared__ __align__(8) uint64_t full[SY_STAGES], empty[SY_STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * per;
+  const int64_t nt = max((int64_t)0, min(ntiles, t0 + per) - t0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SY_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == SY_CONS) {                       // producer
+    if (lane == 0) {
+      for (int64_t k = 0; k < nt; ++k) {
+        int s = (int)(k % SY_STAGES);
+        if (k >= SY_STAGES) mbar_wait(&empty[s], (uint32_t)((k / SY_STAGES - 1) & 1));
+        mbar_expect_tx(&full[s], TILE * 8);
+        bulk_g2s(sm_tiles + (size_t)s * TILE, tiles + (t0 + k) * TILE, TILE * 8, &full[s]);
+      }
+    }
+    return;
+  }
+  for (int64_t k = warp; k < nt; k += SY_CONS) {
+    const int64_t t = t0 + k;
+    const int s = (int)(k % SY_STAGES);
+    const int ts = __ldg(tile_s + t);
+    const int ij = __ldg(tile_ij + t);
+    const int I = ij >> 16, J = ij & 0xffff;
+    const int64_t rb = __ldg(row_base + ts);
+    const double* xJ = xloc + (rb + J) * TB;
+    const double2 xI = *reinterpret_cast<const double2*>(xloc + (rb + I) * TB + 2 * lane);
+    double xj[TB / 32 * 2];
+    // stage x_J in registers: lane l holds x_J[2l], x_J[2l+1]
+    {
+      double2 v = *reinterpret_cast<const double2*>(xJ + 2 * lane);
+      xj[0] = v.x;
+      xj[1] = v.y;
+    }
+    mbar_wait(&full[s], (uint32_t)((k / SY_STAGES) & 1));
+    const double2* A = reinterpret_cast<const double2*>(sm_tiles + (size_t)s * TILE) + lane;
+    double y0 = 0.0, y1 = 0.0;
+    double cp[64];
+#pragma unroll
+    for (int c = 0; c < TB; ++c) {
+      double2 a = A[c * (TB / 2)];
+      double x = __shfl_sync(0xffffffffu, (c & 1) ? xj[1] : xj[0], c >> 1);
+      y0 = fma(a.x, x, y0);
+      y1 = fma(a.y, x, y1);
+      cp[c] = fma(a.x, xI.x, a.y * xI.y);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    reinterpret_cast<double2*>(part_row + t * TB)[lane] = make_double2(y0, y1);
+    if (I == J) continue;
+#pragma unroll
+    for (int k2 = 0; k2 < 32; ++k2) {
+      bool up = lane & 16;
+      double send = up ? cp[k2] : cp[32 + k2];
+      double keep = up ? cp[32 + k2] : cp[k2];
+      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {
+      bool up = lane & 8;
+      double send = up ? cp[k2] : cp[16 + k2];
+      double keep = up ? cp[16 + k2] : cp[k2];
+      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) {
+      bool up = lane & 4;
+      double send = up ? cp[k2] : cp[8 + k2];
+      double keep = up ? cp[8 + k2] : cp[k2];
+      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      bool up = lane & 2;
+      double send = up ? cp[k2] : cp[4 + k2];
+      double keep = up ? cp[4 + k2] : cp[k2];
+      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < 2; ++k2) {
+      bool up = lane & 1;
+      double send = up ? cp[k2] : cp[2 + k2];
+      double keep = up ? cp[2 + k2] : cp[k2];
+      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+    reinterpret_cast<double2*>(part_col + t * TB)[lane] = make_double2(cp[0], cp[1]);
+  }
+}
+
 // y_K = sum_{J<=K} part_row(K,J) + sum_{I>K} part_col(I,K), fixed order
 __global__ void k_symv_reduce(int64_t nrows, const int32_t* __restrict__ row_s,
                               const int32_t* __restrict__ row_k, const int32_t* __restrict__ nb,
@@ -384,8 +537,26 @@ void launch_gather(const DevBatch& b, const double* x, cudaStream_t st) {
   k_gather<<<(unsigned)((b.nloc + 255) / 256), 256, 0, st>>>(b.nloc, b.lmap, x, b.xloc);
 }
 
+static int g_symv_mode = -1;   // 0 = register kernel, 1 = TMA pipeline (default)
+static int g_num_sms = 0;
+
 void launch_symv_tiles(const DevBatch& b, cudaStream_t st) {
   if (b.ntiles <= 0) return;
+  if (g_symv_mode < 0) {
+    const char* e = getenv("HPLMM_SYMV");
+    g_symv_mode = (e && e[0] == '0') ? 0 : 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_symv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SY_STAGES * TILE * 8);
+  }
+  if (g_symv_mode == 1) {
+    int64_t grid = std::min<int64_t>(g_num_sms, b.ntiles);
+    k_symv_tma<<<(unsigned)grid, 32 * (SY_CONS + 1), SY_STAGES * TILE * 8, st>>>(
+        b.ntiles, b.tile_s, b.tile_ij, b.row_base, b.tiles, b.xloc, b.part_row, b.part_col);
+    return;
+  }
   int64_t th = 32 * b.ntiles;
   k_symv_tiles<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(b.ntiles, b.tile_s, b.tile_ij,
                                                              b.row_base, b.tiles, b.xloc,

@@ -131,58 +131,60 @@ void launch_assemble_rhs(int n_nodes, const int32_t* drow_ptr, const int32_t* dc
 }
 
 // ---------------------------------------------------------------------------
-// BSR 3x3 SpMV: one warp per block row.  The warp streams the row's
-// contiguous 9*nnz_row values with 16-byte vector loads (lane-consecutive ->
-// fully coalesced), gathers x (L2-resident) and reduces the 3 row sums with
-// warp shuffles.  y = A x, or y = v - A x (fused residual, eq:multi_precond /
-// eq:local_smoother_CG residual updates).
+// BSR 3x3 SpMV: one warp per block row, one lane per 3x3 block.  The row's
+// contiguous 9*nnz_row values are first staged into shared memory with 16-byte
+// vector loads (lane-consecutive -> fully coalesced; all loads of the row are
+// issued before any is consumed), the column indices are loaded in the same
+// wave, then each lane gathers its x block (L2-resident) and the 3 row sums are
+// reduced with warp shuffles.  Two dependent memory stages per row instead of
+// one per 32 values.  y = A x, or y = v - A x (fused residual, used by
+// eq:multi_precond and eq:local_smoother_CG).
 // ---------------------------------------------------------------------------
+constexpr int SPMV_WARPS = 8;
+constexpr int SPMV_BUF = 32 * 9 + 2;
+
 template <bool RESID>
-__global__ void __launch_bounds__(256) k_spmv(int n, const int32_t* __restrict__ rp,
-                                              const int32_t* __restrict__ col,
-                                              const double* __restrict__ val,
-                                              const double* __restrict__ x,
-                                              const double* __restrict__ v,
-                                              double* __restrict__ y) {
-  int row = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(32 * SPMV_WARPS) k_spmv(int n, const int32_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ x,
+                                                          const double* __restrict__ v,
+                                                          double* __restrict__ y) {
+  __shared__ __align__(16) double buf[SPMV_WARPS][SPMV_BUF];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * SPMV_WARPS + w;
   if (row >= n) return;
-  int s = __ldg(rp + row), e = __ldg(rp + row + 1);
-  int64_t v0 = 9 * (int64_t)s;          // first value of the row
-  int nv = 9 * (e - s);
+  const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  // Vector part: pairs of doubles at even global offsets.
-  int head = (int)(v0 & 1);             // one leading scalar if misaligned
-  if (head && lane == 0 && nv > 0) {
-    double prod = __ldg(val + v0) * __ldg(x + 3 * (int64_t)__ldg(col + s));
-    a0 += prod;                          // t = 0 -> r = 0, c = 0
-  }
-  const double2* vp = reinterpret_cast<const double2*>(val + v0 + head);
-  int npair = (nv - head) >> 1;
-  for (int t2 = lane; t2 < npair; t2 += 32) {
-    double2 pv = __ldg(vp + t2);
-    int t = head + 2 * t2;
+  double* bw = buf[w];
+  for (int cb = s; cb < e; cb += 32) {
+    const int nbk = min(32, e - cb);
+    const int64_t v0 = 9 * (int64_t)cb;
+    const int head = (int)(v0 & 1);
+    const int npair = (9 * nbk + head + 1) >> 1;
+    const double2* src = reinterpret_cast<const double2*>(val + v0 - head);
+    double2 r[5];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int tt = t + u;
-      int b = tt / 9;
-      int rc = tt - 9 * b;
-      int r = rc / 3, c = rc - 3 * r;
-      double prod = (u ? pv.y : pv.x) * __ldg(x + 3 * (int64_t)__ldg(col + s + b) + c);
-      a0 += (r == 0) ? prod : 0.0;
-      a1 += (r == 1) ? prod : 0.0;
-      a2 += (r == 2) ? prod : 0.0;
+    for (int u = 0; u < 5; ++u) {
+      int i = lane + 32 * u;
+      if (i < npair) r[u] = __ldcs(src + i);
     }
-  }
-  if (((nv - head) & 1) && lane == 31) {  // trailing scalar
-    int tt = nv - 1;
-    int b = tt / 9;
-    int rc = tt - 9 * b;
-    int r = rc / 3, c = rc - 3 * r;
-    double prod = __ldg(val + v0 + tt) * __ldg(x + 3 * (int64_t)__ldg(col + s + b) + c);
-    a0 += (r == 0) ? prod : 0.0;
-    a1 += (r == 1) ? prod : 0.0;
-    a2 += (r == 2) ? prod : 0.0;
+    int q = lane < nbk ? __ldg(col + cb + lane) : 0;
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+      int i = lane + 32 * u;
+      if (i < npair) reinterpret_cast<double2*>(bw)[i] = r[u];
+    }
+    __syncwarp();
+    if (lane < nbk) {
+      const double* blk = bw + head + 9 * lane;
+      const double* xq = x + 3 * (int64_t)q;
+      double x0 = __ldg(xq), x1 = __ldg(xq + 1), x2 = __ldg(xq + 2);
+      a0 = fma(blk[0], x0, fma(blk[1], x1, fma(blk[2], x2, a0)));
+      a1 = fma(blk[3], x0, fma(blk[4], x1, fma(blk[5], x2, a1)));
+      a2 = fma(blk[6], x0, fma(blk[7], x1, fma(blk[8], x2, a2)));
+    }
+    __syncwarp();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -200,12 +202,11 @@ __global__ void __launch_bounds__(256) k_spmv(int n, const int32_t* __restrict__
 void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const double* val,
                  const double* x, const double* v, double* y, cudaStream_t st) {
   if (n_nodes <= 0) return;
-  int64_t threads = 32 * (int64_t)n_nodes;
-  int grid = (int)((threads + 255) / 256);
+  int grid = (n_nodes + SPMV_WARPS - 1) / SPMV_WARPS;
   if (v)
-    k_spmv<true><<<grid, 256, 0, st>>>(n_nodes, row_ptr, col, val, x, v, y);
+    k_spmv<true><<<grid, 32 * SPMV_WARPS, 0, st>>>(n_nodes, row_ptr, col, val, x, v, y);
   else
-    k_spmv<false><<<grid, 256, 0, st>>>(n_nodes, row_ptr, col, val, x, v, y);
+    k_spmv<false><<<grid, 32 * SPMV_WARPS, 0, st>>>(n_nodes, row_ptr, col, val, x, v, y);
 }
 
 // ---------------------------------------------------------------------------

@@ -44,20 +44,25 @@ __global__ void __launch_bounds__(KT) k_multidot(int64_t n, int m, const double*
   }
 }
 
+// out[j] = sum_b partial[b*m + j]: one warp per j, fixed lane assignment and
+// fixed butterfly (deterministic)
 __global__ void k_final_sum(int nb, int m, const double* __restrict__ partial,
                             double* __restrict__ out) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
   if (j >= m) return;
   double s = 0.0;
-  for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * m + j];
-  out[j] = s;
+  for (int b = lane; b < nb; b += 32) s += partial[(int64_t)b * m + j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[j] = s;
 }
 
 void launch_multidot(int64_t n, int m, const double* V, int64_t ldv, const double* w,
                      double* partial, double* out, cudaStream_t st) {
   int nb = krylov_blocks(n);
   k_multidot<<<nb, KT, 0, st>>>(n, m, V, ldv, w, partial);
-  k_final_sum<<<(m + 63) / 64, 64, 0, st>>>(nb, m, partial, out);
+  k_final_sum<<<(m + 3) / 4, 128, 0, st>>>(nb, m, partial, out);
 }
 
 // w -= sum_j V[j] h[j]   (+ partial ||w||^2 per block)
@@ -87,7 +92,7 @@ void launch_update(int64_t n, int m, const double* V, int64_t ldv, const double*
                    double* partial, double* out_norm2, cudaStream_t st) {
   int nb = krylov_blocks(n);
   k_update<<<nb, KT, 0, st>>>(n, m, V, ldv, h, w, out_norm2 ? partial : nullptr);
-  if (out_norm2) k_final_sum<<<1, 64, 0, st>>>(nb, 1, partial, out_norm2);
+  if (out_norm2) k_final_sum<<<1, 32, 0, st>>>(nb, 1, partial, out_norm2);
 }
 
 __global__ void __launch_bounds__(KT) k_norm2(int64_t n, const double* __restrict__ x,
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(KT) k_norm2(int64_t n, const double* __restric
 void launch_norm2(int64_t n, const double* x, double* partial, double* out, cudaStream_t st) {
   int nb = krylov_blocks(n);
   k_norm2<<<nb, KT, 0, st>>>(n, x, partial);
-  k_final_sum<<<1, 64, 0, st>>>(nb, 1, partial, out);
+  k_final_sum<<<1, 32, 0, st>>>(nb, 1, partial, out);
 }
 
 // y = x * s  (invert: y = x / sqrt(s))
