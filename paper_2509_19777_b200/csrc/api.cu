@@ -49,6 +49,7 @@ struct hplmm_handle {
   // mesh / matrix
   int n_nodes = 0, n_dof = 0;
   int64_t nnzb = 0;
+  int max_row_blocks = 0;
   int32_t *d_row_ptr = nullptr, *d_col = nullptr, *d_block_row = nullptr, *d_drow_ptr = nullptr,
           *d_dcol = nullptr, *d_ijk = nullptr;
   uint8_t *d_dir = nullptr, *d_solid = nullptr;
@@ -284,7 +285,7 @@ void require_device(hplmm_handle* h) {
 // operator applications (all on device vectors of length n_dof)
 // ---------------------------------------------------------------------------
 void op_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
-  launch_spmv(h->n_nodes, h->d_row_ptr, h->d_col, h->d_val, x, v, y, h->st);
+  launch_spmv(h->n_nodes, h->d_row_ptr, h->d_col, h->d_val, x, v, y, h->st, h->max_row_blocks);
   h->launches++;
 }
 
@@ -432,7 +433,14 @@ hplmm_status hplmm_assemble(hplmm_handle* h, int32_t device, void* stream) {
       for (int p = 0; p < h->n_nodes; ++p)
         for (int e2 = hs.row_ptr[p]; e2 < hs.row_ptr[p + 1]; ++e2) brow[e2] = p;
       h->d_row_ptr = h->upload(hs.row_ptr);
-      h->d_col = h->upload(hs.col_idx);
+      {
+        std::vector<int32_t> colp(hs.col_idx);
+        colp.resize(colp.size() + 4, 0);   // tail padding for 16-byte TMA granules
+        h->d_col = h->upload(colp);
+        h->max_row_blocks = 0;
+        for (int p = 0; p < h->n_nodes; ++p)
+          h->max_row_blocks = std::max(h->max_row_blocks, hs.row_ptr[p + 1] - hs.row_ptr[p]);
+      }
       h->d_block_row = h->upload(brow);
       h->d_drow_ptr = h->upload(hs.drow_ptr);
       h->d_dcol = h->upload(hs.dcol);
@@ -688,6 +696,8 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       for (int c = 0; c < C; ++c)
         for (int e = hs.iface_ptr[c]; e < hs.iface_ptr[c + 1]; ++e) iface_of[e] = c;
       int32_t* d_iface_of = h->upload(iface_of);
+      co.iface_of = d_iface_of;
+      co.n_iface_nodes = (int)iface_of.size();
       launch_mortar_weights((int)iface_of.size(), d_iface_of, co.iface_ptr, co.iface_nodes,
                             co.mortar_ptr, h->upload(hs.mortar_nodes), co.wt_off, h->d_ijk,
                             hs.opt.beta, co.W, h->st);

@@ -8,6 +8,8 @@
 // extra last column of the same block so that restriction and prolongation
 // treat it uniformly (eq:col_cg, R15).  Interface rows of P^_B are the mortar
 // weights Q^o (R12).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace hplmm {
@@ -303,9 +305,80 @@ __global__ void __launch_bounds__(256) k_prolong(DevCoarse c, const int32_t* gpo
   }
 }
 
+// Grain rows in the grain batch's local order (B_g rows are contiguous): one
+// CTA per 64-row block of a grain, each warp 8 rows at once (lane-strided
+// coalesced row reads, 8 independent dot products in flight), 9-shuffle
+// transpose reduction, scatter to x through lmap.  Interface rows separately.
+constexpr int PR_ROWS = 8;
+__global__ void __launch_bounds__(256) k_prolong_rows(DevCoarse c, const int32_t* __restrict__ lmap,
+                                                      const int32_t* __restrict__ row_s,
+                                                      const int64_t* __restrict__ row_base,
+                                                      double* __restrict__ x) {
+  const int64_t ch = blockIdx.x;
+  const int g = row_s[ch];
+  const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = c.ld[g];
+  const int64_t lr0 = (ch - row_base[g]) * 64 + wp * PR_ROWS;   // local row of the grain
+  const double* Bg = c.B + c.b_off[g] + lr0 * L;
+  const double* y = c.yext + c.yext_off[g];
+  const int32_t* lm = lmap + 64 * ch + wp * PR_ROWS;
+  double a[PR_ROWS];
+#pragma unroll
+  for (int q = 0; q < PR_ROWS; ++q) a[q] = 0.0;
+  for (int j = lane; j < L; j += 32) {
+    const double yj = __ldg(y + j);
+#pragma unroll
+    for (int q = 0; q < PR_ROWS; ++q) a[q] = fma(__ldcs(Bg + (int64_t)q * L + j), yj, a[q]);
+  }
+#pragma unroll
+  for (int h = 4, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int t = 0; t < h; ++t) {
+      double send = up ? a[t] : a[h + t];
+      double keep = up ? a[h + t] : a[t];
+      a[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+  a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+  const int q = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  if ((lane & 3) == 0) {
+    const int d = lm[q];
+    if (d >= 0) x[d] = a[0];
+  }
+}
+
+__global__ void k_prolong_iface(DevCoarse c, const double* __restrict__ ym, double* __restrict__ x) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  int n3 = 3 * c.n_iface_nodes;
+  if (e >= n3) return;
+  int en = e / 3, gam = e - 3 * en;
+  int cf = c.iface_of[en];
+  int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
+  const double* w = c.W + c.wt_off[cf] + (int64_t)(en - c.iface_ptr[cf]) * nu;
+  int kb = 3 * c.mortar_ptr[cf] + gam;
+  double acc = 0.0;
+  for (int i = 0; i < nu; ++i) acc += w[i] * ym[kb + 3 * i];
+  x[3 * (int64_t)c.iface_nodes[en] + gam] = acc;
+}
+
+static int g_prolong_mode = -1;
+
 void launch_prolong(const DevCoarse& c, const double* ym, const double* yc, double* x,
                     cudaStream_t st) {
+  if (g_prolong_mode < 0) {
+    const char* e = getenv("HPLMM_PROLONG");
+    g_prolong_mode = (e && e[0] == '0') ? 0 : 1;
+  }
   if (c.n_grains > 0) k_yext<<<c.n_grains, 128, 0, st>>>(c, ym, yc);
+  if (g_prolong_mode == 1) {
+    if (c.n_chunks > 0)
+      k_prolong_rows<<<(unsigned)c.n_chunks, 256, 0, st>>>(c, c.g_lmap, c.g_row_s, c.g_row_base, x);
+    if (c.n_iface_nodes > 0)
+      k_prolong_iface<<<(3 * c.n_iface_nodes + 255) / 256, 256, 0, st>>>(c, ym, x);
+    return;
+  }
   int64_t th = 32 * (int64_t)c.n_dof;
   k_prolong<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(c, c.gpos, c.g_row_s, c.g_row_base, ym,
                                                           x);

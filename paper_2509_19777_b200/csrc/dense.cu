@@ -13,6 +13,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace hplmm {
 
@@ -366,40 +367,6 @@ constexpr int SY_CONS = 3;
 // stage it waits on, which the parity wait requires.
 static_assert(SY_STAGES % SY_CONS == 0, "each stage must belong to one consumer warp");
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(addr),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 __global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
     k_symv_tma(int64_t ntiles, const int32_t* __restrict__ tile_s,
                const int32_t* __restrict__ tile_ij, const int64_t* __restrict__ row_base,
@@ -416,7 +383,7 @@ __global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_fence_init();
   }
   __syncthreads();
   if (warp == SY_CONS) {                       // producer

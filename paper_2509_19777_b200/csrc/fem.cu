@@ -4,9 +4,12 @@
 // eq:stiff_iso, readings R2 (2x2x2 Gauss, unit voxel), R3
 // (node-major 3x3 blocks), R4 (Dirichlet identity rows, lifted RHS);
 // eq:gauss with R11 for the mortar weights.
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace hplmm {
 
@@ -199,9 +202,208 @@ __global__ void __launch_bounds__(32 * SPMV_WARPS) k_spmv(int n, const int32_t* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Streaming BSR SpMV (default).  The block values and column indices of a
+// chunk of SP_ROWS consecutive block rows are contiguous in HBM; a persistent
+// CTA per SM streams its contiguous range of chunks through a ring of
+// SP_STAGES shared-memory stages with 1-D TMA bulk copies (one producer lane,
+// L2 evict-first so the gathered x stays L2-resident), completion by mbarrier
+// transaction counts.  Consumer warp w owns stages s == w (mod SP_CONS) (keeps
+// each waiter within one mbarrier phase).  Per chunk a warp works on its
+// SP_ROWS rows at once: lane l takes block l of every row (<= 27 blocks per
+// row on the voxel lattice), so the x gathers of 4 rows are in flight
+// together; the 12 row sums are reduced with a 16-shuffle recursive-halving
+// transpose (warp-per-block-row reduction).
+// ---------------------------------------------------------------------------
+constexpr int SP_G = 4;      // rows reduced together by one warp pass
+constexpr int SP_MAXB = 27;  // blocks per row on the voxel lattice
+
+template <int ROWS>
+struct SpCfg {
+  static constexpr int VBYTES = ROWS * SP_MAXB * 72 + 16;
+  static constexpr int CBYTES = (ROWS * SP_MAXB * 4 + 16 + 15) / 16 * 16;
+  static constexpr int STAGE = VBYTES + CBYTES;
+};
+
+template <bool RESID, int ROWS, int CONS, int STAGES, int CPS>
+__global__ void __launch_bounds__(32 * (CONS + 1), CPS)
+    k_spmv_tma(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+               const double* __restrict__ val, const double* __restrict__ x,
+               const double* __restrict__ v, double* __restrict__ y) {
+  static_assert(STAGES % CONS == 0, "each stage must belong to one consumer warp");
+  static_assert(ROWS % SP_G == 0, "row groups");
+  using C = SpCfg<ROWS>;
+  extern __shared__ __align__(128) unsigned char sp_smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nchunks = (n + ROWS - 1) / ROWS;
+  const int per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const int c0 = blockIdx.x * per;
+  const int nk = max(0, min(nchunks, c0 + per) - c0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == CONS) {  // producer warp: lanes prefetch row pointers, lane 0 issues
+    const uint64_t pol = policy_evict_first();
+    for (int kb = 0; kb < nk; kb += 32) {
+      // lane j holds rp at the start of chunk kb+j; bend31 = end of chunk kb+31
+      int bstart = __ldg(rp + min(n, (c0 + kb + lane) * ROWS));
+      int bend31 = __ldg(rp + min(n, (c0 + kb + 32) * ROWS));
+      int cnt = min(32, nk - kb);
+      for (int j = 0; j < cnt; ++j) {
+        int b0 = __shfl_sync(0xffffffffu, bstart, j);
+        int b1 = __shfl_sync(0xffffffffu, bstart, (j + 1) & 31);
+        if (j == 31) b1 = bend31;
+        if (lane == 0) {
+          const int k = kb + j;
+          const int s = k % STAGES;
+          if (k >= STAGES) mbar_wait(&empty[s], (uint32_t)((k / STAGES - 1) & 1));
+          const int64_t vs = (72 * (int64_t)b0) & ~(int64_t)15, ve = (72 * (int64_t)b1 + 15) & ~(int64_t)15;
+          const int64_t cs = (4 * (int64_t)b0) & ~(int64_t)15, ce = (4 * (int64_t)b1 + 15) & ~(int64_t)15;
+          unsigned char* st = sp_smem + (size_t)s * C::STAGE;
+          mbar_expect_tx(&full[s], (uint32_t)((ve - vs) + (ce - cs)));
+          bulk_g2s_hint(st, reinterpret_cast<const unsigned char*>(val) + vs, (uint32_t)(ve - vs),
+                        &full[s], pol);
+          bulk_g2s_hint(st + C::VBYTES, reinterpret_cast<const unsigned char*>(col) + cs,
+                        (uint32_t)(ce - cs), &full[s], pol);
+        }
+      }
+    }
+    return;
+  }
+  for (int k = warp; k < nk; k += CONS) {
+    const int s = k % STAGES;
+    const int rc = (c0 + k) * ROWS;
+    int bl = __ldg(rp + min(n, rc + min(lane, ROWS)));
+    const int64_t vs = (72 * (int64_t)__shfl_sync(0xffffffffu, bl, 0)) & ~(int64_t)15;
+    const int64_t cs = (4 * (int64_t)__shfl_sync(0xffffffffu, bl, 0)) & ~(int64_t)15;
+    mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
+    const unsigned char* st = sp_smem + (size_t)s * C::STAGE;
+    const double* sv = reinterpret_cast<const double*>(st) - vs / 8;              // by 9*b
+    const int32_t* sc = reinterpret_cast<const int32_t*>(st + C::VBYTES) - cs / 4;  // by b
+    double res[ROWS / SP_G];
+    // all x gathers of the chunk first (ROWS independent L2 loads per lane)
+    int bq[ROWS + 1];
+#pragma unroll
+    for (int q = 0; q <= ROWS; ++q) bq[q] = __shfl_sync(0xffffffffu, bl, q);
+    double xv[ROWS][3];
+#pragma unroll
+    for (int q = 0; q < ROWS; ++q) {
+      const int b = bq[q] + lane;
+      if (b < bq[q + 1]) {
+        const double* xq = x + 3 * (int64_t)sc[b];
+        xv[q][0] = __ldg(xq);
+        xv[q][1] = __ldg(xq + 1);
+        xv[q][2] = __ldg(xq + 2);
+      } else {
+        xv[q][0] = xv[q][1] = xv[q][2] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int gq = 0; gq < ROWS / SP_G; ++gq) {
+      double a[16];
+#pragma unroll
+      for (int qq = 0; qq < SP_G; ++qq) {
+        const int q = gq * SP_G + qq;
+        const int b = bq[q] + lane;
+        double blk[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) blk[t] = 0.0;
+        if (b < bq[q + 1]) {
+#pragma unroll
+          for (int t = 0; t < 9; ++t) blk[t] = sv[9 * (int64_t)b + t];
+        }
+        a[3 * qq + 0] = fma(blk[0], xv[q][0], fma(blk[1], xv[q][1], blk[2] * xv[q][2]));
+        a[3 * qq + 1] = fma(blk[3], xv[q][0], fma(blk[4], xv[q][1], blk[5] * xv[q][2]));
+        a[3 * qq + 2] = fma(blk[6], xv[q][0], fma(blk[7], xv[q][1], blk[8] * xv[q][2]));
+      }
+#pragma unroll
+      for (int t = 3 * SP_G; t < 16; ++t) a[t] = 0.0;
+      // recursive-halving transpose reduction: 8 + 4 + 2 + 1 + 1 shuffles
+#pragma unroll
+      for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int t = 0; t < h; ++t) {
+          double send = up ? a[t] : a[h + t];
+          double keep = up ? a[h + t] : a[t];
+          a[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      res[gq] = a[0] + __shfl_xor_sync(0xffffffffu, a[0], 1);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // lane pair (2i, 2i+1) holds entry idx(lane) of each 4-row group
+    const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                    ((lane >> 1) & 1);
+#pragma unroll
+    for (int gq = 0; gq < ROWS / SP_G; ++gq) {
+      const int r = rc + gq * SP_G + idx / 3;
+      if (!(lane & 1) && idx < 3 * SP_G && r < n) {
+        const int64_t d = 3 * (int64_t)(rc + gq * SP_G) + idx;
+        y[d] = RESID ? (v[d] - res[gq]) : res[gq];
+      }
+    }
+  }
+}
+
+template <int ROWS, int CONS, int STAGES, int CPS = 1>
+static void spmv_tma(int n, const int32_t* rp, const int32_t* col, const double* val,
+                     const double* x, const double* v, double* y, cudaStream_t st, int nsm) {
+  constexpr int SM = STAGES * SpCfg<ROWS>::STAGE;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_spmv_tma<true, ROWS, CONS, STAGES, CPS>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+    cudaFuncSetAttribute(k_spmv_tma<false, ROWS, CONS, STAGES, CPS>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+    attr = true;
+  }
+  int nchunks = (n + ROWS - 1) / ROWS;
+  int grid = std::min(nsm * CPS, nchunks);
+  if (v)
+    k_spmv_tma<true, ROWS, CONS, STAGES, CPS><<<grid, 32 * (CONS + 1), SM, st>>>(n, rp, col, val, x, v, y);
+  else
+    k_spmv_tma<false, ROWS, CONS, STAGES, CPS><<<grid, 32 * (CONS + 1), SM, st>>>(n, rp, col, val, x, v, y);
+}
+
+static int g_spmv_mode = -1;   // >=1 TMA streaming variants (default 1), 0 = warp-per-row staging
+static int g_num_sms_spmv = 0;
+
+// max_row_blocks: the caller's bound on blocks per row (TMA kernel needs <= 27)
 void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const double* val,
-                 const double* x, const double* v, double* y, cudaStream_t st) {
+                 const double* x, const double* v, double* y, cudaStream_t st,
+                 int max_row_blocks) {
   if (n_nodes <= 0) return;
+  if (g_spmv_mode < 0) {
+    const char* e = getenv("HPLMM_SPMV");
+    g_spmv_mode = e ? atoi(e) : 6;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms_spmv, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (g_spmv_mode >= 1 && max_row_blocks <= SP_MAXB) {
+    switch (g_spmv_mode) {
+      case 2: spmv_tma<8, 6, 12>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+      case 3: spmv_tma<16, 3, 6>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+      case 4: spmv_tma<8, 4, 12>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+      case 5: spmv_tma<4, 12, 24>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+      case 6: spmv_tma<8, 3, 6, 2>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+      case 7: spmv_tma<4, 4, 12, 2>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+      case 8: spmv_tma<12, 4, 8>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+      case 1: spmv_tma<4, 8, 24>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+      case 9: spmv_tma<8, 2, 4, 3>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+      // default (measured best on B200, profiles/r01_spmv_variants.txt): 8-row chunks,
+      // 3 consumer warps x 2 stages, 2 CTAs per SM
+      default: spmv_tma<8, 3, 6, 2>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
+    }
+  }
   int grid = (n_nodes + SPMV_WARPS - 1) / SPMV_WARPS;
   if (v)
     k_spmv<true><<<grid, 32 * SPMV_WARPS, 0, st>>>(n_nodes, row_ptr, col, val, x, v, y);

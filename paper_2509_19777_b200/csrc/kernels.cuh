@@ -49,8 +49,11 @@ void launch_assemble_rhs(int n_nodes, const int32_t* drow_ptr, const int32_t* dc
                          const double* f, const double* uD, double* b, cudaStream_t st);
 // y = A x            (v == nullptr)
 // y = v - A x        (v != nullptr)
+// max_row_blocks: largest row length in blocks (<= 27 on the voxel lattice
+// selects the TMA streaming kernel); col and val need 16 bytes of tail padding.
 void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const double* val,
-                 const double* x, const double* v, double* y, cudaStream_t st);
+                 const double* x, const double* v, double* y, cudaStream_t st,
+                 int max_row_blocks);
 void launch_mortar_weights(int n_iface_nodes, const int32_t* iface_of, const int32_t* iface_ptr,
                            const int32_t* iface_nodes, const int32_t* mortar_ptr,
                            const int32_t* mortar_nodes, const int64_t* wt_off,
@@ -91,6 +94,8 @@ struct DevCoarse {
   double* R = nullptr;                 // scratch R_g / Y_g (setup), same layout
   int32_t* iface_ptr = nullptr;        // [C+1]
   int32_t* iface_nodes = nullptr;
+  int32_t* iface_of = nullptr;         // [n_iface_nodes] interface of each entry
+  int n_iface_nodes = 0;
   int32_t* mortar_ptr = nullptr;       // [C+1]
   int64_t* wt_off = nullptr;           // [C]
   double* W = nullptr;                 // mortar weights

@@ -28,19 +28,43 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;  // valid in thread 0
 }
 
-// partial[b*m + j] = sum_{i in block b's range} V[j][i] w[i]
+// partial[b*m + j] = sum_{i in block b's range} V[j][i] w[i].  MD_J basis
+// vectors per pass share one read of w; per vector the summation order is
+// fixed (per-thread strided fma, warp butterfly, warps in order).
+constexpr int MD_J = 8;
 __global__ void __launch_bounds__(KT) k_multidot(int64_t n, int m, const double* __restrict__ V,
                                                  int64_t ldv, const double* __restrict__ w,
                                                  double* __restrict__ partial) {
-  __shared__ double red[KT / 32];
+  __shared__ double red[MD_J][KT / 32];
+  const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   int64_t i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
-  for (int j = 0; j < m; ++j) {
-    const double* v = V + j * ldv;
-    double s = 0.0;
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) s = fma(v[i], w[i], s);
-    double t = block_sum(s, red);
-    if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * m + j] = t;
+  for (int j0 = 0; j0 < m; j0 += MD_J) {
+    const int nj = min(MD_J, m - j0);
+    double s[MD_J];
+#pragma unroll
+    for (int jj = 0; jj < MD_J; ++jj) s[jj] = 0.0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) {
+      const double wi = w[i];
+#pragma unroll
+      for (int jj = 0; jj < MD_J; ++jj)
+        if (jj < nj) s[jj] = fma(V[(j0 + jj) * ldv + i], wi, s[jj]);
+    }
+#pragma unroll
+    for (int jj = 0; jj < MD_J; ++jj) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s[jj] += __shfl_xor_sync(0xffffffffu, s[jj], o);
+    }
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+      for (int jj = 0; jj < MD_J; ++jj) red[jj][wp] = s[jj];
+    __syncthreads();
+    if (threadIdx.x < nj) {
+      double t = 0.0;
+      for (int q = 0; q < KT / 32; ++q) t += red[threadIdx.x][q];
+      partial[(int64_t)blockIdx.x * m + j0 + threadIdx.x] = t;
+    }
   }
 }
 
