@@ -77,6 +77,16 @@ typedef struct {
   int32_t coarse_refine; /* 1 = one step of iterative refinement of the coarse
                             solve y = S^-1 r with S kept resident (residual
                             ~(kappa u)^2 instead of ~kappa u); default 0        */
+  int32_t local_factor;  /* exact local solves of M_zeta and M_g (eq:Mg_Mz; the
+                            paper's precomputed LU):
+                            0 = explicit dense inverse of every subdomain block
+                                (packed 64x64 lower tiles, one symmetric
+                                mat-vec per apply);
+                            1 = supernodal block-LDL^T factor on a geometric
+                                nested-dissection ordering (W_S = F_RS F_SS^-1,
+                                F_SS^-1; forward + backward sweep per apply,
+                                ~4x fewer bytes, needed for cfg4/cfg5).
+                            default 1                                          */
 } hplmm_options;
 
 typedef struct {
@@ -87,7 +97,8 @@ typedef struct {
   int32_t n_interfaces;   /* contact interfaces N^c = contact grids N^zeta          */
   int32_t n_mortar_dofs;  /* N^o_m = 3 N^m                                          */
   int32_t n_coarse;       /* N^o_m + number of correction columns (after set_rhs)   */
-  int64_t local_bytes;    /* bytes of the packed local inverse tiles                */
+  int64_t local_bytes;    /* bytes of the local operators (packed inverse tiles, or
+                             supernodal factors)                                  */
   int64_t coarse_bytes;   /* bytes of the packed coarse inverse tiles               */
   int64_t prolong_nnz;    /* stored entries of P^_B (grain blocks + Q^o)            */
   /* solve outcome */
@@ -130,8 +141,9 @@ hplmm_status hplmm_assemble(hplmm_handle *h, int32_t device, void *stream);
 hplmm_status hplmm_set_matrix(hplmm_handle *h, const double *val, void *stream);
 
 /* GPU numeric setup, timed separately from the solve (north_star (6)):
- * Gaussian mortar weights (eq:gauss), inverses of every grain block
- * A^{g}_{g} and contact-grid block A^[zeta,zeta] (T_ML), shape vectors
+ * Gaussian mortar weights (eq:gauss), inverses (local_factor 0) or
+ * supernodal factors (local_factor 1) of every grain block A^{g}_{g} and
+ * contact-grid block A^[zeta,zeta] (T_ML), shape vectors
  * B = -A_g^-1 Abar^g_m Q^o (eq:col_pk, R14), S = P_B^T A^ P_B (eq:mg_struct,
  * R16) and its inverse (R17).  Errors: SINGULAR_LOCAL (report.err_index via
  * hplmm_get_report), SINGULAR_COARSE, OOM. */
@@ -203,8 +215,9 @@ hplmm_status hplmm_get_report(hplmm_handle *h, hplmm_report *report);
 hplmm_status hplmm_profile(hplmm_handle *h, int32_t enable, int32_t reset);
 
 /* Statistics of kernel class `kernel` (0 = grain SYMV tiles, 1 = contact-grid
- * SYMV tiles, 2 = coarse SYMV tiles): total device ms and launch count since
- * the last reset; tile_bytes = packed-tile bytes one launch streams. */
+ * SYMV tiles, 2 = coarse SYMV tiles, 3 = grain supernodal solve, 4 =
+ * contact-grid supernodal solve): total device ms and launch count since the
+ * last reset; tile_bytes = factor bytes one launch streams. */
 hplmm_status hplmm_kernel_stats(hplmm_handle *h, int32_t kernel, double *total_ms,
                                 int64_t *launches, int64_t *tile_bytes);
 

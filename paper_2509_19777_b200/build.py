@@ -8,7 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libhplmm.so")
-SOURCES = ["host_setup.cpp", "fem.cu", "dense.cu", "coarse.cu", "krylov.cu", "api.cu"]
+SOURCES = ["host_setup.cpp", "supernodal_host.cpp", "fem.cu", "dense.cu", "coarse.cu", "krylov.cu",
+           "supernodal.cu", "sn_setup.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-ffp-contract=off",
          "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xptxas", "-v",
@@ -37,7 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     os.replace(OUT + ".tmp", OUT)
     if verbose:
-        print(r.stderr)
+        print(r.stderr[-4000:])
     return OUT
 
 

@@ -13,12 +13,16 @@
 
 #include "hplmm_internal.h"
 #include "kernels.cuh"
+#include "sn_setup.h"
 
 using namespace hplmm;
 
 namespace {
 
 thread_local std::string g_last_error;
+
+constexpr int kSnLeaf = 40;                          // ND leaf size (nodes)
+constexpr int64_t kSnPoolBytes = (int64_t)4 << 30;   // frontal matrices per wave
 
 struct HError {
   hplmm_status st;
@@ -33,7 +37,10 @@ struct HError {
                    std::string(#call) + ": " + cudaGetErrorString(e_)};                   \
   } while (0)
 
-enum KernelClass { KC_SYMV_GRAIN = 0, KC_SYMV_CONTACT = 1, KC_SYMV_COARSE = 2, KC_N = 3 };
+enum KernelClass {
+  KC_SYMV_GRAIN = 0, KC_SYMV_CONTACT = 1, KC_SYMV_COARSE = 2, KC_SN_GRAIN = 3, KC_SN_CONTACT = 4,
+  KC_N = 5
+};
 
 }  // namespace
 
@@ -80,8 +87,15 @@ struct hplmm_handle {
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
-  double kc_ms[KC_N] = {0, 0, 0};
-  int64_t kc_launches[KC_N] = {0, 0, 0};
+  double kc_ms[KC_N] = {0, 0, 0, 0, 0};
+  int64_t kc_launches[KC_N] = {0, 0, 0, 0, 0};
+
+  // supernodal local factors (local_factor == 1)
+  SnBatch sg, sc;                       // grains, contact grids
+  int32_t* d_gpos_sn = nullptr;         // global DOF -> position in sg.yloc (or -1)
+  int32_t *d_cptr_sn = nullptr, *d_cidx_sn = nullptr;   // DOF -> positions in sc.yloc
+  int nsm = 148;
+  bool sparse() const { return hs.opt.local_factor == 1; }
   int64_t launches = 0;
 
   template <class T>
@@ -137,6 +151,20 @@ struct hplmm_handle {
     launch_symv_reduce(b, st);
     launches += 2;
   }
+  void sn_solve(SnBatch& b, const double* in, int kc) {
+    if (profile && b.work.nblocks > 0) {
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, st));
+      sn_apply(b, in, st);
+      CK(cudaEventRecord(e1, st));
+      ev_pending.push_back({kc, {e0, e1}});
+    } else {
+      sn_apply(b, in, st);
+    }
+    launches += 1;
+  }
   void flush_profile() {
     for (auto& e : ev_pending) {
       float ms = 0.f;
@@ -172,7 +200,8 @@ hplmm_status fail(const HError& e) {
 // Build a packed-tile batch over subdomains given by node lists (DOFs 3n+c)
 // or, for the coarse block, one subdomain of `ndof_override` identity DOFs.
 void build_batch(hplmm_handle* h, DevBatch& b, const std::vector<int32_t>& ptr,
-                 const std::vector<int32_t>& nodes, int ndof_override, bool setup_buffers) {
+                 const std::vector<int32_t>& nodes, int ndof_override, bool setup_buffers,
+                 bool with_tiles = true) {
   int nsub = ndof_override >= 0 ? 1 : (int)ptr.size() - 1;
   std::vector<int32_t> nb(nsub), ndof(nsub);
   std::vector<int64_t> tile_base(nsub), row_base(nsub);
@@ -216,12 +245,13 @@ void build_batch(hplmm_handle* h, DevBatch& b, const std::vector<int32_t>& ptr,
   b.row_s = h->upload(row_s);
   b.row_k = h->upload(row_k);
   b.lmap = h->upload(lmap);
-  b.tiles = h->dalloc<double>((size_t)nt * TILE);
-  b.part_row = h->dalloc<double>((size_t)nt * TB);
-  b.part_col = h->dalloc<double>((size_t)nt * TB);
   b.xloc = h->dalloc<double>((size_t)b.nloc);
   b.yloc = h->dalloc<double>((size_t)b.nloc);
   b.err = h->dalloc<int32_t>(1);
+  if (!with_tiles) return;   // layout only (supernodal mode: B_g row layout, lmap)
+  b.tiles = h->dalloc<double>((size_t)nt * TILE);
+  b.part_row = h->dalloc<double>((size_t)nt * TB);
+  b.part_col = h->dalloc<double>((size_t)nt * TB);
   if (setup_buffers) {
     b.dinv = h->dalloc<double>((size_t)nsub * TILE, true);
     b.cbuf = h->dalloc<double>((size_t)nr * TILE, true);
@@ -247,6 +277,14 @@ double elapsed(cudaEvent_t a, cudaEvent_t b) {
   cudaEventElapsedTime(&ms, a, b);
   return ms * 1e-3;
 }
+
+struct HandleAlloc : DevAlloc {
+  hplmm_handle* h;
+  explicit HandleAlloc(hplmm_handle* hh) : h(hh) {}
+  void* alloc(size_t bytes, bool setup_only) override {
+    return h->dalloc<char>(bytes, setup_only);
+  }
+};
 
 struct Timer {
   cudaEvent_t a, b;
@@ -290,6 +328,12 @@ void op_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
 }
 
 void op_mzeta(hplmm_handle* h, const double* in, double* out) {
+  if (h->sparse()) {
+    h->sn_solve(h->sc, in, KC_SN_CONTACT);
+    launch_sum_contact(h->n_dof, h->d_cptr_sn, h->d_cidx_sn, h->sc.yloc, out, h->st);
+    h->launches += 1;
+    return;
+  }
   launch_gather(h->cb, in, h->st);
   h->symv(h->cb, KC_SYMV_CONTACT);
   launch_sum_contact(h->n_dof, h->d_cptr, h->d_cidx, h->cb.yloc, out, h->st);
@@ -298,6 +342,12 @@ void op_mzeta(hplmm_handle* h, const double* in, double* out) {
 
 // out = a + b + M_g^-1 in
 void op_mgrain(hplmm_handle* h, const double* in, const double* a, const double* b, double* out) {
+  if (h->sparse()) {
+    h->sn_solve(h->sg, in, KC_SN_GRAIN);
+    launch_combine_grain(h->n_dof, h->d_gpos_sn, h->sg.yloc, a, b, out, h->st);
+    h->launches += 1;
+    return;
+  }
   launch_gather(h->gb, in, h->st);
   h->symv(h->gb, KC_SYMV_GRAIN);
   launch_combine_grain(h->n_dof, h->co.gpos, h->gb.yloc, a, b, out, h->st);
@@ -348,10 +398,18 @@ void op_minv(hplmm_handle* h, const double* in, double* out) {
 
 void do_set_rhs(hplmm_handle* h, const double* b_dev) {
   Timer t(h->st);
-  launch_gather(h->gb, b_dev, h->st);
-  h->symv(h->gb, KC_SYMV_GRAIN);
+  if (h->sparse()) {
+    h->sn_solve(h->sg, b_dev, KC_SN_GRAIN);
+    launch_sn_to_batch(h->gb.nloc, h->gb.lmap, h->d_gpos_sn, b_dev, h->sg.yloc, h->gb.xloc,
+                       h->gb.yloc, h->st);
+    h->launches += 1;
+  } else {
+    launch_gather(h->gb, b_dev, h->st);
+    h->symv(h->gb, KC_SYMV_GRAIN);
+    h->launches += 1;
+  }
   launch_set_correction(h->co, h->gb, h->st);
-  h->launches += 2;
+  h->launches += 1;
   std::vector<double> Dc(h->co.n_grains);
   if (h->co.n_grains)
     CK(cudaMemcpyAsync(Dc.data(), h->co.Dc, Dc.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -379,6 +437,7 @@ void hplmm_default_options(hplmm_options* o) {
   o->max_iter = 300;
   o->n_st = 1;
   o->coarse_refine = 0;
+  o->local_factor = 1;
 }
 
 const char* hplmm_last_error(void) { return g_last_error.c_str(); }
@@ -505,8 +564,9 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         node_local[hs.iface_nodes[e]] = e - hs.iface_ptr[c];
 
     // ---------------- batches --------------------------------------------
-    build_batch(h, h->gb, hs.grain_ptr, hs.grain_nodes, -1, true);
-    build_batch(h, h->cb, hs.contact_ptr, hs.contact_nodes, -1, true);
+    const bool sparse = h->sparse();
+    build_batch(h, h->gb, hs.grain_ptr, hs.grain_nodes, -1, true, !sparse);
+    if (!sparse) build_batch(h, h->cb, hs.contact_ptr, hs.contact_nodes, -1, true);
     build_batch(h, h->sb, {}, {}, Nm, true);
     int64_t lb = (h->gb.ntiles + h->cb.ntiles) * (int64_t)TILE * 8;
     h->rep.local_bytes = lb;
@@ -669,24 +729,61 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     h->d_yc = h->dalloc<double>(std::max(G, 1));
     CK(cudaMemsetAsync(h->d_rm, 0, std::max(Nm, 1) * 8, h->st));
 
-    // ---------------- T_ML: local inversions ------------------------------
+    // ---------------- T_ML: local inversions / factorisations ------------
     Timer tl(h->st);
     int32_t big = INT_MAX;
-    for (DevBatch* b : {&h->gb, &h->cb, &h->sb}) {
-      CK(cudaMemsetAsync(b->tiles, 0, (size_t)b->ntiles * TILE * 8, h->st));
-      CK(cudaMemcpyAsync(b->err, &big, 4, cudaMemcpyHostToDevice, h->st));
+    HandleAlloc halloc(h);
+    CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
+    if (sparse) {
+      std::string err;
+      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, kSnLeaf, h->sg.sym, err) ||
+          !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, kSnLeaf, h->sc.sym, err))
+        throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
+      try {
+        sn_upload(h->sg, halloc, h->st, h->nsm);
+        sn_upload(h->sc, halloc, h->st, h->nsm);
+        sn_factor(h->sg, h->d_val, halloc, h->st, kSnPoolBytes);
+        try {
+          sn_factor(h->sc, h->d_val, halloc, h->st, kSnPoolBytes);
+        } catch (SnError& e) {
+          e.sub += G;   // contact grids are numbered after the grains
+          throw;
+        }
+      } catch (const SnError& e) {
+        h->rep.err_index = e.sub;
+        throw HError{(hplmm_status)e.status, e.msg + " " + std::to_string(e.sub)};
+      }
+      h->rep.local_bytes = 8 * (h->sg.sym.factor_doubles + h->sc.sym.factor_doubles);
+      // maps of the local (elimination-order) solutions back to global DOFs
+      std::vector<int32_t> gpos(h->n_dof, -1);
+      for (size_t p = 0; p < h->sg.sym.gmap.size(); ++p) gpos[h->sg.sym.gmap[p]] = (int32_t)p;
+      h->d_gpos_sn = h->upload(gpos);
+      std::vector<int32_t> cnt(h->n_dof + 1, 0);
+      for (int32_t d : h->sc.sym.gmap) cnt[d + 1]++;
+      for (int d = 0; d < h->n_dof; ++d) cnt[d + 1] += cnt[d];
+      std::vector<int32_t> idx(cnt[h->n_dof]), fill(cnt.begin(), cnt.end() - 1);
+      for (size_t p = 0; p < h->sc.sym.gmap.size(); ++p) idx[fill[h->sc.sym.gmap[p]]++] = (int32_t)p;
+      h->d_cptr_sn = h->upload(cnt);
+      h->d_cidx_sn = h->upload(idx);
+      CK(cudaMemcpyAsync(h->sb.err, &big, 4, cudaMemcpyHostToDevice, h->st));
+      CK(cudaMemsetAsync(h->sb.tiles, 0, (size_t)h->sb.ntiles * TILE * 8, h->st));
+    } else {
+      for (DevBatch* b : {&h->gb, &h->cb, &h->sb}) {
+        CK(cudaMemsetAsync(b->tiles, 0, (size_t)b->ntiles * TILE * 8, h->st));
+        CK(cudaMemcpyAsync(b->err, &big, 4, cudaMemcpyHostToDevice, h->st));
+      }
+      launch_extract_local(h->gb, hs.grain_ptr.back(), h->d_gnode_ptr, h->d_gnodes, h->d_row_ptr,
+                           h->d_col, h->d_val, h->st);
+      launch_extract_local(h->cb, hs.contact_ptr.back(), h->d_cnode_ptr, h->d_cnodes,
+                           h->d_row_ptr, h->d_col, h->d_val, h->st);
+      launch_pad_identity(h->gb, h->st);
+      launch_pad_identity(h->cb, h->st);
+      launch_sweep_invert(h->gb, h->st);
+      launch_sweep_invert(h->cb, h->st);
+      CK(cudaGetLastError());
+      check_batch_err(h, h->gb, 0, false);
+      check_batch_err(h, h->cb, G, false);
     }
-    launch_extract_local(h->gb, hs.grain_ptr.back(), h->d_gnode_ptr, h->d_gnodes, h->d_row_ptr,
-                         h->d_col, h->d_val, h->st);
-    launch_extract_local(h->cb, hs.contact_ptr.back(), h->d_cnode_ptr, h->d_cnodes, h->d_row_ptr,
-                         h->d_col, h->d_val, h->st);
-    launch_pad_identity(h->gb, h->st);
-    launch_pad_identity(h->cb, h->st);
-    launch_sweep_invert(h->gb, h->st);
-    launch_sweep_invert(h->cb, h->st);
-    CK(cudaGetLastError());
-    check_batch_err(h, h->gb, 0, false);
-    check_batch_err(h, h->cb, G, false);
     h->rep.t_setup_local_s = tl.stop();
 
     // ---------------- T_MG: mortars, P_B, S, S^-1 -------------------------
@@ -706,8 +803,11 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     {
       std::vector<int32_t> kc(G);
       for (int g = 0; g < G; ++g) kc[g] = ld[g] - 1;
-      launch_symm_neg(h->gb, co.b_off, co.ld, h->upload(kc), (maxk + TB - 1) / TB, co.R, co.B,
-                      h->st);
+      if (sparse)
+        sn_shape_vectors(h->sg, halloc, h->st, h->nsm, kc, co.b_off, co.ld, co.R, co.B);
+      else
+        launch_symm_neg(h->gb, co.b_off, co.ld, h->upload(kc), (maxk + TB - 1) / TB, co.R, co.B,
+                        h->st);
     }
     launch_grain_AB(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
     launch_grain_BtY(co, h->gb, h->st);
@@ -743,6 +843,9 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     co.Cg = nullptr;
     h->setup_done = true;
     return HPLMM_OK;
+  } catch (const SnError& e) {
+    h->rep.err_index = e.sub;
+    return fail(HError{(hplmm_status)e.status, e.msg});
   } catch (const HError& e) {
     return fail(e);
   }
@@ -1065,6 +1168,10 @@ hplmm_status hplmm_kernel_stats(hplmm_handle* h, int32_t kernel, double* total_m
   if (!h || kernel < 0 || kernel >= KC_N) { g_last_error = "bad argument"; return HPLMM_ERR_ARG; }
   if (total_ms) *total_ms = h->kc_ms[kernel];
   if (launches) *launches = h->kc_launches[kernel];
+  if (kernel >= KC_SN_GRAIN) {
+    if (tile_bytes) *tile_bytes = kernel == KC_SN_GRAIN ? h->sg.solve_bytes : h->sc.solve_bytes;
+    return HPLMM_OK;
+  }
   DevBatch* b = kernel == 0 ? &h->gb : (kernel == 1 ? &h->cb : &h->sb);
   if (tile_bytes) *tile_bytes = b->ntiles * (int64_t)TILE * 8;
   return HPLMM_OK;

@@ -1,0 +1,375 @@
+// Host orchestration of the batched supernodal factors: upload of the
+// symbolic data, LPT work lists, and the level-by-level multifrontal numeric
+// factorisation (setup, T_ML) -- see supernodal.h.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <functional>
+#include <queue>
+
+#include "sn_setup.h"
+
+namespace hplmm {
+
+namespace {
+
+#define SN_CK(call)                                                            \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) throw SnError{-2, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+template <class T>
+T* up(DevAlloc& A, const std::vector<T>& v, cudaStream_t st, bool setup_only = false) {
+  T* p = (T*)A.alloc(std::max<size_t>(v.size(), 1) * sizeof(T), setup_only);
+  if (!v.empty()) SN_CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return p;
+}
+
+// LPT: items with weights -> nb bins; returns CSR (ptr per bin) over item ids
+void lpt(const std::vector<int64_t>& wgt, int nb, std::vector<int32_t>& ptr,
+         std::vector<int32_t>& ids) {
+  std::vector<int32_t> ord(wgt.size());
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int32_t)i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return wgt[a] > wgt[b]; });
+  using P = std::pair<int64_t, int>;
+  std::priority_queue<P, std::vector<P>, std::greater<P>> q;
+  for (int b = 0; b < nb; ++b) q.push({0, b});
+  std::vector<std::vector<int32_t>> bins(nb);
+  for (int i : ord) {
+    P t = q.top();
+    q.pop();
+    bins[t.second].push_back(i);
+    q.push({t.first + wgt[i], t.second});
+  }
+  ptr.assign(nb + 1, 0);
+  ids.clear();
+  for (int b = 0; b < nb; ++b) {
+    std::sort(bins[b].begin(), bins[b].end());
+    ids.insert(ids.end(), bins[b].begin(), bins[b].end());
+    ptr[b + 1] = (int32_t)ids.size();
+  }
+}
+
+}  // namespace
+
+void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nrhs,
+                   const std::vector<int32_t>* ncols, SnWork& wk) {
+  const SnSymbolic& s = B.sym;
+  const bool setup_only = ncols != nullptr;
+  std::vector<int64_t> wgt;
+  std::vector<int32_t> isub, ic0;
+  for (int g = 0; g < s.nsub; ++g) {
+    const int nc = ncols ? (*ncols)[g] : 1;
+    for (int c0 = 0; c0 < nc; c0 += nrhs) {
+      isub.push_back(g);
+      ic0.push_back(c0);
+      wgt.push_back(s.sub_fbytes[g] + 8 * (int64_t)s.sub_n[g] * 64);
+    }
+  }
+  nblocks = std::max(1, std::min<int>(nblocks, (int)isub.size()));
+  std::vector<int32_t> ptr, ids;
+  lpt(wgt, nblocks, ptr, ids);
+  std::vector<int32_t> sub(ids.size()), c0(ids.size());
+  std::vector<int64_t> cptr(nblocks + 1, 0);
+  std::vector<SnChunk> flat;
+  for (int b = 0; b < nblocks; ++b) {
+    for (int t = ptr[b]; t < ptr[b + 1]; ++t) {
+      sub[t] = isub[ids[t]];
+      c0[t] = ic0[ids[t]];
+      const int g = sub[t];
+      const size_t first = flat.size();
+      flat.insert(flat.end(), s.chunks.begin() + s.sub_fc0[g], s.chunks.begin() + s.sub_fc1[g]);
+      flat.insert(flat.end(), s.chunks.begin() + s.sub_bc0[g], s.chunks.begin() + s.sub_bc1[g]);
+      flat[first].info |= SN_INFO_FIRST_ITEM;
+      flat.back().info |= SN_INFO_LAST_ITEM;
+    }
+    cptr[b + 1] = (int64_t)flat.size();
+  }
+  wk.nblocks = isub.empty() ? 0 : nblocks;
+  wk.item_ptr = up(A, ptr, st, setup_only);
+  wk.item_sub = up(A, sub, st, setup_only);
+  wk.item_c0 = up(A, c0, st, setup_only);
+  wk.chunk_ptr = up(A, cptr, st, setup_only);
+  wk.chunks = up(A, flat, st, setup_only);
+}
+
+void sn_upload(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm) {
+  const SnSymbolic& s = B.sym;
+  B.d_sub_n = up(A, s.sub_n, st);
+  B.d_sub_base = up(A, s.sub_base, st);
+  B.d_sub_fc0 = up(A, s.sub_fc0, st);
+  B.d_sub_fc1 = up(A, s.sub_fc1, st);
+  B.d_sub_bc0 = up(A, s.sub_bc0, st);
+  B.d_sub_bc1 = up(A, s.sub_bc1, st);
+  B.d_gmap = up(A, s.gmap, st);
+  B.d_lidx = up(A, s.lidx, st);
+  B.d_sn_w = up(A, s.sn_w, st);
+  B.d_sn_r = up(A, s.sn_r, st);
+  B.d_sn_p0 = up(A, s.sn_p0, st);
+  B.d_sn_ldw = up(A, s.sn_ldw, st);
+  B.d_sn_ldf = up(A, s.sn_ldf, st);
+  B.d_sn_rows_off = up(A, s.sn_rows_off, st);
+  B.d_rows = up(A, s.rows, st);
+  B.factor = (double*)A.alloc(std::max<int64_t>(s.factor_doubles, 2) * 8, false);
+  // zero padding rows (ld is even; the solve reads row pairs)
+  SN_CK(cudaMemsetAsync(B.factor, 0, std::max<int64_t>(s.factor_doubles, 2) * 8, st));
+  B.n_loc = s.sub_base.empty() ? 0 : s.sub_base.back() + s.sub_n.back();
+  B.yloc = (double*)A.alloc(std::max<int64_t>(B.n_loc, 1) * 8, false);
+  B.dev.sub_n = B.d_sub_n;
+  B.dev.sub_base = B.d_sub_base;
+  B.dev.sub_fc0 = B.d_sub_fc0;
+  B.dev.sub_fc1 = B.d_sub_fc1;
+  B.dev.sub_bc0 = B.d_sub_bc0;
+  B.dev.sub_bc1 = B.d_sub_bc1;
+  B.dev.gmap = B.d_gmap;
+  B.dev.sn_w = B.d_sn_w;
+  B.dev.sn_r = B.d_sn_r;
+  B.dev.sn_p0 = B.d_sn_p0;
+  B.dev.sn_ldw = B.d_sn_ldw;
+  B.dev.sn_ldf = B.d_sn_ldf;
+  B.dev.sn_rows_off = B.d_sn_rows_off;
+  B.dev.rows = B.d_rows;
+  B.dev.factor = B.factor;
+  B.solve_bytes = 0;
+  for (int64_t b : s.sub_fbytes) B.solve_bytes += b;
+  sn_build_work(B, A, st, nsm, 1, nullptr, B.work);
+}
+
+void sn_apply(const SnBatch& B, const double* in, cudaStream_t st) {
+  SnIO io;
+  io.mode = 0;
+  io.in = in;
+  io.out = B.yloc;
+  launch_sn_solve(B.dev, io, B.work, 1, B.sym.max_n, st);
+}
+
+// ---------------------------------------------------------------------------
+// numeric factorisation
+// ---------------------------------------------------------------------------
+void sn_factor(SnBatch& B, const double* d_val, DevAlloc& A, cudaStream_t st, int64_t pool_budget) {
+  const SnSymbolic& s = B.sym;
+  if (s.nsn == 0) return;
+  SnNum nm;
+  nm.asm_ptr = up(A, s.asm_ptr, st, true);
+  nm.asm_e = up(A, s.asm_e, st, true);
+  nm.asm_u = up(A, s.asm_u, st, true);
+  nm.asm_v = up(A, s.asm_v, st, true);
+  nm.sn_w = B.d_sn_w;
+  nm.sn_r = B.d_sn_r;
+  nm.sn_parent = up(A, s.sn_parent, st, true);
+  nm.sn_ldw = B.d_sn_ldw;
+  nm.sn_ldf = B.d_sn_ldf;
+  nm.sn_foff = up(A, s.sn_foff, st, true);
+  nm.rel_off = up(A, s.rel_off, st, true);
+  nm.rel = up(A, s.rel, st, true);
+  nm.rows_off = B.d_sn_rows_off;
+  nm.rows = B.d_rows;
+  launch_rows_to_factor(s.nsn, nm, B.factor, st);
+  int64_t* d_front_off = (int64_t*)A.alloc((size_t)s.nsn * 8, true);
+  nm.front_off = d_front_off;
+
+  // waves of consecutive subdomains whose fronts fit the pool budget
+  std::vector<int64_t> fbytes(s.nsub, 0);
+  for (int g = 0; g < s.nsub; ++g)
+    for (int k = s.sub_sn0[g]; k < s.sub_sn1[g]; ++k) {
+      int64_t h = s.sn_w[k] + s.sn_r[k];
+      fbytes[g] += h * h * 8;
+    }
+  std::vector<std::pair<int, int>> waves;
+  int64_t maxwave = 0;
+  for (int g0 = 0; g0 < s.nsub;) {
+    int64_t tot = 0;
+    int g1 = g0;
+    while (g1 < s.nsub && (g1 == g0 || tot + fbytes[g1] <= pool_budget)) tot += fbytes[g1++];
+    waves.push_back({g0, g1});
+    maxwave = std::max(maxwave, tot);
+    g0 = g1;
+  }
+  double* pool = (double*)A.alloc(std::max<int64_t>(maxwave, 8), true);
+  nm.pool = pool;
+
+  // per-level scratch sizes (max over waves)
+  std::vector<int64_t> front_off(s.nsn, 0);
+  int64_t max_list = 1, max_tiles = 1, max_rows = 1, max_work = 1;
+  for (auto& wv : waves) {
+    std::vector<int64_t> ntl(s.n_levels, 0), nrw(s.n_levels, 0), nls(s.n_levels, 0), nwk(s.n_levels, 0);
+    for (int k = s.sub_sn0[wv.first]; k < s.sub_sn1[wv.second - 1]; ++k) {
+      int L = s.sn_level[k];
+      int nb = (s.sn_w[k] + TB - 1) / TB;
+      ntl[L] += (int64_t)nb * (nb + 1) / 2;
+      nrw[L] += nb;
+      nls[L]++;
+      int64_t tr = (s.sn_r[k] + 63) / 64, tw = (s.sn_w[k] + 63) / 64;
+      nwk[L] += std::max(tr * tw, tr * tr);
+    }
+    for (int L = 0; L < s.n_levels; ++L) {
+      max_list = std::max(max_list, nls[L]);
+      max_tiles = std::max(max_tiles, ntl[L]);
+      max_rows = std::max(max_rows, nrw[L]);
+      max_work = std::max(max_work, nwk[L]);
+    }
+  }
+  DevBatch lb;
+  lb.tiles = (double*)A.alloc((size_t)max_tiles * TILE * 8, true);
+  lb.dinv = (double*)A.alloc((size_t)max_list * TILE * 8, true);
+  lb.cbuf = (double*)A.alloc((size_t)max_rows * TILE * 8, true);
+  lb.wbuf = (double*)A.alloc((size_t)max_rows * TILE * 8, true);
+  lb.err = (int32_t*)A.alloc(4, true);
+  int32_t* d_nb = (int32_t*)A.alloc(max_list * 4, true);
+  int32_t* d_ndof = (int32_t*)A.alloc(max_list * 4, true);
+  int64_t* d_tile_base = (int64_t*)A.alloc(max_list * 8, true);
+  int64_t* d_row_base = (int64_t*)A.alloc(max_list * 8, true);
+  int32_t* d_tile_s = (int32_t*)A.alloc(max_tiles * 4, true);
+  int32_t* d_tile_ij = (int32_t*)A.alloc(max_tiles * 4, true);
+  int32_t* d_row_s = (int32_t*)A.alloc(max_rows * 4, true);
+  int32_t* d_row_k = (int32_t*)A.alloc(max_rows * 4, true);
+  int32_t* d_list = (int32_t*)A.alloc(max_list * 4, true);
+  int32_t* d_clist = (int32_t*)A.alloc(max_list * 4 * std::max(1, s.max_children), true);
+  GemmProb* d_probs = (GemmProb*)A.alloc(max_list * sizeof(GemmProb), true);
+  int32_t* d_work = (int32_t*)A.alloc(max_work * 12, true);
+
+  auto h2d = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes) SN_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+  };
+  for (auto& wv : waves) {
+    const int k0 = s.sub_sn0[wv.first], k1 = s.sub_sn1[wv.second - 1];
+    int64_t off = 0;
+    for (int k = k0; k < k1; ++k) {
+      front_off[k] = off;
+      int64_t h = s.sn_w[k] + s.sn_r[k];
+      off += h * h;
+    }
+    h2d(d_front_off + k0, front_off.data() + k0, (size_t)(k1 - k0) * 8);
+    SN_CK(cudaMemsetAsync(pool, 0, (size_t)std::max<int64_t>(off, 1) * 8, st));
+    for (int L = 0; L < s.n_levels; ++L) {
+      std::vector<int32_t> list;
+      for (int k = k0; k < k1; ++k)
+        if (s.sn_level[k] == L) list.push_back(k);
+      if (list.empty()) continue;
+      const int nl = (int)list.size();
+      h2d(d_list, list.data(), nl * 4);
+      launch_front_asm(d_list, nl, nm, d_val, st);
+      for (int rank = 0; rank < s.max_children; ++rank) {
+        std::vector<int32_t> cl;
+        for (int k = k0; k < k1; ++k)
+          if (s.sn_parent[k] >= 0 && s.sn_child_rank[k] == rank && s.sn_level[s.sn_parent[k]] == L)
+            cl.push_back(k);
+        if (cl.empty()) continue;
+        int32_t* dcl = d_clist + (size_t)rank * max_list;
+        h2d(dcl, cl.data(), cl.size() * 4);
+        launch_front_ext(dcl, (int)cl.size(), nm, st);
+      }
+      // F_SS^-1 by the packed-tile sweep (SPD, no pivoting)
+      std::vector<int32_t> nb(nl), nd(nl), tile_s, tile_ij, row_s, row_k;
+      std::vector<int64_t> tile_base(nl), row_base(nl);
+      int64_t nt = 0, nr = 0;
+      int maxnb = 0, maxw = 0;
+      for (int i = 0; i < nl; ++i) {
+        nd[i] = s.sn_w[list[i]];
+        nb[i] = (nd[i] + TB - 1) / TB;
+        maxnb = std::max(maxnb, nb[i]);
+        maxw = std::max(maxw, nd[i]);
+        tile_base[i] = nt;
+        row_base[i] = nr;
+        for (int I = 0; I < nb[i]; ++I) {
+          row_s.push_back(i);
+          row_k.push_back(I);
+          for (int J = 0; J <= I; ++J) {
+            tile_s.push_back(i);
+            tile_ij.push_back((I << 16) | J);
+          }
+        }
+        nt += (int64_t)nb[i] * (nb[i] + 1) / 2;
+        nr += nb[i];
+      }
+      h2d(d_nb, nb.data(), nl * 4);
+      h2d(d_ndof, nd.data(), nl * 4);
+      h2d(d_tile_base, tile_base.data(), nl * 8);
+      h2d(d_row_base, row_base.data(), nl * 8);
+      h2d(d_tile_s, tile_s.data(), tile_s.size() * 4);
+      h2d(d_tile_ij, tile_ij.data(), tile_ij.size() * 4);
+      h2d(d_row_s, row_s.data(), row_s.size() * 4);
+      h2d(d_row_k, row_k.data(), row_k.size() * 4);
+      lb.nsub = nl;
+      lb.max_nb = maxnb;
+      lb.ntiles = nt;
+      lb.nrows = nr;
+      lb.nb = d_nb;
+      lb.ndof = d_ndof;
+      lb.tile_base = d_tile_base;
+      lb.row_base = d_row_base;
+      lb.tile_s = d_tile_s;
+      lb.tile_ij = d_tile_ij;
+      lb.row_s = d_row_s;
+      lb.row_k = d_row_k;
+      int32_t big = INT_MAX;
+      h2d(lb.err, &big, 4);
+      launch_front_to_tiles(lb, d_list, nm, st);
+      launch_pad_identity(lb, st);
+      launch_sweep_invert(lb, st);
+      launch_tiles_to_finv(lb, d_list, nl, maxw, nm, B.factor, st);
+      SN_CK(cudaGetLastError());
+      int32_t bad = INT_MAX;
+      SN_CK(cudaMemcpyAsync(&bad, lb.err, 4, cudaMemcpyDeviceToHost, st));
+      SN_CK(cudaStreamSynchronize(st));
+      if (bad != INT_MAX)
+        throw SnError{-4, "non-positive pivot in the supernodal factor of local subdomain",
+                      s.sn_sub[list[bad]]};
+      // W = F_RS F_SS^-1 ; F_RR -= W F_RS^T
+      for (int phase = 0; phase < 2; ++phase) {
+        std::vector<GemmProb> probs;
+        std::vector<int32_t> work;
+        for (int i = 0; i < nl; ++i) {
+          const int k = list[i];
+          const int w = s.sn_w[k], r = s.sn_r[k], h = w + r;
+          if (r == 0) continue;
+          double* F = pool + front_off[k];
+          double* W = B.factor + s.sn_foff[k] + sn_rows_doubles(r);
+          const double* Fi = W + (int64_t)s.sn_ldw[k] * w;
+          GemmProb g;
+          if (phase == 0) {
+            g = GemmProb{F + w, Fi, W, r, w, w, h, s.sn_ldf[k], s.sn_ldw[k], 1.0, 0.0, 0, 0};
+          } else {
+            g = GemmProb{W, F + w, F + w + (int64_t)w * h, r, r, w, s.sn_ldw[k], h, h, -1.0, 1.0, 1, 0};
+          }
+          const int p = (int)probs.size();
+          probs.push_back(g);
+          for (int ti = 0; ti < (g.m + 63) / 64; ++ti)
+            for (int tj = 0; tj < (g.n + 63) / 64; ++tj) {
+              work.push_back(p);
+              work.push_back(ti);
+              work.push_back(tj);
+            }
+        }
+        if (probs.empty()) continue;
+        h2d(d_probs, probs.data(), probs.size() * sizeof(GemmProb));
+        h2d(d_work, work.data(), work.size() * 4);
+        launch_gemm_batched(d_probs, d_work, (int)(work.size() / 3), st);
+        SN_CK(cudaGetLastError());
+      }
+    }
+  }
+  SN_CK(cudaStreamSynchronize(st));
+}
+
+// shape vectors B_g = -A_g^-1 R_g (eq:col_pk) through the supernodal factor
+void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
+                      const std::vector<int32_t>& kcols, const int64_t* d_b_off,
+                      const int32_t* d_ld, const double* R, double* Bout) {
+  int nrhs = 4;
+  while (nrhs > 1 && sn_solve_stages(B.sym.max_n, nrhs) < 2) nrhs /= 2;
+  SnWork wk;
+  sn_build_work(B, A, st, nsm, nrhs, &kcols, wk);
+  SnIO io;
+  io.mode = 1;
+  io.in = R;
+  io.out = Bout;
+  io.bmap = B.d_lidx;
+  io.b_off = d_b_off;
+  io.ld = d_ld;
+  launch_sn_solve(B.dev, io, wk, nrhs, B.sym.max_n, st);
+  SN_CK(cudaGetLastError());
+}
+
+}  // namespace hplmm

@@ -1,0 +1,55 @@
+// Host-side management of a batch of supernodal local factors (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "supernodal.h"
+#include "supernodal_dev.cuh"
+
+namespace hplmm {
+
+struct SnError {
+  int status;          // hplmm_status value
+  std::string msg;
+  int sub = -1;        // failing subdomain (singular local factor)
+};
+
+// device allocator of the owning handle (setup_only buffers are freed at the
+// end of hplmm_setup)
+struct DevAlloc {
+  virtual void* alloc(size_t bytes, bool setup_only) = 0;
+  virtual ~DevAlloc() = default;
+};
+
+struct SnBatch {
+  SnSymbolic sym;
+  SnDev dev;
+  SnWork work;                 // one CTA per SM, LPT over subdomains (apply)
+  double* factor = nullptr;
+  double* yloc = nullptr;      // solution in local (elimination) order, [n_loc]
+  int64_t n_loc = 0;
+  int64_t solve_bytes = 0;     // factor bytes streamed by one batch solve
+  int32_t *d_sub_n = nullptr, *d_gmap = nullptr, *d_lidx = nullptr, *d_sn_w = nullptr,
+          *d_sn_r = nullptr, *d_sn_p0 = nullptr, *d_sn_ldw = nullptr, *d_sn_ldf = nullptr,
+          *d_rows = nullptr;
+  int64_t *d_sub_base = nullptr, *d_sub_fc0 = nullptr, *d_sub_fc1 = nullptr,
+          *d_sub_bc0 = nullptr, *d_sub_bc1 = nullptr, *d_sn_rows_off = nullptr;
+};
+
+void sn_upload(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm);
+void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nrhs,
+                   const std::vector<int32_t>* ncols, SnWork& wk);
+// numeric factorisation; throws SnError (status -4 + subdomain) on a
+// non-positive pivot.  pool_budget: bytes of frontal matrices per wave.
+void sn_factor(SnBatch& B, const double* d_val, DevAlloc& A, cudaStream_t st,
+               int64_t pool_budget);
+// yloc = A_s^-1 in[gmap] for every subdomain of the batch
+void sn_apply(const SnBatch& B, const double* in, cudaStream_t st);
+// B_g[:, 0:k_g] = -A_g^-1 R_g[:, 0:k_g] (grain batch, gb row layout)
+void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
+                      const std::vector<int32_t>& kcols, const int64_t* d_b_off,
+                      const int32_t* d_ld, const double* R, double* Bout);
+
+}  // namespace hplmm

@@ -1,0 +1,583 @@
+// Batched supernodal block-LDL^T local factors (sm_100a, fp64): numeric
+// multifrontal factorisation (setup, T_ML) and the TMA-streamed solve that
+// applies every grain / contact-grid inverse in the hot path (eq:Mg_Mz).
+// See supernodal.h for the algebra and the layout.
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+
+#include "kernels.cuh"
+#include "supernodal.h"
+#include "supernodal_dev.cuh"
+#include "tma.cuh"
+
+namespace hplmm {
+
+// ===========================================================================
+// Solve: one persistent CTA per SM walks its list of (subdomain, RHS column
+// chunk) items.  The subdomain's right-hand side lives in shared memory
+// (x[p*NRHS + c], p = elimination position); the factor streams through a
+// ring of 32-KiB stages filled by 1-D TMA bulk copies issued by one producer
+// lane, following the static chunk schedule (forward then backward chunks of
+// each item).  All SN_CONS consumer warps take part in every chunk:
+//   W fwd  : acc_i += W[i,j] x_S[j]  (thread per row i; col-major => conflict
+//            free), at the end of the part x_R[i] -= acc_i
+//   F fwd  : acc_i += Finv[i,j] x_S[j], at the end x_S = acc (two barriers)
+//   W bwd  : warp per column j: x_S[j] -= sum_i W[i,j] x_R[i]
+// A stage is released (empty mbarrier, count SN_CONS) as soon as every warp
+// has read it; the producer runs ahead across supernode and item boundaries.
+// ===========================================================================
+constexpr int SN_CONS = 16;
+constexpr int SN_NT = 32 * SN_CONS;
+constexpr int SN_MAXQ = SN_MAX_WR / (2 * SN_NT);   // double2 row pairs per thread (2)
+constexpr int SN_MAXST = 8;
+static_assert(SN_MAXQ * 2 * SN_NT >= SN_MAX_WR, "row coverage");
+
+__device__ __forceinline__ void cons_sync() {
+  asm volatile("bar.sync 1, %0;" ::"r"(SN_NT) : "memory");
+}
+
+// Row-parallel layout of a part with h rows: row pairs are spread over TG
+// threads (a power of two >= 32), the SN_NT consumer threads form G = SN_NT/TG
+// groups and group g takes the chunk columns jj == g (mod G), so every chunk
+// keeps all consumer warps busy whatever the aspect ratio of the panel.
+struct RowLayout {
+  int TG, G, g, t;
+  // lgc = log2(TG) - 5, precomputed on the host per part (chunk descriptor)
+  __device__ __forceinline__ RowLayout(int lgc, int tid) {
+    const int lg = lgc + 5;
+    TG = 1 << lg;
+    G = SN_NT >> lg;
+    g = tid >> lg;
+    t = tid & (TG - 1);
+  }
+};
+static_assert(SN_NT == 512, "RowLayout codes assume TG <= 512");
+
+// acc[q][e][c] += sum over this group's chunk columns of col[2(t + q TG) + e] * x_S
+template <int NQ, int NRHS>
+__device__ __forceinline__ void sn_rows(const double* __restrict__ st, int ld, int nc, int h,
+                                        const double* __restrict__ xcol, const RowLayout& L,
+                                        double (&acc)[SN_MAXQ][2][NRHS]) {
+  for (int jj = L.g; jj < nc; jj += L.G) {
+    double xa[NRHS];
+#pragma unroll
+    for (int c = 0; c < NRHS; ++c) xa[c] = xcol[jj * NRHS + c];
+    const double* ca = st + (size_t)jj * ld;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = 2 * (L.t + q * L.TG);
+      if (i < h) {
+        const double2 a = *reinterpret_cast<const double2*>(ca + i);
+#pragma unroll
+        for (int c = 0; c < NRHS; ++c) {
+          acc[q][0][c] = fma(a.x, xa[c], acc[q][0][c]);
+          acc[q][1][c] = fma(a.y, xa[c], acc[q][1][c]);
+        }
+      }
+    }
+  }
+}
+
+// group partials -> group 0 (fixed order g = 0..G-1), through smem scratch
+template <int NRHS>
+__device__ __forceinline__ void sn_group_reduce(const RowLayout& L, int h, double* scratch,
+                                                double (&acc)[SN_MAXQ][2][NRHS]) {
+  // scratch[(g * 2 TG * SN_MAXQ + row) * NRHS + c], row = 2(t + q TG) + e
+  const int stride = 2 * L.TG * SN_MAXQ;
+  if (L.g > 0) {
+#pragma unroll
+    for (int q = 0; q < SN_MAXQ; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = 2 * (L.t + q * L.TG) + e;
+        if (i < h)
+#pragma unroll
+          for (int c = 0; c < NRHS; ++c) scratch[((size_t)L.g * stride + i) * NRHS + c] = acc[q][e][c];
+      }
+  }
+  cons_sync();
+  if (L.g == 0) {
+    for (int gg = 1; gg < L.G; ++gg)
+#pragma unroll
+      for (int q = 0; q < SN_MAXQ; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 2 * (L.t + q * L.TG) + e;
+          if (i < h)
+#pragma unroll
+            for (int c = 0; c < NRHS; ++c) acc[q][e][c] += scratch[((size_t)gg * stride + i) * NRHS + c];
+        }
+  }
+}
+
+template <int NRHS>
+__global__ void __launch_bounds__(32 * (SN_CONS + 1), 1)
+    k_sn_solve(SnDev d, SnIO io, SnWork wk, int stages, int max_n) {
+  extern __shared__ __align__(128) unsigned char sn_smem[];
+  __shared__ __align__(8) uint64_t full[SN_MAXST], empty[SN_MAXST];
+  double* ring = reinterpret_cast<double*>(sn_smem);
+  double* x = ring + (size_t)stages * SN_CHUNK_DOUBLES;
+  // x_R of the current backward part; scratch of the forward group reductions
+  double* xr = x + (size_t)((max_n + 1) & ~1) * NRHS;   // 16-byte aligned
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k0 = wk.chunk_ptr[blockIdx.x], k1 = wk.chunk_ptr[blockIdx.x + 1];
+  const SnChunk* __restrict__ ch = wk.chunks;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], SN_CONS);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == SN_CONS) {
+    // producer warp: lanes prefetch 32 chunk descriptors, lane 0 issues
+    const uint64_t pol = policy_evict_first();
+    int s = 0;
+    uint32_t ph = 0;
+    int64_t k = 0;
+    for (int64_t kb = k0; kb < k1; kb += 32) {
+      int64_t off = 0;
+      int bytes = 0;
+      if (kb + lane < k1) {
+        off = ch[kb + lane].off;
+        bytes = ch[kb + lane].bytes & 0xffffff;
+      }
+      const int cnt = (int)min((int64_t)32, k1 - kb);
+      for (int j = 0; j < cnt; ++j, ++k) {
+        const int64_t o = __shfl_sync(0xffffffffu, off, j);
+        const int b = __shfl_sync(0xffffffffu, bytes, j);
+        if (lane == 0) {
+          if (k >= stages) mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], (uint32_t)b);
+          bulk_g2s_hint(ring + (size_t)s * SN_CHUNK_DOUBLES, d.factor + o, (uint32_t)b, &full[s],
+                        pol);
+        }
+        if (++s == stages) { s = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+  const int tid = threadIdx.x;
+  double acc[SN_MAXQ][2][NRHS];
+  int item = wk.item_ptr[blockIdx.x] - 1;
+  int n = 0, rc0 = 0, sub = 0;
+  int64_t base = 0;
+  int s = 0;
+  uint32_t ph = 0;
+  // descriptor of the next chunk is loaded one chunk ahead
+  int4 dn0 = make_int4(0, 0, 0, 0), dn1 = make_int4(0, 0, 0, 0);
+  if (k0 < k1) {
+    dn0 = __ldg(reinterpret_cast<const int4*>(ch + k0));
+    dn1 = __ldg(reinterpret_cast<const int4*>(ch + k0) + 1);
+  }
+  for (int64_t kk = k0; kk < k1; ++kk) {
+    // SnChunk = {off (2 ints), bytes, info | p0, w, r, sub}
+    const int info = dn0.w, p0 = dn1.x, w = dn1.y, r = dn1.z, csub = dn1.w;
+    const int lgc = (dn0.z >> 24) & 15;
+    if (kk + 1 < k1) {
+      dn0 = __ldg(reinterpret_cast<const int4*>(ch + kk + 1));
+      dn1 = __ldg(reinterpret_cast<const int4*>(ch + kk + 1) + 1);
+    }
+    const int cc0 = info & 0xfff, nc = ((info >> 12) & 0xfff) + 1, kind = (info >> 24) & 7;
+    const bool last = info & SN_INFO_LAST;
+    if (info & SN_INFO_FIRST_ITEM) {
+      // ---- gather the right-hand side (4 independent loads per thread in flight)
+      ++item;
+      sub = csub;
+      n = d.sub_n[sub];
+      base = d.sub_base[sub];
+      rc0 = wk.item_c0[item];
+      if (io.mode == 0) {
+        for (int q0 = tid; q0 < n; q0 += 4 * SN_NT) {
+          double v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int p = q0 + u * SN_NT;
+            v[u] = p < n ? io.in[__ldg(d.gmap + base + p)] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (q0 + u * SN_NT < n) x[q0 + u * SN_NT] = v[u];
+        }
+      } else {
+        const int L = io.ld[sub];
+        const int ncr = min(NRHS, L - 1 - rc0);
+        const double* R = io.in + io.b_off[sub];
+        for (int p = tid; p < n; p += SN_NT) {
+          const int64_t row = (int64_t)io.bmap[base + p] * L + rc0;
+#pragma unroll
+          for (int c = 0; c < NRHS; ++c) x[p * NRHS + c] = c < ncr ? R[row + c] : 0.0;
+        }
+      }
+      cons_sync();
+    }
+    mbar_wait_sleep(&full[s], ph);
+    const double* st = ring + (size_t)s * SN_CHUNK_DOUBLES;
+    const int cs = s;
+    if (++s == stages) { s = 0; ph ^= 1; }
+    if (kind == SN_W_FWD || kind == SN_F_FWD) {
+      const int h = kind == SN_W_FWD ? r : w;
+      const int ld = h + (h & 1);
+      const RowLayout L(lgc, tid);
+      if (cc0 == 0) {
+#pragma unroll
+        for (int q = 0; q < SN_MAXQ; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int cr = 0; cr < NRHS; ++cr) acc[q][e][cr] = 0.0;
+      }
+      const double* xcol = x + (size_t)(p0 + cc0) * NRHS;
+      if (2 * L.TG >= h) sn_rows<1, NRHS>(st, ld, nc, h, xcol, L, acc);
+      else sn_rows<2, NRHS>(st, ld, nc, h, xcol, L, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);
+      if (last) {
+        if (L.G > 1) sn_group_reduce<NRHS>(L, h, xr, acc);
+        if (kind == SN_W_FWD) {
+          if (L.G > 1) cons_sync();   // scratch is reused by the F part
+        } else {
+          if (L.G == 1) cons_sync();  // every thread is done reading x_S
+          if (L.g == 0) {
+#pragma unroll
+            for (int q = 0; q < SN_MAXQ; ++q)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int i = 2 * (L.t + q * L.TG) + e;
+                if (i < w) {
+#pragma unroll
+                  for (int cr = 0; cr < NRHS; ++cr) x[(p0 + i) * NRHS + cr] = acc[q][e][cr];
+                }
+              }
+          }
+          cons_sync();
+        }
+      }
+    } else if (kind == SN_ROWS_FWD) {
+      // x_R -= W_S x_S (summed over the W part by group 0; rows are distinct)
+      const RowLayout L(lgc, tid);
+      const int32_t* rows = reinterpret_cast<const int32_t*>(st);
+      if (L.g == 0) {
+#pragma unroll
+        for (int q = 0; q < SN_MAXQ; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = 2 * (L.t + q * L.TG) + e;
+            if (i < r) {
+              const int pr = rows[i];
+#pragma unroll
+              for (int cr = 0; cr < NRHS; ++cr) x[pr * NRHS + cr] -= acc[q][e][cr];
+            }
+          }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);
+    } else if (kind == SN_ROWS_BWD) {
+      // stage x_R contiguously (read by every column of the W part)
+      const int32_t* rows = reinterpret_cast<const int32_t*>(st);
+      for (int i = tid; i < r; i += SN_NT) {
+        const int pr = rows[i];
+#pragma unroll
+        for (int cr = 0; cr < NRHS; ++cr) xr[i * NRHS + cr] = x[pr * NRHS + cr];
+      }
+      if ((r & 1) && tid < NRHS) xr[r * NRHS + tid] = 0.0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);
+      cons_sync();
+    } else {  // SN_W_BWD: x_S[j] -= W[:,j] . x_R, LPC lanes per column
+      const int ld = r + (r & 1);
+      const int lpc = r > 256 ? 32 : (r > 128 ? 16 : 8);
+      const int cpw = 32 / lpc;                    // columns per warp pass
+      const int sl = lane & (lpc - 1), cl = lane / lpc;
+      for (int j0 = warp * cpw; j0 < nc; j0 += SN_CONS * cpw) {
+        const int jj = j0 + cl;
+        double sum[NRHS];
+#pragma unroll
+        for (int cr = 0; cr < NRHS; ++cr) sum[cr] = 0.0;
+        if (jj < nc) {
+          const double* col = st + (size_t)jj * ld;
+          for (int i = 2 * sl; i < r; i += 2 * lpc) {
+            const double2 a = *reinterpret_cast<const double2*>(col + i);
+            if (NRHS == 1) {
+              const double2 xv = *reinterpret_cast<const double2*>(xr + i);
+              sum[0] = fma(a.x, xv.x, fma(a.y, xv.y, sum[0]));
+            } else {
+#pragma unroll
+              for (int cr = 0; cr < NRHS; ++cr)
+                sum[cr] = fma(a.x, xr[i * NRHS + cr], fma(a.y, xr[(i + 1) * NRHS + cr], sum[cr]));
+            }
+          }
+        }
+#pragma unroll
+        for (int cr = 0; cr < NRHS; ++cr) {
+          for (int o = lpc >> 1; o > 0; o >>= 1) sum[cr] += __shfl_xor_sync(0xffffffffu, sum[cr], o);
+        }
+        if (jj < nc && sl < NRHS) {
+          double v = sum[0];
+#pragma unroll
+          for (int cr = 1; cr < NRHS; ++cr)
+            if (sl == cr) v = sum[cr];
+          x[(p0 + cc0 + jj) * NRHS + sl] -= v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);
+      if (last) cons_sync();
+    }
+    if (info & SN_INFO_LAST_ITEM) {
+      cons_sync();
+      // ---- write the solution
+      if (io.mode == 0) {
+        for (int p = tid; p < n; p += SN_NT) io.out[base + p] = x[p];
+      } else {
+        const int L = io.ld[sub];
+        const int ncr = min(NRHS, L - 1 - rc0);
+        double* B = io.out + io.b_off[sub];
+        for (int p = tid; p < n; p += SN_NT) {
+          const int64_t row = (int64_t)io.bmap[base + p] * L + rc0;
+#pragma unroll
+          for (int c = 0; c < NRHS; ++c)
+            if (c < ncr) B[row + c] = -x[p * NRHS + c];
+        }
+      }
+      cons_sync();
+    }
+  }
+}
+
+int sn_solve_stages(int max_n, int nrhs) {
+  const int avail = 226 * 1024 - (max_n + SN_MAX_WR + 4) * nrhs * 8;
+  return std::min(SN_MAXST, avail / (SN_CHUNK_DOUBLES * 8));
+}
+
+template <int NRHS>
+static void sn_solve_launch(const SnDev& d, const SnIO& io, const SnWork& wk, int stages,
+                            int max_n, size_t smem, cudaStream_t st) {
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_sn_solve<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  k_sn_solve<NRHS><<<wk.nblocks, 32 * (SN_CONS + 1), smem, st>>>(d, io, wk, stages, max_n);
+}
+
+void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
+                     cudaStream_t st) {
+  if (wk.nblocks <= 0) return;
+  const int stages = sn_solve_stages(max_n, nrhs);
+  const size_t smem =
+      (size_t)stages * SN_CHUNK_DOUBLES * 8 + (size_t)(max_n + SN_MAX_WR + 4) * nrhs * 8;
+  if (nrhs == 1) sn_solve_launch<1>(d, io, wk, stages, max_n, smem, st);
+  else if (nrhs == 2) sn_solve_launch<2>(d, io, wk, stages, max_n, smem, st);
+  else sn_solve_launch<4>(d, io, wk, stages, max_n, smem, st);
+}
+
+// grain-batch layout views of a supernodal grain solve (for the per-RHS
+// correction columns, eq:col_cg): xloc = b[lmap], yloc = y_sn[gpos_sn[lmap]]
+__global__ void k_sn_to_batch(int64_t nloc, const int32_t* __restrict__ lmap,
+                              const int32_t* __restrict__ gpos_sn, const double* __restrict__ b,
+                              const double* __restrict__ ysn, double* __restrict__ xloc,
+                              double* __restrict__ yloc) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nloc) return;
+  const int d = lmap[i];
+  xloc[i] = d >= 0 ? b[d] : 0.0;
+  yloc[i] = d >= 0 ? ysn[gpos_sn[d]] : 0.0;
+}
+
+void launch_sn_to_batch(int64_t nloc, const int32_t* lmap, const int32_t* gpos_sn, const double* b,
+                        const double* ysn, double* xloc, double* yloc, cudaStream_t st) {
+  if (nloc <= 0) return;
+  k_sn_to_batch<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(nloc, lmap, gpos_sn, b, ysn, xloc,
+                                                                 yloc);
+}
+
+// ===========================================================================
+// Numeric factorisation (multifrontal, level by level over the batch)
+// ===========================================================================
+// F (h x h col-major, zeroed) <- A^ blocks with a column node in S
+__global__ void k_front_asm(const int32_t* __restrict__ list, int nlist, const int64_t* asm_ptr,
+                            const int64_t* asm_e, const int32_t* asm_u, const int32_t* asm_v,
+                            const int32_t* sn_w, const int32_t* sn_r, const int64_t* front_off,
+                            const double* __restrict__ val, double* __restrict__ pool) {
+  const int sn = list[blockIdx.x];
+  const int h = sn_w[sn] + sn_r[sn];
+  double* F = pool + front_off[sn];
+  for (int64_t t = asm_ptr[sn] + threadIdx.x; t < asm_ptr[sn + 1]; t += blockDim.x) {
+    const int64_t e = asm_e[t];
+    const int fu = asm_u[t], fv = asm_v[t];
+    const double* blk = val + 9 * e;   // A[v][u] (row node v in S, column node u)
+    if (fu == fv) {
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) F[(3 * fu + i) + (int64_t)(3 * fv + j) * h] = blk[3 * i + j];
+    } else {
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+          const double a = blk[3 * j + i];   // A[u][v](i,j) = A[v][u](j,i)
+          F[(3 * fu + i) + (int64_t)(3 * fv + j) * h] = a;
+          F[(3 * fv + j) + (int64_t)(3 * fu + i) * h] = a;
+        }
+    }
+  }
+}
+
+// parent front += U_child (extend-add through the child's relative indices)
+__global__ void k_front_ext(const int32_t* __restrict__ list, const int32_t* sn_w,
+                            const int32_t* sn_r, const int32_t* sn_parent, const int64_t* rel_off,
+                            const int32_t* rel, const int64_t* front_off, double* pool) {
+  const int c = list[blockIdx.x];
+  const int wc = sn_w[c], rc = sn_r[c], hc = wc + rc;
+  const int par = sn_parent[c];
+  const int hp = sn_w[par] + sn_r[par];
+  const double* Fc = pool + front_off[c];
+  double* Fp = pool + front_off[par];
+  const int32_t* rl = rel + rel_off[c];
+  const int64_t tot = (int64_t)rc * rc;
+  for (int64_t t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int i = (int)(t % rc), j = (int)(t / rc);
+    const int pi = 3 * rl[i / 3] + i % 3, pj = 3 * rl[j / 3] + j % 3;
+    Fp[pi + (int64_t)pj * hp] += Fc[(wc + i) + (int64_t)(wc + j) * hc];
+  }
+}
+
+// F_SS -> packed 64-tiles of the level batch (lower tiles, col-major)
+__global__ void k_front_to_tiles(int64_t ntiles, const int32_t* __restrict__ tile_s,
+                                 const int32_t* __restrict__ tile_ij,
+                                 const int32_t* __restrict__ list, const int32_t* sn_w,
+                                 const int32_t* sn_r, const int64_t* front_off,
+                                 const double* __restrict__ pool, double* __restrict__ tiles) {
+  const int64_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  const int ls = tile_s[t], ij = tile_ij[t];
+  const int I = ij >> 16, J = ij & 0xffff;
+  const int sn = list[ls];
+  const int w = sn_w[sn], h = w + sn_r[sn];
+  const double* F = pool + front_off[sn];
+  double* T = tiles + t * TILE;
+  for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+    const int a = e & 63, b = e >> 6;
+    const int i = TB * I + a, j = TB * J + b;
+    T[e] = (i < w && j < w) ? F[i + (int64_t)j * h] : 0.0;
+  }
+}
+
+// inverse tiles -> Finv (w x w col-major, ld ldf) in the factor storage
+__global__ void k_tiles_to_finv(int nlist, const int32_t* __restrict__ list,
+                                const int64_t* __restrict__ tile_base, const int32_t* __restrict__ nb,
+                                const int32_t* sn_w, const int32_t* sn_r, const int32_t* sn_ldw,
+                                const int32_t* sn_ldf, const int64_t* sn_foff,
+                                const double* __restrict__ tiles, double* __restrict__ factor) {
+  const int ls = blockIdx.y;
+  const int sn = list[ls];
+  const int w = sn_w[sn], ldf = sn_ldf[sn];
+  double* Fi = factor + sn_foff[sn] + sn_rows_doubles(sn_r[sn]) + (int64_t)sn_ldw[sn] * w;
+  const int64_t tot = (int64_t)w * w;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % w), j = (int)(t / w);
+    const int ii = i >= j ? i : j, jj = i >= j ? j : i;
+    const int I = ii / TB, J = jj / TB;
+    const int64_t tix = tile_base[ls] + (int64_t)I * (I + 1) / 2 + J;
+    Fi[i + (int64_t)j * ldf] = tiles[tix * TILE + (ii % TB) + TB * (jj % TB)];
+  }
+}
+
+// Batched FP64 GEMM  C = alpha A op(B) + beta C  (col-major), 64x64 output
+// tiles, BK = 16 through shared memory, 4x4 outputs per thread.
+__global__ void __launch_bounds__(256) k_gemm_batched(const GemmProb* __restrict__ probs,
+                                                      const int32_t* __restrict__ work) {
+  const int p = work[3 * blockIdx.x], ti = work[3 * blockIdx.x + 1], tj = work[3 * blockIdx.x + 2];
+  const GemmProb g = probs[p];
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = ti * 64, j0 = tj * 64;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < g.k; k0 += 16) {
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+      const int r = e & 63, kk = e >> 6;
+      const int gi = i0 + r, gk = k0 + kk;
+      As[kk][r] = (gi < g.m && gk < g.k) ? g.A[gi + (int64_t)gk * g.lda] : 0.0;
+      const int gj = j0 + r;
+      double bv = 0.0;
+      if (gj < g.n && gk < g.k) bv = g.transB ? g.B[gj + (int64_t)gk * g.ldb] : g.B[gk + (int64_t)gj * g.ldb];
+      Bs[kk][r] = bv;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = As[kk][tx + 16 * q];
+        b[q] = Bs[kk][ty + 16 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[q][u] = fma(a[q], b[u], acc[q][u]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int gi = i0 + tx + 16 * q, gj = j0 + ty + 16 * u;
+      if (gi < g.m && gj < g.n) {
+        double* c = g.C + gi + (int64_t)gj * g.ldc;
+        *c = g.beta == 0.0 ? g.alpha * acc[q][u] : fma(g.alpha, acc[q][u], g.beta * *c);
+      }
+    }
+}
+
+void launch_front_asm(const int32_t* list, int nlist, const SnNum& nm, const double* val,
+                      cudaStream_t st) {
+  if (nlist <= 0) return;
+  k_front_asm<<<nlist, 128, 0, st>>>(list, nlist, nm.asm_ptr, nm.asm_e, nm.asm_u, nm.asm_v,
+                                     nm.sn_w, nm.sn_r, nm.front_off, val, nm.pool);
+}
+void launch_front_ext(const int32_t* list, int nlist, const SnNum& nm, cudaStream_t st) {
+  if (nlist <= 0) return;
+  k_front_ext<<<nlist, 256, 0, st>>>(list, nm.sn_w, nm.sn_r, nm.sn_parent, nm.rel_off, nm.rel,
+                                     nm.front_off, nm.pool);
+}
+void launch_front_to_tiles(const DevBatch& b, const int32_t* list, const SnNum& nm,
+                           cudaStream_t st) {
+  if (b.ntiles <= 0) return;
+  k_front_to_tiles<<<(unsigned)b.ntiles, 256, 0, st>>>(b.ntiles, b.tile_s, b.tile_ij, list,
+                                                       nm.sn_w, nm.sn_r, nm.front_off, nm.pool,
+                                                       b.tiles);
+}
+void launch_tiles_to_finv(const DevBatch& b, const int32_t* list, int nlist, int max_w,
+                          const SnNum& nm, double* factor, cudaStream_t st) {
+  if (nlist <= 0) return;
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)max_w * max_w + 255) / 256)),
+            (unsigned)nlist);
+  k_tiles_to_finv<<<grid, 256, 0, st>>>(nlist, list, b.tile_base, b.nb, nm.sn_w, nm.sn_r,
+                                        nm.sn_ldw, nm.sn_ldf, nm.sn_foff, b.tiles, factor);
+}
+__global__ void k_rows_to_factor(int nsn, const int32_t* sn_r, const int64_t* sn_foff,
+                                 const int64_t* rows_off, const int32_t* rows, double* factor) {
+  const int sn = blockIdx.x;
+  if (sn >= nsn) return;
+  const int r = sn_r[sn];
+  int32_t* dst = reinterpret_cast<int32_t*>(factor + sn_foff[sn]);
+  const int rp = (int)(2 * sn_rows_doubles(r));
+  for (int i = threadIdx.x; i < rp; i += blockDim.x) dst[i] = i < r ? rows[rows_off[sn] + i] : 0;
+}
+
+void launch_rows_to_factor(int nsn, const SnNum& nm, double* factor, cudaStream_t st) {
+  if (nsn <= 0) return;
+  k_rows_to_factor<<<nsn, 128, 0, st>>>(nsn, nm.sn_r, nm.sn_foff, nm.rows_off, nm.rows, factor);
+}
+
+void launch_gemm_batched(const GemmProb* probs, const int32_t* work, int nwork, cudaStream_t st) {
+  if (nwork <= 0) return;
+  k_gemm_batched<<<nwork, 256, 0, st>>>(probs, work);
+}
+
+}  // namespace hplmm

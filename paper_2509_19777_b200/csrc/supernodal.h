@@ -1,0 +1,93 @@
+// Batched supernodal block-LDL^T factors of the local subdomain matrices
+// (grain blocks A^{g}_{g} and contact-grid blocks A^[zeta,zeta], eq:Mg_Mz /
+// eq:permute_blk_2) -- SURVEY §8(f) NEXT #1.  Internal (not part of the ABI).
+//
+// Ordering: geometric nested dissection of each subdomain's node set on the
+// voxel lattice (a plane of nodes separates the two halves because A^ couples
+// only nodes within Chebyshev distance 1).  Every ND tree node (leaf set or
+// separator plane) is one supernode S with w = 3|S| columns; its row structure
+// R = struct(S) (r = 3|R| rows) follows from the node graph by the usual
+// symbolic elimination.  Elimination of S from its frontal matrix
+//     F = [F_SS F_SR; F_RS F_RR]
+// gives (block LDL^T with SPD diagonal blocks)
+//     W_S = F_RS F_SS^-1,   U_S = F_RR - W_S F_RS^T  (passed to the parent),
+// and a solve A_s x = b is
+//     forward  (postorder):         b_R -= W_S b_S ;  b_S <- F_SS^-1 b_S
+//     backward (reverse postorder): x_S -= W_S^T x_R
+// so the factor is W_S (r x w) and F_SS^-1 (w x w), both col-major, each read
+// once per sweep that needs it (2 r w + w^2 doubles per supernode and solve).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "hplmm_internal.h"
+
+namespace hplmm {
+
+constexpr int SN_CHUNK_DOUBLES = 4096;   // 32 KiB TMA chunk
+constexpr int SN_MAX_WR = 2048;          // max w and max r (DOFs) per supernode
+
+// chunk kinds of the solve stream (forward per S: W_FWD.., ROWS_FWD, F_FWD..;
+// backward per S: ROWS_BWD, W_BWD..).  ROWS chunks carry the supernode's row
+// list (int32) so the scatter/gather of x_R never waits on a global load.
+enum SnChunkKind : int32_t {
+  SN_W_FWD = 0, SN_F_FWD = 1, SN_W_BWD = 2, SN_ROWS_FWD = 3, SN_ROWS_BWD = 4
+};
+
+// one TMA chunk of the solve stream, denormalised so that the consumer needs
+// exactly one (prefetched) descriptor load per chunk
+struct SnChunk {
+  int64_t off;     // first double of the chunk in the factor array
+  int32_t bytes;   // [0,24): bytes (multiple of 16); [24,28): log2(TG) - 5, the
+                   // row-pair thread-group size of the part (see k_sn_solve)
+  int32_t info;    // c0 [0,12) | (ncols-1) [12,24) | kind [24,27) | last-of-part [27]
+                   // | first-of-item [28] | last-of-item [29]
+  int32_t p0;      // first local DOF of S
+  int32_t w, r;    // supernode width / struct rows
+  int32_t sub;     // subdomain
+};
+constexpr int SN_INFO_LAST = 1 << 27, SN_INFO_FIRST_ITEM = 1 << 28, SN_INFO_LAST_ITEM = 1 << 29;
+
+// rows header of a supernode in the factor array: r int32 padded to 16 bytes
+#ifdef __CUDACC__
+#define SN_HD __host__ __device__
+#else
+#define SN_HD
+#endif
+SN_HD inline int64_t sn_rows_doubles(int r) { return (int64_t)((r + 3) / 4) * 2; }
+
+struct SnSymbolic {
+  int nsub = 0, nsn = 0;
+  int max_n = 0, max_w = 0, max_r = 0, n_levels = 0, max_children = 0;
+  // per subdomain
+  std::vector<int32_t> sub_n;              // DOFs
+  std::vector<int64_t> sub_base;           // offset of its local positions
+  std::vector<int32_t> sub_sn0, sub_sn1;   // supernode range (postorder)
+  std::vector<int64_t> sub_fc0, sub_fc1;   // forward chunk range
+  std::vector<int64_t> sub_bc0, sub_bc1;   // backward chunk range
+  std::vector<int64_t> sub_fbytes;         // factor bytes streamed by one solve
+  std::vector<int32_t> gmap;               // [sum n] global DOF of each local position
+  std::vector<int32_t> lidx;               // [sum n] DOF index in the subdomain's node list
+  // per supernode
+  std::vector<int32_t> sn_w, sn_r, sn_p0, sn_ldw, sn_ldf, sn_level, sn_parent, sn_sub,
+      sn_child_rank;
+  std::vector<int64_t> sn_rows_off, sn_foff;
+  std::vector<int32_t> rows;               // struct rows: local DOF positions (ascending)
+  std::vector<SnChunk> chunks;             // per subdomain: [fc0,fc1) forward, [bc0,bc1) backward
+  int64_t factor_doubles = 0;              // layout per S: [rows][W_S: ldw x w][F_SS^-1: ldf x w]
+  // numeric setup: A-blocks scattered into each front, child -> parent maps
+  std::vector<int64_t> asm_ptr;            // [nsn+1]
+  std::vector<int64_t> asm_e;              // BSR block index (row node v in S, col node u)
+  std::vector<int32_t> asm_u, asm_v;       // front node index of u (row) and v (col)
+  std::vector<int64_t> rel_off;            // [nsn+1] per supernode as a child
+  std::vector<int32_t> rel;                // front node index in the parent
+};
+
+// Symbolic analysis of the subdomains given as ascending node lists
+// (CSR ptr/nodes).  leaf = max nodes of an ND leaf.  Returns false + err on
+// a supernode wider than SN_MAX_WR.
+bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
+                const std::vector<int32_t>& nodes, int leaf, SnSymbolic& out, std::string& err);
+
+}  // namespace hplmm

@@ -1,0 +1,87 @@
+// Device-side views and launchers of the batched supernodal factors.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "supernodal.h"
+
+namespace hplmm {
+
+// read-only view of one factored batch (device pointers)
+struct SnDev {
+  const int32_t* sub_n = nullptr;
+  const int64_t* sub_base = nullptr;
+  const int64_t *sub_fc0 = nullptr, *sub_fc1 = nullptr, *sub_bc0 = nullptr, *sub_bc1 = nullptr;
+  const int32_t* gmap = nullptr;   // local position -> global DOF
+  const int32_t *sn_w = nullptr, *sn_r = nullptr, *sn_p0 = nullptr, *sn_ldw = nullptr,
+                *sn_ldf = nullptr;
+  const int64_t* sn_rows_off = nullptr;
+  const int32_t* rows = nullptr;
+  const double* factor = nullptr;
+};
+
+// mode 0: x = in[gmap], out[base+p] = x (one RHS)
+// mode 1: shape-vector columns of the grain batch: x[p][c] = in[b_off + bmap*L + c0 + c],
+//         out[same] = -x  (L = ld[sub], columns [0, L-1))
+struct SnIO {
+  int mode = 0;
+  const double* in = nullptr;
+  double* out = nullptr;
+  const int32_t* bmap = nullptr;
+  const int64_t* b_off = nullptr;
+  const int32_t* ld = nullptr;
+};
+
+// per-CTA work: items = (subdomain, first RHS column); the CTA's chunk
+// descriptors are materialised in traversal order (flags mark item bounds)
+struct SnWork {
+  int nblocks = 0;
+  const int32_t* item_ptr = nullptr;
+  const int32_t* item_sub = nullptr;
+  const int32_t* item_c0 = nullptr;
+  const int64_t* chunk_ptr = nullptr;   // [nblocks+1]
+  const SnChunk* chunks = nullptr;      // flat, per CTA contiguous
+};
+
+// numeric-factorisation view (device pointers)
+struct SnNum {
+  const int64_t *asm_ptr = nullptr, *asm_e = nullptr;
+  const int32_t *asm_u = nullptr, *asm_v = nullptr;
+  const int32_t *sn_w = nullptr, *sn_r = nullptr, *sn_parent = nullptr, *sn_ldw = nullptr,
+                *sn_ldf = nullptr;
+  const int64_t *sn_foff = nullptr, *rel_off = nullptr;
+  const int64_t* rows_off = nullptr;
+  const int32_t* rows = nullptr;
+  const int32_t* rel = nullptr;
+  const int64_t* front_off = nullptr;   // per supernode of the current wave
+  double* pool = nullptr;
+};
+
+struct GemmProb {
+  const double* A;
+  const double* B;
+  double* C;
+  int m, n, k, lda, ldb, ldc;
+  double alpha, beta;
+  int transB;
+  int pad;
+};
+
+int sn_solve_stages(int max_n, int nrhs);
+void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
+                     cudaStream_t st);
+void launch_front_asm(const int32_t* list, int nlist, const SnNum& nm, const double* val,
+                      cudaStream_t st);
+void launch_front_ext(const int32_t* list, int nlist, const SnNum& nm, cudaStream_t st);
+void launch_front_to_tiles(const DevBatch& b, const int32_t* list, const SnNum& nm,
+                           cudaStream_t st);
+void launch_tiles_to_finv(const DevBatch& b, const int32_t* list, int nlist, int max_w,
+                          const SnNum& nm, double* factor, cudaStream_t st);
+void launch_sn_to_batch(int64_t nloc, const int32_t* lmap, const int32_t* gpos_sn, const double* b,
+                        const double* ysn, double* xloc, double* yloc, cudaStream_t st);
+// rows headers of every supernode into the factor array
+void launch_rows_to_factor(int nsn, const SnNum& nm, double* factor, cudaStream_t st);
+void launch_gemm_batched(const GemmProb* probs, const int32_t* work, int nwork, cudaStream_t st);
+
+}  // namespace hplmm

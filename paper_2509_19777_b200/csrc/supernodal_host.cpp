@@ -1,0 +1,312 @@
+// Host symbolic analysis of the batched supernodal local factors (see
+// supernodal.h): geometric nested dissection per subdomain, supernode row
+// structures, factor layout, TMA chunk schedule, numeric assembly maps.
+// Subdomains are analysed in parallel (std::thread) and concatenated in order,
+// so the result is deterministic.
+#include <algorithm>
+#include <atomic>
+#include <numeric>
+#include <thread>
+
+#include "supernodal.h"
+
+namespace hplmm {
+
+namespace {
+
+struct LocalSn {
+  std::vector<int32_t> members;   // local node ids (ascending)
+  int parent = -1;
+};
+
+struct SubResult {
+  bool ok = true;
+  std::string err;
+  int n_nodes = 0;
+  std::vector<int32_t> order;                       // local node ids in elimination order
+  std::vector<LocalSn> sns;                         // postorder
+  std::vector<std::vector<int32_t>> st;             // struct (node positions) per supernode
+  std::vector<int32_t> level;
+  // assembly entries per supernode
+  std::vector<std::vector<int64_t>> ae;
+  std::vector<std::vector<int32_t>> au, av;
+  std::vector<std::vector<int32_t>> rel;            // per supernode (as child)
+};
+
+class NdBuilder {
+ public:
+  NdBuilder(const int32_t* ijk, const std::vector<int32_t>& gnodes, int leaf)
+      : ijk_(ijk), g_(gnodes), leaf_(leaf) {}
+  std::vector<LocalSn> sns;
+
+  // returns the roots of the subtree built over `ids` (local node ids)
+  std::vector<int> build(std::vector<int32_t> ids) {
+    if (ids.empty()) return {};
+    int lo[3], hi[3];
+    for (int c = 0; c < 3; ++c) { lo[c] = INT32_MAX; hi[c] = INT32_MIN; }
+    for (int a : ids)
+      for (int c = 0; c < 3; ++c) {
+        int v = ijk_[3 * (int64_t)g_[a] + c];
+        lo[c] = std::min(lo[c], v);
+        hi[c] = std::max(hi[c], v);
+      }
+    int ax = 0;
+    for (int c = 1; c < 3; ++c)
+      if (hi[c] - lo[c] > hi[ax] - lo[ax]) ax = c;
+    if ((int)ids.size() <= leaf_ || hi[ax] - lo[ax] < 2) return {leaf(std::move(ids))};
+    std::vector<int> vals(ids.size());
+    for (size_t i = 0; i < ids.size(); ++i) vals[i] = ijk_[3 * (int64_t)g_[ids[i]] + ax];
+    std::vector<int> sorted = vals;
+    std::nth_element(sorted.begin(), sorted.begin() + sorted.size() / 2, sorted.end());
+    int m = sorted[sorted.size() / 2];
+    m = std::max(lo[ax] + 1, std::min(hi[ax] - 1, m));
+    std::vector<int32_t> L, R, S;
+    for (size_t i = 0; i < ids.size(); ++i)
+      (vals[i] < m ? L : (vals[i] > m ? R : S)).push_back(ids[i]);
+    std::vector<int> roots = build(std::move(L));
+    std::vector<int> rr = build(std::move(R));
+    roots.insert(roots.end(), rr.begin(), rr.end());
+    if (S.empty()) return roots;   // halves are not coupled: a forest
+    int s = leaf(std::move(S));
+    for (int c : roots) sns[c].parent = s;
+    return {s};
+  }
+
+ private:
+  int leaf(std::vector<int32_t> ids) {
+    std::sort(ids.begin(), ids.end());
+    sns.push_back(LocalSn{std::move(ids), -1});
+    return (int)sns.size() - 1;
+  }
+  const int32_t* ijk_;
+  const std::vector<int32_t>& g_;
+  int leaf_;
+};
+
+void analyse_one(const HostSetup& hs, const int32_t* gn, int m, int leaf, std::vector<int32_t>& g2l,
+                 SubResult& res) {
+  std::vector<int32_t> gnodes(gn, gn + m);
+  for (int a = 0; a < m; ++a) g2l[gnodes[a]] = a;
+  // local adjacency (includes self)
+  std::vector<int32_t> aptr(m + 1, 0), adj;
+  std::vector<int64_t> aeidx;
+  for (int a = 0; a < m; ++a) {
+    int v = gnodes[a];
+    for (int e = hs.row_ptr[v]; e < hs.row_ptr[v + 1]; ++e) {
+      int l = g2l[hs.col_idx[e]];
+      if (l >= 0) {
+        adj.push_back(l);
+        aeidx.push_back(e);
+      }
+    }
+    aptr[a + 1] = (int32_t)adj.size();
+  }
+  NdBuilder nd(hs.node_ijk.data(), gnodes, leaf);
+  std::vector<int32_t> all(m);
+  std::iota(all.begin(), all.end(), 0);
+  nd.build(all);
+  res.sns = std::move(nd.sns);
+  const int ns = (int)res.sns.size();
+  std::vector<int32_t> pos(m), first(ns), last(ns);
+  int p = 0;
+  for (int s = 0; s < ns; ++s) {
+    first[s] = p;
+    for (int a : res.sns[s].members) {
+      pos[a] = p++;
+      res.order.push_back(a);
+    }
+    last[s] = p - 1;
+  }
+  res.n_nodes = m;
+  std::vector<std::vector<int>> kids(ns);
+  for (int s = 0; s < ns; ++s)
+    if (res.sns[s].parent >= 0) kids[res.sns[s].parent].push_back(s);
+  res.st.assign(ns, {});
+  res.level.assign(ns, 0);
+  res.ae.assign(ns, {});
+  res.au.assign(ns, {});
+  res.av.assign(ns, {});
+  res.rel.assign(ns, {});
+  for (int s = 0; s < ns; ++s) {
+    std::vector<int32_t> st;
+    for (int a : res.sns[s].members)
+      for (int e = aptr[a]; e < aptr[a + 1]; ++e)
+        if (pos[adj[e]] > last[s]) st.push_back(pos[adj[e]]);
+    int lev = 0;
+    for (int c : kids[s]) {
+      for (int q : res.st[c])
+        if (q > last[s]) st.push_back(q);
+      lev = std::max(lev, res.level[c] + 1);
+    }
+    std::sort(st.begin(), st.end());
+    st.erase(std::unique(st.begin(), st.end()), st.end());
+    res.st[s] = std::move(st);
+    res.level[s] = lev;
+    if (3 * (int)res.sns[s].members.size() > SN_MAX_WR || 3 * (int)res.st[s].size() > SN_MAX_WR) {
+      res.ok = false;
+      res.err = "supernode wider than " + std::to_string(SN_MAX_WR) + " DOFs";
+      break;
+    }
+    // front node index of a position q (member or struct row)
+    auto fidx = [&](int q) -> int {
+      if (q >= first[s] && q <= last[s]) return q - first[s];
+      auto it = std::lower_bound(res.st[s].begin(), res.st[s].end(), q);
+      if (it == res.st[s].end() || *it != q) return -1;
+      return (int)res.sns[s].members.size() + (int)(it - res.st[s].begin());
+    };
+    for (int a : res.sns[s].members)
+      for (int e = aptr[a]; e < aptr[a + 1]; ++e) {
+        int q = pos[adj[e]];
+        if (q < pos[a]) continue;
+        res.ae[s].push_back(aeidx[e]);
+        res.au[s].push_back(fidx(q));
+        res.av[s].push_back(fidx(pos[a]));
+      }
+    for (int c : kids[s])
+      for (int q : res.st[c]) {
+        int f = fidx(q);
+        if (f < 0) {
+          res.ok = false;
+          res.err = "supernodal structure not closed under the elimination tree";
+          break;
+        }
+        res.rel[c].push_back(f);
+      }
+  }
+  for (int a = 0; a < m; ++a) g2l[gnodes[a]] = -1;
+}
+
+}  // namespace
+
+bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
+                const std::vector<int32_t>& nodes, int leaf, SnSymbolic& o, std::string& err) {
+  const int nsub = (int)ptr.size() - 1;
+  std::vector<SubResult> res(std::max(nsub, 0));
+  unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::atomic<int> next{0};
+  auto work = [&]() {
+    std::vector<int32_t> g2l(hs.n_nodes, -1);
+    for (int s; (s = next.fetch_add(1)) < nsub;)
+      analyse_one(hs, nodes.data() + ptr[s], ptr[s + 1] - ptr[s], leaf, g2l, res[s]);
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t + 1 < nth; ++t) th.emplace_back(work);
+  work();
+  for (auto& t : th) t.join();
+
+  o = SnSymbolic();
+  o.nsub = nsub;
+  int64_t base = 0, foff = 0, roff = 0;
+  o.asm_ptr.push_back(0);
+  o.rel_off.push_back(0);
+  for (int s = 0; s < nsub; ++s) {
+    SubResult& r = res[s];
+    if (!r.ok) {
+      err = "subdomain " + std::to_string(s) + ": " + r.err;
+      return false;
+    }
+    const int n = 3 * r.n_nodes;
+    const int sn0 = o.nsn;
+    o.sub_n.push_back(n);
+    o.sub_base.push_back(base);
+    o.sub_sn0.push_back(sn0);
+    o.max_n = std::max(o.max_n, n);
+    const int32_t* gn = nodes.data() + ptr[s];
+    for (int a : r.order)
+      for (int c = 0; c < 3; ++c) {
+        o.gmap.push_back(3 * gn[a] + c);
+        o.lidx.push_back(3 * a + c);
+      }
+    int p0 = 0;
+    std::vector<int> nchild(r.sns.size(), 0);
+    for (size_t k = 0; k < r.sns.size(); ++k) {
+      const int w = 3 * (int)r.sns[k].members.size(), rr = 3 * (int)r.st[k].size();
+      o.sn_w.push_back(w);
+      o.sn_r.push_back(rr);
+      o.sn_p0.push_back(p0);
+      o.sn_ldw.push_back(rr + (rr & 1));
+      o.sn_ldf.push_back(w + (w & 1));
+      o.sn_level.push_back(r.level[k]);
+      o.sn_parent.push_back(r.sns[k].parent >= 0 ? sn0 + r.sns[k].parent : -1);
+      o.sn_sub.push_back(s);
+      int rank = 0;
+      if (r.sns[k].parent >= 0) rank = nchild[r.sns[k].parent]++;
+      o.sn_child_rank.push_back(rank);
+      o.max_children = std::max(o.max_children, rank + 1);
+      o.sn_rows_off.push_back(roff);
+      for (int q : r.st[k])
+        for (int c = 0; c < 3; ++c) o.rows.push_back(3 * q + c);
+      roff += rr;
+      o.sn_foff.push_back(foff);
+      foff += sn_rows_doubles(rr) + (int64_t)o.sn_ldw.back() * w + (int64_t)o.sn_ldf.back() * w;
+      o.max_w = std::max(o.max_w, w);
+      o.max_r = std::max(o.max_r, rr);
+      o.n_levels = std::max(o.n_levels, r.level[k] + 1);
+      p0 += w;
+      o.asm_e.insert(o.asm_e.end(), r.ae[k].begin(), r.ae[k].end());
+      o.asm_u.insert(o.asm_u.end(), r.au[k].begin(), r.au[k].end());
+      o.asm_v.insert(o.asm_v.end(), r.av[k].begin(), r.av[k].end());
+      o.asm_ptr.push_back((int64_t)o.asm_e.size());
+      o.rel.insert(o.rel.end(), r.rel[k].begin(), r.rel[k].end());
+      o.rel_off.push_back((int64_t)o.rel.size());
+      o.nsn++;
+    }
+    o.sub_sn1.push_back(o.nsn);
+    base += n;
+    res[s] = SubResult();   // free
+  }
+  o.factor_doubles = foff;
+  // TMA chunk schedule: forward = (W_S, rows, F_SS^-1) per S in postorder,
+  // backward = (rows, W_S) per S in reverse postorder; W/F chunks are whole
+  // columns of at most SN_CHUNK_DOUBLES.
+  auto push = [&](int sn, int kind, int64_t off, int bytes, int c0, int nc, bool last) {
+    SnChunk ch;
+    ch.off = off;
+    // thread-group size for the rows of this part: TG = pow2 >= max(32, ceil(h/2)), <= 512
+    const int h = (kind == SN_F_FWD) ? o.sn_w[sn] : o.sn_r[sn];
+    int lg = 5;
+    while ((1 << lg) < (h + 1) / 2 && lg < 9) ++lg;
+    ch.bytes = bytes | ((lg - 5) << 24);
+    ch.info = c0 | ((nc - 1) << 12) | (kind << 24) | (last ? SN_INFO_LAST : 0);
+    ch.p0 = o.sn_p0[sn];
+    ch.w = o.sn_w[sn];
+    ch.r = o.sn_r[sn];
+    ch.sub = o.sn_sub[sn];
+    o.chunks.push_back(ch);
+  };
+  auto cols = [&](int sn, int kind, int64_t off0, int ld, int ncols_total) {
+    const int per = std::max(1, SN_CHUNK_DOUBLES / ld);
+    for (int c0 = 0; c0 < ncols_total; c0 += per) {
+      int nc = std::min(per, ncols_total - c0);
+      push(sn, kind, off0 + (int64_t)c0 * ld, nc * ld * 8, c0, nc, c0 + nc == ncols_total);
+    }
+  };
+  for (int s = 0; s < nsub; ++s) {
+    int64_t fb = 0;
+    o.sub_fc0.push_back((int64_t)o.chunks.size());
+    for (int k = o.sub_sn0[s]; k < o.sub_sn1[s]; ++k) {
+      const int w = o.sn_w[k], r = o.sn_r[k];
+      const int64_t rows_at = o.sn_foff[k], w_at = rows_at + sn_rows_doubles(r);
+      const int64_t f_at = w_at + (int64_t)o.sn_ldw[k] * w;
+      if (r > 0) {
+        cols(k, SN_W_FWD, w_at, o.sn_ldw[k], w);
+        push(k, SN_ROWS_FWD, rows_at, (int)(8 * sn_rows_doubles(r)), 0, 1, true);
+      }
+      cols(k, SN_F_FWD, f_at, o.sn_ldf[k], w);
+      fb += 8 * (2 * sn_rows_doubles(r) + (int64_t)o.sn_ldw[k] * w * 2 + (int64_t)o.sn_ldf[k] * w);
+    }
+    o.sub_fc1.push_back((int64_t)o.chunks.size());
+    o.sub_bc0.push_back((int64_t)o.chunks.size());
+    for (int k = o.sub_sn1[s] - 1; k >= o.sub_sn0[s]; --k) {
+      const int r = o.sn_r[k];
+      if (r == 0) continue;
+      push(k, SN_ROWS_BWD, o.sn_foff[k], (int)(8 * sn_rows_doubles(r)), 0, 1, true);
+      cols(k, SN_W_BWD, o.sn_foff[k] + sn_rows_doubles(r), o.sn_ldw[k], o.sn_w[k]);
+    }
+    o.sub_bc1.push_back((int64_t)o.chunks.size());
+    o.sub_fbytes.push_back(fb);
+  }
+  return true;
+}
+
+}  // namespace hplmm
