@@ -270,7 +270,8 @@ def main():
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
     prob = make_problem(args.config)
-    sv = Solver(prob).assemble(local).setup()
+    lf = os.environ.get("HPLMM_LOCAL_FACTOR")
+    sv = Solver(prob, local_factor=int(lf) if lf else None).assemble(local).setup()
     rep0 = sv.report()
     b_host = sv.export("RHS")
     b = torch.from_numpy(b_host).cuda()
@@ -296,8 +297,10 @@ def main():
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
     sv.profile(False, False)
-    # roofline of the dominant kernel (packed SYMV tiles: local + coarse inverses)
-    stats = [sv.kernel_stats(k) for k in range(3)]
+    sparse = int(sv.options.local_factor) == 1
+    # kernel classes: 0/1/2 packed SYMV (grain/contact/coarse inverse tiles),
+    # 3/4 supernodal solve (grain/contact factors)
+    stats = [sv.kernel_stats(k) for k in range(5)]
     p = prob
     iters = reps[-1]["iterations"]
 
@@ -314,25 +317,34 @@ def main():
 
     t_s, e2e_s = reduce_max([ms / 1e3, e2e_s], dist)
 
-    # algorithmic bytes per symv launch, per kernel class
+    # algorithmic bytes per launch, per kernel class
     sizes = {0: [], 1: [], 2: []}
-    gp = sv.export("GRAIN_COLS_PTR")  # noqa: F841  (sizes from artifacts below)
     iface_ptr = sv.export("CONTACT_PTR")
-    sizes[1] = list(3 * np.diff(iface_ptr))
+    sizes[1] = [int(v) for v in 3 * np.diff(iface_ptr)]
     cls = sv.export("NODE_CLASS")
     own = sv.export("NODE_OWNER")
     gsz = np.bincount(own[cls != 1], minlength=prob.n_grains)
-    sizes[0] = list(3 * gsz)
+    sizes[0] = [int(v) for v in 3 * gsz]
     sizes[2] = [rep0["n_mortar_dofs"]]
-    alg = {k: symv_algorithmic_bytes([int(s) for s in sizes[k]]) for k in sizes}
-    # dominant kernel = k_symv_tma on the grain batch (largest single launch);
-    # achieved = algorithmic bytes per launch / mean CUDA-event launch time
-    g_ms, g_n, g_tile = stats[0]
-    achieved = alg[0] / (g_ms / g_n / 1e3) / 1e9 if g_n else None
-    tot_ms = sum(st[0] for st in stats)
-    tot_bytes = sum(alg[k] * stats[k][1] for k in range(3))
+    alg = {k: symv_algorithmic_bytes(sizes[k]) for k in sizes}
+    if sparse:
+        # block-LDL^T solve: W_S read twice, F_SS^-1 once, row lists twice
+        # (library-reported stream bytes), plus x gathered and y written (16 B/DOF)
+        alg[3] = stats[3][2] + 16 * sum(sizes[0])
+        alg[4] = stats[4][2] + 16 * sum(sizes[1])
+        dom = 4 if stats[4][1] else 3
+        dom_name = ("k_sn_solve, contact-grid batch (supernodal block-LDL^T forward+backward sweep)"
+                    if dom == 4 else "k_sn_solve, grain batch (supernodal block-LDL^T sweeps)")
+        local_classes = (3, 4)
+    else:
+        dom = 0
+        dom_name = "k_symv_tma, grain batch (packed SPD-inverse apply)"
+        local_classes = (0, 1)
+    d_ms, d_n, _ = stats[dom]
+    achieved = alg[dom] / (d_ms / d_n / 1e3) / 1e9 if d_n else None
+    tot_ms = sum(stats[k][0] for k in local_classes + (2,))
+    tot_bytes = sum(alg[k] * stats[k][1] for k in local_classes + (2,))
     agg_achieved = tot_bytes / (tot_ms / 1e3) / 1e9 if tot_ms > 0 else None
-    tile_bytes = sum(st[2] * st[1] for st in stats)
     peak, peak_kind = _peaks()
     launches_per_step = reps[-1]["kernel_launches"]
     iters_per_s = iters / t_s
@@ -341,15 +353,15 @@ def main():
     n = 3 * rep0["n_nodes"]
     spmv_bytes = 76 * nnzb + 4 * rep0["n_nodes"] + 24 * n
     pb = 12 * rep0["prolong_nnz"]
-    per_iter_bytes = (alg[0] + alg[1] + alg[2] + 3 * spmv_bytes + 2 * pb
-                      + (4 * 11 + 6) * 8 * n)
+    local_bytes = alg[local_classes[0]] + alg[local_classes[1]]
+    per_iter_bytes = (local_bytes + alg[2] + 3 * spmv_bytes + 2 * pb + (4 * 11 + 6) * 8 * n)
     per_iter_frac = (per_iter_bytes / (t_s / max(iters, 1)) / 1e9) / peak
 
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"ncu_symv_{args.config}.json")
+    tp = os.path.join(ROOT, "profiles", f"ncu_{'sn' if sparse else 'symv'}_{args.config}.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp))["dram_bytes_per_launch"]["grain"]
+            traffic = json.load(open(tp))["dram_bytes_per_launch"]["contact" if dom == 4 else "grain"]
         except Exception:
             traffic = None
 
@@ -363,7 +375,8 @@ def main():
                    "mortar_dofs": rep0["n_mortar_dofs"], "n_mortar": p.n_mortar,
                    "contact_h": p.contact_h, "restart": p.restart, "tol": p.tol,
                    "parallelism": f"replicas{world}",
-                   "l2": "no flush: working set (packed local inverses) >> 126 MB L2"},
+                   "local_factor": "supernodal" if sparse else "dense-inverse",
+                   "l2": "no flush: working set (local factors) >> 126 MB L2"},
         "iterations": iters, "iterations_per_s": iters_per_s * world,
         "solves_per_s_aggregate": world / t_s,
         "setup_s": {"host_integer": rep0["t_host_setup_s"], "assemble": rep0["t_assemble_s"],
@@ -372,12 +385,13 @@ def main():
         "final_true_relres": reps[-1]["final_true_relres"],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "k_symv_tma, grain batch (packed SPD-inverse apply)",
-                     "algorithmic_bytes_per_launch": alg[0], "launch_ms": g_ms / max(g_n, 1),
+                     "kernel": dom_name,
+                     "algorithmic_bytes_per_launch": alg[dom], "launch_ms": d_ms / max(d_n, 1),
                      "peak_kind": peak_kind,
-                     "all_symv": {"achieved_gbs": agg_achieved,
-                                  "tile_bytes_per_step": tile_bytes / args.steps,
-                                  "share_of_step": (tot_ms / args.steps) / (t_s * 1e3)}},
+                     "local_and_coarse_solves": {
+                         "achieved_gbs": agg_achieved,
+                         "bytes_per_step": tot_bytes / args.steps,
+                         "share_of_step": (tot_ms / args.steps) / (t_s * 1e3)}},
         "per_iteration": {"algorithmic_bytes": per_iter_bytes, "ms": t_s * 1e3 / max(iters, 1),
                           "roofline_frac": per_iter_frac},
         "gpu_launches": int(launches_per_step * args.steps),

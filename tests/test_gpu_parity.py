@@ -25,15 +25,19 @@ def rel(a, b):
 _solvers = {}
 
 
-def gpu_case(name):
-    if name not in _solvers:
+def gpu_case(name, lf=1):
+    """lf = local_factor: 1 supernodal block-LDL^T (default), 0 dense inverses."""
+    if (name, lf) not in _solvers:
         import __graft_entry__
         __graft_entry__.build()
         from paper_2509_19777_b200 import Solver
         p, s, h = oracle_case(name)
-        sv = Solver(p).assemble(0).setup()
-        _solvers[name] = (p, s, h, sv)
-    return _solvers[name]
+        sv = Solver(p, local_factor=lf).assemble(0).setup()
+        _solvers[(name, lf)] = (p, s, h, sv)
+    return _solvers[(name, lf)]
+
+
+LF = [1, 0]
 
 
 def dev(x):
@@ -58,9 +62,10 @@ def test_spmv(case):
     assert rel(sv.apply("SPMV", v), s.A @ v) <= 1e-12
 
 
+@pytest.mark.parametrize("lf", LF)
 @pytest.mark.parametrize("case", CASES)
-def test_mortar_weights_and_S(case):
-    p, s, h, sv = gpu_case(case)
+def test_mortar_weights_and_S(case, lf):
+    p, s, h, sv = gpu_case(case, lf)
     W = sv.export("MORTAR_W")
     Wo = np.concatenate([w.ravel() for w in h.mor.weights])
     assert np.abs(W - Wo).max() <= 1e-14
@@ -81,10 +86,11 @@ def coarse_floor(h):
     return 10.0 * (ev[-1] / ev[0]) * EPS
 
 
+@pytest.mark.parametrize("lf", LF)
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("op", ["MZETA", "MGRAIN", "MCG", "MG", "MINV"])
-def test_preconditioner_apply(case, op):
-    p, s, h, sv = gpu_case(case)
+def test_preconditioner_apply(case, op, lf):
+    p, s, h, sv = gpu_case(case, lf)
     sv.set_rhs(dev(s.b))
     h.set_rhs(s.b)
     v = np.random.default_rng(12345).standard_normal(s.n_dof)
@@ -110,10 +116,11 @@ def test_coarse_solve_backward_error(case):
     assert be <= max(1e-14, coarse_floor(h)), be
 
 
+@pytest.mark.parametrize("lf", LF)
 @pytest.mark.parametrize("case", CASES)
-def test_restrict_prolong(case):
+def test_restrict_prolong(case, lf):
     import scipy.sparse as sp
-    p, s, h, sv = gpu_case(case)
+    p, s, h, sv = gpu_case(case, lf)
     sv.set_rhs(dev(s.b))
     h.set_rhs(s.b)
     P = sp.hstack([h.PB, h.P_C()]).tocsc()
@@ -124,10 +131,11 @@ def test_restrict_prolong(case):
     assert rel(sv.apply("PROLONG", y), P @ y) <= 1e-12
 
 
+@pytest.mark.parametrize("lf", LF)
 @pytest.mark.parametrize("case", CASES)
-def test_solve(case):
+def test_solve(case, lf):
     from oracle import gmres
-    p, s, h, sv = gpu_case(case)
+    p, s, h, sv = gpu_case(case, lf)
     h.set_rhs(s.b)
     xo, ito, histo, rro, convo = gmres.gmres(s.A, s.b, h.apply_M, tol=1e-8)
     x, rep, hist = sv.solve(dev(s.b), tol=1e-8)
