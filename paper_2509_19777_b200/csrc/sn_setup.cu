@@ -54,7 +54,7 @@ void lpt(const std::vector<int64_t>& wgt, int nb, std::vector<int32_t>& ptr,
 }  // namespace
 
 void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nrhs,
-                   const std::vector<int32_t>* ncols, SnWork& wk) {
+                   const std::vector<int32_t>* ncols, SnWork& wk, int force_cons) {
   const SnSymbolic& s = B.sym;
   const bool setup_only = ncols != nullptr;
   std::vector<int64_t> wgt;
@@ -67,6 +67,8 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
       wgt.push_back(s.sub_fbytes[g] + 8 * (int64_t)s.sub_n[g] * 64);
     }
   }
+  wk.cons = force_cons ? force_cons : sn_solve_cfg((int)isub.size(), nblocks);
+  nblocks *= wk.cons == 8 ? 2 : 1;
   nblocks = std::max(1, std::min<int>(nblocks, (int)isub.size()));
   std::vector<int32_t> ptr, ids;
   lpt(wgt, nblocks, ptr, ids);
@@ -141,7 +143,8 @@ void sn_apply(const SnBatch& B, const double* in, cudaStream_t st) {
   io.mode = 0;
   io.in = in;
   io.out = B.yloc;
-  launch_sn_solve(B.dev, io, B.work, 1, B.sym.max_n, st);
+  launch_sn_solve(B.dev, io, B.work, 1, B.sym.max_n, B.sym.max_r, B.sym.chunk_doubles,
+                  B.work.cons, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -347,6 +350,7 @@ void sn_factor(SnBatch& B, const double* d_val, DevAlloc& A, cudaStream_t st, in
         h2d(d_work, work.data(), work.size() * 4);
         launch_gemm_batched(d_probs, d_work, (int)(work.size() / 3), st);
         SN_CK(cudaGetLastError());
+        if (phase == 0) launch_transpose_w(d_list, nl, nm, B.factor, st);
       }
     }
   }
@@ -358,9 +362,13 @@ void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
                       const std::vector<int32_t>& kcols, const int64_t* d_b_off,
                       const int32_t* d_ld, const double* R, double* Bout) {
   int nrhs = 4;
-  while (nrhs > 1 && sn_solve_stages(B.sym.max_n, nrhs) < 2) nrhs /= 2;
+  int items = 0;
+  for (int k : kcols) items += (k + 3) / 4;
+  const int cons = sn_solve_cfg(items, nsm);
+  while (nrhs > 1 && sn_solve_stages(B.sym.max_n, B.sym.max_r, nrhs, B.sym.chunk_doubles, cons) < 2)
+    nrhs /= 2;
   SnWork wk;
-  sn_build_work(B, A, st, nsm, nrhs, &kcols, wk);
+  sn_build_work(B, A, st, nsm, nrhs, &kcols, wk, cons);
   SnIO io;
   io.mode = 1;
   io.in = R;
@@ -368,7 +376,7 @@ void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
   io.bmap = B.d_lidx;
   io.b_off = d_b_off;
   io.ld = d_ld;
-  launch_sn_solve(B.dev, io, wk, nrhs, B.sym.max_n, st);
+  launch_sn_solve(B.dev, io, wk, nrhs, B.sym.max_n, B.sym.max_r, B.sym.chunk_doubles, wk.cons, st);
   SN_CK(cudaGetLastError());
 }
 

@@ -28,14 +28,18 @@ namespace hplmm {
 // A stage is released (empty mbarrier, count SN_CONS) as soon as every warp
 // has read it; the producer runs ahead across supernode and item boundaries.
 // ===========================================================================
-constexpr int SN_CONS = 16;
-constexpr int SN_NT = 32 * SN_CONS;
-constexpr int SN_MAXQ = SN_MAX_WR / (2 * SN_NT);   // double2 row pairs per thread (2)
-constexpr int SN_MAXST = 8;
-static_assert(SN_MAXQ * 2 * SN_NT >= SN_MAX_WR, "row coverage");
+constexpr int SN_MAXST = 16;
 
+template <int CONS>
+struct SnT {
+  static constexpr int NT = 32 * CONS;                  // consumer threads
+  static constexpr int MAXQ = 4;                        // double2 row pairs per thread
+  static_assert(MAXQ * 2 * 256 >= SN_MAX_WR, "row coverage at TG = 256");
+};
+
+template <int NT>
 __device__ __forceinline__ void cons_sync() {
-  asm volatile("bar.sync 1, %0;" ::"r"(SN_NT) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
 }
 
 // Row-parallel layout of a part with h rows: row pairs are spread over TG
@@ -44,23 +48,75 @@ __device__ __forceinline__ void cons_sync() {
 // keeps all consumer warps busy whatever the aspect ratio of the panel.
 struct RowLayout {
   int TG, G, g, t;
-  // lgc = log2(TG) - 5, precomputed on the host per part (chunk descriptor)
-  __device__ __forceinline__ RowLayout(int lgc, int tid) {
-    const int lg = lgc + 5;
+  // lgc = log2(TG) - 5, precomputed on the host per part (chunk descriptor,
+  // TG <= 512), capped at the CTA's consumer thread count NT
+  __device__ __forceinline__ RowLayout(int lgc, int tid, int nt) {
+    int lg = lgc + 5;
+    while ((1 << lg) > nt) --lg;
     TG = 1 << lg;
-    G = SN_NT >> lg;
+    G = nt >> lg;
     g = tid >> lg;
     t = tid & (TG - 1);
   }
 };
-static_assert(SN_NT == 512, "RowLayout codes assume TG <= 512");
+
+// effective row-group code of a part with h rows: the host's (TG >= h/8), or
+// for NRHS > 1 TG >= h/2 so that the group-reduction scratch fits one stage
+template <int NRHS>
+__device__ __forceinline__ int sn_lg(int lgc, int h) {
+  if (NRHS == 1) return lgc;
+  int lg = 5;
+  while ((1 << lg) < (h + 1) / 2) ++lg;
+  return max(lgc, lg - 5);
+}
 
 // acc[q][e][c] += sum over this group's chunk columns of col[2(t + q TG) + e] * x_S
-template <int NQ, int NRHS>
+// Columns are taken four at a time (all loads issued before the FMAs, two
+// accumulator sets) so that a warp keeps several shared-memory loads in flight.
+template <int NQ, int NRHS, int MAXQ>
 __device__ __forceinline__ void sn_rows(const double* __restrict__ st, int ld, int nc, int h,
                                         const double* __restrict__ xcol, const RowLayout& L,
-                                        double (&acc)[SN_MAXQ][2][NRHS]) {
-  for (int jj = L.g; jj < nc; jj += L.G) {
+                                        double (&acc)[MAXQ][2][NRHS]) {
+  constexpr int U = NQ == 1 ? 4 : (NQ == 2 ? 2 : 1);   // columns per step (register budget)
+  double acc2[NQ][2][NRHS];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int c = 0; c < NRHS; ++c) acc2[q][e][c] = 0.0;
+  int jj = L.g;
+  const int G = L.G;
+  for (; jj + (U - 1) * G < nc; jj += U * G) {
+    double xv[U][NRHS];
+    double2 a[U][NQ];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int c = 0; c < NRHS; ++c) xv[u][c] = xcol[(jj + u * G) * NRHS + c];
+      const double* cu = st + (size_t)(jj + u * G) * ld;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int i = 2 * (L.t + q * L.TG);
+        a[u][q] = i < h ? *reinterpret_cast<const double2*>(cu + i) : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int c = 0; c < NRHS; ++c) {
+          if (u & 1) {
+            acc2[q][0][c] = fma(a[u][q].x, xv[u][c], acc2[q][0][c]);
+            acc2[q][1][c] = fma(a[u][q].y, xv[u][c], acc2[q][1][c]);
+          } else {
+            acc[q][0][c] = fma(a[u][q].x, xv[u][c], acc[q][0][c]);
+            acc[q][1][c] = fma(a[u][q].y, xv[u][c], acc[q][1][c]);
+          }
+        }
+  }
+  for (; jj < nc; jj += G) {
     double xa[NRHS];
 #pragma unroll
     for (int c = 0; c < NRHS; ++c) xa[c] = xcol[jj * NRHS + c];
@@ -78,51 +134,72 @@ __device__ __forceinline__ void sn_rows(const double* __restrict__ st, int ld, i
       }
     }
   }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int c = 0; c < NRHS; ++c) acc[q][e][c] += acc2[q][e][c];
 }
 
 // group partials -> group 0 (fixed order g = 0..G-1), through smem scratch
-template <int NRHS>
+// scratch[((g - 1) h + row) NRHS + c]: (G - 1) h NRHS <= 8 NT (TG >= h/8; NRHS > 1:
+// TG >= h/2) doubles, i.e. within one 32-KiB stage for NT <= 512
+template <int NRHS, int MAXQ, int NT>
 __device__ __forceinline__ void sn_group_reduce(const RowLayout& L, int h, double* scratch,
-                                                double (&acc)[SN_MAXQ][2][NRHS]) {
-  // scratch[(g * 2 TG * SN_MAXQ + row) * NRHS + c], row = 2(t + q TG) + e
-  const int stride = 2 * L.TG * SN_MAXQ;
+                                                double (&acc)[MAXQ][2][NRHS]) {
+  const int stride = h;
   if (L.g > 0) {
 #pragma unroll
-    for (int q = 0; q < SN_MAXQ; ++q)
+    for (int q = 0; q < MAXQ; ++q)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int i = 2 * (L.t + q * L.TG) + e;
         if (i < h)
 #pragma unroll
-          for (int c = 0; c < NRHS; ++c) scratch[((size_t)L.g * stride + i) * NRHS + c] = acc[q][e][c];
+          for (int c = 0; c < NRHS; ++c) scratch[((size_t)(L.g - 1) * stride + i) * NRHS + c] = acc[q][e][c];
       }
   }
-  cons_sync();
+  cons_sync<NT>();
   if (L.g == 0) {
     for (int gg = 1; gg < L.G; ++gg)
 #pragma unroll
-      for (int q = 0; q < SN_MAXQ; ++q)
+      for (int q = 0; q < MAXQ; ++q)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int i = 2 * (L.t + q * L.TG) + e;
           if (i < h)
 #pragma unroll
-            for (int c = 0; c < NRHS; ++c) acc[q][e][c] += scratch[((size_t)gg * stride + i) * NRHS + c];
+            for (int c = 0; c < NRHS; ++c) acc[q][e][c] += scratch[((size_t)(gg - 1) * stride + i) * NRHS + c];
         }
   }
 }
 
-template <int NRHS>
-__global__ void __launch_bounds__(32 * (SN_CONS + 1), 1)
-    k_sn_solve(SnDev d, SnIO io, SnWork wk, int stages, int max_n) {
+template <int NRHS, int CONS, int CPS>
+__global__ void __launch_bounds__(32 * (CONS + 1), CPS)
+    k_sn_solve(SnDev d, SnIO io, SnWork wk, int stages, int stage_doubles, int max_n, int max_r,
+               int flags) {
   extern __shared__ __align__(128) unsigned char sn_smem[];
   __shared__ __align__(8) uint64_t full[SN_MAXST], empty[SN_MAXST];
   double* ring = reinterpret_cast<double*>(sn_smem);
-  double* x = ring + (size_t)stages * SN_CHUNK_DOUBLES;
+  double* x = ring + (size_t)stages * stage_doubles;
   // x_R of the current backward part; scratch of the forward group reductions
-  double* xr = x + (size_t)((max_n + 1) & ~1) * NRHS;   // 16-byte aligned
+  // x_R of a backward part (16-B aligned)
+  double* xr = x + (size_t)((max_n + 1) & ~1) * NRHS;
+  constexpr int SN_NT = SnT<CONS>::NT, SN_MAXQ = SnT<CONS>::MAXQ, SN_CONS = CONS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k0 = wk.chunk_ptr[blockIdx.x], k1 = wk.chunk_ptr[blockIdx.x + 1];
+  // optional per-warp phase timing (flags & 2; printed for a few CTAs)
+  const bool prof = (flags & 2) && (blockIdx.x % 37 == 0);
+  long long t_wait = 0, t_sync = 0;
+  long long t_kind[6] = {0, 0, 0, 0, 0, 0}, n_kind[6] = {0, 0, 0, 0, 0, 0};
+  const long long t_start = prof ? clock64() : 0;
+#define PSYNC()                                        \
+  do {                                                 \
+    const long long ts_ = prof ? clock64() : 0;        \
+    cons_sync<SN_NT>();                                       \
+    if (prof) t_sync += clock64() - ts_;               \
+  } while (0)
   const SnChunk* __restrict__ ch = wk.chunks;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -150,14 +227,21 @@ __global__ void __launch_bounds__(32 * (SN_CONS + 1), 1)
         const int64_t o = __shfl_sync(0xffffffffu, off, j);
         const int b = __shfl_sync(0xffffffffu, bytes, j);
         if (lane == 0) {
-          if (k >= stages) mbar_wait(&empty[s], ph ^ 1);
+          if (k >= stages) {
+            const long long tw = prof ? clock64() : 0;
+            mbar_wait(&empty[s], ph ^ 1);
+            if (prof) t_wait += clock64() - tw;
+          }
           mbar_expect_tx(&full[s], (uint32_t)b);
-          bulk_g2s_hint(ring + (size_t)s * SN_CHUNK_DOUBLES, d.factor + o, (uint32_t)b, &full[s],
+          bulk_g2s_hint(ring + (size_t)s * stage_doubles, d.factor + o, (uint32_t)b, &full[s],
                         pol);
         }
         if (++s == stages) { s = 0; ph ^= 1; }
       }
     }
+    if (prof && lane == 0)
+      printf("sn_prof cta %d producer: total %lld empty-wait %lld chunks %lld\n", blockIdx.x,
+             clock64() - t_start, t_wait, (long long)(k1 - k0));
     return;
   }
   const int tid = threadIdx.x;
@@ -212,16 +296,23 @@ __global__ void __launch_bounds__(32 * (SN_CONS + 1), 1)
           for (int c = 0; c < NRHS; ++c) x[p * NRHS + c] = c < ncr ? R[row + c] : 0.0;
         }
       }
-      cons_sync();
+      PSYNC();
     }
-    mbar_wait_sleep(&full[s], ph);
-    const double* st = ring + (size_t)s * SN_CHUNK_DOUBLES;
+    {
+      const long long tw = prof ? clock64() : 0;
+      if (flags & 1) mbar_wait_sleep(&full[s], ph);
+      else mbar_wait(&full[s], ph);
+      if (prof) t_wait += clock64() - tw;
+    }
+    const double* st = ring + (size_t)s * stage_doubles;
     const int cs = s;
+    const long long t_k0 = prof ? clock64() : 0;
     if (++s == stages) { s = 0; ph ^= 1; }
-    if (kind == SN_W_FWD || kind == SN_F_FWD) {
+    if (kind == SN_W_FWD || kind == SN_F_FWD || kind == SN_WT_BWD) {
+      // row-parallel gemv on a column chunk: W_S (fwd), F_SS^-1, W_S^T (bwd)
       const int h = kind == SN_W_FWD ? r : w;
       const int ld = h + (h & 1);
-      const RowLayout L(lgc, tid);
+      const RowLayout L(sn_lg<NRHS>(lgc, h), tid, SN_NT);
       if (cc0 == 0) {
 #pragma unroll
         for (int q = 0; q < SN_MAXQ; ++q)
@@ -230,17 +321,29 @@ __global__ void __launch_bounds__(32 * (SN_CONS + 1), 1)
 #pragma unroll
             for (int cr = 0; cr < NRHS; ++cr) acc[q][e][cr] = 0.0;
       }
-      const double* xcol = x + (size_t)(p0 + cc0) * NRHS;
-      if (2 * L.TG >= h) sn_rows<1, NRHS>(st, ld, nc, h, xcol, L, acc);
-      else sn_rows<2, NRHS>(st, ld, nc, h, xcol, L, acc);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[cs]);
+      const double* xcol = kind == SN_WT_BWD ? xr + (size_t)cc0 * NRHS : x + (size_t)(p0 + cc0) * NRHS;
+      const int nq = (h + 2 * L.TG - 1) / (2 * L.TG);
+      if (nq <= 1) sn_rows<1, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
+      else if (nq == 2) sn_rows<2, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
+      else if (nq == 3) sn_rows<3, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
+      else sn_rows<4, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
+      if (!(last && L.G > 1)) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cs]);
+      }
       if (last) {
-        if (L.G > 1) sn_group_reduce<NRHS>(L, h, xr, acc);
+        if (L.G > 1) {
+          // the stage just read serves as the scratch of the group reduction;
+          // it is released once group 0 has read the partials
+          double* scratch = const_cast<double*>(st);
+          PSYNC();
+          sn_group_reduce<NRHS, SN_MAXQ, SN_NT>(L, h, scratch, acc);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[cs]);
+        }
         if (kind == SN_W_FWD) {
-          if (L.G > 1) cons_sync();   // scratch is reused by the F part
         } else {
-          if (L.G == 1) cons_sync();  // every thread is done reading x_S
+          if (L.G == 1 && kind == SN_F_FWD) PSYNC();   // every thread is done reading x_S
           if (L.g == 0) {
 #pragma unroll
             for (int q = 0; q < SN_MAXQ; ++q)
@@ -249,16 +352,19 @@ __global__ void __launch_bounds__(32 * (SN_CONS + 1), 1)
                 const int i = 2 * (L.t + q * L.TG) + e;
                 if (i < w) {
 #pragma unroll
-                  for (int cr = 0; cr < NRHS; ++cr) x[(p0 + i) * NRHS + cr] = acc[q][e][cr];
+                  for (int cr = 0; cr < NRHS; ++cr) {
+                    double& xv = x[(p0 + i) * NRHS + cr];
+                    xv = kind == SN_F_FWD ? acc[q][e][cr] : xv - acc[q][e][cr];
+                  }
                 }
               }
           }
-          cons_sync();
+          PSYNC();
         }
       }
     } else if (kind == SN_ROWS_FWD) {
       // x_R -= W_S x_S (summed over the W part by group 0; rows are distinct)
-      const RowLayout L(lgc, tid);
+      const RowLayout L(sn_lg<NRHS>(lgc, r), tid, SN_NT);
       const int32_t* rows = reinterpret_cast<const int32_t*>(st);
       if (L.g == 0) {
 #pragma unroll
@@ -286,49 +392,14 @@ __global__ void __launch_bounds__(32 * (SN_CONS + 1), 1)
       if ((r & 1) && tid < NRHS) xr[r * NRHS + tid] = 0.0;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[cs]);
-      cons_sync();
-    } else {  // SN_W_BWD: x_S[j] -= W[:,j] . x_R, LPC lanes per column
-      const int ld = r + (r & 1);
-      const int lpc = r > 256 ? 32 : (r > 128 ? 16 : 8);
-      const int cpw = 32 / lpc;                    // columns per warp pass
-      const int sl = lane & (lpc - 1), cl = lane / lpc;
-      for (int j0 = warp * cpw; j0 < nc; j0 += SN_CONS * cpw) {
-        const int jj = j0 + cl;
-        double sum[NRHS];
-#pragma unroll
-        for (int cr = 0; cr < NRHS; ++cr) sum[cr] = 0.0;
-        if (jj < nc) {
-          const double* col = st + (size_t)jj * ld;
-          for (int i = 2 * sl; i < r; i += 2 * lpc) {
-            const double2 a = *reinterpret_cast<const double2*>(col + i);
-            if (NRHS == 1) {
-              const double2 xv = *reinterpret_cast<const double2*>(xr + i);
-              sum[0] = fma(a.x, xv.x, fma(a.y, xv.y, sum[0]));
-            } else {
-#pragma unroll
-              for (int cr = 0; cr < NRHS; ++cr)
-                sum[cr] = fma(a.x, xr[i * NRHS + cr], fma(a.y, xr[(i + 1) * NRHS + cr], sum[cr]));
-            }
-          }
-        }
-#pragma unroll
-        for (int cr = 0; cr < NRHS; ++cr) {
-          for (int o = lpc >> 1; o > 0; o >>= 1) sum[cr] += __shfl_xor_sync(0xffffffffu, sum[cr], o);
-        }
-        if (jj < nc && sl < NRHS) {
-          double v = sum[0];
-#pragma unroll
-          for (int cr = 1; cr < NRHS; ++cr)
-            if (sl == cr) v = sum[cr];
-          x[(p0 + cc0 + jj) * NRHS + sl] -= v;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[cs]);
-      if (last) cons_sync();
+      PSYNC();
+    }
+    if (prof) {
+      t_kind[kind] += clock64() - t_k0;
+      n_kind[kind]++;
     }
     if (info & SN_INFO_LAST_ITEM) {
-      cons_sync();
+      PSYNC();
       // ---- write the solution
       if (io.mode == 0) {
         for (int p = tid; p < n; p += SN_NT) io.out[base + p] = x[p];
@@ -343,36 +414,77 @@ __global__ void __launch_bounds__(32 * (SN_CONS + 1), 1)
             if (c < ncr) B[row + c] = -x[p * NRHS + c];
         }
       }
-      cons_sync();
+      PSYNC();
     }
   }
+  if (prof && lane == 0)
+    printf("sn_prof cta %d warp %d: total %lld full-wait %lld sync %lld | Wf %lld/%lld Ff %lld/%lld "
+           "Wb %lld/%lld Rf %lld/%lld Rb %lld/%lld\n", blockIdx.x, warp, clock64() - t_start,
+           t_wait, t_sync, t_kind[0], n_kind[0], t_kind[1], n_kind[1], t_kind[2], n_kind[2],
+           t_kind[3], n_kind[3], t_kind[4], n_kind[4]);
+}
+#undef PSYNC
+// shared memory: ring (stages x chunk) | x (max_n even, NRHS) | x_R / scratch
+static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int nt) {
+  return (size_t)(((max_n + 1) & ~1) + ((max_r + 3) & ~1)) * nrhs;
 }
 
-int sn_solve_stages(int max_n, int nrhs) {
-  const int avail = 226 * 1024 - (max_n + SN_MAX_WR + 4) * nrhs * 8;
-  return std::min(SN_MAXST, avail / (SN_CHUNK_DOUBLES * 8));
+// Launch shape of the solve: 16 consumer warps x 1 CTA per SM, or 8 x 2 (two
+// independent item streams per SM; better latency hiding when there are at
+// least two items per CTA).  cfg: 0 = automatic from the item count,
+// HPLMM_SN_CFG=16|8 forces one.
+int sn_solve_cfg(int nitems, int nsm) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("HPLMM_SN_CFG");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 8 || forced == 16) return forced;
+  return nitems >= 2 * nsm ? 8 : 16;
 }
 
-template <int NRHS>
+static int cfg_cps(int cons) { return cons == 8 ? 2 : 1; }
+
+int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons) {
+  const int p = cfg_cps(cons);
+  const long avail =
+      (226L * 1024) / p - 1024 - (long)sn_tail_doubles(max_n, max_r, nrhs, 32 * cons) * 8;
+  return (int)std::min<long>(SN_MAXST, avail / ((long)chunk * 8));
+}
+
+template <int NRHS, int CONS, int CPS>
 static void sn_solve_launch(const SnDev& d, const SnIO& io, const SnWork& wk, int stages,
-                            int max_n, size_t smem, cudaStream_t st) {
+                            int chunk, int max_n, int max_r, size_t smem, cudaStream_t st) {
   static size_t attr = 0;
   if (smem > attr) {
-    cudaFuncSetAttribute(k_sn_solve<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_sn_solve<NRHS, CONS, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = smem;
   }
-  k_sn_solve<NRHS><<<wk.nblocks, 32 * (SN_CONS + 1), smem, st>>>(d, io, wk, stages, max_n);
+  static int flags = -1;
+  if (flags < 0) {
+    const char* e = getenv("HPLMM_SN_FLAGS");
+    flags = e ? atoi(e) : 0;
+  }
+  k_sn_solve<NRHS, CONS, CPS><<<wk.nblocks, 32 * (CONS + 1), smem, st>>>(d, io, wk, stages, chunk,
+                                                                          max_n, max_r, flags);
+}
+
+template <int CONS, int CPS>
+static void sn_launch_nrhs(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int stages,
+                           int chunk, int max_n, int max_r, size_t smem, cudaStream_t st) {
+  if (nrhs == 1) sn_solve_launch<1, CONS, CPS>(d, io, wk, stages, chunk, max_n, max_r, smem, st);
+  else if (nrhs == 2) sn_solve_launch<2, CONS, CPS>(d, io, wk, stages, chunk, max_n, max_r, smem, st);
+  else sn_solve_launch<4, CONS, CPS>(d, io, wk, stages, chunk, max_n, max_r, smem, st);
 }
 
 void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
-                     cudaStream_t st) {
+                     int max_r, int chunk, int cons, cudaStream_t st) {
   if (wk.nblocks <= 0) return;
-  const int stages = sn_solve_stages(max_n, nrhs);
-  const size_t smem =
-      (size_t)stages * SN_CHUNK_DOUBLES * 8 + (size_t)(max_n + SN_MAX_WR + 4) * nrhs * 8;
-  if (nrhs == 1) sn_solve_launch<1>(d, io, wk, stages, max_n, smem, st);
-  else if (nrhs == 2) sn_solve_launch<2>(d, io, wk, stages, max_n, smem, st);
-  else sn_solve_launch<4>(d, io, wk, stages, max_n, smem, st);
+  const int stages = sn_solve_stages(max_n, max_r, nrhs, chunk, cons);
+  const size_t smem = ((size_t)stages * chunk + sn_tail_doubles(max_n, max_r, nrhs, 32 * cons)) * 8;
+  if (cons == 8) sn_launch_nrhs<8, 2>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
+  else sn_launch_nrhs<16, 1>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
 }
 
 // grain-batch layout views of a supernodal grain solve (for the per-RHS
@@ -560,6 +672,41 @@ void launch_tiles_to_finv(const DevBatch& b, const int32_t* list, int nlist, int
   k_tiles_to_finv<<<grid, 256, 0, st>>>(nlist, list, b.tile_base, b.nb, nm.sn_w, nm.sn_r,
                                         nm.sn_ldw, nm.sn_ldf, nm.sn_foff, b.tiles, factor);
 }
+// W_S^T copy (w x r, ld ldf) for the backward sweep; 32x32 tiles through smem
+__global__ void k_transpose_w(const int32_t* __restrict__ list, const int32_t* sn_w,
+                              const int32_t* sn_r, const int32_t* sn_ldw, const int32_t* sn_ldf,
+                              const int64_t* sn_foff, double* __restrict__ factor) {
+  __shared__ double tile[32][33];
+  const int sn = list[blockIdx.y];
+  const int w = sn_w[sn], r = sn_r[sn];
+  if (r == 0) return;
+  const int ldw = sn_ldw[sn], ldf = sn_ldf[sn];
+  const double* W = factor + sn_foff[sn] + sn_rows_doubles(r);
+  double* Wt = const_cast<double*>(W) + (int64_t)ldw * w + (int64_t)ldf * w;
+  const int ti = (r + 31) / 32, tj = (w + 31) / 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8 threads
+  for (int t = blockIdx.x; t < ti * tj; t += gridDim.x) {
+    const int i0 = (t % ti) * 32, j0 = (t / ti) * 32;
+    __syncthreads();
+    for (int y = ty; y < 32; y += 8) {
+      const int i = i0 + tx, j = j0 + y;
+      tile[y][tx] = (i < r && j < w) ? W[i + (int64_t)j * ldw] : 0.0;
+    }
+    __syncthreads();
+    for (int y = ty; y < 32; y += 8) {
+      const int j = j0 + tx, i = i0 + y;     // Wt[j, i] = W[i, j]
+      if (i < r && j < w) Wt[j + (int64_t)i * ldf] = tile[tx][y];
+    }
+  }
+}
+
+void launch_transpose_w(const int32_t* list, int nlist, const SnNum& nm, double* factor,
+                        cudaStream_t st) {
+  if (nlist <= 0) return;
+  k_transpose_w<<<dim3(16, nlist), 256, 0, st>>>(list, nm.sn_w, nm.sn_r, nm.sn_ldw, nm.sn_ldf,
+                                                 nm.sn_foff, factor);
+}
+
 __global__ void k_rows_to_factor(int nsn, const int32_t* sn_r, const int64_t* sn_foff,
                                  const int64_t* rows_off, const int32_t* rows, double* factor) {
   const int sn = blockIdx.x;

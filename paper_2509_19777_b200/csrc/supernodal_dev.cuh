@@ -37,6 +37,7 @@ struct SnIO {
 // descriptors are materialised in traversal order (flags mark item bounds)
 struct SnWork {
   int nblocks = 0;
+  int cons = 16;                        // consumer warps per CTA (8 => 2 CTAs per SM)
   const int32_t* item_ptr = nullptr;
   const int32_t* item_sub = nullptr;
   const int32_t* item_c0 = nullptr;
@@ -68,9 +69,10 @@ struct GemmProb {
   int pad;
 };
 
-int sn_solve_stages(int max_n, int nrhs);
+int sn_solve_cfg(int nitems, int nsm);   // consumer warps per CTA (8: two CTAs per SM)
+int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons);
 void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
-                     cudaStream_t st);
+                     int max_r, int chunk, int cons, cudaStream_t st);
 void launch_front_asm(const int32_t* list, int nlist, const SnNum& nm, const double* val,
                       cudaStream_t st);
 void launch_front_ext(const int32_t* list, int nlist, const SnNum& nm, cudaStream_t st);
@@ -80,6 +82,9 @@ void launch_tiles_to_finv(const DevBatch& b, const int32_t* list, int nlist, int
                           const SnNum& nm, double* factor, cudaStream_t st);
 void launch_sn_to_batch(int64_t nloc, const int32_t* lmap, const int32_t* gpos_sn, const double* b,
                         const double* ysn, double* xloc, double* yloc, cudaStream_t st);
+// W_S^T copies of the level's supernodes (after W_S is formed)
+void launch_transpose_w(const int32_t* list, int nlist, const SnNum& nm, double* factor,
+                        cudaStream_t st);
 // rows headers of every supernode into the factor array
 void launch_rows_to_factor(int nsn, const SnNum& nm, double* factor, cudaStream_t st);
 void launch_gemm_batched(const GemmProb* probs, const int32_t* work, int nwork, cudaStream_t st);

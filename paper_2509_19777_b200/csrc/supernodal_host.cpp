@@ -5,6 +5,7 @@
 // so the result is deterministic.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <numeric>
 #include <thread>
 
@@ -178,6 +179,18 @@ void analyse_one(const HostSetup& hs, const int32_t* gn, int m, int leaf, std::v
 
 }  // namespace
 
+int sn_chunk_doubles() {
+  static int v = [] {
+    const char* e = getenv("HPLMM_SN_CHUNK");
+    int c = e ? atoi(e) : SN_CHUNK_DOUBLES_MAX;
+    // >= 4096: the group-reduction scratch of the solve lives in one stage
+    if (c < SN_CHUNK_DOUBLES_MAX) c = SN_CHUNK_DOUBLES_MAX;
+    if (c > SN_CHUNK_DOUBLES_MAX) c = SN_CHUNK_DOUBLES_MAX;
+    return c;
+  }();
+  return v;
+}
+
 bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
                 const std::vector<int32_t>& nodes, int leaf, SnSymbolic& o, std::string& err) {
   const int nsub = (int)ptr.size() - 1;
@@ -238,7 +251,8 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
         for (int c = 0; c < 3; ++c) o.rows.push_back(3 * q + c);
       roff += rr;
       o.sn_foff.push_back(foff);
-      foff += sn_rows_doubles(rr) + (int64_t)o.sn_ldw.back() * w + (int64_t)o.sn_ldf.back() * w;
+      foff += sn_rows_doubles(rr) + (int64_t)o.sn_ldw.back() * w + (int64_t)o.sn_ldf.back() * w +
+              (int64_t)o.sn_ldf.back() * rr;
       o.max_w = std::max(o.max_w, w);
       o.max_r = std::max(o.max_r, rr);
       o.n_levels = std::max(o.n_levels, r.level[k] + 1);
@@ -256,16 +270,18 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     res[s] = SubResult();   // free
   }
   o.factor_doubles = foff;
+  o.chunk_doubles = sn_chunk_doubles();
   // TMA chunk schedule: forward = (W_S, rows, F_SS^-1) per S in postorder,
   // backward = (rows, W_S) per S in reverse postorder; W/F chunks are whole
   // columns of at most SN_CHUNK_DOUBLES.
   auto push = [&](int sn, int kind, int64_t off, int bytes, int c0, int nc, bool last) {
     SnChunk ch;
     ch.off = off;
-    // thread-group size for the rows of this part: TG = pow2 >= max(32, ceil(h/2)), <= 512
-    const int h = (kind == SN_F_FWD) ? o.sn_w[sn] : o.sn_r[sn];
+    // thread-group size for the rows of this part: TG = pow2 >= max(32, ceil(h/8)),
+    // so a thread holds up to 4 row pairs and the remaining threads take other columns
+    const int h = (kind == SN_F_FWD || kind == SN_WT_BWD) ? o.sn_w[sn] : o.sn_r[sn];
     int lg = 5;
-    while ((1 << lg) < (h + 1) / 2 && lg < 9) ++lg;
+    while ((1 << lg) < (h + 7) / 8 && lg < 9) ++lg;
     ch.bytes = bytes | ((lg - 5) << 24);
     ch.info = c0 | ((nc - 1) << 12) | (kind << 24) | (last ? SN_INFO_LAST : 0);
     ch.p0 = o.sn_p0[sn];
@@ -275,7 +291,7 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     o.chunks.push_back(ch);
   };
   auto cols = [&](int sn, int kind, int64_t off0, int ld, int ncols_total) {
-    const int per = std::max(1, SN_CHUNK_DOUBLES / ld);
+    const int per = std::max(1, o.chunk_doubles / ld);
     for (int c0 = 0; c0 < ncols_total; c0 += per) {
       int nc = std::min(per, ncols_total - c0);
       push(sn, kind, off0 + (int64_t)c0 * ld, nc * ld * 8, c0, nc, c0 + nc == ncols_total);
@@ -293,7 +309,7 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
         push(k, SN_ROWS_FWD, rows_at, (int)(8 * sn_rows_doubles(r)), 0, 1, true);
       }
       cols(k, SN_F_FWD, f_at, o.sn_ldf[k], w);
-      fb += 8 * (2 * sn_rows_doubles(r) + (int64_t)o.sn_ldw[k] * w * 2 + (int64_t)o.sn_ldf[k] * w);
+      fb += 8 * (2 * sn_rows_doubles(r) + (int64_t)o.sn_ldw[k] * w + (int64_t)o.sn_ldf[k] * (w + r));
     }
     o.sub_fc1.push_back((int64_t)o.chunks.size());
     o.sub_bc0.push_back((int64_t)o.chunks.size());
@@ -301,7 +317,9 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
       const int r = o.sn_r[k];
       if (r == 0) continue;
       push(k, SN_ROWS_BWD, o.sn_foff[k], (int)(8 * sn_rows_doubles(r)), 0, 1, true);
-      cols(k, SN_W_BWD, o.sn_foff[k] + sn_rows_doubles(r), o.sn_ldw[k], o.sn_w[k]);
+      const int64_t wt_at = o.sn_foff[k] + sn_rows_doubles(r) + (int64_t)o.sn_ldw[k] * o.sn_w[k] +
+                            (int64_t)o.sn_ldf[k] * o.sn_w[k];
+      cols(k, SN_WT_BWD, wt_at, o.sn_ldf[k], r);
     }
     o.sub_bc1.push_back((int64_t)o.chunks.size());
     o.sub_fbytes.push_back(fb);
