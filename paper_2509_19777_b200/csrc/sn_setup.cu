@@ -67,7 +67,12 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
       wgt.push_back(s.sub_fbytes[g] + 8 * (int64_t)s.sub_n[g] * 64);
     }
   }
-  wk.cons = force_cons ? force_cons : sn_solve_cfg((int)isub.size(), nblocks);
+  wk.cons = force_cons ? force_cons
+                       : sn_solve_cfg((int)isub.size(), nblocks, s.max_n, s.max_r, nrhs,
+                                      s.chunk_doubles);
+  if (wk.cons == 0)
+    throw SnError{-1, "subdomain of " + std::to_string(s.max_n) +
+                          " DOFs does not fit the supernodal solve's shared memory"};
   nblocks *= wk.cons == 8 ? 2 : 1;
   nblocks = std::max(1, std::min<int>(nblocks, (int)isub.size()));
   std::vector<int32_t> ptr, ids;
@@ -362,11 +367,14 @@ void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
                       const std::vector<int32_t>& kcols, const int64_t* d_b_off,
                       const int32_t* d_ld, const double* R, double* Bout) {
   int nrhs = 4;
-  int items = 0;
-  for (int k : kcols) items += (k + 3) / 4;
-  const int cons = sn_solve_cfg(items, nsm);
-  while (nrhs > 1 && sn_solve_stages(B.sym.max_n, B.sym.max_r, nrhs, B.sym.chunk_doubles, cons) < 2)
-    nrhs /= 2;
+  int cons = 0;
+  for (; nrhs >= 1; nrhs /= 2) {
+    int items = 0;
+    for (int k : kcols) items += (k + nrhs - 1) / nrhs;
+    cons = sn_solve_cfg(items, nsm, B.sym.max_n, B.sym.max_r, nrhs, B.sym.chunk_doubles);
+    if (cons) break;
+  }
+  if (!cons) throw SnError{-1, "shape-vector solve does not fit in shared memory"};
   SnWork wk;
   sn_build_work(B, A, st, nsm, nrhs, &kcols, wk, cons);
   SnIO io;

@@ -433,14 +433,21 @@ static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int nt) {
 // independent item streams per SM; better latency hiding when there are at
 // least two items per CTA).  cfg: 0 = automatic from the item count,
 // HPLMM_SN_CFG=16|8 forces one.
-int sn_solve_cfg(int nitems, int nsm) {
+int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons);
+
+int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk) {
   static int forced = -1;
   if (forced < 0) {
     const char* e = getenv("HPLMM_SN_CFG");
     forced = e ? atoi(e) : 0;
   }
-  if (forced == 8 || forced == 16) return forced;
-  return nitems >= 2 * nsm ? 8 : 16;
+  const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8) >= 2;
+  const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16) >= 2;
+  if (forced == 8 && fit8) return 8;
+  if (forced == 16 && fit16) return 16;
+  if (fit8 && nitems >= 2 * nsm) return 8;
+  if (fit16) return 16;
+  return 0;   // does not fit
 }
 
 static int cfg_cps(int cons) { return cons == 8 ? 2 : 1; }

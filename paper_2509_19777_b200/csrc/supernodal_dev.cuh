@@ -69,7 +69,9 @@ struct GemmProb {
   int pad;
 };
 
-int sn_solve_cfg(int nitems, int nsm);   // consumer warps per CTA (8: two CTAs per SM)
+// consumer warps per CTA (8: two CTAs per SM; 16: one), 0 if the subdomain
+// vectors do not fit in shared memory with >= 2 ring stages
+int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk);
 int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons);
 void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
                      int max_r, int chunk, int cons, cudaStream_t st);
