@@ -362,29 +362,113 @@ void sn_factor(SnBatch& B, const double* d_val, DevAlloc& A, cudaStream_t st, in
   SN_CK(cudaStreamSynchronize(st));
 }
 
-// shape vectors B_g = -A_g^-1 R_g (eq:col_pk) through the supernodal factor
+// shape vectors B_g = -A_g^-1 R_g (eq:col_pk) through the supernodal factor,
+// as a level-3 multi-RHS sweep: step t handles the t-th supernode (postorder)
+// of every grain at once with batched GEMMs
+//   forward : T = W_S X_S ; X_R -= T ; T = F_SS^-1 X_S ; X_S = T
+//   backward: T = X_R ; X_S -= W_S^T T
+// (sequential within a grain, so deterministic; all k_g columns at once).
 void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
                       const std::vector<int32_t>& kcols, const int64_t* d_b_off,
                       const int32_t* d_ld, const double* R, double* Bout) {
-  int nrhs = 4;
-  int cons = 0;
-  for (; nrhs >= 1; nrhs /= 2) {
-    int items = 0;
-    for (int k : kcols) items += (k + nrhs - 1) / nrhs;
-    cons = sn_solve_cfg(items, nsm, B.sym.max_n, B.sym.max_r, nrhs, B.sym.chunk_doubles);
-    if (cons) break;
+  (void)nsm;
+  const SnSymbolic& s = B.sym;
+  const int G = s.nsub;
+  std::vector<int64_t> xoff(G, 0);
+  int64_t xtot = 0, tmax = 0;
+  int maxsteps = 0;
+  for (int g = 0; g < G; ++g) {
+    xoff[g] = xtot;
+    xtot += (int64_t)s.sub_n[g] * kcols[g];
+    maxsteps = std::max(maxsteps, s.sub_sn1[g] - s.sub_sn0[g]);
   }
-  if (!cons) throw SnError{-1, "shape-vector solve does not fit in shared memory"};
-  SnWork wk;
-  sn_build_work(B, A, st, nsm, nrhs, &kcols, wk, cons);
-  SnIO io;
-  io.mode = 1;
-  io.in = R;
-  io.out = Bout;
-  io.bmap = B.d_lidx;
-  io.b_off = d_b_off;
-  io.ld = d_ld;
-  launch_sn_solve(B.dev, io, wk, nrhs, B.sym.max_n, B.sym.max_r, B.sym.chunk_doubles, wk.cons, st);
+  if (xtot == 0) return;
+  double* X = (double*)A.alloc((size_t)xtot * 8, true);
+  // temporaries: per grain max_S h_S x k_g, reused by every step
+  std::vector<int64_t> toff(G, 0);
+  for (int g = 0; g < G; ++g) {
+    int hmax = 0;
+    for (int k = s.sub_sn0[g]; k < s.sub_sn1[g]; ++k) hmax = std::max(hmax, std::max(s.sn_w[k], s.sn_r[k]));
+    toff[g] = tmax;
+    tmax += (int64_t)hmax * kcols[g];
+  }
+  double* T = (double*)A.alloc((size_t)std::max<int64_t>(tmax, 1) * 8, true);
+  int32_t* d_p0 = B.d_sn_p0;
+  SnNum nm;
+  nm.sn_w = B.d_sn_w;
+  nm.sn_r = B.d_sn_r;
+  nm.rows = B.d_rows;
+  nm.rows_off = B.d_sn_rows_off;
+
+  // items: one per grain for IO, one per (grain, supernode) per step
+  std::vector<SnMrItem> io_items, items;
+  std::vector<int64_t> step_ptr(maxsteps + 1, 0);
+  for (int g = 0; g < G; ++g)
+    if (kcols[g] > 0) io_items.push_back(SnMrItem{g, -1, s.sub_n[g], kcols[g], s.sub_base[g], xoff[g], 0});
+  for (int t = 0; t < maxsteps; ++t) {
+    for (int g = 0; g < G; ++g) {
+      const int k = s.sub_sn0[g] + t;
+      if (kcols[g] == 0 || k >= s.sub_sn1[g]) continue;
+      items.push_back(SnMrItem{g, k, s.sub_n[g], kcols[g], s.sub_base[g], xoff[g], toff[g]});
+    }
+    step_ptr[t + 1] = (int64_t)items.size();
+  }
+  SnMrItem* d_io = up(A, io_items, st, true);
+  SnMrItem* d_items = up(A, items, st, true);
+  // GEMM problems per item: 0 = W X_S, 1 = F^-1 X_S, 2 = X_S -= W^T T
+  std::vector<GemmProb> probs(items.size() * 3);
+  for (size_t q = 0; q < items.size(); ++q) {
+    const SnMrItem& m = items[q];
+    const int k = m.sn, w = s.sn_w[k], r = s.sn_r[k];
+    const double* W = B.factor + s.sn_foff[k] + sn_rows_doubles(r);
+    const double* F = W + (int64_t)s.sn_ldw[k] * w;
+    const double* Wt = F + (int64_t)s.sn_ldf[k] * w;
+    double* XS = X + m.xoff + s.sn_p0[k];
+    double* Tm = T + m.toff;
+    probs[3 * q + 0] = GemmProb{W, XS, Tm, r, m.k, w, s.sn_ldw[k], m.n, std::max(r, 1), 1.0, 0.0, 0, 0};
+    probs[3 * q + 1] = GemmProb{F, XS, Tm, w, m.k, w, s.sn_ldf[k], m.n, w, 1.0, 0.0, 0, 0};
+    probs[3 * q + 2] = GemmProb{Wt, Tm, XS, w, m.k, r, s.sn_ldf[k], std::max(r, 1), m.n, -1.0, 1.0, 0, 0};
+  }
+  GemmProb* d_probs = up(A, probs, st, true);
+  // tile work lists per (step, kind)
+  std::vector<int32_t> work;
+  std::vector<int64_t> wptr;   // [(t * 3 + kind) + 1]
+  wptr.push_back(0);
+  for (int t = 0; t < maxsteps; ++t)
+    for (int kind = 0; kind < 3; ++kind) {
+      for (int64_t q = step_ptr[t]; q < step_ptr[t + 1]; ++q) {
+        const GemmProb& gp = probs[3 * q + kind];
+        if (gp.m == 0 || gp.n == 0 || gp.k == 0) continue;
+        for (int ti = 0; ti < (gp.m + 63) / 64; ++ti)
+          for (int tj = 0; tj < (gp.n + 63) / 64; ++tj) {
+            work.push_back((int32_t)(3 * q + kind));
+            work.push_back(ti);
+            work.push_back(tj);
+          }
+      }
+      wptr.push_back((int64_t)work.size() / 3);
+    }
+  int32_t* d_work = up(A, work, st, true);
+  auto gemm = [&](int t, int kind) {
+    const int64_t a = wptr[t * 3 + kind], b = wptr[t * 3 + kind + 1];
+    if (b > a) launch_gemm_batched(d_probs, d_work + 3 * a, (int)(b - a), st);
+  };
+  launch_mr_io((int)io_items.size(), d_io, B.d_lidx, d_b_off, d_ld, R, X, nullptr, 1, st);
+  for (int t = 0; t < maxsteps; ++t) {
+    const int n = (int)(step_ptr[t + 1] - step_ptr[t]);
+    const SnMrItem* it = d_items + step_ptr[t];
+    gemm(t, 0);                                        // T = W_S X_S
+    launch_mr_rows(n, it, nm, d_p0, X, T, 0, st);      // X_R -= T
+    gemm(t, 1);                                        // T = F^-1 X_S
+    launch_mr_rows(n, it, nm, d_p0, X, T, 2, st);      // X_S = T
+  }
+  for (int t = maxsteps - 1; t >= 0; --t) {
+    const int n = (int)(step_ptr[t + 1] - step_ptr[t]);
+    const SnMrItem* it = d_items + step_ptr[t];
+    launch_mr_rows(n, it, nm, d_p0, X, T, 1, st);      // T = X_R
+    gemm(t, 2);                                        // X_S -= W^T T
+  }
+  launch_mr_io((int)io_items.size(), d_io, B.d_lidx, d_b_off, d_ld, nullptr, X, Bout, 0, st);
   SN_CK(cudaGetLastError());
 }
 

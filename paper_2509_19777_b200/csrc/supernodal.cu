@@ -714,6 +714,58 @@ void launch_transpose_w(const int32_t* list, int nlist, const SnNum& nm, double*
                                                  nm.sn_foff, factor);
 }
 
+// ---------------------------------------------------------------------------
+// multi-RHS sweeps (shape vectors): X (n x k col-major per subdomain, elimination
+// order) gathered from / written to the grain-batch row layout of R / B, and the
+// row gathers/scatters between GEMM steps.  One CTA per step item.
+// ---------------------------------------------------------------------------
+__global__ void k_mr_io(int nitems, const SnMrItem* __restrict__ it, const int32_t* __restrict__ lidx,
+                        const int64_t* __restrict__ b_off, const int32_t* __restrict__ ld,
+                        const double* __restrict__ R, double* __restrict__ X,
+                        double* __restrict__ B, int to_x) {
+  const SnMrItem m = it[blockIdx.x];
+  const int L = ld[m.g];
+  const int64_t tot = (int64_t)m.n * m.k;
+  for (int64_t t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int p = (int)(t % m.n), c = (int)(t / m.n);
+    const int64_t row = b_off[m.g] + (int64_t)lidx[m.base + p] * L + c;
+    if (to_x) X[m.xoff + t] = R[row];
+    else B[row] = -X[m.xoff + t];
+  }
+}
+
+// mode 0: X[rows] -= T   mode 1: T = X[rows]   mode 2: X[p0 + i] = T (i < w)
+__global__ void k_mr_rows(const SnMrItem* __restrict__ it, const int32_t* __restrict__ rows,
+                          const int64_t* __restrict__ rows_off, const int32_t* __restrict__ sn_r,
+                          const int32_t* __restrict__ sn_w, const int32_t* __restrict__ sn_p0,
+                          double* __restrict__ X, double* __restrict__ T, int mode) {
+  const SnMrItem m = it[blockIdx.x];
+  const int h = mode == 2 ? sn_w[m.sn] : sn_r[m.sn];
+  const int p0 = sn_p0[m.sn];
+  const int32_t* rw = rows + rows_off[m.sn];
+  const int64_t tot = (int64_t)h * m.k;
+  for (int64_t t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int i = (int)(t % h), c = (int)(t / h);
+    const int64_t xi = m.xoff + (int64_t)c * m.n + (mode == 2 ? p0 + i : rw[i]);
+    const int64_t ti = m.toff + t;
+    if (mode == 0) X[xi] -= T[ti];
+    else if (mode == 1) T[ti] = X[xi];
+    else X[xi] = T[ti];
+  }
+}
+
+void launch_mr_io(int nitems, const SnMrItem* it, const int32_t* lidx, const int64_t* b_off,
+                  const int32_t* ld, const double* R, double* X, double* B, int to_x,
+                  cudaStream_t st) {
+  if (nitems <= 0) return;
+  k_mr_io<<<nitems, 256, 0, st>>>(nitems, it, lidx, b_off, ld, R, X, B, to_x);
+}
+void launch_mr_rows(int nitems, const SnMrItem* it, const SnNum& nm, const int32_t* sn_p0,
+                    double* X, double* T, int mode, cudaStream_t st) {
+  if (nitems <= 0) return;
+  k_mr_rows<<<nitems, 256, 0, st>>>(it, nm.rows, nm.rows_off, nm.sn_r, nm.sn_w, sn_p0, X, T, mode);
+}
+
 __global__ void k_rows_to_factor(int nsn, const int32_t* sn_r, const int64_t* sn_foff,
                                  const int64_t* rows_off, const int32_t* rows, double* factor) {
   const int sn = blockIdx.x;

@@ -59,6 +59,16 @@ struct SnNum {
   double* pool = nullptr;
 };
 
+// one (subdomain, supernode) of a multi-RHS sweep step
+struct SnMrItem {
+  int g;          // subdomain
+  int sn;         // supernode (global index)
+  int n, k;       // subdomain DOFs, right-hand sides
+  int64_t base;   // offset of the subdomain's local positions (gmap / lidx)
+  int64_t xoff;   // X block of the subdomain (n x k col-major, ld n)
+  int64_t toff;   // temporary (h x k col-major, ld h)
+};
+
 struct GemmProb {
   const double* A;
   const double* B;
@@ -87,6 +97,11 @@ void launch_sn_to_batch(int64_t nloc, const int32_t* lmap, const int32_t* gpos_s
 // W_S^T copies of the level's supernodes (after W_S is formed)
 void launch_transpose_w(const int32_t* list, int nlist, const SnNum& nm, double* factor,
                         cudaStream_t st);
+void launch_mr_io(int nitems, const SnMrItem* it, const int32_t* lidx, const int64_t* b_off,
+                  const int32_t* ld, const double* R, double* X, double* B, int to_x,
+                  cudaStream_t st);
+void launch_mr_rows(int nitems, const SnMrItem* it, const SnNum& nm, const int32_t* sn_p0,
+                    double* X, double* T, int mode, cudaStream_t st);
 // rows headers of every supernode into the factor array
 void launch_rows_to_factor(int nsn, const SnNum& nm, double* factor, cudaStream_t st);
 void launch_gemm_batched(const GemmProb* probs, const int32_t* work, int nwork, cudaStream_t st);
