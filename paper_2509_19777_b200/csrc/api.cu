@@ -7,6 +7,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -98,10 +99,15 @@ struct hplmm_handle {
   bool sparse() const { return hs.opt.local_factor == 1; }
   int64_t launches = 0;
 
+  size_t alloc_bytes = 0, alloc_peak = 0;
   template <class T>
   T* dalloc(size_t n, bool setup_only = false) {
     void* p = nullptr;
     if (n == 0) n = 1;
+    static const bool dbg = getenv("HPLMM_DEBUG_ALLOC") != nullptr;
+    if (dbg && n * sizeof(T) > ((size_t)256 << 20))
+      fprintf(stderr, "hplmm alloc %.3f GB (%s), total %.3f GB\n", n * sizeof(T) / 1e9,
+              setup_only ? "setup" : "kept", (alloc_bytes + n * sizeof(T)) / 1e9);
     cudaError_t e = cudaMalloc(&p, n * sizeof(T));
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -109,6 +115,8 @@ struct hplmm_handle {
                                       cudaGetErrorString(e)};
     }
     (setup_only ? setup_allocs : allocs).push_back(p);
+    alloc_bytes += n * sizeof(T);
+    alloc_peak = std::max(alloc_peak, alloc_bytes);
     return (T*)p;
   }
   template <class T>
@@ -120,6 +128,7 @@ struct hplmm_handle {
   void free_setup() {
     for (void* p : setup_allocs) cudaFree(p);
     setup_allocs.clear();
+    alloc_bytes = 0;   // approximate after the setup-only buffers are released
   }
   ~hplmm_handle() {
     if (device >= 0) {
@@ -804,7 +813,13 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       std::vector<int32_t> kc(G);
       for (int g = 0; g < G; ++g) kc[g] = ld[g] - 1;
       if (sparse)
-        sn_shape_vectors(h->sg, halloc, h->st, h->nsm, kc, co.b_off, co.ld, co.R, co.B);
+      {
+        // R serves as the workspace of the multi-RHS sweep; rebuild it for S
+        sn_shape_vectors(h->sg, halloc, h->st, h->nsm, kc, co.b_off, co.ld, co.R, co.B,
+                         std::max<int64_t>(off, 1));
+        CK(cudaMemsetAsync(co.R, 0, std::max<int64_t>(off, 1) * 8, h->st));
+        launch_build_R(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
+      }
       else
         launch_symm_neg(h->gb, co.b_off, co.ld, h->upload(kc), (maxk + TB - 1) / TB, co.R, co.B,
                         h->st);
@@ -812,13 +827,23 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     launch_grain_AB(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
     launch_grain_BtY(co, h->gb, h->st);
     int64_t npS = (int64_t)TB * h->sb.max_nb;
-    h->lds = npS;
+    // small S: dense copy kept for export (HPLMM_ART_S); large S (cfg5: 67 GB
+    // dense) is assembled straight into the packed lower tiles
     bool keepS = (npS * npS * 8) <= (int64_t)512 << 20;
-    h->d_Sdense = h->dalloc<double>(std::max<int64_t>(npS * npS, 1), !keepS);
-    CK(cudaMemsetAsync(h->d_Sdense, 0, std::max<int64_t>(npS * npS, 1) * 8, h->st));
-    launch_S_iface(co, h->d_row_ptr, h->d_col, h->d_val, h->d_Sdense, npS, h->st);
-    launch_S_grain(co, h->d_Sdense, npS, h->st);
-    launch_pack_dense(h->sb, h->d_Sdense, npS, h->st);
+    if (keepS) {
+      h->lds = npS;
+      h->d_Sdense = h->dalloc<double>(std::max<int64_t>(npS * npS, 1));
+      CK(cudaMemsetAsync(h->d_Sdense, 0, std::max<int64_t>(npS * npS, 1) * 8, h->st));
+      launch_S_iface(co, h->d_row_ptr, h->d_col, h->d_val, h->d_Sdense, npS, h->st);
+      launch_S_grain(co, h->d_Sdense, npS, h->st);
+      launch_pack_dense(h->sb, h->d_Sdense, npS, h->st);
+    } else {
+      h->lds = 0;
+      h->d_Sdense = nullptr;
+      CK(cudaMemsetAsync(h->sb.tiles, 0, (size_t)h->sb.ntiles * TILE * 8, h->st));
+      launch_S_iface(co, h->d_row_ptr, h->d_col, h->d_val, h->sb.tiles, 0, h->st);
+      launch_S_grain(co, h->sb.tiles, 0, h->st);
+    }
     launch_pad_identity(h->sb, h->st);
     if (hs.opt.coarse_refine) {
       h->sS = h->sb;
@@ -833,7 +858,6 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     check_batch_err(h, h->sb, 0, true);
     h->rep.t_setup_coarse_s = tc.stop();
     CK(cudaStreamSynchronize(h->st));
-    if (!keepS) h->d_Sdense = nullptr;
     h->free_setup();
     h->gb.dinv = h->gb.cbuf = h->gb.wbuf = nullptr;
     h->cb.dinv = h->cb.cbuf = h->cb.wbuf = nullptr;

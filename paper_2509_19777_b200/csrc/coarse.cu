@@ -131,6 +131,18 @@ void launch_grain_BtY(const DevCoarse& c, const DevBatch& gb, cudaStream_t st) {
 // Interface-row part of S = P_B^T (A^ P_B):  for every interface DOF d,
 //   S[k, :] += Q^o[d,k] * (A^[d,:] P_B)       (one CTA per interface; rows k
 // of S belong to exactly one interface, so CTAs never share an entry)
+// S entry (k, j) += v: dense row-major (lds > 0), or straight into the packed
+// lower 64-tiles of the coarse batch (lds == 0; entries above the diagonal are
+// dropped -- S is taken from its lower triangle either way, R16)
+__device__ __forceinline__ void s_add(double* S, int64_t lds, int k, int j, double v) {
+  if (lds > 0) {
+    S[(int64_t)k * lds + j] += v;
+  } else if (k >= j) {
+    const int64_t I = k >> 6, J = j >> 6;
+    S[(I * (I + 1) / 2 + J) * TILE + (k & 63) + 64 * (j & 63)] += v;
+  }
+}
+
 __global__ void k_S_iface(DevCoarse c, const int32_t* rp, const int32_t* col, const double* val,
                           double* S, int64_t lds) {
   int cf = blockIdx.x;
@@ -153,7 +165,7 @@ __global__ void k_S_iface(DevCoarse c, const int32_t* rp, const int32_t* col, co
             const int32_t* cols = c.gcols + c.gcols_ptr[g];
             for (int t = threadIdx.x; t < nu * k; t += blockDim.x) {
               int i = t / k, j = t - i * k;
-              S[(int64_t)(kbase + 3 * i + gam) * lds + cols[j]] += wy[i] * aa * Brow[j];
+              s_add(S, lds, kbase + 3 * i + gam, cols[j], wy[i] * aa * Brow[j]);
             }
           } else {                           // interface row of P_B (Q^o)
             int nq = c.mortar_ptr[cq + 1] - c.mortar_ptr[cq];
@@ -161,7 +173,7 @@ __global__ void k_S_iface(DevCoarse c, const int32_t* rp, const int32_t* col, co
             int qbase = 3 * c.mortar_ptr[cq];
             for (int t = threadIdx.x; t < nu * nq; t += blockDim.x) {
               int i = t / nq, i2 = t - i * nq;
-              S[(int64_t)(kbase + 3 * i + gam) * lds + qbase + 3 * i2 + c3] += wy[i] * aa * wq[i2];
+              s_add(S, lds, kbase + 3 * i + gam, qbase + 3 * i2 + c3, wy[i] * aa * wq[i2]);
             }
           }
           __syncthreads();
@@ -186,7 +198,7 @@ __global__ void k_S_grain(DevCoarse c, double* S, int64_t lds) {
     int k = c.ld[g] - 1;
     const double* C = c.Cg + c.cg_off[g] + (int64_t)jk * k;
     const int32_t* cols = c.gcols + c.gcols_ptr[g];
-    for (int j = threadIdx.x; j < k; j += blockDim.x) S[(int64_t)kk * lds + cols[j]] += C[j];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) s_add(S, lds, kk, cols[j], C[j]);
     __syncthreads();
   }
 }

@@ -355,7 +355,6 @@ void sn_factor(SnBatch& B, const double* d_val, DevAlloc& A, cudaStream_t st, in
         h2d(d_work, work.data(), work.size() * 4);
         launch_gemm_batched(d_probs, d_work, (int)(work.size() / 3), st);
         SN_CK(cudaGetLastError());
-        if (phase == 0) launch_transpose_w(d_list, nl, nm, B.factor, st);
       }
     }
   }
@@ -370,7 +369,7 @@ void sn_factor(SnBatch& B, const double* d_val, DevAlloc& A, cudaStream_t st, in
 // (sequential within a grain, so deterministic; all k_g columns at once).
 void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
                       const std::vector<int32_t>& kcols, const int64_t* d_b_off,
-                      const int32_t* d_ld, const double* R, double* Bout) {
+                      const int32_t* d_ld, double* R, double* Bout, int64_t rb_doubles) {
   (void)nsm;
   const SnSymbolic& s = B.sym;
   const int G = s.nsub;
@@ -383,7 +382,13 @@ void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
     maxsteps = std::max(maxsteps, s.sub_sn1[g] - s.sub_sn0[g]);
   }
   if (xtot == 0) return;
-  double* X = (double*)A.alloc((size_t)xtot * 8, true);
+  // X (elimination order, n x k per grain) lives in R's memory: R is first
+  // copied into B's storage (same row layout; its zero padding rows and zero
+  // correction column are what B needs there), X is gathered from that copy,
+  // and the result is written back into B with the sign of eq:col_pk
+  if (xtot > rb_doubles) throw SnError{-1, "shape-vector workspace larger than R"};
+  SN_CK(cudaMemcpyAsync(Bout, R, (size_t)rb_doubles * 8, cudaMemcpyDeviceToDevice, st));
+  double* X = R;
   // temporaries: per grain max_S h_S x k_g, reused by every step
   std::vector<int64_t> toff(G, 0);
   for (int g = 0; g < G; ++g) {
@@ -422,12 +427,12 @@ void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
     const int k = m.sn, w = s.sn_w[k], r = s.sn_r[k];
     const double* W = B.factor + s.sn_foff[k] + sn_rows_doubles(r);
     const double* F = W + (int64_t)s.sn_ldw[k] * w;
-    const double* Wt = F + (int64_t)s.sn_ldf[k] * w;
     double* XS = X + m.xoff + s.sn_p0[k];
     double* Tm = T + m.toff;
     probs[3 * q + 0] = GemmProb{W, XS, Tm, r, m.k, w, s.sn_ldw[k], m.n, std::max(r, 1), 1.0, 0.0, 0, 0};
     probs[3 * q + 1] = GemmProb{F, XS, Tm, w, m.k, w, s.sn_ldf[k], m.n, w, 1.0, 0.0, 0, 0};
-    probs[3 * q + 2] = GemmProb{Wt, Tm, XS, w, m.k, r, s.sn_ldf[k], std::max(r, 1), m.n, -1.0, 1.0, 0, 0};
+    // X_S -= W_S^T T  (transA)
+    probs[3 * q + 2] = GemmProb{W, Tm, XS, w, m.k, r, s.sn_ldw[k], std::max(r, 1), m.n, -1.0, 1.0, 0, 1};
   }
   GemmProb* d_probs = up(A, probs, st, true);
   // tile work lists per (step, kind)
@@ -453,7 +458,7 @@ void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
     const int64_t a = wptr[t * 3 + kind], b = wptr[t * 3 + kind + 1];
     if (b > a) launch_gemm_batched(d_probs, d_work + 3 * a, (int)(b - a), st);
   };
-  launch_mr_io((int)io_items.size(), d_io, B.d_lidx, d_b_off, d_ld, R, X, nullptr, 1, st);
+  launch_mr_io((int)io_items.size(), d_io, B.d_lidx, d_b_off, d_ld, Bout, X, nullptr, 1, st);
   for (int t = 0; t < maxsteps; ++t) {
     const int n = (int)(step_ptr[t + 1] - step_ptr[t]);
     const SnMrItem* it = d_items + step_ptr[t];

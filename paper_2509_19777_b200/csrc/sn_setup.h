@@ -48,8 +48,9 @@ void sn_factor(SnBatch& B, const double* d_val, DevAlloc& A, cudaStream_t st,
 // yloc = A_s^-1 in[gmap] for every subdomain of the batch
 void sn_apply(const SnBatch& B, const double* in, cudaStream_t st);
 // B_g[:, 0:k_g] = -A_g^-1 R_g[:, 0:k_g] (grain batch, gb row layout)
+// (R is overwritten: it serves as the workspace; rb_doubles = size of R and B)
 void sn_shape_vectors(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm,
                       const std::vector<int32_t>& kcols, const int64_t* d_b_off,
-                      const int32_t* d_ld, const double* R, double* Bout);
+                      const int32_t* d_ld, double* R, double* Bout, int64_t rb_doubles);
 
 }  // namespace hplmm

@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     const int cs = s;
     const long long t_k0 = prof ? clock64() : 0;
     if (++s == stages) { s = 0; ph ^= 1; }
-    if (kind == SN_W_FWD || kind == SN_F_FWD || kind == SN_WT_BWD) {
-      // row-parallel gemv on a column chunk: W_S (fwd), F_SS^-1, W_S^T (bwd)
+    if (kind == SN_W_FWD || kind == SN_F_FWD) {
+      // row-parallel gemv on a column chunk: W_S, F_SS^-1
       const int h = kind == SN_W_FWD ? r : w;
       const int ld = h + (h & 1);
       const RowLayout L(sn_lg<NRHS>(lgc, h), tid, SN_NT);
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
 #pragma unroll
             for (int cr = 0; cr < NRHS; ++cr) acc[q][e][cr] = 0.0;
       }
-      const double* xcol = kind == SN_WT_BWD ? xr + (size_t)cc0 * NRHS : x + (size_t)(p0 + cc0) * NRHS;
+      const double* xcol = x + (size_t)(p0 + cc0) * NRHS;
       const int nq = (h + 2 * L.TG - 1) / (2 * L.TG);
       if (nq <= 1) sn_rows<1, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
       else if (nq == 2) sn_rows<2, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
         }
         if (kind == SN_W_FWD) {
         } else {
-          if (L.G == 1 && kind == SN_F_FWD) PSYNC();   // every thread is done reading x_S
+          if (L.G == 1) PSYNC();   // every thread is done reading x_S
           if (L.g == 0) {
 #pragma unroll
             for (int q = 0; q < SN_MAXQ; ++q)
@@ -352,10 +352,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
                 const int i = 2 * (L.t + q * L.TG) + e;
                 if (i < w) {
 #pragma unroll
-                  for (int cr = 0; cr < NRHS; ++cr) {
-                    double& xv = x[(p0 + i) * NRHS + cr];
-                    xv = kind == SN_F_FWD ? acc[q][e][cr] : xv - acc[q][e][cr];
-                  }
+                  for (int cr = 0; cr < NRHS; ++cr) x[(p0 + i) * NRHS + cr] = acc[q][e][cr];
                 }
               }
           }
@@ -393,6 +390,53 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[cs]);
       PSYNC();
+    } else {  // SN_W_BWD: x_S[j] -= W[:,j] . x_R, LPC lanes per column
+      const int ld = r + (r & 1);
+      const int lpc = r > 256 ? 32 : (r > 128 ? 16 : 8);
+      const int cpw = 32 / lpc;                    // columns per warp pass
+      const int sl = lane & (lpc - 1), cl = lane / lpc;
+      for (int j0 = warp * cpw; j0 < nc; j0 += SN_CONS * cpw) {
+        const int jj = j0 + cl;
+        double sum[NRHS];
+#pragma unroll
+        for (int cr = 0; cr < NRHS; ++cr) sum[cr] = 0.0;
+        if (jj < nc) {
+          const double* col = st + (size_t)jj * ld;
+          int i = 2 * sl;
+          if (NRHS == 1) {
+            double s2 = 0.0;
+            for (; i + 2 * lpc < r; i += 4 * lpc) {
+              const double2 a = *reinterpret_cast<const double2*>(col + i);
+              const double2 b = *reinterpret_cast<const double2*>(col + i + 2 * lpc);
+              const double2 xa = *reinterpret_cast<const double2*>(xr + i);
+              const double2 xb = *reinterpret_cast<const double2*>(xr + i + 2 * lpc);
+              sum[0] = fma(a.x, xa.x, fma(a.y, xa.y, sum[0]));
+              s2 = fma(b.x, xb.x, fma(b.y, xb.y, s2));
+            }
+            sum[0] += s2;
+          }
+          for (; i < r; i += 2 * lpc) {
+            const double2 a = *reinterpret_cast<const double2*>(col + i);
+#pragma unroll
+            for (int cr = 0; cr < NRHS; ++cr)
+              sum[cr] = fma(a.x, xr[i * NRHS + cr], fma(a.y, xr[(i + 1) * NRHS + cr], sum[cr]));
+          }
+        }
+#pragma unroll
+        for (int cr = 0; cr < NRHS; ++cr) {
+          for (int o = lpc >> 1; o > 0; o >>= 1) sum[cr] += __shfl_xor_sync(0xffffffffu, sum[cr], o);
+        }
+        if (jj < nc && sl < NRHS) {
+          double v = sum[0];
+#pragma unroll
+          for (int cr = 1; cr < NRHS; ++cr)
+            if (sl == cr) v = sum[cr];
+          x[(p0 + cc0 + jj) * NRHS + sl] -= v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);
+      if (last) PSYNC();
     }
     if (prof) {
       t_kind[kind] += clock64() - t_k0;
@@ -619,7 +663,9 @@ __global__ void __launch_bounds__(256) k_gemm_batched(const GemmProb* __restrict
     for (int e = threadIdx.x; e < 1024; e += 256) {
       const int r = e & 63, kk = e >> 6;
       const int gi = i0 + r, gk = k0 + kk;
-      As[kk][r] = (gi < g.m && gk < g.k) ? g.A[gi + (int64_t)gk * g.lda] : 0.0;
+      As[kk][r] = (gi < g.m && gk < g.k)
+                      ? (g.transA ? g.A[gk + (int64_t)gi * g.lda] : g.A[gi + (int64_t)gk * g.lda])
+                      : 0.0;
       const int gj = j0 + r;
       double bv = 0.0;
       if (gj < g.n && gk < g.k) bv = g.transB ? g.B[gj + (int64_t)gk * g.ldb] : g.B[gk + (int64_t)gj * g.ldb];
@@ -679,41 +725,6 @@ void launch_tiles_to_finv(const DevBatch& b, const int32_t* list, int nlist, int
   k_tiles_to_finv<<<grid, 256, 0, st>>>(nlist, list, b.tile_base, b.nb, nm.sn_w, nm.sn_r,
                                         nm.sn_ldw, nm.sn_ldf, nm.sn_foff, b.tiles, factor);
 }
-// W_S^T copy (w x r, ld ldf) for the backward sweep; 32x32 tiles through smem
-__global__ void k_transpose_w(const int32_t* __restrict__ list, const int32_t* sn_w,
-                              const int32_t* sn_r, const int32_t* sn_ldw, const int32_t* sn_ldf,
-                              const int64_t* sn_foff, double* __restrict__ factor) {
-  __shared__ double tile[32][33];
-  const int sn = list[blockIdx.y];
-  const int w = sn_w[sn], r = sn_r[sn];
-  if (r == 0) return;
-  const int ldw = sn_ldw[sn], ldf = sn_ldf[sn];
-  const double* W = factor + sn_foff[sn] + sn_rows_doubles(r);
-  double* Wt = const_cast<double*>(W) + (int64_t)ldw * w + (int64_t)ldf * w;
-  const int ti = (r + 31) / 32, tj = (w + 31) / 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8 threads
-  for (int t = blockIdx.x; t < ti * tj; t += gridDim.x) {
-    const int i0 = (t % ti) * 32, j0 = (t / ti) * 32;
-    __syncthreads();
-    for (int y = ty; y < 32; y += 8) {
-      const int i = i0 + tx, j = j0 + y;
-      tile[y][tx] = (i < r && j < w) ? W[i + (int64_t)j * ldw] : 0.0;
-    }
-    __syncthreads();
-    for (int y = ty; y < 32; y += 8) {
-      const int j = j0 + tx, i = i0 + y;     // Wt[j, i] = W[i, j]
-      if (i < r && j < w) Wt[j + (int64_t)i * ldf] = tile[tx][y];
-    }
-  }
-}
-
-void launch_transpose_w(const int32_t* list, int nlist, const SnNum& nm, double* factor,
-                        cudaStream_t st) {
-  if (nlist <= 0) return;
-  k_transpose_w<<<dim3(16, nlist), 256, 0, st>>>(list, nm.sn_w, nm.sn_r, nm.sn_ldw, nm.sn_ldf,
-                                                 nm.sn_foff, factor);
-}
-
 // ---------------------------------------------------------------------------
 // multi-RHS sweeps (shape vectors): X (n x k col-major per subdomain, elimination
 // order) gathered from / written to the grain-batch row layout of R / B, and the

@@ -14,9 +14,11 @@
 // and a solve A_s x = b is
 //     forward  (postorder):         b_R -= W_S b_S ;  b_S <- F_SS^-1 b_S
 //     backward (reverse postorder): x_S -= W_S^T x_R
-// so the factor is W_S (r x w), F_SS^-1 (w x w) and a copy of W_S^T (w x r),
-// all col-major, so that every sweep is a row-parallel gemv (no per-column
-// reductions); a solve streams 2 r w + w^2 doubles per supernode.
+// so the factor is W_S (r x w) and F_SS^-1 (w x w), both col-major; a solve
+// streams W_S twice (forward gemv, backward column dot products) and F_SS^-1
+// once: 2 r w + w^2 doubles per supernode.  (A transposed copy of W_S made the
+// backward sweep a row-parallel gemv as well, measured no faster, and cost a
+// third more memory -- cfg5 does not fit with it.)
 #pragma once
 #include <cstdint>
 #include <string>
@@ -34,7 +36,7 @@ constexpr int SN_MAX_WR = 2048;          // max w and max r (DOFs) per supernode
 // backward per S: ROWS_BWD, W_BWD..).  ROWS chunks carry the supernode's row
 // list (int32) so the scatter/gather of x_R never waits on a global load.
 enum SnChunkKind : int32_t {
-  SN_W_FWD = 0, SN_F_FWD = 1, SN_WT_BWD = 2, SN_ROWS_FWD = 3, SN_ROWS_BWD = 4
+  SN_W_FWD = 0, SN_F_FWD = 1, SN_W_BWD = 2, SN_ROWS_FWD = 3, SN_ROWS_BWD = 4
 };
 
 // one TMA chunk of the solve stream, denormalised so that the consumer needs
@@ -79,7 +81,6 @@ struct SnSymbolic {
   std::vector<int32_t> rows;               // struct rows: local DOF positions (ascending)
   std::vector<SnChunk> chunks;             // per subdomain: [fc0,fc1) forward, [bc0,bc1) backward
   int64_t factor_doubles = 0;              // layout per S: [rows][W_S: ldw x w][F_SS^-1: ldf x w]
-                                           //                [W_S^T: ldf x r]
   // numeric setup: A-blocks scattered into each front, child -> parent maps
   std::vector<int64_t> asm_ptr;            // [nsn+1]
   std::vector<int64_t> asm_e;              // BSR block index (row node v in S, col node u)

@@ -76,7 +76,7 @@ struct GemmProb {
   int m, n, k, lda, ldb, ldc;
   double alpha, beta;
   int transB;
-  int pad;
+  int transA;     // op(A) = A^T: A stored k x m (lda >= k)
 };
 
 // consumer warps per CTA (8: two CTAs per SM; 16: one), 0 if the subdomain
@@ -94,9 +94,6 @@ void launch_tiles_to_finv(const DevBatch& b, const int32_t* list, int nlist, int
                           const SnNum& nm, double* factor, cudaStream_t st);
 void launch_sn_to_batch(int64_t nloc, const int32_t* lmap, const int32_t* gpos_sn, const double* b,
                         const double* ysn, double* xloc, double* yloc, cudaStream_t st);
-// W_S^T copies of the level's supernodes (after W_S is formed)
-void launch_transpose_w(const int32_t* list, int nlist, const SnNum& nm, double* factor,
-                        cudaStream_t st);
 void launch_mr_io(int nitems, const SnMrItem* it, const int32_t* lidx, const int64_t* b_off,
                   const int32_t* ld, const double* R, double* X, double* B, int to_x,
                   cudaStream_t st);

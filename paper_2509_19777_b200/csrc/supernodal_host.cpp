@@ -251,8 +251,7 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
         for (int c = 0; c < 3; ++c) o.rows.push_back(3 * q + c);
       roff += rr;
       o.sn_foff.push_back(foff);
-      foff += sn_rows_doubles(rr) + (int64_t)o.sn_ldw.back() * w + (int64_t)o.sn_ldf.back() * w +
-              (int64_t)o.sn_ldf.back() * rr;
+      foff += sn_rows_doubles(rr) + (int64_t)o.sn_ldw.back() * w + (int64_t)o.sn_ldf.back() * w;
       o.max_w = std::max(o.max_w, w);
       o.max_r = std::max(o.max_r, rr);
       o.n_levels = std::max(o.n_levels, r.level[k] + 1);
@@ -279,7 +278,7 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     ch.off = off;
     // thread-group size for the rows of this part: TG = pow2 >= max(32, ceil(h/8)),
     // so a thread holds up to 4 row pairs and the remaining threads take other columns
-    const int h = (kind == SN_F_FWD || kind == SN_WT_BWD) ? o.sn_w[sn] : o.sn_r[sn];
+    const int h = (kind == SN_F_FWD) ? o.sn_w[sn] : o.sn_r[sn];
     int lg = 5;
     while ((1 << lg) < (h + 7) / 8 && lg < 9) ++lg;
     ch.bytes = bytes | ((lg - 5) << 24);
@@ -309,7 +308,7 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
         push(k, SN_ROWS_FWD, rows_at, (int)(8 * sn_rows_doubles(r)), 0, 1, true);
       }
       cols(k, SN_F_FWD, f_at, o.sn_ldf[k], w);
-      fb += 8 * (2 * sn_rows_doubles(r) + (int64_t)o.sn_ldw[k] * w + (int64_t)o.sn_ldf[k] * (w + r));
+      fb += 8 * (2 * sn_rows_doubles(r) + 2 * (int64_t)o.sn_ldw[k] * w + (int64_t)o.sn_ldf[k] * w);
     }
     o.sub_fc1.push_back((int64_t)o.chunks.size());
     o.sub_bc0.push_back((int64_t)o.chunks.size());
@@ -317,9 +316,7 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
       const int r = o.sn_r[k];
       if (r == 0) continue;
       push(k, SN_ROWS_BWD, o.sn_foff[k], (int)(8 * sn_rows_doubles(r)), 0, 1, true);
-      const int64_t wt_at = o.sn_foff[k] + sn_rows_doubles(r) + (int64_t)o.sn_ldw[k] * o.sn_w[k] +
-                            (int64_t)o.sn_ldf[k] * o.sn_w[k];
-      cols(k, SN_WT_BWD, wt_at, o.sn_ldf[k], r);
+      cols(k, SN_W_BWD, o.sn_foff[k] + sn_rows_doubles(r), o.sn_ldw[k], o.sn_w[k]);
     }
     o.sub_bc1.push_back((int64_t)o.chunks.size());
     o.sub_fbytes.push_back(fb);
