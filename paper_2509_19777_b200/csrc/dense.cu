@@ -13,6 +13,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "dmma.cuh"
 #include "tma.cuh"
 
 namespace hplmm {
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(256) k_sweep_pivot(int p, int nsub, const int3
 }
 
 // C_i = A_ip (old), W_i = C_i D^-1 for every row block i != p
+template <bool DMMA>
 __global__ void __launch_bounds__(256) k_sweep_panel(int p, int64_t nrows, const int32_t* row_s,
                                                      const int32_t* row_k, const int32_t* nb,
                                                      const int64_t* tile_base,
@@ -180,20 +182,34 @@ __global__ void __launch_bounds__(256) k_sweep_panel(int p, int64_t nrows, const
   else load_tile_T(As, tiles + tidx(tile_base, s, p, i) * TILE);
   load_tile(Bs, dinv + (int64_t)s * TILE);   // (k,c) at c*64+k; D^-1 symmetric
   __syncthreads();
-  int r0 = (threadIdx.x & 15) * 4, c0 = (threadIdx.x >> 4) * 4;
-  double acc[4][4] = {};
-  // Bs is used as Bs[k*64 + c] = D^-1[c][k] = D^-1[k][c]
-  tile_mma(As, Bs, acc, r0, c0);
   double* W = wbuf + rb * TILE;
   double* C = cbuf + rb * TILE;
   for (int t = threadIdx.x; t < TILE / 2; t += blockDim.x)
     reinterpret_cast<double2*>(C)[t] = reinterpret_cast<const double2*>(As)[t];
+  // Bs is used as Bs[k*64 + c] = D^-1[c][k] = D^-1[k][c]
+  if (DMMA) {
+    double acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+    tile_dmma(As, TB, Bs, TB, TB, acc);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      int r, c;
+      dmma_rc(t, r, c);
+      W[c * TB + r] = acc[t];
+    }
+    return;
+  }
+  int r0 = (threadIdx.x & 15) * 4, c0 = (threadIdx.x >> 4) * 4;
+  double acc[4][4] = {};
+  tile_mma(As, Bs, acc, r0, c0);
 #pragma unroll
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int i2 = 0; i2 < 4; ++i2) W[(c0 + j) * TB + r0 + i2] = acc[i2][j];
 }
 
+template <bool DMMA>
 __global__ void __launch_bounds__(256) k_sweep_update(int p, int64_t ntiles, const int32_t* tile_s,
                                                       const int32_t* tile_ij, const int32_t* nb,
                                                       const int64_t* row_base, double* tiles,
@@ -229,6 +245,20 @@ __global__ void __launch_bounds__(256) k_sweep_update(int p, int64_t ntiles, con
   load_tile(As, wbuf + (row_base[s] + I) * TILE);   // W_I (r,k) at k*64+r
   load_tile(Bs, cbuf + (row_base[s] + J) * TILE);   // C_J (c,k) at k*64+c  == (C_J^T)(k,c)
   __syncthreads();
+  if (DMMA) {
+    double acc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+    tile_dmma(As, TB, Bs, TB, TB, acc);
+#pragma unroll
+    for (int q = 0; q < 16; q += 2) {
+      int r, c;
+      dmma_rc(q, r, c);                 // (r, c), (r, c + 1)
+      T[c * TB + r] -= acc[q];
+      T[(c + 1) * TB + r] -= acc[q + 1];
+    }
+    return;
+  }
   int r0 = (threadIdx.x & 15) * 4, c0 = (threadIdx.x >> 4) * 4;
   double acc[4][4] = {};
   tile_mma(As, Bs, acc, r0, c0);
@@ -247,28 +277,47 @@ __global__ void k_negate(int64_t n, double* x) {
     x[i] = -x[i];
 }
 
+static int g_dmma = -1;   // FP64 tensor cores (DMMA) in the setup tile products; HPLMM_DMMA=0 off
+
+bool use_dmma() {
+  if (g_dmma < 0) {
+    const char* e = getenv("HPLMM_DMMA");
+    g_dmma = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_dmma == 1;
+}
+
+template <bool DMMA>
+static void sweep_steps(const DevBatch& b, cudaStream_t st) {
+  size_t sm1 = (TILE + TB) * sizeof(double);
+  size_t sm2 = 2 * TILE * sizeof(double);
+  for (int p = 0; p < b.max_nb; ++p) {
+    k_sweep_pivot<<<b.nsub, 256, sm1, st>>>(p, b.nsub, b.nb, b.tile_base, b.tiles, b.dinv, b.err);
+    k_sweep_panel<DMMA><<<(unsigned)b.nrows, 256, sm2, st>>>(p, b.nrows, b.row_s, b.row_k, b.nb,
+                                                             b.tile_base, b.row_base, b.tiles,
+                                                             b.dinv, b.cbuf, b.wbuf);
+    k_sweep_update<DMMA><<<(unsigned)b.ntiles, 256, sm2, st>>>(p, b.ntiles, b.tile_s, b.tile_ij,
+                                                               b.nb, b.row_base, b.tiles, b.dinv,
+                                                               b.cbuf, b.wbuf);
+  }
+}
+
 void launch_sweep_invert(const DevBatch& b, cudaStream_t st) {
   if (b.nsub <= 0) return;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sweep_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    cudaFuncSetAttribute(k_sweep_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    cudaFuncSetAttribute(k_sweep_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    cudaFuncSetAttribute(k_sweep_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    cudaFuncSetAttribute(k_sweep_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    cudaFuncSetAttribute(k_sweep_panel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    cudaFuncSetAttribute(k_sweep_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
     attr = true;
   }
-  size_t sm1 = (TILE + TB) * sizeof(double);
-  size_t sm2 = 2 * TILE * sizeof(double);
-  for (int p = 0; p < b.max_nb; ++p) {
-    k_sweep_pivot<<<b.nsub, 256, sm1, st>>>(p, b.nsub, b.nb, b.tile_base, b.tiles, b.dinv, b.err);
-    k_sweep_panel<<<(unsigned)b.nrows, 256, sm2, st>>>(p, b.nrows, b.row_s, b.row_k, b.nb,
-                                                       b.tile_base, b.row_base, b.tiles, b.dinv,
-                                                       b.cbuf, b.wbuf);
-    k_sweep_update<<<(unsigned)b.ntiles, 256, sm2, st>>>(p, b.ntiles, b.tile_s, b.tile_ij, b.nb,
-                                                         b.row_base, b.tiles, b.dinv, b.cbuf,
-                                                         b.wbuf);
-  }
+  if (use_dmma()) sweep_steps<true>(b, st);
+  else sweep_steps<false>(b, st);
   k_negate<<<148 * 8, 256, 0, st>>>(b.ntiles * TILE, b.tiles);
 }
+
 
 // ---------------------------------------------------------------------------
 // Packed symmetric matrix-vector product, one warp per lower tile (I,J):

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "dmma.cuh"
 #include "kernels.cuh"
 #include "supernodal.h"
 #include "supernodal_dev.cuh"
@@ -648,55 +649,69 @@ __global__ void k_tiles_to_finv(int nlist, const int32_t* __restrict__ list,
   }
 }
 
-// Batched FP64 GEMM  C = alpha A op(B) + beta C  (col-major), 64x64 output
-// tiles, BK = 16 through shared memory, 4x4 outputs per thread.
+// Batched FP64 GEMM  C = alpha op(A) op(B) + beta C  (col-major), 64x64 output
+// tiles, BK = 16 through shared memory; FP64 tensor cores (DMMA m8n8k4) or
+// 4x4 FMA outputs per thread.
+template <bool DMMA>
 __global__ void __launch_bounds__(256) k_gemm_batched(const GemmProb* __restrict__ probs,
                                                       const int32_t* __restrict__ work) {
   const int p = work[3 * blockIdx.x], ti = work[3 * blockIdx.x + 1], tj = work[3 * blockIdx.x + 2];
   const GemmProb g = probs[p];
-  __shared__ double As[16][64 + 1];
-  __shared__ double Bs[16][64 + 1];
+  constexpr int LD = 72;   // smem row stride (bank spread of the DMMA fragments)
+  __shared__ double As[16 * LD];
+  __shared__ double Bs[16 * LD];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int i0 = ti * 64, j0 = tj * 64;
-  double acc[4][4] = {};
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
   for (int k0 = 0; k0 < g.k; k0 += 16) {
     for (int e = threadIdx.x; e < 1024; e += 256) {
       const int r = e & 63, kk = e >> 6;
       const int gi = i0 + r, gk = k0 + kk;
-      As[kk][r] = (gi < g.m && gk < g.k)
-                      ? (g.transA ? g.A[gk + (int64_t)gi * g.lda] : g.A[gi + (int64_t)gk * g.lda])
-                      : 0.0;
+      As[kk * LD + r] = (gi < g.m && gk < g.k)
+                            ? (g.transA ? g.A[gk + (int64_t)gi * g.lda] : g.A[gi + (int64_t)gk * g.lda])
+                            : 0.0;
       const int gj = j0 + r;
       double bv = 0.0;
       if (gj < g.n && gk < g.k) bv = g.transB ? g.B[gj + (int64_t)gk * g.ldb] : g.B[gk + (int64_t)gj * g.ldb];
-      Bs[kk][r] = bv;
+      Bs[kk * LD + r] = bv;
     }
     __syncthreads();
+    if (DMMA) {
+      tile_dmma(As, LD, Bs, LD, 16, acc);
+    } else {
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      double a[4], b[4];
+      for (int kk = 0; kk < 16; ++kk) {
+        double a[4], b[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = As[kk][tx + 16 * q];
-        b[q] = Bs[kk][ty + 16 * q];
+        for (int q = 0; q < 4; ++q) {
+          a[q] = As[kk * LD + tx + 16 * q];
+          b[q] = Bs[kk * LD + ty + 16 * q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[q * 4 + u] = fma(a[q], b[u], acc[q * 4 + u]);
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[q][u] = fma(a[q], b[u], acc[q][u]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int gi = i0 + tx + 16 * q, gj = j0 + ty + 16 * u;
-      if (gi < g.m && gj < g.n) {
-        double* c = g.C + gi + (int64_t)gj * g.ldc;
-        *c = g.beta == 0.0 ? g.alpha * acc[q][u] : fma(g.alpha, acc[q][u], g.beta * *c);
-      }
+  for (int q = 0; q < 16; ++q) {
+    int r, c;
+    if (DMMA) {
+      dmma_rc(q, r, c);
+    } else {
+      r = tx + 16 * (q >> 2);
+      c = ty + 16 * (q & 3);
     }
+    const int gi = i0 + r, gj = j0 + c;
+    if (gi < g.m && gj < g.n) {
+      double* cp = g.C + gi + (int64_t)gj * g.ldc;
+      *cp = g.beta == 0.0 ? g.alpha * acc[q] : fma(g.alpha, acc[q], g.beta * *cp);
+    }
+  }
 }
 
 void launch_front_asm(const int32_t* list, int nlist, const SnNum& nm, const double* val,
@@ -794,7 +809,8 @@ void launch_rows_to_factor(int nsn, const SnNum& nm, double* factor, cudaStream_
 
 void launch_gemm_batched(const GemmProb* probs, const int32_t* work, int nwork, cudaStream_t st) {
   if (nwork <= 0) return;
-  k_gemm_batched<<<nwork, 256, 0, st>>>(probs, work);
+  if (use_dmma()) k_gemm_batched<true><<<nwork, 256, 0, st>>>(probs, work);
+  else k_gemm_batched<false><<<nwork, 256, 0, st>>>(probs, work);
 }
 
 }  // namespace hplmm
