@@ -745,15 +745,28 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
     if (sparse) {
       std::string err;
+      static const bool dbg = getenv("HPLMM_DEBUG") != nullptr;
+      auto wall = [&]() {
+        if (dbg) CK(cudaStreamSynchronize(h->st));
+        return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+      };
+      double t0 = wall();
       if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, kSnLeaf, h->sg.sym, err) ||
           !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, kSnLeaf, h->sc.sym, err))
         throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
+      double t1 = wall();
       try {
         sn_upload(h->sg, halloc, h->st, h->nsm);
         sn_upload(h->sc, halloc, h->st, h->nsm);
+        double t2 = wall();
         sn_factor(h->sg, h->d_val, halloc, h->st, kSnPoolBytes);
+        double t3 = wall();
+        if (dbg)
+          fprintf(stderr, "hplmm T_ML: analyse %.3f s, upload %.3f s, grain factor %.3f s\n", t1 - t0,
+                  t2 - t1, t3 - t2);
         try {
           sn_factor(h->sc, h->d_val, halloc, h->st, kSnPoolBytes);
+          if (dbg) fprintf(stderr, "hplmm T_ML: contact factor %.3f s\n", wall() - t3);
         } catch (SnError& e) {
           e.sub += G;   // contact grids are numbered after the grains
           throw;

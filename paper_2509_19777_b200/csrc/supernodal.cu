@@ -486,8 +486,9 @@ int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk)
     const char* e = getenv("HPLMM_SN_CFG");
     forced = e ? atoi(e) : 0;
   }
-  const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8) >= 2;
-  const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16) >= 2;
+  // the group-reduction scratch (8 x 32 x cons x nrhs doubles) must fit one stage
+  const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8) >= 2 && chunk >= 8 * 256 * nrhs;
+  const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16) >= 2 && chunk >= 8 * 512 * nrhs;
   if (forced == 8 && fit8) return 8;
   if (forced == 16 && fit16) return 16;
   if (fit8 && nitems >= 2 * nsm) return 8;

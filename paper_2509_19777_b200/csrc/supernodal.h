@@ -28,7 +28,7 @@
 
 namespace hplmm {
 
-constexpr int SN_CHUNK_DOUBLES_MAX = 4096;   // largest TMA chunk (32 KiB)
+constexpr int SN_CHUNK_DOUBLES_MAX = 8192;   // largest TMA chunk (64 KiB)
 int sn_chunk_doubles();                          // chunk size in use (4096)
 constexpr int SN_MAX_WR = 2048;          // max w and max r (DOFs) per supernode
 

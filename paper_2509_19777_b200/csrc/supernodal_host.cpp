@@ -182,9 +182,11 @@ void analyse_one(const HostSetup& hs, const int32_t* gn, int m, int leaf, std::v
 int sn_chunk_doubles() {
   static int v = [] {
     const char* e = getenv("HPLMM_SN_CHUNK");
-    int c = e ? atoi(e) : SN_CHUNK_DOUBLES_MAX;
-    // >= 4096: the group-reduction scratch of the solve lives in one stage
-    if (c < SN_CHUNK_DOUBLES_MAX) c = SN_CHUNK_DOUBLES_MAX;
+    int c = e ? atoi(e) : 4096;
+    // >= 2048: the group-reduction scratch of the solve (8 x consumer threads
+    // doubles) lives in one stage; 16-warp CTAs need 4096 (sn_solve_cfg)
+    if (c < 2048) c = 2048;
+    c &= ~1;
     if (c > SN_CHUNK_DOUBLES_MAX) c = SN_CHUNK_DOUBLES_MAX;
     return c;
   }();

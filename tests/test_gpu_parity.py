@@ -213,3 +213,51 @@ def test_full_cap_one_iteration():
     s = fem.build_system(p)
     x, rep, _ = sv.solve(s.b, tol=1e-8)
     assert rep["iterations"] == 1 and rep["converged"] == 1
+
+
+@pytest.mark.parametrize("lf", LF)
+@pytest.mark.parametrize("n", [1, 2, 8])
+def test_mortar_count_sweep(n, lf):
+    """NEXT #3 (App. B): n = 1 (PLMM), 2 and 8 mortar nodes per
+    interface on cfg1 -- M^-1 parity and GMRES iterations (+-1) vs the oracle."""
+    from oracle import gmres, hplmm
+    from paper_2509_19777_b200 import Solver
+    from workloads import make_problem
+    p = make_problem("cfg1", n_mortar=n)
+    s, h = hplmm.setup(p)
+    import __graft_entry__
+    __graft_entry__.build()
+    sv = Solver(p, local_factor=lf).assemble(0).setup()
+    h.set_rhs(s.b)
+    sv.set_rhs(s.b)
+    v = np.random.default_rng(12345).standard_normal(s.n_dof)
+    assert rel(sv.apply("MINV", v), h.apply_M(v)) <= max(1e-12, coarse_floor(h))
+    xo, ito, _, _, convo = gmres.gmres(s.A, s.b, h.apply_M, tol=1e-8)
+    x, rep, _ = sv.solve(s.b.copy(), tol=1e-8)
+    assert convo and rep["converged"] == 1
+    assert abs(rep["iterations"] - ito) <= 1, (n, rep["iterations"], ito)
+    assert rel(x, xo) <= 1e-8
+
+
+@pytest.mark.parametrize("lf", LF)
+def test_singular_local_reports_subdomain(lf):
+    """A non-SPD grain block must fail setup with ERR_SINGULAR_LOCAL and name
+    the subdomain in report.err_index (hplmm.h)."""
+    from paper_2509_19777_b200 import HPLMMError, Solver
+    p, s, h, _ = gpu_case("cube8")
+    val = np.ascontiguousarray(s.val.reshape(-1, 3, 3).copy())
+    grain = 5
+    nodes = set(int(q) for q in h.dec.grain_nodes[grain]) if hasattr(h, "dec") else None
+    if nodes is None:
+        pytest.skip("oracle decomposition not exposed")
+    rp, col = s.row_ptr, s.col_idx
+    for pnode in nodes:
+        for e in range(rp[pnode], rp[pnode + 1]):
+            if col[e] == pnode:
+                val[e] = -val[e]          # negative diagonal blocks: A_g not SPD
+    sv = Solver(p, local_factor=lf).assemble(0)
+    sv.set_matrix(val.reshape(-1))
+    with pytest.raises(HPLMMError) as ei:
+        sv.setup()
+    assert ei.value.status == -4
+    assert sv.report()["err_index"] == grain
