@@ -706,6 +706,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     co.mcol_g = h->upload(mcol_g);
     co.mcol_j = h->upload(mcol_j);
     co.yext = h->dalloc<double>(std::max<int64_t>(yo, 1));
+    co.gpart = h->dalloc<double>(std::max<int64_t>(yo, 1));
     co.yext_off = h->upload(yext_off);
     co.Dc = h->dalloc<double>(std::max(G, 1));
     co.Cg = h->dalloc<double>(std::max<int64_t>(co2, 1), true);

@@ -214,27 +214,67 @@ void launch_S_grain(const DevCoarse& c, double* S, int64_t lds, cudaStream_t st)
 // per mortar column k, fixed-order sum over the grains/chunks touching k plus
 // the Q^o part; per grain the correction entry c_g^T r_g.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_restrict_chunks(DevCoarse c, const int32_t* lmap,
+// 256 threads: warp w sums rows 8w .. 8w+7 of the 64-row chunk for the columns
+// j = lane + 32 t (8 independent row loads in flight per column), then the 8
+// warp partials of each column are added in warp order through shared memory.
+constexpr int RS_MAXL = 640;   // columns kept in shared memory per pass
+__global__ void __launch_bounds__(256) k_restrict_chunks(DevCoarse c, const int32_t* lmap,
                                                          const int64_t* row_base,
                                                          const double* __restrict__ r) {
-  int64_t ch = blockIdx.x;                 // chunk = one 64-row block of a grain
+  const int64_t ch = blockIdx.x;           // chunk = one 64-row block of a grain
   if (ch >= c.n_chunks) return;
-  int g = c.chunk_g[ch];
-  int r0 = c.chunk_r0[ch];
-  int L = c.ld[g];
-  const double* Bg = c.B + c.b_off[g];
+  const int g = c.chunk_g[ch];
+  const int r0 = c.chunk_r0[ch];
+  const int L = c.ld[g];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* Bg = c.B + c.b_off[g] + (int64_t)(r0 + 8 * w) * L;
   const int32_t* lm = lmap + 64 * row_base[g];
   __shared__ double rv[64];
+  __shared__ double part[8][RS_MAXL + 1];
   if (threadIdx.x < 64) {
-    int d = lm[r0 + threadIdx.x];
+    const int d = lm[r0 + threadIdx.x];
     rv[threadIdx.x] = d >= 0 ? r[d] : 0.0;
   }
   __syncthreads();
+  double rr[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) rr[q] = rv[8 * w + q];
   double* out = c.tpart + c.chunk_t[ch];
+  for (int j0 = 0; j0 < L; j0 += RS_MAXL) {
+    const int jn = min(RS_MAXL, L - j0);
+    for (int jj = lane; jj < jn; jj += 32) {
+      const double* col = Bg + j0 + jj;
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldcs(col + (int64_t)q * L);
+      double a = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a = fma(v[q], rr[q], a);
+      part[w][jj] = a;
+    }
+    __syncthreads();
+    for (int jj = threadIdx.x; jj < jn; jj += blockDim.x) {
+      double a = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a += part[q][jj];
+      out[j0 + jj] = a;
+    }
+    __syncthreads();
+  }
+}
+
+// per grain: gpart[j] = sum over its 64-row chunks of tpart (chunk order; the
+// chunks of a grain are contiguous with stride ld_g, so reads are coalesced)
+__global__ void k_restrict_grain(DevCoarse c) {
+  const int g = blockIdx.x;
+  const int L = c.ld[g];
+  const int c0 = c.chunk_ptr[g], c1 = c.chunk_ptr[g + 1];
+  if (c1 <= c0) return;
+  const double* t = c.tpart + c.chunk_t[c0];
+  double* out = c.gpart + c.yext_off[g];
   for (int j = threadIdx.x; j < L; j += blockDim.x) {
     double acc = 0.0;
-#pragma unroll 4
-    for (int rr = 0; rr < 64; ++rr) acc += __ldcs(Bg + (int64_t)(r0 + rr) * L + j) * rv[rr];
+    for (int ch = 0; ch < c1 - c0; ++ch) acc += t[(int64_t)ch * L + j];
     out[j] = acc;
   }
 }
@@ -246,7 +286,7 @@ __global__ void k_restrict_final(DevCoarse c, const int32_t* mortar_iface, const
     double acc = 0.0;
     for (int e = c.mcol_ptr[k]; e < c.mcol_ptr[k + 1]; ++e) {
       int g = c.mcol_g[e], j = c.mcol_j[e];
-      for (int ch = c.chunk_ptr[g]; ch < c.chunk_ptr[g + 1]; ++ch) acc += c.tpart[c.chunk_t[ch] + j];
+      acc += c.gpart[c.yext_off[g] + j];
     }
     int m = k / 3, gam = k - 3 * m;
     int cf = mortar_iface[m];
@@ -259,9 +299,7 @@ __global__ void k_restrict_final(DevCoarse c, const int32_t* mortar_iface, const
   } else if (k < c.Nm + c.n_grains) {
     int g = k - c.Nm;
     double acc = 0.0;
-    int j = c.ld[g] - 1;
-    if (c.Dc[g] != 0.0)
-      for (int ch = c.chunk_ptr[g]; ch < c.chunk_ptr[g + 1]; ++ch) acc += c.tpart[c.chunk_t[ch] + j];
+    if (c.Dc[g] != 0.0) acc = c.gpart[c.yext_off[g] + c.ld[g] - 1];
     rc[g] = acc;
   }
 }
@@ -269,8 +307,9 @@ __global__ void k_restrict_final(DevCoarse c, const int32_t* mortar_iface, const
 void launch_restrict(const DevCoarse& c, const double* r, double* rm, double* rc,
                      cudaStream_t st) {
   if (c.n_chunks > 0)
-    k_restrict_chunks<<<(unsigned)c.n_chunks, 128, 0, st>>>(c, c.g_lmap, c.g_row_base, r);
+    k_restrict_chunks<<<(unsigned)c.n_chunks, 256, 0, st>>>(c, c.g_lmap, c.g_row_base, r);
   int n = c.Nm + c.n_grains;
+  if (c.n_grains > 0) k_restrict_grain<<<c.n_grains, 256, 0, st>>>(c);
   if (n > 0) k_restrict_final<<<(n + 127) / 128, 128, 0, st>>>(c, c.mortar_iface, r, rm, rc);
 }
 

@@ -110,6 +110,7 @@ struct DevCoarse {
   int32_t* chunk_r0 = nullptr;         // [n_chunks] first DOF row
   int64_t* chunk_t = nullptr;          // [n_chunks] offset into tpart
   double* tpart = nullptr;             // partial B_g^T r per chunk (ld_g each)
+  double* gpart = nullptr;             // per grain sum of its chunks (yext layout)
   int32_t* chunk_ptr = nullptr;        // [G+1] chunks of each grain
   int32_t* mcol_ptr = nullptr;         // [Nm+1] grains touching mortar column k
   int32_t* mcol_g = nullptr;           // grain

@@ -307,6 +307,12 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     }
     const double* st = ring + (size_t)s * stage_doubles;
     const int cs = s;
+    if (flags & 4) {   // streaming-only probe: no compute (results invalid)
+      if (++s == stages) { s = 0; ph ^= 1; }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);
+      continue;
+    }
     const long long t_k0 = prof ? clock64() : 0;
     if (++s == stages) { s = 0; ph ^= 1; }
     if (kind == SN_W_FWD || kind == SN_F_FWD) {
