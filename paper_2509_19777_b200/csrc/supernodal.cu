@@ -30,10 +30,17 @@ namespace hplmm {
 // has read it; the producer runs ahead across supernode and item boundaries.
 // ===========================================================================
 constexpr int SN_MAXST = 16;
+// per-warp phase timing of k_sn_solve (printf for a few CTAs when flags & 2);
+// compiled out unless built with -DHPLMM_SN_PROF=1
+#ifndef HPLMM_SN_PROF
+#define HPLMM_SN_PROF 0
+#endif
 
 template <int CONS>
 struct SnT {
   static constexpr int NT = 32 * CONS;                  // consumer threads
+  static constexpr int LGNT = CONS == 16 ? 9 : (CONS == 8 ? 8 : (CONS == 4 ? 7 : 5));
+  static_assert((1 << LGNT) == NT, "power-of-two consumer threads");
   static constexpr int MAXQ = 4;                        // double2 row pairs per thread
   static_assert(MAXQ * 2 * 256 >= SN_MAX_WR, "row coverage at TG = 256");
 };
@@ -48,17 +55,18 @@ __device__ __forceinline__ void cons_sync() {
 // groups and group g takes the chunk columns jj == g (mod G), so every chunk
 // keeps all consumer warps busy whatever the aspect ratio of the panel.
 struct RowLayout {
-  int TG, G, g, t;
+  int TG, G, g, t, lg;
   // lgc = log2(TG) - 5, precomputed on the host per part (chunk descriptor,
-  // TG <= 512), capped at the CTA's consumer thread count NT
-  __device__ __forceinline__ RowLayout(int lgc, int tid, int nt) {
-    int lg = lgc + 5;
-    while ((1 << lg) > nt) --lg;
+  // TG <= 512), capped at the CTA's consumer thread count NT = 2^lgnt
+  __device__ __forceinline__ RowLayout(int lgc, int tid, int lgnt) {
+    lg = min(lgc + 5, lgnt);
     TG = 1 << lg;
-    G = nt >> lg;
+    G = 1 << (lgnt - lg);
     g = tid >> lg;
     t = tid & (TG - 1);
   }
+  // row-pair slots per thread for h rows
+  __device__ __forceinline__ int nq(int h) const { return (h + 2 * TG - 1) >> (lg + 1); }
 };
 
 // effective row-group code of a part with h rows: the host's (TG >= h/8), or
@@ -188,10 +196,11 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
   // x_R of a backward part (16-B aligned)
   double* xr = x + (size_t)((max_n + 1) & ~1) * NRHS;
   constexpr int SN_NT = SnT<CONS>::NT, SN_MAXQ = SnT<CONS>::MAXQ, SN_CONS = CONS;
+  constexpr int SN_LGNT = SnT<CONS>::LGNT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k0 = wk.chunk_ptr[blockIdx.x], k1 = wk.chunk_ptr[blockIdx.x + 1];
   // optional per-warp phase timing (flags & 2; printed for a few CTAs)
-  const bool prof = (flags & 2) && (blockIdx.x % 37 == 0);
+  const bool prof = HPLMM_SN_PROF && (flags & 2) && (blockIdx.x % 37 == 0);
   long long t_wait = 0, t_sync = 0;
   long long t_kind[6] = {0, 0, 0, 0, 0, 0}, n_kind[6] = {0, 0, 0, 0, 0, 0};
   const long long t_start = prof ? clock64() : 0;
@@ -230,7 +239,8 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
         if (lane == 0) {
           if (k >= stages) {
             const long long tw = prof ? clock64() : 0;
-            mbar_wait(&empty[s], ph ^ 1);
+            if (flags & 8) mbar_wait_sleep(&empty[s], ph ^ 1);
+            else mbar_wait(&empty[s], ph ^ 1);
             if (prof) t_wait += clock64() - tw;
           }
           mbar_expect_tx(&full[s], (uint32_t)b);
@@ -319,7 +329,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       // row-parallel gemv on a column chunk: W_S, F_SS^-1
       const int h = kind == SN_W_FWD ? r : w;
       const int ld = h + (h & 1);
-      const RowLayout L(sn_lg<NRHS>(lgc, h), tid, SN_NT);
+      const RowLayout L(sn_lg<NRHS>(lgc, h), tid, SN_LGNT);
       if (cc0 == 0) {
 #pragma unroll
         for (int q = 0; q < SN_MAXQ; ++q)
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
             for (int cr = 0; cr < NRHS; ++cr) acc[q][e][cr] = 0.0;
       }
       const double* xcol = x + (size_t)(p0 + cc0) * NRHS;
-      const int nq = (h + 2 * L.TG - 1) / (2 * L.TG);
+      const int nq = L.nq(h);
       if (nq <= 1) sn_rows<1, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
       else if (nq == 2) sn_rows<2, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
       else if (nq == 3) sn_rows<3, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
@@ -368,7 +378,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       }
     } else if (kind == SN_ROWS_FWD) {
       // x_R -= W_S x_S (summed over the W part by group 0; rows are distinct)
-      const RowLayout L(sn_lg<NRHS>(lgc, r), tid, SN_NT);
+      const RowLayout L(sn_lg<NRHS>(lgc, r), tid, SN_LGNT);
       const int32_t* rows = reinterpret_cast<const int32_t*>(st);
       if (L.g == 0) {
 #pragma unroll
@@ -542,6 +552,13 @@ void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs,
   if (wk.nblocks <= 0) return;
   const int stages = sn_solve_stages(max_n, max_r, nrhs, chunk, cons);
   const size_t smem = ((size_t)stages * chunk + sn_tail_doubles(max_n, max_r, nrhs, 32 * cons)) * 8;
+  static const bool dbg = getenv("HPLMM_DEBUG") != nullptr;
+  static int printed = 0;
+  if (dbg && printed < 4) {
+    ++printed;
+    fprintf(stderr, "hplmm sn_solve: blocks %d cons %d nrhs %d max_n %d max_r %d chunk %d stages %d smem %zu\n",
+            wk.nblocks, cons, nrhs, max_n, max_r, chunk, stages, smem);
+  }
   if (cons == 8) sn_launch_nrhs<8, 2>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
   else sn_launch_nrhs<16, 1>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
 }
