@@ -87,6 +87,13 @@ typedef struct {
                                 F_SS^-1; forward + backward sweep per apply,
                                 ~4x fewer bytes, needed for cfg4/cfg5).
                             default 1                                          */
+  int32_t coarse_solver; /* coarse mortar-block solve y = S^-1 r (eq:mg_struct,
+                            P:741 "direct solver"):
+                            0 = explicit S^-1 (packed lower tiles) applied by one
+                                symmetric mat-vec (default; half the bytes of
+                                two triangular sweeps, no dependency chain);
+                            1 = Cholesky factor S = L L^T applied by a forward
+                                and a backward triangular solve               */
 } hplmm_options;
 
 typedef struct {

@@ -91,6 +91,21 @@ struct hplmm_handle {
   double kc_ms[KC_N] = {0, 0, 0, 0, 0};
   int64_t kc_launches[KC_N] = {0, 0, 0, 0, 0};
 
+  // coarse Cholesky (coarse_solver == 1)
+  double *d_linv = nullptr, *d_linvT = nullptr, *d_zc = nullptr;
+  int *d_cflag_f = nullptr, *d_cflag_b = nullptr;
+  int coarse_epoch = 0;
+  bool chol() const { return hs.opt.coarse_solver == 1; }
+  void coarse_apply(DevBatch& b) {   // b.yloc = S^-1 b.xloc
+    if (chol()) {
+      launch_chol_solve(b, d_linv, d_linvT, b.xloc, d_zc, b.yloc, d_cflag_f, d_cflag_b,
+                        ++coarse_epoch, st);
+      launches += 2;
+    } else {
+      symv(b, KC_SYMV_COARSE);
+    }
+  }
+
   // supernodal local factors (local_factor == 1)
   SnBatch sg, sc;                       // grains, contact grids
   int32_t* d_gpos_sn = nullptr;         // global DOF -> position in sg.yloc (or -1)
@@ -366,7 +381,7 @@ void op_mgrain(hplmm_handle* h, const double* in, const double* a, const double*
 // y_m = S^-1 r_m by the packed inverse; optional refinement y += S^-1 (r - S y)
 const double* op_coarse(hplmm_handle* h, const double* rm) {
   launch_gather(h->sb, rm, h->st);
-  h->symv(h->sb, KC_SYMV_COARSE);
+  h->coarse_apply(h->sb);
   h->launches += 1;
   if (!h->hs.opt.coarse_refine || h->co.Nm == 0) return h->sb.yloc;
   const int Nm = h->co.Nm;
@@ -375,7 +390,7 @@ const double* op_coarse(hplmm_handle* h, const double* rm) {
   h->symv(h->sS, KC_SYMV_COARSE);
   launch_gather(h->sb, rm, h->st);
   launch_axpy(h->sb.nloc, -1.0, h->sS.yloc, h->sb.xloc, h->st);
-  h->symv(h->sb, KC_SYMV_COARSE);
+  h->coarse_apply(h->sb);
   launch_axpy(Nm, 1.0, h->sb.yloc, h->d_ym, h->st);
   h->launches += 4;
   return h->d_ym;
@@ -447,6 +462,7 @@ void hplmm_default_options(hplmm_options* o) {
   o->n_st = 1;
   o->coarse_refine = 0;
   o->local_factor = 1;
+  o->coarse_solver = 0;
 }
 
 const char* hplmm_last_error(void) { return g_last_error.c_str(); }
@@ -867,7 +883,20 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       CK(cudaMemcpyAsync(h->sS.tiles, h->sb.tiles, (size_t)h->sb.ntiles * TILE * 8,
                          cudaMemcpyDeviceToDevice, h->st));
     }
-    launch_sweep_invert(h->sb, h->st);
+    if (h->chol()) {
+      const int nbS = h->sb.max_nb;
+      h->d_linv = h->dalloc<double>((size_t)std::max(nbS, 1) * TILE);
+      h->d_linvT = h->dalloc<double>((size_t)std::max(nbS, 1) * TILE);
+      h->d_zc = h->dalloc<double>((size_t)std::max(nbS, 1) * TB);
+      h->d_cflag_f = h->dalloc<int>(std::max(nbS, 1));
+      h->d_cflag_b = h->dalloc<int>(std::max(nbS, 1));
+      CK(cudaMemsetAsync(h->d_cflag_f, 0, std::max(nbS, 1) * 4, h->st));
+      CK(cudaMemsetAsync(h->d_cflag_b, 0, std::max(nbS, 1) * 4, h->st));
+      h->coarse_epoch = 0;
+      launch_chol_factor(h->sb, h->d_linv, h->d_linvT, h->st);
+    } else {
+      launch_sweep_invert(h->sb, h->st);
+    }
     CK(cudaGetLastError());
     check_batch_err(h, h->sb, 0, true);
     h->rep.t_setup_coarse_s = tc.stop();

@@ -146,6 +146,13 @@ void launch_coarse_diag(int G, const double* rc, const double* Dc, double* yc, c
 // correction column from a grain-batch y_loc (c_g) and D_c = b_g . c_g
 void launch_set_correction(const DevCoarse& c, const DevBatch& gb, cudaStream_t st);
 
+// ---- coarse Cholesky factor and triangular solves (cholesky.cu) -----------
+void launch_chol_factor(const DevBatch& b, double* linv, double* linvT, cudaStream_t st);
+// y = L^-T L^-1 r  (r, y, zbuf: 64 nb doubles); epoch > every earlier epoch
+void launch_chol_solve(const DevBatch& b, const double* linv, const double* linvT,
+                       const double* r, double* zbuf, double* y, int* flags_fwd, int* flags_bwd,
+                       int epoch, cudaStream_t st);
+
 // ---- combine / scatter (dense.cu) -------------------------------------------
 // out[d] = (a? a[d]:0) + (b? b[d]:0) + yloc_grain[gpos[d]] (if gpos>=0)
 void launch_combine_grain(int n_dof, const int32_t* gpos, const double* yloc, const double* a,

@@ -261,3 +261,27 @@ def test_singular_local_reports_subdomain(lf):
         sv.setup()
     assert ei.value.status == -4
     assert sv.report()["err_index"] == grain
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_coarse_cholesky_solver(case):
+    """coarse_solver=1: dense Cholesky factor of S applied by forward and
+    backward triangular solves (SURVEY §8(a) a3 as written).  Backward stable,
+    so its normwise backward error is ~u whatever kappa(S); M^-1 and the solve
+    match the oracle as for the default explicit-inverse coarse solve."""
+    from oracle import gmres
+    from paper_2509_19777_b200 import Solver
+    p, s, h, _ = gpu_case(case)
+    sv = Solver(p, coarse_solver=1).assemble(0).setup()
+    r = np.random.default_rng(12345).standard_normal(h.Nm)
+    y = sv.apply("COARSE", r)
+    be = np.linalg.norm(h.S @ y - r) / (np.linalg.norm(h.S, 2) * np.linalg.norm(y) + np.linalg.norm(r))
+    assert be <= 1e-14, be
+    sv.set_rhs(s.b)
+    h.set_rhs(s.b)
+    v = np.random.default_rng(12345).standard_normal(s.n_dof)
+    assert rel(sv.apply("MINV", v), h.apply_M(v)) <= max(1e-12, coarse_floor(h))
+    xo, ito, _, _, convo = gmres.gmres(s.A, s.b, h.apply_M, tol=1e-8)
+    x, rep, _ = sv.solve(s.b.copy(), tol=1e-8)
+    assert convo and rep["converged"] == 1 and abs(rep["iterations"] - ito) <= 1
+    assert rel(x, xo) <= 1e-8
