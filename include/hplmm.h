@@ -169,6 +169,15 @@ hplmm_status hplmm_solve(hplmm_handle *h, const double *b, double tol, double *x
                          hplmm_report *report, double *hist, int32_t hist_cap,
                          void *stream);
 
+/* Multi-RHS reuse (the paper's economic argument, P:743,
+ * P:819): solve A^ X = B for nrhs right-hand sides with one setup -- the
+ * local factors and S^-1 are reused, only the correction columns (eq:col_cg,
+ * R15) are rebuilt per column.  B, X: nrhs x n_dof doubles, column-contiguous
+ * (column i at B + i n_dof), host or device.  reports: nrhs entries or NULL.
+ * Returns the worst status over the columns (an error stops at that column). */
+hplmm_status hplmm_solve_many(hplmm_handle *h, int32_t nrhs, const double *B, double tol,
+                              double *X, hplmm_report *reports, void *stream);
+
 typedef enum {
   HPLMM_OP_SPMV = 0,   /* out = A^ in                                           */
   HPLMM_OP_MG = 1,     /* out = M_G^-1 in        (needs set_rhs)                */

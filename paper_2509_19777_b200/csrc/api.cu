@@ -1148,6 +1148,21 @@ hplmm_status hplmm_solve(hplmm_handle* h, const double* b, double tol, double* x
   }
 }
 
+hplmm_status hplmm_solve_many(hplmm_handle* h, int32_t nrhs, const double* B, double tol,
+                              double* X, hplmm_report* reports, void* stream) {
+  if (!h || !B || !X || nrhs < 0) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
+  const int64_t n = 3 * (int64_t)h->hs.n_nodes;
+  hplmm_status worst = HPLMM_OK;
+  for (int32_t i = 0; i < nrhs; ++i) {
+    hplmm_report rep{};
+    const hplmm_status st = hplmm_solve(h, B + i * n, tol, X + i * n, &rep, nullptr, 0, stream);
+    if (reports) reports[i] = rep;
+    if (st < 0) return st;
+    if (st > worst) worst = st;
+  }
+  return worst;
+}
+
 hplmm_status hplmm_export(hplmm_handle* h, int32_t art, void* buf, int64_t cap, int64_t* len) {
   if (!h || !len) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
   try {

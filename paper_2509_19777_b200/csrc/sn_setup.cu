@@ -73,7 +73,7 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   if (wk.cons == 0)
     throw SnError{-1, "subdomain of " + std::to_string(s.max_n) +
                           " DOFs does not fit the supernodal solve's shared memory"};
-  nblocks *= wk.cons == 8 ? 2 : 1;
+  nblocks *= wk.cons == 16 ? 1 : 2;
   nblocks = std::max(1, std::min<int>(nblocks, (int)isub.size()));
   std::vector<int32_t> ptr, ids;
   lpt(wgt, nblocks, ptr, ids);

@@ -505,6 +505,8 @@ int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk)
   // the group-reduction scratch (8 x 32 x cons x nrhs doubles) must fit one stage
   const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8) >= 2 && chunk >= 8 * 256 * nrhs;
   const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16) >= 2 && chunk >= 8 * 512 * nrhs;
+  if (forced == 4 && sn_solve_stages(max_n, max_r, nrhs, chunk, 4) >= 2 && chunk >= 8 * 128 * nrhs)
+    return 4;
   if (forced == 8 && fit8) return 8;
   if (forced == 16 && fit16) return 16;
   if (fit8 && nitems >= 2 * nsm) return 8;
@@ -512,7 +514,7 @@ int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk)
   return 0;   // does not fit
 }
 
-static int cfg_cps(int cons) { return cons == 8 ? 2 : 1; }
+static int cfg_cps(int cons) { return cons == 16 ? 1 : 2; }
 
 int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons) {
   const int p = cfg_cps(cons);
@@ -559,7 +561,8 @@ void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs,
     fprintf(stderr, "hplmm sn_solve: blocks %d cons %d nrhs %d max_n %d max_r %d chunk %d stages %d smem %zu\n",
             wk.nblocks, cons, nrhs, max_n, max_r, chunk, stages, smem);
   }
-  if (cons == 8) sn_launch_nrhs<8, 2>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
+  if (cons == 4) sn_launch_nrhs<4, 2>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
+  else if (cons == 8) sn_launch_nrhs<8, 2>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
   else sn_launch_nrhs<16, 1>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
 }
 

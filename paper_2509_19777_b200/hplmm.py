@@ -27,7 +27,8 @@ ART = dict(NODE_KEY=0, ROW_PTR=1, COL_IDX=2, NODE_CLASS=3, NODE_IFACE=4, NODE_OW
 _ART_DTYPE = {0: np.int64, 14: np.float64, 15: np.float64, 16: np.float64, 17: np.float64}
 
 EXPORTED = ["hplmm_default_options", "hplmm_create", "hplmm_assemble", "hplmm_set_matrix",
-            "hplmm_setup", "hplmm_set_rhs", "hplmm_solve", "hplmm_apply", "hplmm_export",
+            "hplmm_setup", "hplmm_set_rhs", "hplmm_solve", "hplmm_solve_many", "hplmm_apply",
+            "hplmm_export",
             "hplmm_get_report", "hplmm_profile", "hplmm_kernel_stats", "hplmm_destroy",
             "hplmm_last_error"]
 
@@ -83,6 +84,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hplmm_setup": (C.c_int, [vp, vp]),
         "hplmm_set_rhs": (C.c_int, [vp, vp, vp]),
         "hplmm_solve": (C.c_int, [vp, vp, dbl, vp, vp, vp, i32, vp]),
+        "hplmm_solve_many": (C.c_int, [vp, i32, vp, dbl, vp, vp, vp]),
         "hplmm_apply": (C.c_int, [vp, i32, vp, vp, vp]),
         "hplmm_export": (C.c_int, [vp, i32, vp, C.c_int64, vp]),
         "hplmm_get_report": (C.c_int, [vp, vp]),
@@ -224,6 +226,20 @@ class Solver:
         if isinstance(x, np.ndarray) and kx is not x:
             x[:] = kx
         return x, rep.as_dict(), hist[:rep.hist_len].copy()
+
+    def solve_many(self, B, tol=1e-8, X=None, stream=None):
+        """B: (nrhs, n_dof) NumPy or torch CUDA array; returns (X, [report dicts])."""
+        nrhs = int(B.shape[0])
+        if X is None:
+            X = np.zeros_like(B) if isinstance(B, np.ndarray) else B.new_zeros(B.shape)
+        pb, kb = _ptr(B)
+        px, kx = _ptr(X)
+        reps = (Report * max(nrhs, 1))()
+        st = self._lib.hplmm_solve_many(self._h, nrhs, pb, float(tol), px, reps, _stream(stream))
+        _check(st, allow=(OK, NOT_CONVERGED))
+        if isinstance(X, np.ndarray) and kx is not X:
+            X[:] = kx
+        return X, [reps[i].as_dict() for i in range(nrhs)]
 
     def apply(self, op, v, out=None, stream=None):
         opi = OP[op] if isinstance(op, str) else int(op)

@@ -285,3 +285,18 @@ def test_coarse_cholesky_solver(case):
     x, rep, _ = sv.solve(s.b.copy(), tol=1e-8)
     assert convo and rep["converged"] == 1 and abs(rep["iterations"] - ito) <= 1
     assert rel(x, xo) <= 1e-8
+
+
+def test_solve_many_reuses_setup():
+    """hplmm_solve_many (NEXT #2): several right-hand sides on one setup give
+    the same iterates as separate solves (the correction columns are rebuilt
+    per right-hand side, R15)."""
+    p, s, h, sv = gpu_case("cfg1")
+    rng = np.random.default_rng(4)
+    B = np.stack([s.b, rng.standard_normal(s.n_dof), s.b * 2.0])
+    X, reps = sv.solve_many(B, tol=1e-8)
+    for i in range(B.shape[0]):
+        x, rep, _ = sv.solve(B[i].copy(), tol=1e-8)
+        assert reps[i]["converged"] == 1 and reps[i]["iterations"] == rep["iterations"]
+        assert np.array_equal(X[i], x)
+        assert np.linalg.norm(B[i] - s.A @ X[i]) / np.linalg.norm(B[i]) < 1e-8
