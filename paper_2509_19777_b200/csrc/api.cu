@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "hplmm_internal.h"
 #include "kernels.cuh"
 #include "sn_setup.h"
@@ -301,6 +303,13 @@ double elapsed(cudaEvent_t a, cudaEvent_t b) {
   cudaEventElapsedTime(&ms, a, b);
   return ms * 1e-3;
 }
+
+// NVTX range for the profiler timelines (ncu --nvtx, nsys): setup phases,
+// each solve, each Arnoldi step
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 struct HandleAlloc : DevAlloc {
   hplmm_handle* h;
@@ -756,6 +765,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     CK(cudaMemsetAsync(h->d_rm, 0, std::max(Nm, 1) * 8, h->st));
 
     // ---------------- T_ML: local inversions / factorisations ------------
+    Nvtx nv_ml("hplmm_setup:T_ML");
     Timer tl(h->st);
     int32_t big = INT_MAX;
     HandleAlloc halloc(h);
@@ -826,6 +836,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     h->rep.t_setup_local_s = tl.stop();
 
     // ---------------- T_MG: mortars, P_B, S, S^-1 -------------------------
+    Nvtx nv_mg("hplmm_setup:T_MG");
     Timer tc(h->st);
     {
       std::vector<int32_t> iface_of(hs.iface_nodes.size());
@@ -1030,6 +1041,7 @@ hplmm_status hplmm_solve(hplmm_handle* h, const double* b, double tol, double* x
       h->d_hbuf = h->dalloc<double>(2 * (m + 1) + 8);
       h->Vcap = m + 1;
     }
+    Nvtx nv_solve("hplmm_solve");
     Timer tt(st);
     double* dB = h->d_bb;
     to_device(h, dB, b, n);
@@ -1067,6 +1079,7 @@ hplmm_status hplmm_solve(hplmm_handle* h, const double* b, double tol, double* x
         g[0] = beta;
         int k = 0;
         for (int j = 0; j < m; ++j) {
+          Nvtx nv_step("arnoldi_step");
           double* vj = V + j * h->ldv;
           double* w = V + (j + 1) * h->ldv;
           op_minv(h, vj, h->d_u);

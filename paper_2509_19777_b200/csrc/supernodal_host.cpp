@@ -211,6 +211,32 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
 
   o = SnSymbolic();
   o.nsub = nsub;
+  {  // reserve the concatenated arrays (tens of millions of entries at cfg3)
+    size_t nn = 0, ns = 0, nr = 0, na = 0, nrel = 0;
+    for (const SubResult& r : res) {
+      nn += 3 * (size_t)r.n_nodes;
+      ns += r.sns.size();
+      for (size_t k = 0; k < r.sns.size(); ++k) {
+        nr += 3 * r.st[k].size();
+        na += r.ae[k].size();
+        nrel += r.rel[k].size();
+      }
+    }
+    o.gmap.reserve(nn);
+    o.lidx.reserve(nn);
+    o.rows.reserve(nr);
+    o.asm_e.reserve(na);
+    o.asm_u.reserve(na);
+    o.asm_v.reserve(na);
+    o.rel.reserve(nrel);
+    for (auto* v : {&o.sn_w, &o.sn_r, &o.sn_p0, &o.sn_ldw, &o.sn_ldf, &o.sn_level, &o.sn_parent,
+                    &o.sn_sub, &o.sn_child_rank})
+      v->reserve(ns);
+    o.sn_rows_off.reserve(ns);
+    o.sn_foff.reserve(ns);
+    o.asm_ptr.reserve(ns + 1);
+    o.rel_off.reserve(ns + 1);
+  }
   int64_t base = 0, foff = 0, roff = 0;
   o.asm_ptr.push_back(0);
   o.rel_off.push_back(0);
