@@ -54,27 +54,29 @@ class _Local:
 
 class HPLMM:
     def __init__(self, system: System, n_mortar: int = 4, beta: float = 4.0,
-                 contact_h: int = 1):
+                 contact_h: int = 1, mortar: str = "gaussian"):
         self.sys = system
         A = system.A
         self.A = A
         n_dof = system.n_dof
         mesh = system.mesh
         self.dec = Decomposition(system, contact_h)
-        self.mor = Mortars(self.dec, mesh.node_ijk, n_mortar, beta)
+        self.mor = Mortars(self.dec, mesh.node_ijk, n_mortar, beta, kind=mortar, A=A)
         dec, mor = self.dec, self.mor
         Nm = mor.n_mortar_dofs
         self.Nm = Nm
 
-        # Q^o (eq:reduced_defs, R12/R13): column 3*(off_c + i) + gamma
+        # Q^o (eq:reduced_defs, R12/R13): column 3*(off_c + i) + gamma,
+        # rows 3*F[f] + d, values M^{c}[3f + d, 3i + gamma]
         r, c, v = [], [], []
         for ci, F in enumerate(dec.interfaces):
-            W = mor.weights[ci]
-            for i in range(W.shape[1]):
-                for g in range(3):
-                    r.append(3 * F + g)
-                    c.append(np.full(F.size, 3 * (mor.offset[ci] + i) + g))
-                    v.append(W[:, i])
+            M = mor.blocks[ci]
+            rows = (3 * np.asarray(F)[:, None] + np.arange(3)[None, :]).ravel()
+            for q in range(M.shape[1]):
+                nz = M[:, q] != 0.0
+                r.append(rows[nz])
+                c.append(np.full(int(nz.sum()), 3 * mor.offset[ci] + q))
+                v.append(M[nz, q])
         self.Qo = sp.csc_matrix((np.concatenate(v), (np.concatenate(r), np.concatenate(c))),
                                 shape=(n_dof, Nm)) if r else sp.csc_matrix((n_dof, Nm))
 
@@ -205,5 +207,6 @@ class HPLMM:
 def setup(prob, **kw) -> tuple[System, HPLMM]:
     s = build_system(prob)
     h = HPLMM(s, n_mortar=kw.get("n_mortar", prob.n_mortar), beta=kw.get("beta", prob.beta),
-              contact_h=kw.get("contact_h", prob.contact_h))
+              contact_h=kw.get("contact_h", prob.contact_h),
+              mortar=kw.get("mortar", getattr(prob, "mortar", "gaussian")))
     return s, h

@@ -10,6 +10,16 @@ PAPER.md §3.3 "Mortar nodes and mortar functions":
   * Gaussian mortars eta_{m_i gamma}^{(d)} = delta_{d gamma} alpha_i/sum_j alpha_j,
     alpha_i(x) = exp(-||x-x_{m_i}||^2 / (beta min_j ||x_{m_i}-x_{m_j}||^2))
     (eq:gauss, P:145-155), beta = 4 (P:156, P:484).
+  * Algebraic mortars (eq:algebra) built as in the Remark:
+    column (m_i, gamma) of the interface block M^{c} solves the interface
+    matrix A^{c}_{c} = A^[F_c, F_c] with Dirichlet constraints on the mortar
+    nodes -- 1 for component gamma of m_i, 0 for every other mortar-node
+    component -- i.e. x_free = -(A~)^-1 e_1 expanded with the 0/1 values
+    (reading R25: A^{c}_{c} is the principal interface block of A^; all 3
+    components of every mortar node are constrained; global x/y/z frame).
+Every interface is stored as a dense block M^{c} of 3|F_c| x 3 nu_c: row 3f + d
+(f-th node of F_c, component d), column 3i + gamma (mortar i, component
+gamma).  Gaussian blocks are component-diagonal: M[3f+d, 3i+g] = W[f,i] d_{dg}.
 Readings: R9 (nu_c = min(n, |F_c|)), R10 (deterministic placement: integer d^2,
 IEEE 1/sqrt, sequential sums in chosen order, lowest id on ties, ascending
 sweep order, move only on a > 1e-12 relative improvement, <= 20 sweeps; nu=|F|
@@ -114,18 +124,62 @@ def gaussian_weights(F: np.ndarray, ijk: np.ndarray, mortars, beta: float) -> np
     return alpha / alpha.sum(axis=1, keepdims=True)
 
 
-class Mortars:
-    """Mortar nodes + weights for every interface; coarse column ordering R13:
-    interface id -> mortar index (placement order) -> gamma in {x,y,z}."""
+def gaussian_block(W: np.ndarray) -> np.ndarray:
+    """3|F| x 3nu block of component-diagonal Gaussian mortars."""
+    nf, nu = W.shape
+    M = np.zeros((3 * nf, 3 * nu))
+    for g in range(3):
+        M[g::3, g::3] = W
+    return M
 
-    def __init__(self, decomp, node_ijk, n_mortar: int, beta: float):
+
+def algebraic_block(F: np.ndarray, A, mortars) -> np.ndarray:
+    """Algebraic mortars by the Remark, steps (1)-(4) as written:
+    (1) drop the rows of the 0/1-constrained DOFs (all components of the
+    mortar nodes) from A^{c}_{c}; (2) take the column of the 1-constraint;
+    (3) drop the constrained columns -> A~; (4) x = -(A~)^-1 e_1, expanded by
+    the 0/1 values.  A: the (Dirichlet-constrained) fine matrix A^ (sparse)."""
+    F = np.asarray(F)
+    dofs = (3 * F[:, None] + np.arange(3)[None, :]).ravel()
+    Acc = A[dofs][:, dofs].toarray()
+    pos = {int(y): f for f, y in enumerate(F)}
+    con = np.array([3 * pos[int(x)] + g for x in mortars for g in range(3)], dtype=np.int64)
+    free = np.setdiff1d(np.arange(dofs.size), con)
+    nu = len(mortars)
+    M = np.zeros((dofs.size, 3 * nu))
+    for q in range(3 * nu):              # q = 3 i + gamma, i.e. con[q]
+        M[con[q], q] = 1.0
+        if free.size:
+            e1 = Acc[np.ix_(free, [con[q]])][:, 0]
+            At = Acc[np.ix_(free, free)]
+            M[free, q] = -np.linalg.solve(At, e1)
+    return M
+
+
+class Mortars:
+    """Mortar nodes + mortar blocks for every interface; coarse column ordering
+    R13: interface id -> mortar index (placement order) -> gamma in {x,y,z}.
+    kind: "gaussian" (eq:gauss, the paper's choice for its results) or
+    "algebraic" (eq:algebra via the Remark; needs A)."""
+
+    def __init__(self, decomp, node_ijk, n_mortar: int, beta: float, kind: str = "gaussian",
+                 A=None):
+        self.kind = kind
         self.nodes = []
-        self.weights = []
+        self.weights = []       # Gaussian W[f, i] (kind == "gaussian")
+        self.blocks = []        # 3|F| x 3nu per interface (both kinds)
         self.offset = [0]
         for F in decomp.interfaces:
             X = place_mortars(F, node_ijk, n_mortar)
             self.nodes.append(X)
-            self.weights.append(gaussian_weights(F, node_ijk, X, beta))
+            if kind == "gaussian":
+                W = gaussian_weights(F, node_ijk, X, beta)
+                self.weights.append(W)
+                self.blocks.append(gaussian_block(W))
+            elif kind == "algebraic":
+                self.blocks.append(algebraic_block(F, A, X))
+            else:
+                raise ValueError(kind)
             self.offset.append(self.offset[-1] + len(X))
         self.offset = np.array(self.offset, dtype=np.int64)
         self.n_mortar_nodes = int(self.offset[-1])

@@ -148,3 +148,68 @@ def test_full_cap_places_every_node(cfg1):
     _, s, h = cfg1
     F = h.dec.interfaces[0]
     assert mortar.place_mortars(F, s.mesh.node_ijk, 10 ** 6) == list(map(int, F))
+
+
+# ---- Algebraic mortars (eq:algebra via the Remark P:356; reading R25) -----
+def _alg_case(h, s, ci, n):
+    F = h.dec.interfaces[ci]
+    X = mortar.place_mortars(F, s.mesh.node_ijk, n)
+    M = mortar.algebraic_block(F, s.A, X)
+    dofs = (3 * np.asarray(F)[:, None] + np.arange(3)[None, :]).ravel()
+    Acc = s.A[dofs][:, dofs].toarray()
+    pos = {int(y): f for f, y in enumerate(F)}
+    con = np.array([3 * pos[int(x)] + g for x in X for g in range(3)])
+    free = np.setdiff1d(np.arange(dofs.size), con)
+    return F, X, M, Acc, con, free
+
+
+@pytest.mark.parametrize("ci", [0, 3, 7])
+def test_algebraic_mortars_constraints_and_harmonicity(porous20, ci):
+    """Each column meets its 0/1 mortar constraints exactly and is A^{c}_{c}-
+    harmonic on the free interface DOFs (the Remark's local problem)."""
+    p, s, h = porous20
+    F, X, M, Acc, con, free = _alg_case(h, s, ci, 4)
+    assert np.array_equal(M[con], np.eye(len(con)))
+    res = Acc[free] @ M
+    assert np.abs(res).max() <= 1e-12 * np.abs(Acc).max() * max(1.0, np.abs(M).max())
+
+
+def test_algebraic_mortars_minimise_interface_energy(porous20):
+    """The constrained solve is the minimiser of x^T A^{c}_{c} x under the
+    0/1 constraints: any admissible perturbation raises the energy."""
+    p, s, h = porous20
+    F, X, M, Acc, con, free = _alg_case(h, s, 1, 4)
+    rng = np.random.default_rng(3)
+    for q in range(M.shape[1]):
+        e0 = M[:, q] @ Acc @ M[:, q]
+        for _ in range(5):
+            d = np.zeros(M.shape[0])
+            d[free] = 1e-3 * rng.standard_normal(free.size)
+            x = M[:, q] + d
+            assert x @ Acc @ x > e0
+
+
+def test_algebraic_full_cap_is_identity(cfg1):
+    """nu = |F| (every interface node a mortar): no free DOFs, M = I."""
+    _, s, h = cfg1
+    F = h.dec.interfaces[2]
+    X = mortar.place_mortars(F, s.mesh.node_ijk, 10 ** 6)
+    M = mortar.algebraic_block(F, s.A, X)
+    assert np.array_equal(M, np.eye(3 * F.size))
+
+
+def test_algebraic_hplmm_projection_and_gmres():
+    """With Algebraic mortars the two-level operator keeps the M_G projection
+    identity M_G^-1 A^ P^ z = P^ z, and GMRES converges (cube8)."""
+    import scipy.sparse as sp
+    from oracle import gmres, hplmm
+    from workloads import make_problem
+    p = make_problem("cube8", mortar="algebraic")
+    s, h = hplmm.setup(p)
+    h.set_rhs(s.b)
+    P = sp.hstack([h.PB, h.P_C()]).tocsc()
+    z = np.random.default_rng(5).standard_normal(P.shape[1])
+    Pz = P @ z
+    assert np.linalg.norm(h.apply_MG(s.A @ Pz) - Pz) <= 1e-10 * np.linalg.norm(Pz)
+    x, it, hist, rr, conv = gmres.gmres(s.A, s.b, h.apply_M, tol=1e-8)
+    assert conv and it < 60

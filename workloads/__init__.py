@@ -52,6 +52,7 @@ class Problem:
     # method parameters (BASELINE configs)
     n_mortar: int = 4
     beta: float = 4.0
+    mortar: str = "gaussian"     # or "algebraic" (eq:algebra via the Remark)
     contact_h: int = 1
     restart: int = 50
     tol: float = 1e-8
