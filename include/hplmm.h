@@ -94,6 +94,10 @@ typedef struct {
                                 two triangular sweeps, no dependency chain);
                             1 = Cholesky factor S = L L^T applied by a forward
                                 and a backward triangular solve               */
+  int32_t mortar_kind;   /* mortar functions: 0 = Gaussian (eq:gauss,
+                            the paper's choice, default); 1 = Algebraic
+                            (eq:algebra, built by the Remark's constrained
+                            interface solves; reading R25)             */
 } hplmm_options;
 
 typedef struct {
@@ -213,7 +217,8 @@ typedef enum {
   HPLMM_ART_VAL = 14,         /* double[nnzb*9] values of A^ (after assemble)   */
   HPLMM_ART_RHS = 15,         /* double[n_dof] b^ (after assemble)              */
   HPLMM_ART_S = 16,           /* double[N_m*N_m] coarse mortar block S (setup)  */
-  HPLMM_ART_MORTAR_W = 17     /* double[sum |F_c| nu_c] weights, row-major per interface */
+  HPLMM_ART_MORTAR_W = 17     /* double[sum 9 |F_c| nu_c] mortar blocks M^{c} (3|F_c| x 3nu_c,
+                                 row 3f+d, column 3i+gamma), row-major per interface */
 } hplmm_artifact;
 
 /* Copy an artifact to the host buffer `buf` of `cap` BYTES; *len receives the

@@ -137,8 +137,8 @@ struct hplmm_handle {
     return (T*)p;
   }
   template <class T>
-  T* upload(const std::vector<T>& v) {
-    T* p = dalloc<T>(v.size());
+  T* upload(const std::vector<T>& v, bool setup_only = false) {
+    T* p = dalloc<T>(v.size(), setup_only);
     if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     return p;
   }
@@ -227,7 +227,7 @@ hplmm_status fail(const HError& e) {
 // or, for the coarse block, one subdomain of `ndof_override` identity DOFs.
 void build_batch(hplmm_handle* h, DevBatch& b, const std::vector<int32_t>& ptr,
                  const std::vector<int32_t>& nodes, int ndof_override, bool setup_buffers,
-                 bool with_tiles = true) {
+                 bool with_tiles = true, bool transient = false) {
   int nsub = ndof_override >= 0 ? 1 : (int)ptr.size() - 1;
   std::vector<int32_t> nb(nsub), ndof(nsub);
   std::vector<int64_t> tile_base(nsub), row_base(nsub);
@@ -262,22 +262,22 @@ void build_batch(hplmm_handle* h, DevBatch& b, const std::vector<int32_t>& ptr,
   b.ntiles = nt;
   b.nrows = nr;
   b.nloc = nr * TB;
-  b.nb = h->upload(nb);
-  b.ndof = h->upload(ndof);
-  b.tile_base = h->upload(tile_base);
-  b.row_base = h->upload(row_base);
-  b.tile_s = h->upload(tile_s);
-  b.tile_ij = h->upload(tile_ij);
-  b.row_s = h->upload(row_s);
-  b.row_k = h->upload(row_k);
-  b.lmap = h->upload(lmap);
-  b.xloc = h->dalloc<double>((size_t)b.nloc);
-  b.yloc = h->dalloc<double>((size_t)b.nloc);
-  b.err = h->dalloc<int32_t>(1);
+  b.nb = h->upload(nb, transient);
+  b.ndof = h->upload(ndof, transient);
+  b.tile_base = h->upload(tile_base, transient);
+  b.row_base = h->upload(row_base, transient);
+  b.tile_s = h->upload(tile_s, transient);
+  b.tile_ij = h->upload(tile_ij, transient);
+  b.row_s = h->upload(row_s, transient);
+  b.row_k = h->upload(row_k, transient);
+  b.lmap = h->upload(lmap, transient);
+  b.xloc = h->dalloc<double>((size_t)b.nloc, transient);
+  b.yloc = h->dalloc<double>((size_t)b.nloc, transient);
+  b.err = h->dalloc<int32_t>(1, transient);
   if (!with_tiles) return;   // layout only (supernodal mode: B_g row layout, lmap)
-  b.tiles = h->dalloc<double>((size_t)nt * TILE);
-  b.part_row = h->dalloc<double>((size_t)nt * TB);
-  b.part_col = h->dalloc<double>((size_t)nt * TB);
+  b.tiles = h->dalloc<double>((size_t)nt * TILE, transient);
+  b.part_row = h->dalloc<double>((size_t)nt * TB, transient);
+  b.part_col = h->dalloc<double>((size_t)nt * TB, transient);
   if (setup_buffers) {
     b.dinv = h->dalloc<double>((size_t)nsub * TILE, true);
     b.cbuf = h->dalloc<double>((size_t)nr * TILE, true);
@@ -472,6 +472,7 @@ void hplmm_default_options(hplmm_options* o) {
   o->coarse_refine = 0;
   o->local_factor = 1;
   o->coarse_solver = 0;
+  o->mortar_kind = 0;
 }
 
 const char* hplmm_last_error(void) { return g_last_error.c_str(); }
@@ -675,7 +676,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     for (int c = 0; c < C; ++c) {
       wt_off[c] = wo;
       int nu = hs.mortar_ptr[c + 1] - hs.mortar_ptr[c];
-      wo += (int64_t)(hs.iface_ptr[c + 1] - hs.iface_ptr[c]) * nu;
+      wo += (int64_t)9 * (hs.iface_ptr[c + 1] - hs.iface_ptr[c]) * nu;   // 3|F| x 3nu block
       for (int m = hs.mortar_ptr[c]; m < hs.mortar_ptr[c + 1]; ++m) mortar_iface[m] = c;
     }
     std::vector<int32_t> mcol_ptr(Nm + 1, 0), mcol_g, mcol_j;
@@ -742,7 +743,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     co.g_row_s = h->gb.row_s;
     co.g_row_base = h->gb.row_base;
     co.max_k = maxk;
-    h->rep.prolong_nnz = off + wo * 3;
+    h->rep.prolong_nnz = off + wo / 3;   // Q^o entries with a nonzero (Gaussian) pattern
     CK(cudaMemsetAsync(co.B, 0, std::max<int64_t>(off, 1) * 8, h->st));
     CK(cudaMemsetAsync(co.R, 0, std::max<int64_t>(off, 1) * 8, h->st));
     CK(cudaMemsetAsync(co.Dc, 0, std::max(G, 1) * 8, h->st));
@@ -845,9 +846,60 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       int32_t* d_iface_of = h->upload(iface_of);
       co.iface_of = d_iface_of;
       co.n_iface_nodes = (int)iface_of.size();
-      launch_mortar_weights((int)iface_of.size(), d_iface_of, co.iface_ptr, co.iface_nodes,
-                            co.mortar_ptr, h->upload(hs.mortar_nodes), co.wt_off, h->d_ijk,
-                            hs.opt.beta, co.W, h->st);
+      int32_t* d_mortar_nodes = h->upload(hs.mortar_nodes);
+      if (hs.opt.mortar_kind == 0) {
+        launch_mortar_weights((int)iface_of.size(), d_iface_of, co.iface_ptr, co.iface_nodes,
+                              co.mortar_ptr, d_mortar_nodes, co.wt_off, h->d_ijk, hs.opt.beta,
+                              co.W, h->st);
+      } else {
+        // Algebraic mortars: batch of SPD interface blocks A~ = A^[free, free]
+        // (free = interface nodes that are not mortar nodes), inverted by the
+        // packed-tile sweep, applied to the 3 nu_c constraint columns
+        std::vector<int32_t> free_ptr(C + 1, 0), free_nodes, free_pos, con_pos;
+        int maxq = 0;
+        for (int c = 0; c < C; ++c) {
+          std::vector<int32_t> X(hs.mortar_nodes.begin() + hs.mortar_ptr[c],
+                                 hs.mortar_nodes.begin() + hs.mortar_ptr[c + 1]);
+          maxq = std::max(maxq, 3 * (int)X.size());
+          std::sort(X.begin(), X.end());
+          for (int e = hs.iface_ptr[c]; e < hs.iface_ptr[c + 1]; ++e) {
+            const int y = hs.iface_nodes[e];
+            if (!std::binary_search(X.begin(), X.end(), y)) {
+              free_nodes.push_back(y);
+              free_pos.push_back(e - hs.iface_ptr[c]);
+            }
+          }
+          free_ptr[c + 1] = (int32_t)free_nodes.size();
+        }
+        for (int m = 0; m < hs.n_mortar_nodes(); ++m) {
+          const int c = mortar_iface[m], x = hs.mortar_nodes[m];
+          const int* F = hs.iface_nodes.data() + hs.iface_ptr[c];
+          const int nF = hs.iface_ptr[c + 1] - hs.iface_ptr[c];
+          con_pos.push_back((int32_t)(std::lower_bound(F, F + nF, x) - F));
+        }
+        DevBatch ab;
+        build_batch(h, ab, free_ptr, free_nodes, -1, true, true, /*transient=*/true);
+        int32_t big2 = INT_MAX;
+        CK(cudaMemsetAsync(ab.tiles, 0, (size_t)ab.ntiles * TILE * 8, h->st));
+        CK(cudaMemcpyAsync(ab.err, &big2, 4, cudaMemcpyHostToDevice, h->st));
+        launch_extract_local(ab, free_ptr.back(), h->upload(free_ptr), h->upload(free_nodes),
+                             h->d_row_ptr, h->d_col, h->d_val, h->st);
+        launch_pad_identity(ab, h->st);
+        launch_sweep_invert(ab, h->st);
+        CK(cudaGetLastError());
+        check_batch_err(h, ab, 0, false);
+        int32_t* d_free_ptr = h->upload(free_ptr);
+        int32_t* d_free_pos = h->upload(free_pos);
+        int32_t* d_con_pos = h->upload(con_pos);
+        for (int q = 0; q < maxq; ++q) {
+          launch_alg_rhs(q, ab, co.mortar_ptr, d_mortar_nodes, h->d_row_ptr, h->d_col, h->d_val,
+                         h->st);
+          launch_symv(ab, h->st);
+          launch_alg_store(q, C, ab, co.mortar_ptr, d_free_ptr, d_free_pos, d_con_pos, co.wt_off,
+                           co.W, h->st);
+        }
+        CK(cudaGetLastError());
+      }
     }
     launch_build_R(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
     {
@@ -1220,7 +1272,8 @@ hplmm_status hplmm_export(hplmm_handle* h, int32_t art, void* buf, int64_t cap, 
         if (!h->setup_done) throw HError{HPLMM_ERR_STATE, "weights before setup"};
         int64_t wo = 0;
         for (int c = 0; c < hs.n_ifaces(); ++c)
-          wo += (int64_t)(hs.iface_ptr[c + 1] - hs.iface_ptr[c]) * (hs.mortar_ptr[c + 1] - hs.mortar_ptr[c]);
+          wo += (int64_t)9 * (hs.iface_ptr[c + 1] - hs.iface_ptr[c]) *
+                (hs.mortar_ptr[c + 1] - hs.mortar_ptr[c]);
         src = h->co.W; n = wo; esz = 8; dev = true; break;
       }
       default: throw HError{HPLMM_ERR_ARG, "unknown artifact"};

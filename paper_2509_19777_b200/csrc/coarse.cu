@@ -44,11 +44,14 @@ __global__ void k_build_R(DevCoarse c, int64_t nloc, const int32_t* lmap, const 
     if (cf < 0) continue;
     int jb = grain_col_base(c, g, cf, c.mortar_ptr);
     if (jb < 0) continue;
-    int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
-    const double* w = c.W + c.wt_off[cf] + (int64_t)c.node_local[q] * nu;
+    const int nq3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
+    // mortar block rows of node q (3 components): M[3 lq + d][col]
+    const double* w = c.W + c.wt_off[cf] + (int64_t)(3 * c.node_local[q]) * nq3;
     const double* a = val + 9 * (int64_t)e + 3 * r;
-    for (int m = 0; m < nu; ++m)
-      for (int gam = 0; gam < 3; ++gam) R[jb + 3 * m + gam] += a[gam] * w[m];
+    for (int col = 0; col < nq3; ++col) {
+      const double t = a[0] * w[col] + a[1] * w[nq3 + col] + a[2] * w[2 * nq3 + col];
+      R[jb + col] += t;
+    }
   }
 }
 
@@ -146,12 +149,14 @@ __device__ __forceinline__ void s_add(double* S, int64_t lds, int k, int j, doub
 __global__ void k_S_iface(DevCoarse c, const int32_t* rp, const int32_t* col, const double* val,
                           double* S, int64_t lds) {
   int cf = blockIdx.x;
-  int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
+  const int nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
   int kbase = 3 * c.mortar_ptr[cf];
   for (int e0 = c.iface_ptr[cf]; e0 < c.iface_ptr[cf + 1]; ++e0) {
     int y = c.iface_nodes[e0];
-    const double* wy = c.W + c.wt_off[cf] + (int64_t)(e0 - c.iface_ptr[cf]) * nu;
+    // rows 3 yl + gam of this interface's mortar block
+    const double* My = c.W + c.wt_off[cf] + (int64_t)(3 * (e0 - c.iface_ptr[cf])) * nu3;
     for (int gam = 0; gam < 3; ++gam) {
+      const double* wy = My + (int64_t)gam * nu3;   // wy[q]: coefficient of S row kbase + q
       for (int e = rp[y]; e < rp[y + 1]; ++e) {
         int q = col[e];
         const double* a = val + 9 * (int64_t)e + 3 * gam;
@@ -163,17 +168,18 @@ __global__ void k_S_iface(DevCoarse c, const int32_t* rp, const int32_t* col, co
             int L = c.ld[g], k = L - 1;
             const double* Brow = c.B + c.b_off[g] + (int64_t)(3 * c.node_local[q] + c3) * L;
             const int32_t* cols = c.gcols + c.gcols_ptr[g];
-            for (int t = threadIdx.x; t < nu * k; t += blockDim.x) {
+            for (int t = threadIdx.x; t < nu3 * k; t += blockDim.x) {
               int i = t / k, j = t - i * k;
-              s_add(S, lds, kbase + 3 * i + gam, cols[j], wy[i] * aa * Brow[j]);
+              if (wy[i] != 0.0) s_add(S, lds, kbase + i, cols[j], wy[i] * aa * Brow[j]);
             }
           } else {                           // interface row of P_B (Q^o)
-            int nq = c.mortar_ptr[cq + 1] - c.mortar_ptr[cq];
-            const double* wq = c.W + c.wt_off[cq] + (int64_t)c.node_local[q] * nq;
+            const int nq3 = 3 * (c.mortar_ptr[cq + 1] - c.mortar_ptr[cq]);
+            const double* wq = c.W + c.wt_off[cq] + (int64_t)(3 * c.node_local[q] + c3) * nq3;
             int qbase = 3 * c.mortar_ptr[cq];
-            for (int t = threadIdx.x; t < nu * nq; t += blockDim.x) {
-              int i = t / nq, i2 = t - i * nq;
-              s_add(S, lds, kbase + 3 * i + gam, qbase + 3 * i2 + c3, wy[i] * aa * wq[i2]);
+            for (int t = threadIdx.x; t < nu3 * nq3; t += blockDim.x) {
+              int i = t / nq3, i2 = t - i * nq3;
+              if (wy[i] != 0.0 && wq[i2] != 0.0)
+                s_add(S, lds, kbase + i, qbase + i2, wy[i] * aa * wq[i2]);
             }
           }
           __syncthreads();
@@ -206,6 +212,80 @@ __global__ void k_S_grain(DevCoarse c, double* S, int64_t lds) {
 void launch_S_grain(const DevCoarse& c, double* S, int64_t lds, cudaStream_t st) {
   if (c.Nm <= 0) return;
   k_S_grain<<<c.Nm, 128, 0, st>>>(c, S, lds);
+}
+
+// ---------------------------------------------------------------------------
+// Algebraic mortars (eq:algebra via the Remark P:356, reading R25): column q =
+// 3i + gamma of interface c's block solves A~ x_free = -A^[free, (x_i, gamma)]
+// on the interface's free (non-mortar) nodes; the constrained rows are 0/1.
+// One pass per column q: k_alg_rhs writes the right-hand sides into the
+// interface batch's xloc (its packed A~^-1 is then applied by the batched
+// SYMV), k_alg_store scatters y_loc and the 0/1 rows into the blocks.
+// ---------------------------------------------------------------------------
+__global__ void k_alg_rhs(int q, int64_t nloc, const int32_t* __restrict__ lmap,
+                          const int32_t* __restrict__ row_s, const int32_t* mortar_ptr,
+                          const int32_t* mortar_nodes, const int32_t* rp,
+                          const int32_t* col, const double* val, double* xloc) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nloc) return;
+  const int d = lmap[t];
+  double v = 0.0;
+  if (d >= 0) {
+    const int c = row_s[t >> 6];
+    const int nu = mortar_ptr[c + 1] - mortar_ptr[c];
+    if (q < 3 * nu) {
+      const int x = mortar_nodes[mortar_ptr[c] + q / 3], gam = q % 3;
+      const int y = d / 3, r = d - 3 * y;
+      for (int e = rp[y]; e < rp[y + 1]; ++e)
+        if (col[e] == x) {
+          v = -val[9 * (int64_t)e + 3 * r + gam];
+          break;
+        }
+    }
+  }
+  xloc[t] = v;
+}
+
+// free rows from y_loc (interface batch local order = free nodes of F_c in
+// ascending order, 3 DOFs each); constrained rows 0/1.  free_pos / con_pos:
+// position of each free / mortar node within F_c.
+__global__ void k_alg_store(int q, int C, const int32_t* mortar_ptr, const int32_t* free_ptr,
+                            const int32_t* free_pos, const int32_t* con_pos,
+                            const int64_t* row_base, const int64_t* wt_off,
+                            const double* __restrict__ yloc, double* W) {
+  const int c = blockIdx.x;
+  if (c >= C) return;
+  const int nu = mortar_ptr[c + 1] - mortar_ptr[c];
+  const int nu3 = 3 * nu;
+  if (q >= nu3) return;
+  double* M = W + wt_off[c];
+  const int nf = free_ptr[c + 1] - free_ptr[c];
+  const double* y = yloc + 64 * row_base[c];
+  for (int t = threadIdx.x; t < 3 * nf; t += blockDim.x) {
+    const int f = free_pos[free_ptr[c] + t / 3];
+    M[(int64_t)(3 * f + t % 3) * nu3 + q] = y[t];
+  }
+  for (int t = threadIdx.x; t < nu3; t += blockDim.x) {
+    const int f = con_pos[mortar_ptr[c] + t / 3];
+    M[(int64_t)(3 * f + t % 3) * nu3 + q] = (t == q) ? 1.0 : 0.0;
+  }
+}
+
+void launch_alg_rhs(int q, const DevBatch& ab, const int32_t* mortar_ptr,
+                    const int32_t* mortar_nodes, const int32_t* rp, const int32_t* col,
+                    const double* val, cudaStream_t st) {
+  if (ab.nloc <= 0) return;
+  k_alg_rhs<<<(unsigned)((ab.nloc + 255) / 256), 256, 0, st>>>(q, ab.nloc, ab.lmap, ab.row_s,
+                                                               mortar_ptr, mortar_nodes, rp, col,
+                                                               val, ab.xloc);
+}
+
+void launch_alg_store(int q, int C, const DevBatch& ab, const int32_t* mortar_ptr,
+                      const int32_t* free_ptr, const int32_t* free_pos, const int32_t* con_pos,
+                      const int64_t* wt_off, double* W, cudaStream_t st) {
+  if (C <= 0) return;
+  k_alg_store<<<C, 128, 0, st>>>(q, C, mortar_ptr, free_ptr, free_pos, con_pos, ab.row_base,
+                                 wt_off, ab.yloc, W);
 }
 
 // ---------------------------------------------------------------------------
@@ -288,13 +368,16 @@ __global__ void k_restrict_final(DevCoarse c, const int32_t* mortar_iface, const
       int g = c.mcol_g[e], j = c.mcol_j[e];
       acc += c.gpart[c.yext_off[g] + j];
     }
-    int m = k / 3, gam = k - 3 * m;
+    int m = k / 3;
     int cf = mortar_iface[m];
-    int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
-    int i = m - c.mortar_ptr[cf];
-    const double* w = c.W + c.wt_off[cf] + i;
-    for (int e = c.iface_ptr[cf]; e < c.iface_ptr[cf + 1]; ++e)
-      acc += w[(int64_t)(e - c.iface_ptr[cf]) * nu] * r[3 * (int64_t)c.iface_nodes[e] + gam];
+    const int nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
+    const int q = k - 3 * c.mortar_ptr[cf];   // column of the interface block
+    const double* w = c.W + c.wt_off[cf] + q;
+    for (int e = c.iface_ptr[cf]; e < c.iface_ptr[cf + 1]; ++e) {
+      const int64_t row = 3 * (int64_t)(e - c.iface_ptr[cf]);
+      const double* ry = r + 3 * (int64_t)c.iface_nodes[e];
+      acc += w[row * nu3] * ry[0] + w[(row + 1) * nu3] * ry[1] + w[(row + 2) * nu3] * ry[2];
+    }
     rm[k] = acc;
   } else if (k < c.Nm + c.n_grains) {
     int g = k - c.Nm;
@@ -347,11 +430,11 @@ __global__ void __launch_bounds__(256) k_prolong(DevCoarse c, const int32_t* gpo
   } else if (lane == 0) {
     int p = (int)(d / 3), gam = (int)(d - 3 * p);
     int cf = c.node_iface[p];
-    int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
-    const double* w = c.W + c.wt_off[cf] + (int64_t)c.node_local[p] * nu;
-    int kb = 3 * c.mortar_ptr[cf] + gam;
+    const int nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
+    const double* w = c.W + c.wt_off[cf] + (int64_t)(3 * c.node_local[p] + gam) * nu3;
+    int kb = 3 * c.mortar_ptr[cf];
     double acc = 0.0;
-    for (int i = 0; i < nu; ++i) acc += w[i] * ym[kb + 3 * i];
+    for (int q = 0; q < nu3; ++q) acc += w[q] * ym[kb + q];
     x[d] = acc;
   }
 }
@@ -406,11 +489,11 @@ __global__ void k_prolong_iface(DevCoarse c, const double* __restrict__ ym, doub
   if (e >= n3) return;
   int en = e / 3, gam = e - 3 * en;
   int cf = c.iface_of[en];
-  int nu = c.mortar_ptr[cf + 1] - c.mortar_ptr[cf];
-  const double* w = c.W + c.wt_off[cf] + (int64_t)(en - c.iface_ptr[cf]) * nu;
-  int kb = 3 * c.mortar_ptr[cf] + gam;
+  const int nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
+  const double* w = c.W + c.wt_off[cf] + (int64_t)(3 * (en - c.iface_ptr[cf]) + gam) * nu3;
+  int kb = 3 * c.mortar_ptr[cf];
   double acc = 0.0;
-  for (int i = 0; i < nu; ++i) acc += w[i] * ym[kb + 3 * i];
+  for (int q = 0; q < nu3; ++q) acc += w[q] * ym[kb + q];
   x[3 * (int64_t)c.iface_nodes[en] + gam] = acc;
 }
 

@@ -432,6 +432,8 @@ __device__ double gauss_exponent(const int32_t* ijk, const int32_t* X, int nu, i
   return -(double)d2i(ijk, y, X[i]) / (beta * (double)dmin);
 }
 
+// Gaussian mortar block rows of interface node y (index yl in F_c):
+// M[3 yl + d][3 i + gamma] = w_i(y) delta_{d gamma}   (row-major, 3 nu columns)
 __global__ void k_mortar_weights(int n, const int32_t* iface_of, const int32_t* iface_ptr,
                                  const int32_t* iface_nodes, const int32_t* mortar_ptr,
                                  const int32_t* mortar_nodes, const int64_t* wt_off,
@@ -443,16 +445,19 @@ __global__ void k_mortar_weights(int n, const int32_t* iface_of, const int32_t* 
   int yl = e - iface_ptr[c];
   const int32_t* X = mortar_nodes + mortar_ptr[c];
   int nu = mortar_ptr[c + 1] - mortar_ptr[c];
-  double* out = W + wt_off[c] + (int64_t)yl * nu;
-  if (nu == 1) {
-    out[0] = 1.0;
-    return;
+  double* out = W + wt_off[c] + (int64_t)(3 * yl) * (3 * nu);
+  double m = 0.0, s = 1.0;
+  if (nu > 1) {
+    m = -DBL_MAX;
+    for (int i = 0; i < nu; ++i) m = fmax(m, gauss_exponent(ijk, X, nu, i, y, beta));
+    s = 0.0;
+    for (int i = 0; i < nu; ++i) s += exp(gauss_exponent(ijk, X, nu, i, y, beta) - m);
   }
-  double m = -DBL_MAX;
-  for (int i = 0; i < nu; ++i) m = fmax(m, gauss_exponent(ijk, X, nu, i, y, beta));
-  double s = 0.0;
-  for (int i = 0; i < nu; ++i) s += exp(gauss_exponent(ijk, X, nu, i, y, beta) - m);
-  for (int i = 0; i < nu; ++i) out[i] = exp(gauss_exponent(ijk, X, nu, i, y, beta) - m) / s;
+  for (int i = 0; i < nu; ++i) {
+    const double wi = nu == 1 ? 1.0 : exp(gauss_exponent(ijk, X, nu, i, y, beta) - m) / s;
+    for (int d = 0; d < 3; ++d)
+      for (int g = 0; g < 3; ++g) out[(int64_t)d * 3 * nu + 3 * i + g] = (d == g) ? wi : 0.0;
+  }
 }
 
 void launch_mortar_weights(int n_iface_nodes, const int32_t* iface_of, const int32_t* iface_ptr,

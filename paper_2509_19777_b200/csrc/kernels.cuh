@@ -136,6 +136,13 @@ void launch_grain_BtY(const DevCoarse& c, const DevBatch& gb, cudaStream_t st);
 void launch_S_iface(const DevCoarse& c, const int32_t* row_ptr, const int32_t* col,
                     const double* val, double* S, int64_t lds, cudaStream_t st);
 void launch_S_grain(const DevCoarse& c, double* S, int64_t lds, cudaStream_t st);
+// Algebraic mortar blocks (column q of every interface block)
+void launch_alg_rhs(int q, const DevBatch& ab, const int32_t* mortar_ptr,
+                    const int32_t* mortar_nodes, const int32_t* rp, const int32_t* col,
+                    const double* val, cudaStream_t st);
+void launch_alg_store(int q, int C, const DevBatch& ab, const int32_t* mortar_ptr,
+                      const int32_t* free_ptr, const int32_t* free_pos, const int32_t* con_pos,
+                      const int64_t* wt_off, double* W, cudaStream_t st);
 // r_m (Nm) and r_c (G, correction part) from r (n_dof)
 void launch_restrict(const DevCoarse& c, const double* r, double* rm, double* rc,
                      cudaStream_t st);

@@ -44,7 +44,7 @@ class Options(C.Structure):
     _fields_ = [("n_mortar", C.c_int32), ("beta", C.c_double), ("contact_h", C.c_int32),
                 ("restart", C.c_int32), ("max_iter", C.c_int32), ("n_st", C.c_int32),
                 ("coarse_refine", C.c_int32), ("local_factor", C.c_int32),
-                ("coarse_solver", C.c_int32)]
+                ("coarse_solver", C.c_int32), ("mortar_kind", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -150,7 +150,8 @@ class Solver:
     """Handle over one voxel problem (a ``workloads.Problem``-like object)."""
 
     def __init__(self, prob, n_mortar=None, beta=None, contact_h=None, restart=None,
-                 max_iter=None, coarse_refine=0, local_factor=None, coarse_solver=None):
+                 max_iter=None, coarse_refine=0, local_factor=None, coarse_solver=None,
+                 mortar=None):
         lib = load()
         self._lib = lib
         self._keep = []
@@ -178,6 +179,8 @@ class Solver:
             o.local_factor = int(local_factor)
         if coarse_solver is not None:
             o.coarse_solver = int(coarse_solver)
+        mk = mortar if mortar is not None else getattr(prob, "mortar", "gaussian")
+        o.mortar_kind = {"gaussian": 0, "algebraic": 1}[mk]
         self.options = o
         h = C.c_void_p()
         _check(lib.hplmm_create(C.byref(p), C.byref(o), C.byref(h)))

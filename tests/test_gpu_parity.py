@@ -67,7 +67,7 @@ def test_spmv(case):
 def test_mortar_weights_and_S(case, lf):
     p, s, h, sv = gpu_case(case, lf)
     W = sv.export("MORTAR_W")
-    Wo = np.concatenate([w.ravel() for w in h.mor.weights])
+    Wo = np.concatenate([M.ravel() for M in h.mor.blocks])
     assert np.abs(W - Wo).max() <= 1e-14
     S = sv.export("S").reshape(h.Nm, h.Nm)
     So = h.S
@@ -300,3 +300,30 @@ def test_solve_many_reuses_setup():
         assert reps[i]["converged"] == 1 and reps[i]["iterations"] == rep["iterations"]
         assert np.array_equal(X[i], x)
         assert np.linalg.norm(B[i] - s.A @ X[i]) / np.linalg.norm(B[i]) < 1e-8
+
+
+@pytest.mark.parametrize("lf", LF)
+@pytest.mark.parametrize("case", CASES)
+def test_algebraic_mortars(case, lf):
+    """Algebraic mortars (eq:algebra via the Remark, NEXT #3, reading R25):
+    the GPU's batched constrained interface solves give the oracle's mortar
+    blocks, and M^-1 / the solve match the oracle built with them."""
+    from oracle import gmres, hplmm
+    from paper_2509_19777_b200 import Solver
+    from workloads import make_problem
+    p = make_problem(case, mortar="algebraic")
+    s, h = hplmm.setup(p)
+    import __graft_entry__
+    __graft_entry__.build()
+    sv = Solver(p, local_factor=lf).assemble(0).setup()
+    W = sv.export("MORTAR_W")
+    Wo = np.concatenate([M.ravel() for M in h.mor.blocks])
+    assert np.abs(W - Wo).max() <= 1e-12 * max(1.0, np.abs(Wo).max())
+    h.set_rhs(s.b)
+    sv.set_rhs(s.b)
+    v = np.random.default_rng(12345).standard_normal(s.n_dof)
+    assert rel(sv.apply("MINV", v), h.apply_M(v)) <= max(1e-12, coarse_floor(h))
+    xo, ito, _, _, convo = gmres.gmres(s.A, s.b, h.apply_M, tol=1e-8)
+    x, rep, _ = sv.solve(s.b.copy(), tol=1e-8)
+    assert convo and rep["converged"] == 1 and abs(rep["iterations"] - ito) <= 1, (rep["iterations"], ito)
+    assert rel(x, xo) <= 1e-8
