@@ -7,7 +7,12 @@
 // mortar-placement potentials (the only floating point here) are the IEEE
 // sequence R10 prescribes: sum_j 1.0/sqrt((double)d2), in chosen order.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
+#include <thread>
 #include <cstring>
 #include <numeric>
 
@@ -141,6 +146,15 @@ bool host_setup(const hplmm_problem* p, const hplmm_options* opt, HostSetup& hs,
     return hs.solid[v] ? v : -1;
   };
 
+  static const bool dbg = getenv("HPLMM_DEBUG") != nullptr;
+  auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double tph = now();
+  auto phase = [&](const char* name) {
+    if (!dbg) return;
+    const double t = now();
+    fprintf(stderr, "hplmm host setup: %-18s %.3f s\n", name, t - tph);
+    tph = t;
+  };
   // ---- mesh: solid nodes in ascending lattice key (R3) -------------------
   hs.lat_id.assign(nlat, -1);
   for (int k = 0; k < LZ; ++k)
@@ -169,15 +183,16 @@ bool host_setup(const hplmm_problem* p, const hplmm_options* opt, HostSetup& hs,
     }
   }
 
+  phase("mesh");
   // ---- pattern: p~q iff they share a solid voxel; D rows keep only the
   //      diagonal, free rows drop D columns (R4) ---------------------------
+  // two passes over node ranges in parallel (row lengths, then fill); the
+  // result is independent of the thread count
   hs.row_ptr.assign(N + 1, 0);
   hs.drow_ptr.assign(N + 1, 0);
-  std::vector<int32_t> nb;
-  nb.reserve(27);
-  for (int q = 0; q < N; ++q) {
+  auto neighbours = [&](int q, int32_t* nb) -> int {
     const int32_t* x = &hs.node_ijk[3 * (size_t)q];
-    nb.clear();
+    int cnt = 0;
     for (int dz = -1; dz <= 1; ++dz)
       for (int dy = -1; dy <= 1; ++dy)
         for (int dx = -1; dx <= 1; ++dx) {
@@ -194,21 +209,59 @@ bool host_setup(const hplmm_problem* p, const hplmm_options* opt, HostSetup& hs,
               for (int c = 0; c < ei && !share; ++c)
                 share = vox(vi0 - (dx == 0 ? c : 0), vj0 - (dy == 0 ? b : 0),
                             vk0 - (dz == 0 ? a : 0)) >= 0;
-          if (share) nb.push_back(r);
+          if (share) nb[cnt++] = r;
         }
-    std::sort(nb.begin(), nb.end());
-    if (hs.dir[q]) {
-      hs.col_idx.push_back(q);
-    } else {
-      for (int r : nb) {
-        if (hs.dir[r]) hs.dcol.push_back(r);
-        else hs.col_idx.push_back(r);
+    std::sort(nb, nb + cnt);   // lattice-scan order is already ascending; kept for clarity
+    return cnt;
+  };
+  const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  auto parallel = [&](auto&& body) {
+    std::vector<std::thread> th;
+    const int per = (N + (int)nth - 1) / (int)nth;
+    for (unsigned t = 0; t < nth; ++t) {
+      const int q0 = (int)t * per, q1 = std::min(N, q0 + per);
+      if (q0 < q1) th.emplace_back([&, q0, q1] { body(q0, q1); });
+    }
+    for (auto& t : th) t.join();
+  };
+  parallel([&](int q0, int q1) {
+    int32_t nb[27];
+    for (int q = q0; q < q1; ++q) {
+      const int cnt = neighbours(q, nb);
+      int nf = 0, nd = 0;
+      if (hs.dir[q]) {
+        nf = 1;
+      } else {
+        for (int t = 0; t < cnt; ++t) (hs.dir[nb[t]] ? nd : nf)++;
+      }
+      hs.row_ptr[q + 1] = nf;
+      hs.drow_ptr[q + 1] = nd;
+    }
+  });
+  for (int q = 0; q < N; ++q) {
+    hs.row_ptr[q + 1] += hs.row_ptr[q];
+    hs.drow_ptr[q + 1] += hs.drow_ptr[q];
+  }
+  hs.col_idx.resize(hs.row_ptr[N]);
+  hs.dcol.resize(hs.drow_ptr[N]);
+  parallel([&](int q0, int q1) {
+    int32_t nb[27];
+    for (int q = q0; q < q1; ++q) {
+      int32_t* cf = hs.col_idx.data() + hs.row_ptr[q];
+      int32_t* cd = hs.dcol.data() + hs.drow_ptr[q];
+      if (hs.dir[q]) {
+        *cf = q;
+        continue;
+      }
+      const int cnt = neighbours(q, nb);
+      for (int t = 0; t < cnt; ++t) {
+        if (hs.dir[nb[t]]) *cd++ = nb[t];
+        else *cf++ = nb[t];
       }
     }
-    hs.row_ptr[q + 1] = (int32_t)hs.col_idx.size();
-    hs.drow_ptr[q + 1] = (int32_t)hs.dcol.size();
-  }
+  });
 
+  phase("pattern");
   // ---- node classes (R6) -------------------------------------------------
   hs.node_class.assign(N, CLS_GRAIN);
   hs.node_owner.assign(N, -1);
@@ -235,6 +288,7 @@ bool host_setup(const hplmm_problem* p, const hplmm_options* opt, HostSetup& hs,
     }
   }
 
+  phase("node classes");
   // ---- interfaces: connected components per pair (R7) --------------------
   struct Comp { int32_t g1, g2, first; std::vector<int32_t> nodes; };
   std::vector<Comp> comps;
@@ -277,6 +331,7 @@ bool host_setup(const hplmm_problem* p, const hplmm_options* opt, HostSetup& hs,
   }
   const int NC = (int)comps.size();
 
+  phase("interfaces");
   // ---- grain-interior sets I_g (R18) -------------------------------------
   hs.grain_ptr.assign(p->n_grains + 1, 0);
   for (int q = 0; q < N; ++q)
@@ -289,41 +344,69 @@ bool host_setup(const hplmm_problem* p, const hplmm_options* opt, HostSetup& hs,
       if (hs.node_class[q] != CLS_IFACE) hs.grain_nodes[fill[hs.node_owner[q]]++] = q;
   }
 
+  phase("grain sets");
   // ---- contact grids: Chebyshev dilation by h, non-D nodes (R8) ----------
   const int h = opt->contact_h;
-  std::vector<int32_t> stamp(N, -1);
   hs.contact_ptr.assign(1, 0);
-  std::vector<int32_t> zeta;
-  for (int c = 0; c < NC; ++c) {
-    zeta.clear();
-    for (int e = hs.iface_ptr[c]; e < hs.iface_ptr[c + 1]; ++e) {
-      const int32_t* x = &hs.node_ijk[3 * (size_t)hs.iface_nodes[e]];
-      for (int dz = -h; dz <= h; ++dz)
-        for (int dy = -h; dy <= h; ++dy)
-          for (int dx = -h; dx <= h; ++dx) {
-            int i = x[0] + dx, j = x[1] + dy, k = x[2] + dz;
-            if (i < 0 || j < 0 || k < 0 || i >= LX || j >= LY || k >= LZ) continue;
-            int r = hs.lat_id[i + (int64_t)LX * (j + (int64_t)LY * k)];
-            if (r < 0 || hs.dir[r] || stamp[r] == c) continue;
-            stamp[r] = c;
-            zeta.push_back(r);
-          }
+  {
+    std::vector<std::vector<int32_t>> zs(NC);
+    std::atomic<int> next{0};
+    auto work = [&]() {
+      std::vector<int32_t> stamp(N, -1);
+      for (int c; (c = next.fetch_add(1)) < NC;) {
+        std::vector<int32_t>& zeta = zs[c];
+        for (int e = hs.iface_ptr[c]; e < hs.iface_ptr[c + 1]; ++e) {
+          const int32_t* x = &hs.node_ijk[3 * (size_t)hs.iface_nodes[e]];
+          for (int dz = -h; dz <= h; ++dz)
+            for (int dy = -h; dy <= h; ++dy)
+              for (int dx = -h; dx <= h; ++dx) {
+                int i = x[0] + dx, j = x[1] + dy, k = x[2] + dz;
+                if (i < 0 || j < 0 || k < 0 || i >= LX || j >= LY || k >= LZ) continue;
+                int r = hs.lat_id[i + (int64_t)LX * (j + (int64_t)LY * k)];
+                if (r < 0 || hs.dir[r] || stamp[r] == c) continue;
+                stamp[r] = c;
+                zeta.push_back(r);
+              }
+        }
+        std::sort(zeta.begin(), zeta.end());
+      }
+    };
+    const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t + 1 < nth; ++t) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    for (int c = 0; c < NC; ++c) {
+      hs.contact_nodes.insert(hs.contact_nodes.end(), zs[c].begin(), zs[c].end());
+      hs.contact_ptr.push_back((int32_t)hs.contact_nodes.size());
     }
-    std::sort(zeta.begin(), zeta.end());
-    hs.contact_nodes.insert(hs.contact_nodes.end(), zeta.begin(), zeta.end());
-    hs.contact_ptr.push_back((int32_t)hs.contact_nodes.size());
   }
 
+  phase("contact grids");
   // ---- mortar placement (eq:node_init, R9, R10) --------------------------
+  // interfaces are independent: placed in parallel, concatenated in order
+  // (each placement is sequential and deterministic, so the result is too)
   hs.mortar_ptr.assign(1, 0);
-  for (int c = 0; c < NC; ++c) {
-    std::vector<int32_t> X = place_mortars(&hs.iface_nodes[hs.iface_ptr[c]],
-                                           hs.iface_ptr[c + 1] - hs.iface_ptr[c],
-                                           hs.node_ijk.data(), opt->n_mortar);
-    hs.mortar_nodes.insert(hs.mortar_nodes.end(), X.begin(), X.end());
-    hs.mortar_ptr.push_back((int32_t)hs.mortar_nodes.size());
+  {
+    std::vector<std::vector<int32_t>> Xs(NC);
+    std::atomic<int> next{0};
+    auto work = [&]() {
+      for (int c; (c = next.fetch_add(1)) < NC;)
+        Xs[c] = place_mortars(&hs.iface_nodes[hs.iface_ptr[c]], hs.iface_ptr[c + 1] - hs.iface_ptr[c],
+                              hs.node_ijk.data(), opt->n_mortar);
+    };
+    const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t + 1 < nth; ++t) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    for (int c = 0; c < NC; ++c) {
+      hs.mortar_nodes.insert(hs.mortar_nodes.end(), Xs[c].begin(), Xs[c].end());
+      hs.mortar_ptr.push_back((int32_t)hs.mortar_nodes.size());
+    }
   }
 
+  phase("mortar placement");
   // ---- shape-vector column sets (R14, structural option B) ---------------
   hs.gcols_ptr.assign(1, 0);
   hs.giface_ptr.assign(1, 0);
