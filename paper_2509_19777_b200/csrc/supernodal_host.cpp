@@ -5,6 +5,8 @@
 // so the result is deterministic.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 #include <thread>
@@ -204,100 +206,135 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     for (int s; (s = next.fetch_add(1)) < nsub;)
       analyse_one(hs, nodes.data() + ptr[s], ptr[s + 1] - ptr[s], leaf, g2l, res[s]);
   };
+  static const bool dbg = getenv("HPLMM_DEBUG") != nullptr;
+  auto now = [] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t0 = now();
   std::vector<std::thread> th;
   for (unsigned t = 0; t + 1 < nth; ++t) th.emplace_back(work);
   work();
   for (auto& t : th) t.join();
+  const double t1 = now();
 
   o = SnSymbolic();
   o.nsub = nsub;
-  {  // reserve the concatenated arrays (tens of millions of entries at cfg3)
-    size_t nn = 0, ns = 0, nr = 0, na = 0, nrel = 0;
-    for (const SubResult& r : res) {
-      nn += 3 * (size_t)r.n_nodes;
-      ns += r.sns.size();
-      for (size_t k = 0; k < r.sns.size(); ++k) {
-        nr += 3 * r.st[k].size();
-        na += r.ae[k].size();
-        nrel += r.rel[k].size();
-      }
-    }
-    o.gmap.reserve(nn);
-    o.lidx.reserve(nn);
-    o.rows.reserve(nr);
-    o.asm_e.reserve(na);
-    o.asm_u.reserve(na);
-    o.asm_v.reserve(na);
-    o.rel.reserve(nrel);
-    for (auto* v : {&o.sn_w, &o.sn_r, &o.sn_p0, &o.sn_ldw, &o.sn_ldf, &o.sn_level, &o.sn_parent,
-                    &o.sn_sub, &o.sn_child_rank})
-      v->reserve(ns);
-    o.sn_rows_off.reserve(ns);
-    o.sn_foff.reserve(ns);
-    o.asm_ptr.reserve(ns + 1);
-    o.rel_off.reserve(ns + 1);
-  }
-  int64_t base = 0, foff = 0, roff = 0;
-  o.asm_ptr.push_back(0);
-  o.rel_off.push_back(0);
-  for (int s = 0; s < nsub; ++s) {
-    SubResult& r = res[s];
-    if (!r.ok) {
-      err = "subdomain " + std::to_string(s) + ": " + r.err;
+  for (int s = 0; s < nsub; ++s)
+    if (!res[s].ok) {
+      err = "subdomain " + std::to_string(s) + ": " + res[s].err;
       return false;
     }
-    const int n = 3 * r.n_nodes;
-    const int sn0 = o.nsn;
-    o.sub_n.push_back(n);
-    o.sub_base.push_back(base);
-    o.sub_sn0.push_back(sn0);
-    o.max_n = std::max(o.max_n, n);
-    const int32_t* gn = nodes.data() + ptr[s];
-    for (int a : r.order)
-      for (int c = 0; c < 3; ++c) {
-        o.gmap.push_back(3 * gn[a] + c);
-        o.lidx.push_back(3 * a + c);
-      }
-    int p0 = 0;
-    std::vector<int> nchild(r.sns.size(), 0);
+  // pass 1 (serial, per subdomain): offsets of every concatenated array
+  std::vector<int64_t> o_loc(nsub + 1, 0), o_sn(nsub + 1, 0), o_rows(nsub + 1, 0),
+      o_asm(nsub + 1, 0), o_rel(nsub + 1, 0), o_f(nsub + 1, 0);
+  for (int s = 0; s < nsub; ++s) {
+    const SubResult& r = res[s];
+    int64_t nr = 0, na = 0, nl = 0, nf = 0;
     for (size_t k = 0; k < r.sns.size(); ++k) {
       const int w = 3 * (int)r.sns[k].members.size(), rr = 3 * (int)r.st[k].size();
-      o.sn_w.push_back(w);
-      o.sn_r.push_back(rr);
-      o.sn_p0.push_back(p0);
-      o.sn_ldw.push_back(rr + (rr & 1));
-      o.sn_ldf.push_back(w + (w & 1));
-      o.sn_level.push_back(r.level[k]);
-      o.sn_parent.push_back(r.sns[k].parent >= 0 ? sn0 + r.sns[k].parent : -1);
-      o.sn_sub.push_back(s);
-      int rank = 0;
-      if (r.sns[k].parent >= 0) rank = nchild[r.sns[k].parent]++;
-      o.sn_child_rank.push_back(rank);
-      o.max_children = std::max(o.max_children, rank + 1);
-      o.sn_rows_off.push_back(roff);
-      for (int q : r.st[k])
-        for (int c = 0; c < 3; ++c) o.rows.push_back(3 * q + c);
-      roff += rr;
-      o.sn_foff.push_back(foff);
-      foff += sn_rows_doubles(rr) + (int64_t)o.sn_ldw.back() * w + (int64_t)o.sn_ldf.back() * w;
-      o.max_w = std::max(o.max_w, w);
-      o.max_r = std::max(o.max_r, rr);
-      o.n_levels = std::max(o.n_levels, r.level[k] + 1);
-      p0 += w;
-      o.asm_e.insert(o.asm_e.end(), r.ae[k].begin(), r.ae[k].end());
-      o.asm_u.insert(o.asm_u.end(), r.au[k].begin(), r.au[k].end());
-      o.asm_v.insert(o.asm_v.end(), r.av[k].begin(), r.av[k].end());
-      o.asm_ptr.push_back((int64_t)o.asm_e.size());
-      o.rel.insert(o.rel.end(), r.rel[k].begin(), r.rel[k].end());
-      o.rel_off.push_back((int64_t)o.rel.size());
-      o.nsn++;
+      nr += rr;
+      na += (int64_t)r.ae[k].size();
+      nl += (int64_t)r.rel[k].size();
+      nf += sn_rows_doubles(rr) + (int64_t)(rr + (rr & 1)) * w + (int64_t)(w + (w & 1)) * w;
     }
-    o.sub_sn1.push_back(o.nsn);
-    base += n;
-    res[s] = SubResult();   // free
+    o_loc[s + 1] = o_loc[s] + 3 * (int64_t)r.n_nodes;
+    o_sn[s + 1] = o_sn[s] + (int64_t)r.sns.size();
+    o_rows[s + 1] = o_rows[s] + nr;
+    o_asm[s + 1] = o_asm[s] + na;
+    o_rel[s + 1] = o_rel[s] + nl;
+    o_f[s + 1] = o_f[s] + nf;
   }
+  const int64_t NS = o_sn[nsub];
+  o.nsn = (int)NS;
+  o.sub_n.resize(nsub);
+  o.sub_base.resize(nsub);
+  o.sub_sn0.resize(nsub);
+  o.sub_sn1.resize(nsub);
+  o.gmap.resize(o_loc[nsub]);
+  o.lidx.resize(o_loc[nsub]);
+  o.rows.resize(o_rows[nsub]);
+  o.asm_e.resize(o_asm[nsub]);
+  o.asm_u.resize(o_asm[nsub]);
+  o.asm_v.resize(o_asm[nsub]);
+  o.rel.resize(o_rel[nsub]);
+  for (auto* v : {&o.sn_w, &o.sn_r, &o.sn_p0, &o.sn_ldw, &o.sn_ldf, &o.sn_level, &o.sn_parent,
+                  &o.sn_sub, &o.sn_child_rank})
+    v->resize(NS);
+  o.sn_rows_off.resize(NS);
+  o.sn_foff.resize(NS);
+  o.asm_ptr.resize(NS + 1);
+  o.rel_off.resize(NS + 1);
+  o.asm_ptr[0] = 0;
+  o.rel_off[0] = 0;
+  // pass 2 (parallel over subdomains): fill
+  std::atomic<int> next2{0};
+  auto fill = [&]() {
+    for (int s; (s = next2.fetch_add(1)) < nsub;) {
+      SubResult& r = res[s];
+      const int sn0 = (int)o_sn[s];
+      o.sub_n[s] = 3 * r.n_nodes;
+      o.sub_base[s] = o_loc[s];
+      o.sub_sn0[s] = sn0;
+      o.sub_sn1[s] = (int)o_sn[s + 1];
+      const int32_t* gn = nodes.data() + ptr[s];
+      int64_t t = o_loc[s];
+      for (int a : r.order)
+        for (int c = 0; c < 3; ++c, ++t) {
+          o.gmap[t] = 3 * gn[a] + c;
+          o.lidx[t] = 3 * a + c;
+        }
+      int p0 = 0;
+      int64_t roff = o_rows[s], aoff = o_asm[s], loff = o_rel[s], foff = o_f[s];
+      std::vector<int> nchild(r.sns.size(), 0);
+      for (size_t k = 0; k < r.sns.size(); ++k) {
+        const int64_t g = sn0 + (int64_t)k;
+        const int w = 3 * (int)r.sns[k].members.size(), rr = 3 * (int)r.st[k].size();
+        o.sn_w[g] = w;
+        o.sn_r[g] = rr;
+        o.sn_p0[g] = p0;
+        o.sn_ldw[g] = rr + (rr & 1);
+        o.sn_ldf[g] = w + (w & 1);
+        o.sn_level[g] = r.level[k];
+        o.sn_parent[g] = r.sns[k].parent >= 0 ? sn0 + r.sns[k].parent : -1;
+        o.sn_sub[g] = s;
+        int rank = 0;
+        if (r.sns[k].parent >= 0) rank = nchild[r.sns[k].parent]++;
+        o.sn_child_rank[g] = rank;
+        o.sn_rows_off[g] = roff;
+        for (int q : r.st[k])
+          for (int c = 0; c < 3; ++c) o.rows[roff++] = 3 * q + c;
+        o.sn_foff[g] = foff;
+        foff += sn_rows_doubles(rr) + (int64_t)o.sn_ldw[g] * w + (int64_t)o.sn_ldf[g] * w;
+        p0 += w;
+        std::copy(r.ae[k].begin(), r.ae[k].end(), o.asm_e.begin() + aoff);
+        std::copy(r.au[k].begin(), r.au[k].end(), o.asm_u.begin() + aoff);
+        std::copy(r.av[k].begin(), r.av[k].end(), o.asm_v.begin() + aoff);
+        aoff += (int64_t)r.ae[k].size();
+        o.asm_ptr[g + 1] = aoff;
+        std::copy(r.rel[k].begin(), r.rel[k].end(), o.rel.begin() + loff);
+        loff += (int64_t)r.rel[k].size();
+        o.rel_off[g + 1] = loff;
+      }
+      r = SubResult();   // free
+    }
+  };
+  {
+    std::vector<std::thread> th2;
+    for (unsigned t = 0; t + 1 < nth; ++t) th2.emplace_back(fill);
+    fill();
+    for (auto& t : th2) t.join();
+  }
+  for (int64_t g = 0; g < NS; ++g) {
+    o.max_w = std::max(o.max_w, o.sn_w[g]);
+    o.max_r = std::max(o.max_r, o.sn_r[g]);
+    o.n_levels = std::max(o.n_levels, o.sn_level[g] + 1);
+    o.max_children = std::max(o.max_children, o.sn_child_rank[g] + 1);
+  }
+  for (int s = 0; s < nsub; ++s) o.max_n = std::max(o.max_n, o.sub_n[s]);
+  const int64_t foff = o_f[nsub];
   o.factor_doubles = foff;
   o.chunk_doubles = sn_chunk_doubles();
+  const double t2 = now();
   // TMA chunk schedule: forward = (W_S, rows, F_SS^-1) per S in postorder,
   // backward = (rows, W_S) per S in reverse postorder; W/F chunks are whole
   // columns of at most SN_CHUNK_DOUBLES.
@@ -349,6 +386,9 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     o.sub_bc1.push_back((int64_t)o.chunks.size());
     o.sub_fbytes.push_back(fb);
   }
+  if (dbg)
+    fprintf(stderr, "hplmm sn_analyse: %d subdomains, %u threads: per-subdomain %.3f s, concat %.3f s, "
+            "schedule %.3f s\n", nsub, nth, t1 - t0, t2 - t1, now() - t2);
   return true;
 }
 
