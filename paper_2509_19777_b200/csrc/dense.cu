@@ -240,25 +240,44 @@ __global__ void __launch_bounds__(256) k_sweep_update(int p, int64_t ntiles, con
     return;
   }
   extern __shared__ double sm[];
+  if (DMMA) {
+    // padded rows (72 doubles) spread the DMMA fragment loads over the banks
+    constexpr int LDP = 72;
+    double* As = sm;
+    double* Bs = sm + TB * LDP;
+    const double* Wg = wbuf + (row_base[s] + I) * TILE;
+    const double* Cg = cbuf + (row_base[s] + J) * TILE;
+    for (int e = threadIdx.x; e < TILE / 2; e += blockDim.x) {
+      const int k = e >> 5, r2 = (e & 31) * 2;
+      *reinterpret_cast<double2*>(As + k * LDP + r2) = reinterpret_cast<const double2*>(Wg)[e];
+      *reinterpret_cast<double2*>(Bs + k * LDP + r2) = reinterpret_cast<const double2*>(Cg)[e];
+    }
+    // target values first: their DRAM latency overlaps the tile product
+    double tv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      int r, c;
+      dmma_rc(q, r, c);
+      tv[q] = T[c * TB + r];
+    }
+    __syncthreads();
+    double acc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+    tile_dmma(As, LDP, Bs, LDP, TB, acc);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      int r, c;
+      dmma_rc(q, r, c);
+      T[c * TB + r] = tv[q] - acc[q];
+    }
+    return;
+  }
   double* As = sm;
   double* Bs = sm + TILE;
   load_tile(As, wbuf + (row_base[s] + I) * TILE);   // W_I (r,k) at k*64+r
   load_tile(Bs, cbuf + (row_base[s] + J) * TILE);   // C_J (c,k) at k*64+c  == (C_J^T)(k,c)
   __syncthreads();
-  if (DMMA) {
-    double acc[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-    tile_dmma(As, TB, Bs, TB, TB, acc);
-#pragma unroll
-    for (int q = 0; q < 16; q += 2) {
-      int r, c;
-      dmma_rc(q, r, c);                 // (r, c), (r, c + 1)
-      T[c * TB + r] -= acc[q];
-      T[(c + 1) * TB + r] -= acc[q + 1];
-    }
-    return;
-  }
   int r0 = (threadIdx.x & 15) * 4, c0 = (threadIdx.x >> 4) * 4;
   double acc[4][4] = {};
   tile_mma(As, Bs, acc, r0, c0);
@@ -296,7 +315,7 @@ static void sweep_steps(const DevBatch& b, cudaStream_t st) {
     k_sweep_panel<DMMA><<<(unsigned)b.nrows, 256, sm2, st>>>(p, b.nrows, b.row_s, b.row_k, b.nb,
                                                              b.tile_base, b.row_base, b.tiles,
                                                              b.dinv, b.cbuf, b.wbuf);
-    k_sweep_update<DMMA><<<(unsigned)b.ntiles, 256, sm2, st>>>(p, b.ntiles, b.tile_s, b.tile_ij,
+    k_sweep_update<DMMA><<<(unsigned)b.ntiles, 256, DMMA ? 2 * TB * 72 * 8 : sm2, st>>>(p, b.ntiles, b.tile_s, b.tile_ij,
                                                                b.nb, b.row_base, b.tiles, b.dinv,
                                                                b.cbuf, b.wbuf);
   }
@@ -308,7 +327,7 @@ void launch_sweep_invert(const DevBatch& b, cudaStream_t st) {
   if (!attr) {
     cudaFuncSetAttribute(k_sweep_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
     cudaFuncSetAttribute(k_sweep_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    cudaFuncSetAttribute(k_sweep_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    cudaFuncSetAttribute(k_sweep_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TB * 72 * 8);
     cudaFuncSetAttribute(k_sweep_panel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
     cudaFuncSetAttribute(k_sweep_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
     attr = true;
