@@ -282,6 +282,17 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     int bl = __ldg(rp + min(n, rc + min(lane, ROWS)));
     const int64_t vs = (72 * (int64_t)__shfl_sync(0xffffffffu, bl, 0)) & ~(int64_t)15;
     const int64_t cs = (4 * (int64_t)__shfl_sync(0xffffffffu, bl, 0)) & ~(int64_t)15;
+    // lane pair (2i, 2i+1) will hold entry idx(lane) of each 4-row group; the
+    // fused-residual operand v is loaded now so its latency overlaps the wait
+    const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                    ((lane >> 1) & 1);
+    double vpre[ROWS / SP_G];
+#pragma unroll
+    for (int gq = 0; gq < ROWS / SP_G; ++gq) {
+      vpre[gq] = 0.0;
+      if (RESID && !(lane & 1) && idx < 3 * SP_G && rc + gq * SP_G + idx / 3 < n)
+        vpre[gq] = __ldcs(v + 3 * (int64_t)(rc + gq * SP_G) + idx);
+    }
     mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
     const unsigned char* st = sp_smem + (size_t)s * C::STAGE;
     const double* sv = reinterpret_cast<const double*>(st) - vs / 8;              // by 9*b
@@ -339,15 +350,12 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    // lane pair (2i, 2i+1) holds entry idx(lane) of each 4-row group
-    const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                    ((lane >> 1) & 1);
 #pragma unroll
     for (int gq = 0; gq < ROWS / SP_G; ++gq) {
       const int r = rc + gq * SP_G + idx / 3;
       if (!(lane & 1) && idx < 3 * SP_G && r < n) {
         const int64_t d = 3 * (int64_t)(rc + gq * SP_G) + idx;
-        y[d] = RESID ? (v[d] - res[gq]) : res[gq];
+        y[d] = RESID ? (vpre[gq] - res[gq]) : res[gq];
       }
     }
   }
