@@ -4,7 +4,9 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 PAPER.md §4 "Multiscale preconditioner":
   eq:multi_precond (P:238-240)   M^-1 = M_G^-1 + M_L^-1 (I - A^ M_G^-1)       [O16]
-  eq:local_smoother (P:242-244)  n_st = 1 (P:484) => M_L = M_CG              [R20]
+  eq:local_smoother  M_L = n_st stages of a base smoother M_l:
+                                 M_CG (default, n_st = 1 => M_L = M_CG, R20)
+                                 or ILU(0) (P:245, P:484; oracle/ilu.py, R26-R28)
   eq:mg_struct / eq:WQP  M_G^-1 = P^ (R^ A^ P^)^-1 R^, R^ = P^T,
                                  P^ = W Q P                                  [O13]
   eq:reduced_defs (P:309-329)    Q = diag(I, Q^o), Q^o from mortar blocks M^{m_i}
@@ -34,6 +36,7 @@ from scipy.sparse.linalg import splu
 
 from .decomp import CLASS_G, Decomposition, node_dofs
 from .fem import System, build_system
+from .ilu import ILU0, block_pattern_csr, local_smoother
 from .mortar import Mortars
 
 
@@ -54,7 +57,11 @@ class _Local:
 
 class HPLMM:
     def __init__(self, system: System, n_mortar: int = 4, beta: float = 4.0,
-                 contact_h: int = 1, mortar: str = "gaussian"):
+                 contact_h: int = 1, mortar: str = "gaussian", smoother: str = "cg",
+                 n_st: int = 1):
+        if smoother not in ("cg", "ilu0") or n_st < 1:
+            raise ValueError("smoother must be 'cg' or 'ilu0' and n_st >= 1")
+        self.smoother, self.n_st = smoother, int(n_st)
         self.sys = system
         A = system.A
         self.A = A
@@ -86,6 +93,11 @@ class HPLMM:
         # contact grids (eq:Mg_Mz, R8/R19)
         self.contact_dofs = [node_dofs(nodes) for nodes in dec.contact_nodes]
         self.contact_solve = [_Local(A, d) for d in self.contact_dofs]
+        # ILU(0) base smoother (R26): scalar pattern = all 9 entries of
+        # every stored block, natural DOF order
+        self.ilu = (ILU0(block_pattern_csr(system.row_ptr, system.col_idx, system.val,
+                                           mesh.n_nodes))
+                    if smoother == "ilu0" else None)
 
         # cols_g (R14 option B, structural): every mortar column of an interface
         # that has a node coupled (a block of A^) to a class-G node of grain g.
@@ -198,15 +210,24 @@ class HPLMM:
         z1 = self.apply_Mzeta(r)
         return z1 + self.apply_Mg(r - self.A @ z1)
 
+    def apply_Ml(self, r):
+        """The base smoother M_l^-1 r: M_CG (eq:local_smoother_CG) or ILU(0) (R27)."""
+        return self.apply_MCG(r) if self.smoother == "cg" else self.ilu.solve(r)
+
+    def apply_ML(self, r):
+        """M_L^-1 r with n_st stages of M_l (eq:local_smoother, R28)."""
+        return local_smoother(self.A, self.apply_Ml, r, self.n_st)
+
     def apply_M(self, r):
-        """M^-1 r = y + M_L^-1 (r - A^ y), y = M_G^-1 r (eq:multi_precond, n_st=1)."""
+        """M^-1 r = y + M_L^-1 (r - A^ y), y = M_G^-1 r (eq:multi_precond)."""
         y = self.apply_MG(r)
-        return y + self.apply_MCG(r - self.A @ y)
+        return y + self.apply_ML(r - self.A @ y)
 
 
 def setup(prob, **kw) -> tuple[System, HPLMM]:
     s = build_system(prob)
     h = HPLMM(s, n_mortar=kw.get("n_mortar", prob.n_mortar), beta=kw.get("beta", prob.beta),
               contact_h=kw.get("contact_h", prob.contact_h),
-              mortar=kw.get("mortar", getattr(prob, "mortar", "gaussian")))
+              mortar=kw.get("mortar", getattr(prob, "mortar", "gaussian")),
+              smoother=kw.get("smoother", "cg"), n_st=kw.get("n_st", 1))
     return s, h
