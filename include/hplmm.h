@@ -73,7 +73,10 @@ typedef struct {
   int32_t contact_h;  /* contact-grid Chebyshev dilation h in nodes (R8); <0 invalid */
   int32_t restart;    /* GMRES restart m (R22, default 50; 1..512)                  */
   int32_t max_iter;   /* total Arnoldi steps cap (default 300)               */
-  int32_t n_st;       /* smoother stages (eq:local_smoother); only 1 is supported   */
+  int32_t n_st;       /* smoother stages of eq:local_smoother, 1..64:
+                         M_L^-1 = sum_i M_l^-1 prod_{j<i} (I - A^ M_l^-1),
+                         evaluated as t_1 = r, u_i = M_l^-1 t_i,
+                         t_{i+1} = t_i - A^ u_i (R28).  default 1            */
   int32_t coarse_refine; /* 1 = one step of iterative refinement of the coarse
                             solve y = S^-1 r with S kept resident (residual
                             ~(kappa u)^2 instead of ~kappa u); default 0        */
@@ -98,6 +101,14 @@ typedef struct {
                             the paper's choice, default); 1 = Algebraic
                             (eq:algebra, built by the Remark's constrained
                             interface solves; reading R25)             */
+  int32_t smoother;      /* base smoother M_l of eq:local_smoother:
+                            0 = contact-grain M_CG (eq:local_smoother_CG, the
+                                paper's choice with n_st = 1; default);
+                            1 = ILU(0) of A^ (paper: n_st = 6):
+                                scalar ILU(0) in the natural DOF order on the
+                                pattern of every stored 3x3 block (R26), held
+                                as block ILU(0) factors in A^'s BSR layout;
+                                contact-grid factors are not built        */
 } hplmm_options;
 
 typedef struct {
@@ -191,7 +202,10 @@ typedef enum {
   HPLMM_OP_MINV = 5,   /* out = M^-1 in          (eq:multi_precond; set_rhs)     */
   HPLMM_OP_RESTRICT = 6,/* out[n_coarse] = P^T in                               */
   HPLMM_OP_PROLONG = 7, /* out[n_dof] = P^ in, in has n_coarse entries          */
-  HPLMM_OP_COARSE = 8   /* out[N_m] = S^-1 in[N_m]: the coarse mortar-block solve  */
+  HPLMM_OP_COARSE = 8,  /* out[N_m] = S^-1 in[N_m]: the coarse mortar-block solve  */
+  HPLMM_OP_MILU = 9,    /* out = U^-1 L^-1 in: one ILU(0) apply (smoother = 1)     */
+  HPLMM_OP_ML = 10      /* out = M_L^-1 in: n_st stages of the base smoother
+                           (eq:local_smoother)                                   */
 } hplmm_op;
 
 /* One application of an operator (parity entry point).  in/out: host or
@@ -217,8 +231,10 @@ typedef enum {
   HPLMM_ART_VAL = 14,         /* double[nnzb*9] values of A^ (after assemble)   */
   HPLMM_ART_RHS = 15,         /* double[n_dof] b^ (after assemble)              */
   HPLMM_ART_S = 16,           /* double[N_m*N_m] coarse mortar block S (setup)  */
-  HPLMM_ART_MORTAR_W = 17     /* double[sum 9 |F_c| nu_c] mortar blocks M^{c} (3|F_c| x 3nu_c,
+  HPLMM_ART_MORTAR_W = 17,    /* double[sum 9 |F_c| nu_c] mortar blocks M^{c} (3|F_c| x 3nu_c,
                                  row 3f+d, column 3i+gamma), row-major per interface */
+  HPLMM_ART_ILU = 18          /* double[nnzb*9] block ILU(0) factor in A^'s BSR layout
+                                 (smoother = 1): L_IK (K<I), A~_IJ (J>I), A~_II^-1 */
 } hplmm_artifact;
 
 /* Copy an artifact to the host buffer `buf` of `cap` BYTES; *len receives the

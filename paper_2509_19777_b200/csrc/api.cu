@@ -116,6 +116,11 @@ struct hplmm_handle {
   bool sparse() const { return hs.opt.local_factor == 1; }
   int64_t launches = 0;
 
+  // ILU(0) base smoother (smoother == 1) and the n_st-stage buffers
+  IluDev ilu;
+  double *d_ls_u = nullptr, *d_ls_t0 = nullptr, *d_ls_t1 = nullptr, *d_ls_acc = nullptr;
+  bool ilu_smoother() const { return hs.opt.smoother == 1; }
+
   size_t alloc_bytes = 0, alloc_peak = 0;
   template <class T>
   T* dalloc(size_t n, bool setup_only = false) {
@@ -353,6 +358,72 @@ void require_device(hplmm_handle* h) {
 }
 
 // ---------------------------------------------------------------------------
+// ILU(0) base smoother setup (smoother == 1; R26): level schedules of the
+// forward and backward elimination DAGs of A^'s block pattern (host, integer),
+// then the block factorisation on the device.
+void setup_ilu(hplmm_handle* h) {
+  const HostSetup& hs = h->hs;
+  const int n = h->n_nodes;
+  const std::vector<int32_t>& rp = hs.row_ptr;
+  const std::vector<int32_t>& ci = hs.col_idx;
+  std::vector<int32_t> diag(n), lf(n, 0), lb(n, 0);
+  int nlf = 0, nlb = 0;
+  for (int I = 0; I < n; ++I) {
+    int d = -1, l = 0;
+    for (int e = rp[I]; e < rp[I + 1]; ++e) {
+      if (ci[e] == I) d = e;
+      else if (ci[e] < I) l = std::max(l, lf[ci[e]] + 1);
+    }
+    if (d < 0) throw HError{HPLMM_ERR_ARG, "ILU(0): row " + std::to_string(I) + " has no diagonal block"};
+    diag[I] = d;
+    lf[I] = l;
+    nlf = std::max(nlf, l + 1);
+  }
+  for (int I = n - 1; I >= 0; --I) {
+    int l = 0;
+    for (int e = diag[I] + 1; e < rp[I + 1]; ++e) l = std::max(l, lb[ci[e]] + 1);
+    lb[I] = l;
+    nlb = std::max(nlb, l + 1);
+  }
+  auto order = [n](const std::vector<int32_t>& lev, int nl) {   // stable counting sort
+    std::vector<int32_t> cnt(nl + 1, 0), ord(n);
+    for (int I = 0; I < n; ++I) cnt[lev[I] + 1]++;
+    for (int l = 0; l < nl; ++l) cnt[l + 1] += cnt[l];
+    for (int I = 0; I < n; ++I) ord[cnt[lev[I]]++] = I;
+    return ord;
+  };
+  IluDev& f = h->ilu;
+  f.n = n;
+  f.row_ptr = h->d_row_ptr;
+  f.col = h->d_col;
+  f.diag = h->upload(diag);
+  f.ord_f = h->upload(order(lf, nlf));
+  f.ord_b = h->upload(order(lb, nlb));
+  f.levels_f = nlf;
+  f.levels_b = nlb;
+  f.val = h->dalloc<double>((size_t)h->nnzb * 9);
+  f.flag_f = h->dalloc<int>(n);
+  f.ticket = h->dalloc<unsigned long long>(1);
+  f.ybuf = h->dalloc<double>((size_t)3 * n);
+  CK(cudaMemsetAsync(f.ybuf, 0xff, (size_t)24 * n, h->st));
+  f.err = h->dalloc<int>(1);
+  CK(cudaMemsetAsync(f.flag_f, 0, (size_t)n * 4, h->st));
+  CK(cudaMemsetAsync(f.ticket, 0, 8, h->st));
+  const int big = INT_MAX;
+  CK(cudaMemcpyAsync(f.err, &big, 4, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(f.val, h->d_val, (size_t)h->nnzb * 72, cudaMemcpyDeviceToDevice, h->st));
+  launch_ilu_factor(f, h->st);
+  CK(cudaGetLastError());
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, f.err, 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (bad != INT_MAX)
+    throw HError{HPLMM_ERR_SINGULAR_LOCAL,
+                 "ILU(0): singular or non-finite pivot block at node " + std::to_string(bad)};
+  h->rep.local_bytes += (int64_t)h->nnzb * 72;
+}
+
+// ---------------------------------------------------------------------------
 // operator applications (all on device vectors of length n_dof)
 // ---------------------------------------------------------------------------
 void op_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
@@ -361,6 +432,8 @@ void op_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
 }
 
 void op_mzeta(hplmm_handle* h, const double* in, double* out) {
+  if (h->ilu_smoother())
+    throw HError{HPLMM_ERR_STATE, "M_zeta / M_CG: contact grids are not built with smoother = 1"};
   if (h->sparse()) {
     h->sn_solve(h->sc, in, KC_SN_CONTACT);
     launch_sum_contact(h->n_dof, h->d_cptr_sn, h->d_cidx_sn, h->sc.yloc, out, h->st);
@@ -420,13 +493,56 @@ void op_mcg(hplmm_handle* h, const double* in, double* out) {
   op_mgrain(h, h->d_t, h->d_z1, nullptr, out);
 }
 
-// M^-1: y = M_G^-1 in ; r1 = in - A y ; out = y + M_CG^-1 r1     (eq:multi_precond)
+// M_ILU^-1 (R27): out = U^-1 L^-1 in
+void op_milu(hplmm_handle* h, const double* in, double* out) {
+  launch_ilu_solve(h->ilu, in, out, h->st);
+  h->launches += 2;
+}
+
+// out = (y ? y : 0) + M_L^-1 r, n_st stages of the base smoother in the order
+// of eq:local_smoother (R28): t_1 = r, u_i = M_l^-1 t_i, t_{i+1} = t_i - A^ u_i
+void op_ml(hplmm_handle* h, const double* r, const double* y, double* out) {
+  const int nst = h->hs.opt.n_st;
+  if (!h->ilu_smoother() && nst == 1) {   // M_CG, fused: out = y + z1 + M_g^-1 (r - A z1)
+    op_mzeta(h, r, h->d_z1);
+    op_spmv(h, h->d_z1, r, h->d_t);
+    op_mgrain(h, h->d_t, y, h->d_z1, out);
+    return;
+  }
+  if (h->ilu_smoother() && nst == 1) {
+    if (!y) { op_milu(h, r, out); return; }
+    op_milu(h, r, h->d_ls_u);
+    launch_lincomb(h->n_dof, y, h->d_ls_u, out, h->st);
+    h->launches += 1;
+    return;
+  }
+  const double* t = r;
+  double* tb[2] = {h->d_ls_t0, h->d_ls_t1};
+  for (int i = 0; i < nst; ++i) {
+    double* u = h->d_ls_u;
+    if (h->ilu_smoother()) {
+      op_milu(h, t, u);
+    } else {                               // u = M_CG^-1 t
+      op_mzeta(h, t, h->d_z1);
+      op_spmv(h, h->d_z1, t, h->d_t);
+      op_mgrain(h, h->d_t, h->d_z1, nullptr, u);
+    }
+    // acc = (i == 0 ? y : acc) + u, written to out at the last stage
+    double* acc = (i + 1 == nst) ? out : h->d_ls_acc;
+    launch_lincomb(h->n_dof, i == 0 ? y : h->d_ls_acc, u, acc, h->st);
+    h->launches += 1;
+    if (i + 1 < nst) {
+      op_spmv(h, u, t, tb[i & 1]);         // t_{i+1} = t_i - A^ u_i
+      t = tb[i & 1];
+    }
+  }
+}
+
+// M^-1: y = M_G^-1 in ; r1 = in - A y ; out = y + M_L^-1 r1     (eq:multi_precond)
 void op_minv(hplmm_handle* h, const double* in, double* out) {
   op_mg(h, in, h->d_y);
   op_spmv(h, h->d_y, in, h->d_r1);
-  op_mzeta(h, h->d_r1, h->d_z1);
-  op_spmv(h, h->d_z1, h->d_r1, h->d_t);
-  op_mgrain(h, h->d_t, h->d_y, h->d_z1, out);
+  op_ml(h, h->d_r1, h->d_y, out);
 }
 
 void do_set_rhs(hplmm_handle* h, const double* b_dev) {
@@ -473,6 +589,7 @@ void hplmm_default_options(hplmm_options* o) {
   o->local_factor = 1;
   o->coarse_solver = 0;
   o->mortar_kind = 0;
+  o->smoother = 0;
 }
 
 const char* hplmm_last_error(void) { return g_last_error.c_str(); }
@@ -601,7 +718,8 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     // ---------------- batches --------------------------------------------
     const bool sparse = h->sparse();
     build_batch(h, h->gb, hs.grain_ptr, hs.grain_nodes, -1, true, !sparse);
-    if (!sparse) build_batch(h, h->cb, hs.contact_ptr, hs.contact_nodes, -1, true);
+    const bool ilu = h->ilu_smoother();
+    if (!sparse && !ilu) build_batch(h, h->cb, hs.contact_ptr, hs.contact_nodes, -1, true);
     build_batch(h, h->sb, {}, {}, Nm, true);
     int64_t lb = (h->gb.ntiles + h->cb.ntiles) * (int64_t)TILE * 8;
     h->rep.local_bytes = lb;
@@ -780,19 +898,19 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       };
       double t0 = wall();
       if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, kSnLeaf, h->sg.sym, err) ||
-          !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, kSnLeaf, h->sc.sym, err))
+          (!ilu && !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, kSnLeaf, h->sc.sym, err)))
         throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
       double t1 = wall();
       try {
         sn_upload(h->sg, halloc, h->st, h->nsm);
-        sn_upload(h->sc, halloc, h->st, h->nsm);
+        if (!ilu) sn_upload(h->sc, halloc, h->st, h->nsm);
         double t2 = wall();
         sn_factor(h->sg, h->d_val, halloc, h->st, kSnPoolBytes);
         double t3 = wall();
         if (dbg)
           fprintf(stderr, "hplmm T_ML: analyse %.3f s, upload %.3f s, grain factor %.3f s\n", t1 - t0,
                   t2 - t1, t3 - t2);
-        try {
+        if (!ilu) try {
           sn_factor(h->sc, h->d_val, halloc, h->st, kSnPoolBytes);
           if (dbg) fprintf(stderr, "hplmm T_ML: contact factor %.3f s\n", wall() - t3);
         } catch (SnError& e) {
@@ -819,21 +937,28 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       CK(cudaMemsetAsync(h->sb.tiles, 0, (size_t)h->sb.ntiles * TILE * 8, h->st));
     } else {
       for (DevBatch* b : {&h->gb, &h->cb, &h->sb}) {
+        if (b == &h->cb && ilu) continue;
         CK(cudaMemsetAsync(b->tiles, 0, (size_t)b->ntiles * TILE * 8, h->st));
         CK(cudaMemcpyAsync(b->err, &big, 4, cudaMemcpyHostToDevice, h->st));
       }
       launch_extract_local(h->gb, hs.grain_ptr.back(), h->d_gnode_ptr, h->d_gnodes, h->d_row_ptr,
                            h->d_col, h->d_val, h->st);
-      launch_extract_local(h->cb, hs.contact_ptr.back(), h->d_cnode_ptr, h->d_cnodes,
-                           h->d_row_ptr, h->d_col, h->d_val, h->st);
       launch_pad_identity(h->gb, h->st);
-      launch_pad_identity(h->cb, h->st);
       launch_sweep_invert(h->gb, h->st);
-      launch_sweep_invert(h->cb, h->st);
+      if (!ilu) {
+        launch_extract_local(h->cb, hs.contact_ptr.back(), h->d_cnode_ptr, h->d_cnodes,
+                             h->d_row_ptr, h->d_col, h->d_val, h->st);
+        launch_pad_identity(h->cb, h->st);
+        launch_sweep_invert(h->cb, h->st);
+      }
       CK(cudaGetLastError());
       check_batch_err(h, h->gb, 0, false);
-      check_batch_err(h, h->cb, G, false);
+      if (!ilu) check_batch_err(h, h->cb, G, false);
     }
+    if (ilu) setup_ilu(h);
+    if (ilu || hs.opt.n_st > 1)
+      for (double** p : {&h->d_ls_u, &h->d_ls_t0, &h->d_ls_t1, &h->d_ls_acc})
+        *p = h->dalloc<double>(h->n_dof);
     h->rep.t_setup_local_s = tl.stop();
 
     // ---------------- T_MG: mortars, P_B, S, S^-1 -------------------------
@@ -1047,6 +1172,11 @@ hplmm_status hplmm_apply(hplmm_handle* h, int32_t op, const double* in, double* 
         case HPLMM_OP_MGRAIN: op_mgrain(h, din, nullptr, nullptr, dout); break;
         case HPLMM_OP_MCG: op_mcg(h, din, dout); break;
         case HPLMM_OP_MINV: op_minv(h, din, dout); break;
+        case HPLMM_OP_MILU:
+          if (!h->ilu_smoother()) throw HError{HPLMM_ERR_STATE, "MILU needs smoother = 1"};
+          op_milu(h, din, dout);
+          break;
+        case HPLMM_OP_ML: op_ml(h, din, nullptr, dout); break;
         case HPLMM_OP_RESTRICT: {
           launch_restrict(h->co, din, h->d_rm, h->d_rc, h->st);
           std::vector<double> rm(std::max(Nm, 0)), rc(std::max(h->co.n_grains, 1));
@@ -1276,6 +1406,9 @@ hplmm_status hplmm_export(hplmm_handle* h, int32_t art, void* buf, int64_t cap, 
                 (hs.mortar_ptr[c + 1] - hs.mortar_ptr[c]);
         src = h->co.W; n = wo; esz = 8; dev = true; break;
       }
+      case HPLMM_ART_ILU:
+        if (!h->setup_done || !h->ilu.val) throw HError{HPLMM_ERR_STATE, "ILU factor not built"};
+        src = h->ilu.val; n = h->nnzb * 9; esz = 8; dev = true; break;
       default: throw HError{HPLMM_ERR_ARG, "unknown artifact"};
     }
     *len = n;

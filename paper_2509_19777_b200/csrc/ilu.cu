@@ -1,0 +1,364 @@
+// ILU(0) base smoother ("incomplete LU-factorization
+// (M_ILU(k))", used with n_st = 6 stages of eq:local_smoother).
+//
+// Reading R26: scalar ILU(0) of A^ in the natural DOF order on the pattern of
+// every stored 3x3 block.  Because that pattern is closed under 3x3 blocks, the
+// scalar factors are those of the BLOCK ILU(0) with exact pivot blocks:
+//   L_IK = A~_IK A~_KK^-1 (K < I),   A~_IJ -= L_IK A~_KJ (K < J, (I,J) stored),
+// and M_ILU^-1 r = U^-1 L^-1 r becomes
+//   forward   y_I = r_I - sum_{K<I} L_IK y_K
+//   backward  x_I = A~_II^-1 (y_I - sum_{J>I} A~_IJ x_J).
+// The factor lives in A^'s BSR layout (same row_ptr / col_idx): L_IK below the
+// diagonal, A~_IJ above it, A~_II^-1 on it.
+//
+// Scheduling: the elimination DAG (row I needs every K < I it couples to) has
+// depth ~ i + 2j + 4k on the lattice (~670 levels at cfg3), so all three
+// kernels are sync-free: a warp per block row, rows handed out in level order
+// by an atomic ticket (only running warps hold tickets, so the oldest
+// unfinished row never waits: no co-residency assumption).  The factorisation
+// publishes an epoch stamp per finished row (st.release / ld.acquire); the
+// solve sweeps use the values themselves as flags (sentinel-filled outputs,
+// see below).  Bandwidth is not the limit here (0.6 GB
+// of factor per sweep at cfg3); the dependency chain is.
+#include <algorithm>
+#include <climits>
+
+#include "kernels.cuh"
+
+namespace hplmm {
+
+namespace {
+
+__device__ __forceinline__ int ilu_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ilu_st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void ilu_wait(const int* flag, int epoch) {
+  while (ilu_ld_acquire(flag) < epoch) {
+  }
+}
+
+// next row position in level order for this warp (lane 0 draws, broadcast)
+__device__ __forceinline__ long long ilu_ticket(unsigned long long* ctr,
+                                                unsigned long long base, int lane) {
+  unsigned long long t = 0;
+  if (lane == 0) t = atomicAdd(ctr, 1ull) - base;
+  return (long long)__shfl_sync(0xffffffffu, t, 0);
+}
+
+// c = a b (3x3 row-major)
+__device__ __forceinline__ void mm3(const double* a, const double* b, double* c) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      c[3 * i + j] = fma(a[3 * i], b[j], fma(a[3 * i + 1], b[3 + j], a[3 * i + 2] * b[6 + j]));
+}
+
+constexpr int ILU_WARPS = 8;
+
+// block ILU(0) factorisation, one warp per block row (lane j <-> block j)
+__global__ void __launch_bounds__(32 * ILU_WARPS)
+    k_ilu_factor(int n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                 const int32_t* __restrict__ diag, const int32_t* __restrict__ ord, double* val,
+                 int* flag, int epoch, unsigned long long* ctr, unsigned long long base,
+                 int* err) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const long long t = ilu_ticket(ctr, base, lane);
+    if (t >= n) break;
+    const int I = __ldg(ord + t);
+    const int b0 = __ldg(row_ptr + I), nb = __ldg(row_ptr + I + 1) - b0;
+    const int dI = __ldg(diag + I) - b0;
+    const int cj = lane < nb ? __ldg(col + b0 + lane) : INT_MAX;
+    double v[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) v[q] = lane < nb ? val[(int64_t)(b0 + lane) * 9 + q] : 0.0;
+    for (int jj = 0; jj < dI; ++jj) {   // K < I, ascending (col_idx is sorted)
+      const int K = __shfl_sync(0xffffffffu, cj, jj);
+      if (lane == 0) ilu_wait(flag + K, epoch);
+      __syncwarp();
+      // L_IK = A~_IK A~_KK^-1 (A~_KK^-1 is stored on row K's diagonal)
+      double a[9], dk[9], L[9];
+      const int dK = __ldg(diag + K);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        a[q] = __shfl_sync(0xffffffffu, v[q], jj);
+        dk[q] = __ldcg(val + (int64_t)dK * 9 + q);
+      }
+      mm3(a, dk, L);
+      if (lane == jj) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) v[q] = L[q];
+      }
+      // A~_IJ -= L_IK A~_KJ for J > K stored in both rows
+      if (cj > K && lane < nb) {
+        int lo = dK + 1, hi = __ldg(row_ptr + K + 1) - 1;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1;
+          const int cm = __ldg(col + mid);
+          if (cm == cj) {
+            double u[9], p[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) u[q] = __ldcg(val + (int64_t)mid * 9 + q);
+            mm3(L, u, p);
+#pragma unroll
+            for (int q = 0; q < 9; ++q) v[q] -= p[q];
+            break;
+          }
+          if (cm < cj) lo = mid + 1; else hi = mid - 1;
+        }
+      }
+    }
+    if (lane == dI) {   // pivot block A~_II -> its inverse (adjugate / determinant)
+      double inv[9];
+      inv[0] = v[4] * v[8] - v[5] * v[7];
+      inv[1] = v[2] * v[7] - v[1] * v[8];
+      inv[2] = v[1] * v[5] - v[2] * v[4];
+      inv[3] = v[5] * v[6] - v[3] * v[8];
+      inv[4] = v[0] * v[8] - v[2] * v[6];
+      inv[5] = v[2] * v[3] - v[0] * v[5];
+      inv[6] = v[3] * v[7] - v[4] * v[6];
+      inv[7] = v[1] * v[6] - v[0] * v[7];
+      inv[8] = v[0] * v[4] - v[1] * v[3];
+      const double det = v[0] * inv[0] + v[1] * inv[3] + v[2] * inv[6];
+      if (!(det != 0.0) || !isfinite(det)) atomicMin(err, I);
+      const double rd = 1.0 / det;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) v[q] = inv[q] * rd;
+    }
+    if (lane < nb) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) __stcg(val + (int64_t)(b0 + lane) * 9 + q, v[q]);
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) ilu_st_release(flag + I, epoch);
+  }
+}
+
+// 16-lane sums (a row has at most 13 blocks on either side of its diagonal)
+__device__ __forceinline__ void half_sum3(double& a, double& b, double& c) {
+#pragma unroll
+  for (int o = 8; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+}
+
+// Solve-sweep synchronisation: the VALUE is the flag.  Output buffers are
+// filled with a NaN bit pattern no arithmetic produces (all ones; results
+// equal to it are canonicalised), rows store their 3 doubles with plain
+// relaxed stores, and a consumer polls the 3 doubles it needs until none is
+// the sentinel (8-byte stores are single-copy atomic).  One L2 round trip per
+// dependency hop instead of data + flag, and no fences.
+constexpr unsigned long long ILU_SENT = 0xffffffffffffffffull;
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool is_sent(double v) {
+  return (unsigned long long)__double_as_longlong(v) == ILU_SENT;
+}
+__device__ __forceinline__ double unsent(double v) {   // never publish the sentinel
+  return is_sent(v) ? __longlong_as_double(0x7fffffffffffffffll) : v;
+}
+__device__ __forceinline__ void poll3(const double* p, double& a, double& b, double& c) {
+  a = ld_relaxed(p);
+  b = ld_relaxed(p + 1);
+  c = ld_relaxed(p + 2);
+  while (is_sent(a) || is_sent(b) || is_sent(c)) {
+    if (is_sent(a)) a = ld_relaxed(p);
+    if (is_sent(b)) b = ld_relaxed(p + 1);
+    if (is_sent(c)) c = ld_relaxed(p + 2);
+  }
+}
+
+// Waiting discipline (measured at cfg3): ONE lane per row spins,
+// on the dependency one level down that is issued last (the largest K in the
+// forward sweep = the x-neighbour, the smallest J in the backward sweep); the
+// other lanes then load their (by then almost always published) operands
+// once.  Letting every lane spin on its own dependency is ~1.7x slower: each
+// published row is then polled by up to 13 consumers at once, and those
+// same-line reads delay the producer's stores in L2.  Walking whole x-lines
+// per warp (the x-neighbour in registers) does not shorten the chain either:
+// the lattice level i + 2j + 4k makes every level wait on another line.
+
+// forward: y_I = r_I - sum_{K<I} L_IK y_K (rows in forward level order);
+// y must hold the sentinel on entry
+__global__ void __launch_bounds__(32 * ILU_WARPS)
+    k_ilu_fwd(int n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+              const int32_t* __restrict__ diag, const int32_t* __restrict__ ord,
+              const double* __restrict__ val, const double* __restrict__ r, double* y,
+              unsigned long long* ctr, unsigned long long base) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const long long t = ilu_ticket(ctr, base, lane);
+    if (t >= n) break;
+    const int I = __ldg(ord + t);
+    const int b0 = __ldg(row_ptr + I);
+    const int nl = __ldg(diag + I) - b0;   // blocks left of the diagonal
+    const int crit = nl - 1;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    int K = 0;
+    double L[9];
+    if (lane < nl) {
+      K = __ldg(col + b0 + lane);
+      const double* Lb = val + (int64_t)(b0 + lane) * 9;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) L[q] = __ldcs(Lb + q);
+    }
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    if (lane == max(crit, 0)) {
+      r0 = __ldg(r + 3 * (int64_t)I);
+      r1 = __ldg(r + 3 * (int64_t)I + 1);
+      r2 = __ldg(r + 3 * (int64_t)I + 2);
+    }
+    if (crit >= 0) {
+      if (lane == crit) poll3(y + 3 * (int64_t)K, c0, c1, c2);
+      __syncwarp();
+      if (lane < crit) {
+        double y0, y1, y2;
+        poll3(y + 3 * (int64_t)K, y0, y1, y2);
+        s0 = fma(L[0], y0, fma(L[1], y1, L[2] * y2));
+        s1 = fma(L[3], y0, fma(L[4], y1, L[5] * y2));
+        s2 = fma(L[6], y0, fma(L[7], y1, L[8] * y2));
+      }
+      if (crit > 0) half_sum3(s0, s1, s2);
+    }
+    if (lane == max(crit, 0)) {
+      if (crit >= 0) {
+        s0 = fma(L[0], c0, fma(L[1], c1, fma(L[2], c2, s0)));
+        s1 = fma(L[3], c0, fma(L[4], c1, fma(L[5], c2, s1)));
+        s2 = fma(L[6], c0, fma(L[7], c1, fma(L[8], c2, s2)));
+      }
+      const int64_t d = 3 * (int64_t)I;
+      __stcg(y + d, unsent(r0 - s0));
+      __stcg(y + d + 1, unsent(r1 - s1));
+      __stcg(y + d + 2, unsent(r2 - s2));
+    }
+  }
+}
+
+// backward: x_I = A~_II^-1 (y_I - sum_{J>I} A~_IJ x_J) (backward level order).
+// x must hold the sentinel on entry; y_I is reset to the sentinel once used,
+// so y is ready for the next forward sweep.
+__global__ void __launch_bounds__(32 * ILU_WARPS)
+    k_ilu_bwd(int n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+              const int32_t* __restrict__ diag, const int32_t* __restrict__ ord,
+              const double* __restrict__ val, double* y, double* x, unsigned long long* ctr,
+              unsigned long long base) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const long long t = ilu_ticket(ctr, base, lane);
+    if (t >= n) break;
+    const int I = __ldg(ord + t);
+    const int dI = __ldg(diag + I);
+    const int nu = __ldg(row_ptr + I + 1) - dI - 1;   // blocks right of the diagonal
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    int J = 0;
+    double U[9];
+    if (lane < nu) {
+      J = __ldg(col + dI + 1 + lane);
+      const double* Ub = val + (int64_t)(dI + 1 + lane) * 9;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) U[q] = __ldcs(Ub + q);
+    }
+    double D[9], z0 = 0.0, z1 = 0.0, z2 = 0.0;
+    if (lane == 0) {
+      const double* Db = val + (int64_t)dI * 9;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) D[q] = __ldcs(Db + q);
+      const int64_t d = 3 * (int64_t)I;
+      z0 = __ldcg(y + d);
+      z1 = __ldcg(y + d + 1);
+      z2 = __ldcg(y + d + 2);
+    }
+    if (nu > 0) {   // the smallest J is the critical dependency (lane 0)
+      if (lane == 0) poll3(x + 3 * (int64_t)J, c0, c1, c2);
+      __syncwarp();
+      if (lane >= 1 && lane < nu) {
+        double x0, x1, x2;
+        poll3(x + 3 * (int64_t)J, x0, x1, x2);
+        s0 = fma(U[0], x0, fma(U[1], x1, U[2] * x2));
+        s1 = fma(U[3], x0, fma(U[4], x1, U[5] * x2));
+        s2 = fma(U[6], x0, fma(U[7], x1, U[8] * x2));
+      }
+      if (nu > 1) half_sum3(s0, s1, s2);
+    }
+    if (lane == 0) {
+      if (nu > 0) {
+        s0 = fma(U[0], c0, fma(U[1], c1, fma(U[2], c2, s0)));
+        s1 = fma(U[3], c0, fma(U[4], c1, fma(U[5], c2, s1)));
+        s2 = fma(U[6], c0, fma(U[7], c1, fma(U[8], c2, s2)));
+      }
+      const int64_t d = 3 * (int64_t)I;
+      z0 -= s0;
+      z1 -= s1;
+      z2 -= s2;
+      __stcg(x + d, unsent(fma(D[0], z0, fma(D[1], z1, D[2] * z2))));
+      __stcg(x + d + 1, unsent(fma(D[3], z0, fma(D[4], z1, D[5] * z2))));
+      __stcg(x + d + 2, unsent(fma(D[6], z0, fma(D[7], z1, D[8] * z2))));
+      const double sent = __longlong_as_double((long long)ILU_SENT);
+      __stcg(y + d, sent);
+      __stcg(y + d + 1, sent);
+      __stcg(y + d + 2, sent);
+    }
+  }
+}
+
+__global__ void k_lincomb(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                          double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a ? a[i] + b[i] : b[i];
+}
+
+int ilu_grid(int n) {
+  static int cap = 0;
+  if (!cap) {
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_factor, 32 * ILU_WARPS, 0);
+    cap = nsm * std::max(occ, 1);
+  }
+  return std::max(1, std::min(cap, (n + ILU_WARPS - 1) / ILU_WARPS));
+}
+
+}  // namespace
+
+// Every launch consumes exactly n + (warps launched) tickets: each warp draws
+// until it gets one >= n.  The host keeps the running base.
+void launch_ilu_factor(IluDev& f, cudaStream_t st) {
+  const int grid = ilu_grid(f.n);
+  k_ilu_factor<<<grid, 32 * ILU_WARPS, 0, st>>>(f.n, f.row_ptr, f.col, f.diag, f.ord_f, f.val,
+                                                f.flag_f, ++f.epoch_f, f.ticket, f.ticket_base,
+                                                f.err);
+  f.ticket_base += (unsigned long long)f.n + (unsigned long long)grid * ILU_WARPS;
+}
+
+void launch_ilu_solve(IluDev& f, const double* r, double* x, cudaStream_t st) {
+  const int grid = ilu_grid(f.n);
+  (void)cudaMemsetAsync(x, 0xff, (size_t)f.n * 24, st);   // sentinel (errors surface at the next check)
+  k_ilu_fwd<<<grid, 32 * ILU_WARPS, 0, st>>>(f.n, f.row_ptr, f.col, f.diag, f.ord_f, f.val, r,
+                                             f.ybuf, f.ticket, f.ticket_base);
+  f.ticket_base += (unsigned long long)f.n + (unsigned long long)grid * ILU_WARPS;
+  k_ilu_bwd<<<grid, 32 * ILU_WARPS, 0, st>>>(f.n, f.row_ptr, f.col, f.diag, f.ord_b, f.val,
+                                             f.ybuf, x, f.ticket, f.ticket_base);
+  f.ticket_base += (unsigned long long)f.n + (unsigned long long)grid * ILU_WARPS;
+}
+
+void launch_lincomb(int64_t n, const double* a, const double* b, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_lincomb<<<grid, 256, 0, st>>>(n, a, b, out);
+}
+
+}  // namespace hplmm

@@ -184,4 +184,33 @@ void launch_combine_basis(int64_t n, int m, const double* V, int64_t ldv, const 
                           double* x, cudaStream_t st);
 void launch_axpy(int64_t n, double a, const double* x, double* y, cudaStream_t st);
 
+// ---- ILU(0) base smoother (ilu.cu) -----------------------------------------
+// Block ILU(0) factor of A^ in its own BSR layout (row_ptr/col of A^):
+// L_IK below the diagonal, A~_IJ above, A~_II^-1 on it.  Rows are processed
+// in level order (ord_f / ord_b) by sync-free kernels (epoch-stamped flags,
+// atomic tickets with a host-tracked running base).
+struct IluDev {
+  int n = 0;                                   // block rows
+  const int32_t* row_ptr = nullptr;
+  const int32_t* col = nullptr;
+  const int32_t* diag = nullptr;               // position of block (I,I)
+  const int32_t* ord_f = nullptr;              // rows by forward level
+  const int32_t* ord_b = nullptr;              // rows by backward level
+  double* val = nullptr;                       // nnzb*9 factor values
+  int* flag_f = nullptr;                       // factorisation epoch stamps
+  double* ybuf = nullptr;                      // forward-sweep output (sentinel between sweeps)
+  int epoch_f = 0;
+  unsigned long long* ticket = nullptr;
+  unsigned long long ticket_base = 0;
+  int* err = nullptr;                          // first row with a singular pivot
+  int levels_f = 0, levels_b = 0;
+};
+// val must hold A^'s values on entry
+void launch_ilu_factor(IluDev& f, cudaStream_t st);
+// x = U^-1 L^-1 r  (r and x distinct, neither is ybuf); ybuf must hold the
+// all-ones sentinel on entry and holds it again on exit
+void launch_ilu_solve(IluDev& f, const double* r, double* x, cudaStream_t st);
+// out = a + b (a may be null: out = b)
+void launch_lincomb(int64_t n, const double* a, const double* b, double* out, cudaStream_t st);
+
 }  // namespace hplmm

@@ -19,12 +19,15 @@ LIB_PATH = os.path.join(_HERE, "libhplmm.so")
 OK, NOT_CONVERGED = 0, 1
 ERR_NAMES = {-1: "ERR_ARG", -2: "ERR_CUDA", -3: "ERR_OOM", -4: "ERR_SINGULAR_LOCAL",
              -5: "ERR_SINGULAR_COARSE", -6: "ERR_NONFINITE", -7: "ERR_STATE"}
-OP = dict(SPMV=0, MG=1, MZETA=2, MGRAIN=3, MCG=4, MINV=5, RESTRICT=6, PROLONG=7, COARSE=8)
+OP = dict(SPMV=0, MG=1, MZETA=2, MGRAIN=3, MCG=4, MINV=5, RESTRICT=6, PROLONG=7, COARSE=8,
+          MILU=9, ML=10)
 ART = dict(NODE_KEY=0, ROW_PTR=1, COL_IDX=2, NODE_CLASS=3, NODE_IFACE=4, NODE_OWNER=5,
            IFACE_PTR=6, IFACE_NODES=7, CONTACT_PTR=8, CONTACT_NODES=9, MORTAR_PTR=10,
            MORTAR_NODES=11, GRAIN_COLS_PTR=12, GRAIN_COLS=13, VAL=14, RHS=15, S=16,
-           MORTAR_W=17)
-_ART_DTYPE = {0: np.int64, 14: np.float64, 15: np.float64, 16: np.float64, 17: np.float64}
+           MORTAR_W=17, ILU=18)
+_ART_DTYPE = {0: np.int64, 14: np.float64, 15: np.float64, 16: np.float64, 17: np.float64,
+              18: np.float64}
+SMOOTHER = dict(cg=0, ilu0=1)
 
 EXPORTED = ["hplmm_default_options", "hplmm_create", "hplmm_assemble", "hplmm_set_matrix",
             "hplmm_setup", "hplmm_set_rhs", "hplmm_solve", "hplmm_solve_many", "hplmm_apply",
@@ -44,7 +47,8 @@ class Options(C.Structure):
     _fields_ = [("n_mortar", C.c_int32), ("beta", C.c_double), ("contact_h", C.c_int32),
                 ("restart", C.c_int32), ("max_iter", C.c_int32), ("n_st", C.c_int32),
                 ("coarse_refine", C.c_int32), ("local_factor", C.c_int32),
-                ("coarse_solver", C.c_int32), ("mortar_kind", C.c_int32)]
+                ("coarse_solver", C.c_int32), ("mortar_kind", C.c_int32),
+                ("smoother", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -151,7 +155,7 @@ class Solver:
 
     def __init__(self, prob, n_mortar=None, beta=None, contact_h=None, restart=None,
                  max_iter=None, coarse_refine=0, local_factor=None, coarse_solver=None,
-                 mortar=None):
+                 mortar=None, smoother=None, n_st=None):
         lib = load()
         self._lib = lib
         self._keep = []
@@ -181,6 +185,10 @@ class Solver:
             o.coarse_solver = int(coarse_solver)
         mk = mortar if mortar is not None else getattr(prob, "mortar", "gaussian")
         o.mortar_kind = {"gaussian": 0, "algebraic": 1}[mk]
+        if smoother is not None:
+            o.smoother = SMOOTHER[smoother] if isinstance(smoother, str) else int(smoother)
+        if n_st is not None:
+            o.n_st = int(n_st)
         self.options = o
         h = C.c_void_p()
         _check(lib.hplmm_create(C.byref(p), C.byref(o), C.byref(h)))

@@ -136,3 +136,46 @@ def test_cfg3_solve(cfg3):
     x = x.cpu().numpy()
     assert rep["converged"] == 1
     assert np.linalg.norm(s.b - s.A @ x) / np.linalg.norm(s.b) < p.tol
+
+
+# ---- ILU(0) base smoother, n_st = 6 at full size ---------------------
+def _ilu_full_checks(p, s, sv, rows_sample=None):
+    from tests.test_gpu_ilu import block_factors
+    L, U = block_factors(sv, s)
+    A = s.A.tocsr()
+    # ILU(0) defining equations (L U)_ij = a_ij on the stored pattern, on all or
+    # sampled block rows
+    rp, ci = s.row_ptr, s.col_idx
+    nodes = np.arange(rp.size - 1) if rows_sample is None else rows_sample
+    dofs = (3 * nodes[:, None] + np.arange(3)).ravel()
+    LUr = (L[dofs] @ U).tocsr()
+    Ar = A[dofs]
+    cols = [(3 * ci[rp[q]:rp[q + 1]][:, None] + np.arange(3)).ravel() for q in nodes]
+    rr = np.concatenate([np.full(c.size, 3 * i + a) for i, c in enumerate(cols) for a in range(3)])
+    cc = np.concatenate([c for c in cols for a in range(3)])
+    d = np.asarray(LUr[rr, cc]).ravel() - np.asarray(Ar[rr, cc]).ravel()
+    assert np.abs(d).max() <= 1e-12 * np.abs(s.val).max()
+    # the apply is U^-1 L^-1 on the whole vector: L (U z) = v
+    v = np.random.default_rng(12345).standard_normal(s.n_dof)
+    z = sv.apply("MILU", dev(v)).cpu().numpy()
+    assert rel(L @ (U @ z), v) <= 1e-12
+    x, rep, _ = sv.solve(dev(s.b), tol=p.tol)
+    x = x.cpu().numpy()
+    assert rep["converged"] == 1
+    assert np.linalg.norm(s.b - s.A @ x) / np.linalg.norm(s.b) < p.tol
+    return rep
+
+
+def test_cfg2_ilu(cfg2):
+    from paper_2509_19777_b200 import Solver
+    p, s, h, _, _ = cfg2
+    sv = Solver(p, smoother="ilu0", n_st=6).assemble(0).setup()
+    _ilu_full_checks(p, s, sv)
+
+
+def test_cfg3_ilu(cfg3):
+    from paper_2509_19777_b200 import Solver
+    p, s, d, _ = cfg3
+    sv = Solver(p, smoother="ilu0", n_st=6).assemble(0).setup()
+    sample = np.random.default_rng(9).choice(s.row_ptr.size - 1, 4000, replace=False)
+    _ilu_full_checks(p, s, sv, np.sort(sample))
