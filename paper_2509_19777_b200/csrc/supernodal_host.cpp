@@ -386,6 +386,16 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     o.sub_bc1.push_back((int64_t)o.chunks.size());
     o.sub_fbytes.push_back(fb);
   }
+  if (dbg) {
+    double bw = 0, bf = 0, br = 0;
+    for (int64_t g = 0; g < NS; ++g) {
+      bw += 2.0 * 8 * o.sn_ldw[g] * o.sn_w[g];
+      bf += 8.0 * o.sn_ldf[g] * o.sn_w[g];
+      br += 2.0 * 8 * sn_rows_doubles(o.sn_r[g]);
+    }
+    fprintf(stderr, "hplmm sn_analyse: solve bytes W (fwd+bwd) %.3f GB, F_SS^-1 %.3f GB, rows %.3f GB\n",
+            bw / 1e9, bf / 1e9, br / 1e9);
+  }
   if (dbg)
     fprintf(stderr, "hplmm sn_analyse: %d subdomains, %u threads: per-subdomain %.3f s, concat %.3f s, "
             "schedule %.3f s\n", nsub, nth, t1 - t0, t2 - t1, now() - t2);

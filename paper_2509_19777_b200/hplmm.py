@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhplmm.so")
+# HPLMM_LIB: an alternative in-tree build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("HPLMM_LIB") or os.path.join(_HERE, "libhplmm.so")
 
 # status codes / ops / artifacts (mirror include/hplmm.h)
 OK, NOT_CONVERGED = 0, 1
