@@ -352,38 +352,59 @@ __global__ void k_restrict_grain(DevCoarse c) {
   if (c1 <= c0) return;
   const double* t = c.tpart + c.chunk_t[c0];
   double* out = c.gpart + c.yext_off[g];
+  const int nch = c1 - c0;
   for (int j = threadIdx.x; j < L; j += blockDim.x) {
-    double acc = 0.0;
-    for (int ch = 0; ch < c1 - c0; ++ch) acc += t[(int64_t)ch * L + j];
-    out[j] = acc;
+    // four interleaved partial sums keep four loads in flight (fixed order)
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int ch = 0;
+    for (; ch + 3 < nch; ch += 4) {
+      a0 += t[(int64_t)ch * L + j];
+      a1 += t[(int64_t)(ch + 1) * L + j];
+      a2 += t[(int64_t)(ch + 2) * L + j];
+      a3 += t[(int64_t)(ch + 3) * L + j];
+    }
+    for (; ch < nch; ++ch) a0 += t[(int64_t)ch * L + j];
+    out[j] = (a0 + a1) + (a2 + a3);
   }
 }
 
+// rm[k] = sum over grains of the pre-summed B_g^T r parts + the interface term
+// Q^o[:, k]^T r; RF_LPC lanes per column split the interface rows (fixed
+// order: lane-strided partial sums, then a butterfly), rc[g] = correction part
+constexpr int RF_LPC = 8;
 __global__ void k_restrict_final(DevCoarse c, const int32_t* mortar_iface, const double* r,
                                  double* rm, double* rc) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int k = (int)(gt / RF_LPC), sl = (int)(gt % RF_LPC);
+  double acc = 0.0;
   if (k < c.Nm) {
-    double acc = 0.0;
+    const int m = k / 3;
+    const int cf = mortar_iface[m];
+    const int nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
+    const int q = k - 3 * c.mortar_ptr[cf];   // column of the interface block
+    const double* w = c.W + c.wt_off[cf] + q;
+    const int e0 = c.iface_ptr[cf], e1 = c.iface_ptr[cf + 1];
+    for (int e = e0 + sl; e < e1; e += RF_LPC) {
+      const int64_t row = 3 * (int64_t)(e - e0);
+      const double* ry = r + 3 * (int64_t)c.iface_nodes[e];
+      acc += w[row * nu3] * ry[0] + w[(row + 1) * nu3] * ry[1] + w[(row + 2) * nu3] * ry[2];
+    }
+  }
+  // every lane of the warp takes part (the grid is a whole number of warps)
+#pragma unroll
+  for (int o = RF_LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, RF_LPC);
+  if (sl != 0) return;
+  if (k < c.Nm) {
     for (int e = c.mcol_ptr[k]; e < c.mcol_ptr[k + 1]; ++e) {
       int g = c.mcol_g[e], j = c.mcol_j[e];
       acc += c.gpart[c.yext_off[g] + j];
     }
-    int m = k / 3;
-    int cf = mortar_iface[m];
-    const int nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
-    const int q = k - 3 * c.mortar_ptr[cf];   // column of the interface block
-    const double* w = c.W + c.wt_off[cf] + q;
-    for (int e = c.iface_ptr[cf]; e < c.iface_ptr[cf + 1]; ++e) {
-      const int64_t row = 3 * (int64_t)(e - c.iface_ptr[cf]);
-      const double* ry = r + 3 * (int64_t)c.iface_nodes[e];
-      acc += w[row * nu3] * ry[0] + w[(row + 1) * nu3] * ry[1] + w[(row + 2) * nu3] * ry[2];
-    }
     rm[k] = acc;
   } else if (k < c.Nm + c.n_grains) {
     int g = k - c.Nm;
-    double acc = 0.0;
-    if (c.Dc[g] != 0.0) acc = c.gpart[c.yext_off[g] + c.ld[g] - 1];
-    rc[g] = acc;
+    double v = 0.0;
+    if (c.Dc[g] != 0.0) v = c.gpart[c.yext_off[g] + c.ld[g] - 1];
+    rc[g] = v;
   }
 }
 
@@ -393,7 +414,9 @@ void launch_restrict(const DevCoarse& c, const double* r, double* rm, double* rc
     k_restrict_chunks<<<(unsigned)c.n_chunks, 256, 0, st>>>(c, c.g_lmap, c.g_row_base, r);
   int n = c.Nm + c.n_grains;
   if (c.n_grains > 0) k_restrict_grain<<<c.n_grains, 256, 0, st>>>(c);
-  if (n > 0) k_restrict_final<<<(n + 127) / 128, 128, 0, st>>>(c, c.mortar_iface, r, rm, rc);
+  if (n > 0)
+    k_restrict_final<<<(unsigned)(((int64_t)n * RF_LPC + 255) / 256), 256, 0, st>>>(
+        c, c.mortar_iface, r, rm, rc);
 }
 
 // ---------------------------------------------------------------------------

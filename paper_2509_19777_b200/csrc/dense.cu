@@ -537,26 +537,49 @@ __global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
 }
 
 // y_K = sum_{J<=K} part_row(K,J) + sum_{I>K} part_col(I,K), fixed order
-__global__ void k_symv_reduce(int64_t nrows, const int32_t* __restrict__ row_s,
-                              const int32_t* __restrict__ row_k, const int32_t* __restrict__ nb,
-                              const int64_t* __restrict__ tile_base,
-                              const int64_t* __restrict__ row_base,
-                              const double* __restrict__ part_row,
-                              const double* __restrict__ part_col, double* __restrict__ yloc) {
-  int64_t rbi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (rbi >= nrows) return;
-  int s = row_s[rbi], K = row_k[rbi], n = nb[s];
-  double2 acc = make_double2(0.0, 0.0);
-  for (int J = 0; J <= K; ++J) {
-    double2 v = reinterpret_cast<const double2*>(part_row + tidx(tile_base, s, K, J) * TB)[lane];
-    acc.x += v.x; acc.y += v.y;
+// y_K = sum_{J<=K} part_row(K,J) + sum_{I>K} part_col(I,K): one CTA of SR_WARPS
+// warps per row block; warp w sums the partials of index = w (mod SR_WARPS) in
+// ascending order (four loads in flight), then warp 0 adds the warp sums in
+// order w = 0..SR_WARPS-1 (fixed order, no atomics)
+constexpr int SR_WARPS = 8;
+__global__ void __launch_bounds__(32 * SR_WARPS)
+    k_symv_reduce(int64_t nrows, const int32_t* __restrict__ row_s,
+                  const int32_t* __restrict__ row_k, const int32_t* __restrict__ nb,
+                  const int64_t* __restrict__ tile_base, const int64_t* __restrict__ row_base,
+                  const double* __restrict__ part_row, const double* __restrict__ part_col,
+                  double* __restrict__ yloc) {
+  __shared__ double2 red[SR_WARPS][32];
+  const int64_t rbi = blockIdx.x;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = row_s[rbi], K = row_k[rbi], n = nb[s];
+  // index t < n: t <= K -> part_row(K, t), t > K -> part_col(t, K)
+  auto part = [&](int t) {
+    const double* p = t <= K ? part_row + tidx(tile_base, s, K, t) * TB
+                             : part_col + tidx(tile_base, s, t, K) * TB;
+    return __ldcs(reinterpret_cast<const double2*>(p) + lane);
+  };
+  double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+  int t = w;
+  for (; t + SR_WARPS < n; t += 2 * SR_WARPS) {
+    const double2 u = part(t), v = part(t + SR_WARPS);
+    a0.x += u.x; a0.y += u.y;
+    a1.x += v.x; a1.y += v.y;
   }
-  for (int I = K + 1; I < n; ++I) {
-    double2 v = reinterpret_cast<const double2*>(part_col + tidx(tile_base, s, I, K) * TB)[lane];
-    acc.x += v.x; acc.y += v.y;
+  if (t < n) {
+    const double2 u = part(t);
+    a0.x += u.x; a0.y += u.y;
   }
-  reinterpret_cast<double2*>(yloc + (row_base[s] + K) * TB)[lane] = acc;
+  red[w][lane] = make_double2(a0.x + a1.x, a0.y + a1.y);
+  __syncthreads();
+  if (w == 0) {
+    double2 acc = red[0][lane];
+#pragma unroll
+    for (int q = 1; q < SR_WARPS; ++q) {
+      acc.x += red[q][lane].x;
+      acc.y += red[q][lane].y;
+    }
+    reinterpret_cast<double2*>(yloc + (row_base[s] + K) * TB)[lane] = acc;
+  }
 }
 
 __global__ void k_gather(int64_t n, const int32_t* __restrict__ lmap, const double* __restrict__ x,
@@ -600,8 +623,7 @@ void launch_symv_tiles(const DevBatch& b, cudaStream_t st) {
 
 void launch_symv_reduce(const DevBatch& b, cudaStream_t st) {
   if (b.nrows <= 0) return;
-  int64_t th2 = 32 * b.nrows;
-  k_symv_reduce<<<(unsigned)((th2 + 255) / 256), 256, 0, st>>>(b.nrows, b.row_s, b.row_k, b.nb,
+  k_symv_reduce<<<(unsigned)b.nrows, 32 * SR_WARPS, 0, st>>>(b.nrows, b.row_s, b.row_k, b.nb,
                                                                b.tile_base, b.row_base,
                                                                b.part_row, b.part_col, b.yloc);
 }
