@@ -107,7 +107,11 @@ __device__ __forceinline__ void sn_rows(const double* __restrict__ st, int ld, i
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int i = 2 * (L.t + q * L.TG);
-        a[u][q] = i < h ? *reinterpret_cast<const double2*>(cu + i) : make_double2(0.0, 0.0);
+        // NRHS == 1: rows >= h are read unconditionally (whatever follows in
+        // shared memory; sn_tail_doubles keeps a guard after the ring) into
+        // accumulator rows that are never used -- no predicate, no zeroing
+        if (NRHS == 1) a[u][q] = *reinterpret_cast<const double2*>(cu + i);
+        else a[u][q] = i < h ? *reinterpret_cast<const double2*>(cu + i) : make_double2(0.0, 0.0);
       }
     }
 #pragma unroll
@@ -133,7 +137,7 @@ __device__ __forceinline__ void sn_rows(const double* __restrict__ st, int ld, i
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int i = 2 * (L.t + q * L.TG);
-      if (i < h) {
+      if (NRHS == 1 || i < h) {
         const double2 a = *reinterpret_cast<const double2*>(ca + i);
 #pragma unroll
         for (int c = 0; c < NRHS; ++c) {
@@ -486,8 +490,12 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
 }
 #undef PSYNC
 // shared memory: ring (stages x chunk) | x (max_n even, NRHS) | x_R / scratch
+// x_S (max_n) and x_R (max_r) after the ring; at least SN_GUARD doubles, the
+// largest row overrun of an unpredicated sn_rows read (2 TG - 1, TG <= 256)
+constexpr int SN_GUARD = 512;
 static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int nt) {
-  return (size_t)(((max_n + 1) & ~1) + ((max_r + 3) & ~1)) * nrhs;
+  const size_t t = (size_t)(((max_n + 1) & ~1) + ((max_r + 3) & ~1)) * nrhs;
+  return t < SN_GUARD ? SN_GUARD : t;
 }
 
 // Launch shape of the solve: 16 consumer warps x 1 CTA per SM, or 8 x 2 (two
