@@ -287,12 +287,14 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = []
     with Clocks(local) as clk:
+        torch.cuda.profiler.start()   # ncu --profile-from-start off: the timed steps only
         e0.record(stream)
         for _ in range(args.steps):
             _, rep, hist = sv.solve(b, tol=prob.tol, x=x)
             reps.append(rep)
         e1.record(stream)
         torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     if dist:
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps

@@ -75,17 +75,8 @@ __global__ void k_final_sum(int nb, int m, const double* __restrict__ partial,
   int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (j >= m) return;
-  // four interleaved partial sums (fixed order) keep four loads in flight
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int b = lane;
-  for (; b + 96 < nb; b += 128) {
-    s0 += partial[(int64_t)b * m + j];
-    s1 += partial[(int64_t)(b + 32) * m + j];
-    s2 += partial[(int64_t)(b + 64) * m + j];
-    s3 += partial[(int64_t)(b + 96) * m + j];
-  }
-  for (; b < nb; b += 32) s0 += partial[(int64_t)b * m + j];
-  double s = (s0 + s1) + (s2 + s3);
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += partial[(int64_t)b * m + j];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) out[j] = s;
