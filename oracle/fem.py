@@ -199,6 +199,49 @@ class System:
         return int(self.col_idx.size)
 
 
+def assemble_rows(mesh: Mesh, nodes):
+    """Block rows of the constrained A^ and entries of b^ for selected nodes,
+    one node at a time straight from the element sum (eq:stiff_iso; R3, R4):
+    row p = sum over the solid voxels v touching p (p = local node a of v) of
+    E_v K0[a, b] scattered to the node of local index b; Dirichlet columns
+    dropped (their u_D moved to the right-hand side); a Dirichlet row is the
+    identity with b_p = u_D(p).  A second route to the same rows as System
+    (for sampled checks where the full assembly is too large).
+
+    Returns [(cols ascending int64, blocks (len, 3, 3), b_p (3,))]."""
+    K0 = element_K0(mesh.prob.nu)
+    prob = mesh.prob
+    out = []
+    for p in np.asarray(nodes, dtype=np.int64):
+        if mesh.dirichlet[p]:
+            out.append((np.array([p]), np.eye(3)[None], mesh.u_D[p].copy()))
+            continue
+        i, j, k = (int(t) for t in mesh.node_ijk[p])
+        acc = {}
+        for a in range(8):
+            dx, dy, dz = _corner(a)
+            vi, vj, vk = i - dx, j - dy, k - dz
+            if not (0 <= vi < prob.nx and 0 <= vj < prob.ny and 0 <= vk < prob.nz):
+                continue
+            if not prob.solid[vk, vj, vi]:
+                continue
+            E = float(prob.E[vk, vj, vi])
+            for b in range(8):
+                cx, cy, cz = _corner(b)
+                q = int(mesh.lat_id[vk + cz, vj + cy, vi + cx])
+                blk = E * K0[3 * a:3 * a + 3, 3 * b:3 * b + 3]
+                acc[q] = acc[q] + blk if q in acc else blk.copy()
+        bp = mesh.f[p].copy()
+        cols = []
+        for q in sorted(acc):
+            if mesh.dirichlet[q]:
+                bp -= acc[q] @ mesh.u_D[q]
+            else:
+                cols.append(q)
+        out.append((np.array(cols, dtype=np.int64), np.array([acc[q] for q in cols]), bp))
+    return out
+
+
 def build_system(prob) -> System:
     return System(Mesh(prob))
 

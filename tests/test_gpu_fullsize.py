@@ -179,3 +179,4 @@ def test_cfg3_ilu(cfg3):
     sv = Solver(p, smoother="ilu0", n_st=6).assemble(0).setup()
     sample = np.random.default_rng(9).choice(s.row_ptr.size - 1, 4000, replace=False)
     _ilu_full_checks(p, s, sv, np.sort(sample))
+

@@ -94,3 +94,22 @@ def test_cfg1_load_equilibrium():
     reac = (s.full @ x).reshape(-1, 3)[s.mesh.dirichlet]
     assert abs(reac[:, 2].sum() - 256.0) <= 1e-10 * 256.0
     assert np.abs(reac[:, :2].sum(0)).max() <= 1e-9
+
+
+@pytest.mark.parametrize("case", ["porous20", "cfg1"])
+def test_assemble_rows_matches_system(case):
+    """The per-node row assembly (used for sampled checks at cfg4/cfg5 sizes)
+    reproduces the full constrained assembly, pattern exactly and values to
+    roundoff (different summation order)."""
+    from oracle.fem import assemble_rows, build_system
+    from workloads import make_problem
+    s = build_system(make_problem(case))
+    nodes = np.arange(s.mesh.n_nodes)
+    if nodes.size > 2000:
+        nodes = np.sort(np.random.default_rng(3).choice(nodes, 2000, replace=False))
+    scale = np.abs(s.val).max()
+    for p, (cols, blocks, bp) in zip(nodes, assemble_rows(s.mesh, nodes)):
+        lo, hi = s.row_ptr[p], s.row_ptr[p + 1]
+        assert np.array_equal(cols, s.col_idx[lo:hi])
+        assert np.abs(blocks - s.val[lo:hi]).max() <= 1e-14 * scale
+        assert np.abs(bp - s.b[3 * p:3 * p + 3]).max() <= 1e-13 * max(1.0, np.abs(s.b).max())
