@@ -897,8 +897,9 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
       };
       double t0 = wall();
-      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, kSnLeaf, h->sg.sym, err) ||
-          (!ilu && !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, kSnLeaf, h->sc.sym, err)))
+      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, kSnLeaf, h->sg.sym, err, h->nsm) ||
+          (!ilu &&
+           !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, kSnLeaf, h->sc.sym, err, h->nsm)))
         throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
       double t1 = wall();
       try {

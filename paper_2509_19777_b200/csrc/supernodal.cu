@@ -524,6 +524,20 @@ int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk)
 
 static int cfg_cps(int cons) { return cons == 16 ? 1 : 2; }
 
+// Chunk size of a batch's solve stream: 32 KiB when the batch runs 8 warps x 2
+// CTAs per SM; a batch that needs 16 x 1 (few subdomains, or x_S too large for
+// two CTAs) streams 64 KiB (else 48 KiB) chunks -- half the per-chunk
+// overhead for its 16 consumer warps (cfg5 grain / contact solves -13% / -8%).
+// HPLMM_SN_CHUNK overrides.
+int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r) {
+  if (getenv("HPLMM_SN_CHUNK")) return sn_chunk_doubles();
+  const int base = sn_chunk_doubles();
+  if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base) == 8) return base;
+  for (int c : {SN_CHUNK_DOUBLES_MAX, 6144})
+    if (c > base && sn_solve_stages(max_n, max_r, 1, c, 16) >= 2) return c;
+  return base;
+}
+
 int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons) {
   const int p = cfg_cps(cons);
   const long avail =

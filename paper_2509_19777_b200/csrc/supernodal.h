@@ -92,7 +92,11 @@ struct SnSymbolic {
 // Symbolic analysis of the subdomains given as ascending node lists
 // (CSR ptr/nodes).  leaf = max nodes of an ND leaf.  Returns false + err on
 // a supernode wider than SN_MAX_WR.
+// nsm: SMs of the device (the chunk size of the solve stream depends on the
+// launch shape, sn_pick_chunk)
 bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
-                const std::vector<int32_t>& nodes, int leaf, SnSymbolic& out, std::string& err);
+                const std::vector<int32_t>& nodes, int leaf, SnSymbolic& out, std::string& err,
+                int nsm = 148);
+int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r);
 
 }  // namespace hplmm

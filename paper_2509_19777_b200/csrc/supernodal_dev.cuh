@@ -83,6 +83,7 @@ struct GemmProb {
 // vectors do not fit in shared memory with >= 2 ring stages
 int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk);
 int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons);
+int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r);
 void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
                      int max_r, int chunk, int cons, cudaStream_t st);
 void launch_front_asm(const int32_t* list, int nlist, const SnNum& nm, const double* val,
