@@ -32,23 +32,42 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // vectors per pass share one read of w; per vector the summation order is
 // fixed (per-thread strided fma, warp butterfly, warps in order).
 constexpr int MD_J = 8;
+// block ranges: even-sized (element pairs), so that every block's first
+// element is 16-byte aligned (ldv is a multiple of 32)
+__device__ __forceinline__ void pair_range(int64_t n, int64_t& i0, int64_t& i1) {
+  const int64_t chunk = (((n + gridDim.x - 1) / gridDim.x) + 1) & ~(int64_t)1;
+  i0 = min(n, blockIdx.x * chunk);
+  i1 = min(n, i0 + chunk);
+}
+
 __global__ void __launch_bounds__(KT) k_multidot(int64_t n, int m, const double* __restrict__ V,
                                                  int64_t ldv, const double* __restrict__ w,
                                                  double* __restrict__ partial) {
   __shared__ double red[MD_J][KT / 32];
   const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-  int64_t i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  int64_t i0, i1;
+  pair_range(n, i0, i1);
+  const int64_t p1 = i0 + ((i1 - i0) & ~(int64_t)1);   // end of the paired part
   for (int j0 = 0; j0 < m; j0 += MD_J) {
     const int nj = min(MD_J, m - j0);
     double s[MD_J];
 #pragma unroll
     for (int jj = 0; jj < MD_J; ++jj) s[jj] = 0.0;
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) {
-      const double wi = w[i];
+    // two elements per thread per step (128-bit loads)
+    for (int64_t i = i0 + 2 * threadIdx.x; i < p1; i += 2 * KT) {
+      const double2 wi = *reinterpret_cast<const double2*>(w + i);
 #pragma unroll
       for (int jj = 0; jj < MD_J; ++jj)
-        if (jj < nj) s[jj] = fma(V[(j0 + jj) * ldv + i], wi, s[jj]);
+        if (jj < nj) {
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(V + (j0 + jj) * ldv + i));
+          s[jj] = fma(v.y, wi.y, fma(v.x, wi.x, s[jj]));
+        }
+    }
+    if (p1 < i1 && threadIdx.x == 0) {
+      const double wi = w[p1];
+#pragma unroll
+      for (int jj = 0; jj < MD_J; ++jj)
+        if (jj < nj) s[jj] = fma(V[(j0 + jj) * ldv + p1], wi, s[jj]);
     }
 #pragma unroll
     for (int jj = 0; jj < MD_J; ++jj) {
@@ -89,7 +108,8 @@ void launch_multidot(int64_t n, int m, const double* V, int64_t ldv, const doubl
   k_final_sum<<<(m + 3) / 4, 128, 0, st>>>(nb, m, partial, out);
 }
 
-// w -= sum_j V[j] h[j]   (+ partial ||w||^2 per block)
+// w -= sum_j V[j] h[j]   (+ partial ||w||^2 per block); per element the
+// j-order of the update is fixed; two elements per thread (128-bit loads)
 __global__ void __launch_bounds__(KT) k_update(int64_t n, int m, const double* __restrict__ V,
                                                int64_t ldv, const double* __restrict__ h,
                                                double* __restrict__ w, double* __restrict__ partial) {
@@ -97,13 +117,40 @@ __global__ void __launch_bounds__(KT) k_update(int64_t n, int m, const double* _
   __shared__ double red[KT / 32];
   for (int j = threadIdx.x; j < m; j += KT) hs[j] = h[j];
   __syncthreads();
-  int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-  int64_t i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  int64_t i0, i1;
+  pair_range(n, i0, i1);
+  const int64_t p1 = i0 + ((i1 - i0) & ~(int64_t)1);
   double s = 0.0;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) {
-    double acc = w[i];
-    for (int j = 0; j < m; ++j) acc = fma(-V[j * ldv + i], hs[j], acc);
-    w[i] = acc;
+  for (int64_t i = i0 + 2 * threadIdx.x; i < p1; i += 2 * KT) {
+    double2 acc = *reinterpret_cast<const double2*>(w + i);
+    int j = 0;
+    for (; j + 3 < m; j += 4) {
+      const double2 v0 = __ldcs(reinterpret_cast<const double2*>(V + j * ldv + i));
+      const double2 v1 = __ldcs(reinterpret_cast<const double2*>(V + (j + 1) * ldv + i));
+      const double2 v2 = __ldcs(reinterpret_cast<const double2*>(V + (j + 2) * ldv + i));
+      const double2 v3 = __ldcs(reinterpret_cast<const double2*>(V + (j + 3) * ldv + i));
+      acc.x = fma(-v0.x, hs[j], acc.x);
+      acc.y = fma(-v0.y, hs[j], acc.y);
+      acc.x = fma(-v1.x, hs[j + 1], acc.x);
+      acc.y = fma(-v1.y, hs[j + 1], acc.y);
+      acc.x = fma(-v2.x, hs[j + 2], acc.x);
+      acc.y = fma(-v2.y, hs[j + 2], acc.y);
+      acc.x = fma(-v3.x, hs[j + 3], acc.x);
+      acc.y = fma(-v3.y, hs[j + 3], acc.y);
+    }
+    for (; j < m; ++j) {
+      const double2 v = __ldcs(reinterpret_cast<const double2*>(V + j * ldv + i));
+      acc.x = fma(-v.x, hs[j], acc.x);
+      acc.y = fma(-v.y, hs[j], acc.y);
+    }
+    *reinterpret_cast<double2*>(w + i) = acc;
+    s = fma(acc.x, acc.x, s);
+    s = fma(acc.y, acc.y, s);
+  }
+  if (p1 < i1 && threadIdx.x == 0) {
+    double acc = w[p1];
+    for (int j = 0; j < m; ++j) acc = fma(-V[j * ldv + p1], hs[j], acc);
+    w[p1] = acc;
     s = fma(acc, acc, s);
   }
   if (partial) {
