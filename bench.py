@@ -271,7 +271,10 @@ def main():
     stream = torch.cuda.current_stream()
     prob = make_problem(args.config)
     lf = os.environ.get("HPLMM_LOCAL_FACTOR")
-    sv = Solver(prob, local_factor=int(lf) if lf else None).assemble(local).setup()
+    smoother = os.environ.get("HPLMM_SMOOTHER", "cg")       # cg (default) | ilu0 (NEXT #4)
+    n_st = int(os.environ.get("HPLMM_NST", "6" if smoother == "ilu0" else "1"))
+    sv = Solver(prob, local_factor=int(lf) if lf else None, smoother=smoother,
+                n_st=n_st).assemble(local).setup()
     rep0 = sv.report()
     b_host = sv.export("RHS")
     b = torch.from_numpy(b_host).cuda()
@@ -302,7 +305,7 @@ def main():
     sparse = int(sv.options.local_factor) == 1
     # kernel classes: 0/1/2 packed SYMV (grain/contact/coarse inverse tiles),
     # 3/4 supernodal solve (grain/contact factors)
-    stats = [sv.kernel_stats(k) for k in range(5)]
+    stats = [sv.kernel_stats(k) for k in range(6)]
     p = prob
     iters = reps[-1]["iterations"]
 
@@ -331,7 +334,18 @@ def main():
     sizes[0] = [int(v) for v in 3 * gsz]
     sizes[2] = [rep0["n_mortar_dofs"]]
     alg = {k: symv_algorithmic_bytes(sizes[k]) for k in sizes}
-    if sparse:
+    ilu = smoother == "ilu0"
+    if ilu:
+        # ILU(0) apply: every stored 3x3 block once (L forward, U and A~_II^-1
+        # backward) + r read, y written and read, x written, sentinel fill
+        alg[5] = stats[5][2] + 24 * 5 * rep0["n_nodes"]
+        alg[3] = stats[3][2] + 16 * sum(sizes[0])
+        alg[4] = 0
+        dom = 5
+        dom_name = ("k_ilu_fwd + k_ilu_bwd (ILU(0) apply, level-ordered sync-free sweeps; "
+                    "bound by the dependency chain, not by HBM)")
+        local_classes = (5, 4)
+    elif sparse:
         # block-LDL^T solve: W_S read twice, F_SS^-1 once, row lists twice
         # (library-reported stream bytes), plus x gathered and y written (16 B/DOF)
         alg[3] = stats[3][2] + 16 * sum(sizes[0])
@@ -357,13 +371,17 @@ def main():
     n = 3 * rep0["n_nodes"]
     spmv_bytes = 76 * nnzb + 4 * rep0["n_nodes"] + 24 * n
     pb = 12 * rep0["prolong_nnz"]
-    local_bytes = alg[local_classes[0]] + alg[local_classes[1]]
-    per_iter_bytes = (local_bytes + alg[2] + 3 * spmv_bytes + 2 * pb + (4 * 11 + 6) * 8 * n)
+    if ilu:   # n_st ILU applies + their n_st - 1 stage residuals; y and w SpMVs
+        per_iter_bytes = (n_st * alg[5] + alg[2] + (2 + n_st - 1) * spmv_bytes + 2 * pb
+                          + (4 * 11 + 6) * 8 * n)
+    else:
+        local_bytes = alg[local_classes[0]] + alg[local_classes[1]]
+        per_iter_bytes = (local_bytes + alg[2] + 3 * spmv_bytes + 2 * pb + (4 * 11 + 6) * 8 * n)
     per_iter_frac = (per_iter_bytes / (t_s / max(iters, 1)) / 1e9) / peak
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_{'sn' if sparse else 'symv'}_{args.config}.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and not ilu:
         try:
             traffic = json.load(open(tp))["dram_bytes_per_launch"]["contact" if dom == 4 else "grain"]
         except Exception:
@@ -380,6 +398,7 @@ def main():
                    "contact_h": p.contact_h, "restart": p.restart, "tol": p.tol,
                    "parallelism": f"replicas{world}",
                    "local_factor": "supernodal" if sparse else "dense-inverse",
+                   "smoother": smoother, "n_st": n_st,
                    "l2": "no flush: working set (local factors) >> 126 MB L2"},
         "iterations": iters, "iterations_per_s": iters_per_s * world,
         "solves_per_s_aggregate": world / t_s,

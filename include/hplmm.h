@@ -253,8 +253,9 @@ hplmm_status hplmm_profile(hplmm_handle *h, int32_t enable, int32_t reset);
 
 /* Statistics of kernel class `kernel` (0 = grain SYMV tiles, 1 = contact-grid
  * SYMV tiles, 2 = coarse SYMV tiles, 3 = grain supernodal solve, 4 =
- * contact-grid supernodal solve): total device ms and launch count since the
- * last reset; tile_bytes = factor bytes one launch streams. */
+ * contact-grid supernodal solve, 5 = ILU(0) apply = forward + backward sweep):
+ * total device ms and launch count since the last reset; tile_bytes = factor
+ * bytes one launch streams. */
 hplmm_status hplmm_kernel_stats(hplmm_handle *h, int32_t kernel, double *total_ms,
                                 int64_t *launches, int64_t *tile_bytes);
 

@@ -42,7 +42,7 @@ struct HError {
 
 enum KernelClass {
   KC_SYMV_GRAIN = 0, KC_SYMV_CONTACT = 1, KC_SYMV_COARSE = 2, KC_SN_GRAIN = 3, KC_SN_CONTACT = 4,
-  KC_N = 5
+  KC_ILU = 5, KC_N = 6
 };
 
 }  // namespace
@@ -90,8 +90,8 @@ struct hplmm_handle {
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
-  double kc_ms[KC_N] = {0, 0, 0, 0, 0};
-  int64_t kc_launches[KC_N] = {0, 0, 0, 0, 0};
+  double kc_ms[KC_N] = {0, 0, 0, 0, 0, 0};
+  int64_t kc_launches[KC_N] = {0, 0, 0, 0, 0, 0};
 
   // coarse Cholesky (coarse_solver == 1)
   double *d_linv = nullptr, *d_linvT = nullptr, *d_zc = nullptr;
@@ -495,7 +495,17 @@ void op_mcg(hplmm_handle* h, const double* in, double* out) {
 
 // M_ILU^-1 (R27): out = U^-1 L^-1 in
 void op_milu(hplmm_handle* h, const double* in, double* out) {
-  launch_ilu_solve(h->ilu, in, out, h->st);
+  if (h->profile) {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, h->st));
+    launch_ilu_solve(h->ilu, in, out, h->st);
+    CK(cudaEventRecord(e1, h->st));
+    h->ev_pending.push_back({KC_ILU, {e0, e1}});
+  } else {
+    launch_ilu_solve(h->ilu, in, out, h->st);
+  }
   h->launches += 2;
 }
 
@@ -1450,6 +1460,10 @@ hplmm_status hplmm_kernel_stats(hplmm_handle* h, int32_t kernel, double* total_m
   if (!h || kernel < 0 || kernel >= KC_N) { g_last_error = "bad argument"; return HPLMM_ERR_ARG; }
   if (total_ms) *total_ms = h->kc_ms[kernel];
   if (launches) *launches = h->kc_launches[kernel];
+  if (kernel == KC_ILU) {   // every stored block once per apply (L in fwd, U + D in bwd)
+    if (tile_bytes) *tile_bytes = h->ilu.val ? h->nnzb * 72 : 0;
+    return HPLMM_OK;
+  }
   if (kernel >= KC_SN_GRAIN) {
     if (tile_bytes) *tile_bytes = kernel == KC_SN_GRAIN ? h->sg.solve_bytes : h->sc.solve_bytes;
     return HPLMM_OK;
