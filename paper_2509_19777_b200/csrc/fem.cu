@@ -396,21 +396,12 @@ void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms_spmv, cudaDevAttrMultiProcessorCount, dev);
   }
-  if (g_spmv_mode >= 1 && max_row_blocks <= SP_MAXB) {
-    switch (g_spmv_mode) {
-      case 2: spmv_tma<8, 6, 12>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-      case 3: spmv_tma<16, 3, 6>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-      case 4: spmv_tma<8, 4, 12>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-      case 5: spmv_tma<4, 12, 24>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-      case 6: spmv_tma<8, 3, 6, 2>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-      case 7: spmv_tma<4, 4, 12, 2>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-      case 8: spmv_tma<12, 4, 8>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-      case 1: spmv_tma<4, 8, 24>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-      case 9: spmv_tma<8, 2, 4, 3>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-      // default (measured best on B200, profiles/r01_spmv_variants.txt): 8-row chunks,
-      // 3 consumer warps x 2 stages, 2 CTAs per SM
-      default: spmv_tma<8, 3, 6, 2>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv); return;
-    }
+  // TMA-streamed kernel (measured best of the ROWS / CONS / STAGES variants on
+  // B200, profiles/r01_spmv_variants.txt: 8-row chunks, 3 consumer warps x 2
+  // stages, 2 CTAs per SM); HPLMM_SPMV=0 selects the plain warp-per-row kernel
+  if (g_spmv_mode != 0 && max_row_blocks <= SP_MAXB) {
+    spmv_tma<8, 3, 6, 2>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv);
+    return;
   }
   int grid = (n_nodes + SPMV_WARPS - 1) / SPMV_WARPS;
   if (v)
