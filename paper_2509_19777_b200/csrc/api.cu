@@ -25,6 +25,10 @@ namespace {
 thread_local std::string g_last_error;
 
 constexpr int kSnLeaf = 40;                          // ND leaf size (nodes)
+static int sn_leaf() {   // HPLMM_SN_LEAF overrides (ordering experiments)
+  static const int v = getenv("HPLMM_SN_LEAF") ? std::max(4, atoi(getenv("HPLMM_SN_LEAF"))) : kSnLeaf;
+  return v;
+}
 constexpr int64_t kSnPoolBytes = (int64_t)4 << 30;   // frontal matrices per wave
 
 struct HError {
@@ -907,9 +911,9 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
       };
       double t0 = wall();
-      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, kSnLeaf, h->sg.sym, err, h->nsm) ||
+      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, sn_leaf(), h->sg.sym, err, h->nsm) ||
           (!ilu &&
-           !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, kSnLeaf, h->sc.sym, err, h->nsm)))
+           !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, sn_leaf(), h->sc.sym, err, h->nsm)))
         throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
       double t1 = wall();
       try {
@@ -975,6 +979,17 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     // ---------------- T_MG: mortars, P_B, S, S^-1 -------------------------
     Nvtx nv_mg("hplmm_setup:T_MG");
     Timer tc(h->st);
+    static const bool dbg_mg = getenv("HPLMM_DEBUG") != nullptr;
+    double tmg = 0;
+    auto mg_mark = [&](const char* what) {   // phase wall times under HPLMM_DEBUG
+      if (!dbg_mg) return;
+      CK(cudaStreamSynchronize(h->st));
+      const double now =
+          std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+      if (tmg > 0) fprintf(stderr, "hplmm T_MG: %-22s %.3f s\n", what, now - tmg);
+      tmg = now;
+    };
+    mg_mark("start");
     {
       std::vector<int32_t> iface_of(hs.iface_nodes.size());
       for (int c = 0; c < C; ++c)
@@ -1037,6 +1052,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         CK(cudaGetLastError());
       }
     }
+    mg_mark("mortars");
     launch_build_R(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
     {
       std::vector<int32_t> kc(G);
@@ -1053,8 +1069,10 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         launch_symm_neg(h->gb, co.b_off, co.ld, h->upload(kc), (maxk + TB - 1) / TB, co.R, co.B,
                         h->st);
     }
+    mg_mark("shape vectors");
     launch_grain_AB(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
     launch_grain_BtY(co, h->gb, h->st);
+    mg_mark("grain A B, B^T Y");
     int64_t npS = (int64_t)TB * h->sb.max_nb;
     // small S: dense copy kept for export (HPLMM_ART_S); large S (cfg5: 67 GB
     // dense) is assembled straight into the packed lower tiles
@@ -1074,6 +1092,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       launch_S_grain(co, h->sb.tiles, 0, h->st);
     }
     launch_pad_identity(h->sb, h->st);
+    mg_mark("S assembly");
     if (hs.opt.coarse_refine) {
       h->sS = h->sb;
       h->sS.tiles = h->dalloc<double>((size_t)h->sb.ntiles * TILE);
@@ -1098,6 +1117,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     }
     CK(cudaGetLastError());
     check_batch_err(h, h->sb, 0, true);
+    mg_mark("coarse inversion");
     h->rep.t_setup_coarse_s = tc.stop();
     CK(cudaStreamSynchronize(h->st));
     h->free_setup();
