@@ -327,3 +327,26 @@ def test_algebraic_mortars(case, lf):
     x, rep, _ = sv.solve(s.b.copy(), tol=1e-8)
     assert convo and rep["converged"] == 1 and abs(rep["iterations"] - ito) <= 1, (rep["iterations"], ito)
     assert rel(x, xo) <= 1e-8
+
+
+@pytest.mark.parametrize("shape", [(6, 6, 6), (5, 1, 1), (1, 4, 4)])
+@pytest.mark.parametrize("smoother", ["cg", "ilu0"])
+def test_degenerate_single_grain(shape, smoother):
+    """Degenerate decompositions: one grain (no interfaces, no mortars, N_m = 0;
+    M_G is then the correction column alone, so M_G^-1 b = A^-1 b exactly and
+    GMRES takes one iteration), a 1 x 1 x n voxel column and a one-voxel slab."""
+    from oracle import gmres, hplmm
+    from paper_2509_19777_b200 import Solver
+    from tests.test_oracle_ilu import _box_problem
+    import __graft_entry__
+    __graft_entry__.build()
+    p = _box_problem(*shape)
+    s, h = hplmm.setup(p, smoother=smoother, n_st=6 if smoother == "ilu0" else 1)
+    assert h.Nm == 0
+    h.set_rhs(s.b)
+    xo, ito, _, _, _ = gmres.gmres(s.A, s.b, h.apply_M, tol=1e-8)
+    sv = Solver(p, smoother=smoother, n_st=6 if smoother == "ilu0" else 1).assemble(0).setup()
+    x, rep, _ = sv.solve(s.b.copy(), tol=1e-8)
+    assert rep["converged"] == 1 and rep["iterations"] == ito == 1
+    assert rel(x, xo) <= 1e-12
+    assert rel(x, np.linalg.solve(s.A.toarray(), s.b)) <= 1e-10
