@@ -53,6 +53,16 @@ void lpt(const std::vector<int64_t>& wgt, int nb, std::vector<int32_t>& ptr,
 
 }  // namespace
 
+// LPT cost of a subdomain: bytes streamed + gather/scatter + a fixed cost per
+// chunk in byte equivalents (the solve's per-chunk overhead).  Measured at
+// cfg3 (contact / grain solve): 0 -> 1.975 / 1.346 ms, 16 KiB -> 1.938 / 1.327,
+// 32 KiB -> 1.925 / 1.313, >= 64 KiB -> 1.918 / 1.305 (plateau).  HPLMM_SN_WGT
+// overrides.
+static int64_t sn_chunk_cost() {
+  static const int64_t v = getenv("HPLMM_SN_WGT") ? atoll(getenv("HPLMM_SN_WGT")) : 65536;
+  return v;
+}
+
 void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nrhs,
                    const std::vector<int32_t>* ncols, SnWork& wk, int force_cons) {
   const SnSymbolic& s = B.sym;
@@ -64,7 +74,8 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
     for (int c0 = 0; c0 < nc; c0 += nrhs) {
       isub.push_back(g);
       ic0.push_back(c0);
-      wgt.push_back(s.sub_fbytes[g] + 8 * (int64_t)s.sub_n[g] * 64);
+      wgt.push_back(s.sub_fbytes[g] + 8 * (int64_t)s.sub_n[g] * 64 +
+                    sn_chunk_cost() * ((s.sub_fc1[g] - s.sub_fc0[g]) + (s.sub_bc1[g] - s.sub_bc0[g])));
     }
   }
   wk.cons = force_cons ? force_cons
