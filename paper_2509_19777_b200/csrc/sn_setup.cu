@@ -3,6 +3,8 @@
 // factorisation (setup, T_ML) -- see supernodal.h.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <queue>
@@ -88,6 +90,18 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   nblocks = std::max(1, std::min<int>(nblocks, (int)isub.size()));
   std::vector<int32_t> ptr, ids;
   lpt(wgt, nblocks, ptr, ids);
+  if (getenv("HPLMM_DEBUG")) {   // balance of the static assignment
+    double tot = 0, mx = 0, big = 0;
+    for (int b = 0; b < nblocks; ++b) {
+      double w = 0;
+      for (int e = ptr[b]; e < ptr[b + 1]; ++e) w += (double)wgt[ids[e]];
+      tot += w;
+      mx = std::max(mx, w);
+    }
+    for (int64_t w : wgt) big = std::max(big, (double)w);
+    fprintf(stderr, "hplmm sn work: %zu items on %d CTAs, max/mean CTA weight %.3f, largest item %.3f of the mean\n",
+            wgt.size(), nblocks, mx / (tot / nblocks), big / (tot / nblocks));
+  }
   std::vector<int32_t> sub(ids.size()), c0(ids.size());
   std::vector<int64_t> cptr(nblocks + 1, 0);
   std::vector<SnChunk> flat;
