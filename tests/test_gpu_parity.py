@@ -350,3 +350,27 @@ def test_degenerate_single_grain(shape, smoother):
     assert rep["converged"] == 1 and rep["iterations"] == ito == 1
     assert rel(x, xo) <= 1e-12
     assert rel(x, np.linalg.solve(s.A.toarray(), s.b)) <= 1e-10
+
+
+@pytest.mark.parametrize("restart,max_iter", [(8, 300), (5, 12)])
+def test_restart_and_iteration_cap(restart, max_iter):
+    """GMRES(m) restarts (R22: x += M^-1 V y and the true residual at every
+    cycle end) and the iteration cap (NOT_CONVERGED keeps the last iterate and
+    the full history), against the oracle's GMRES with the same m / cap."""
+    from oracle import gmres
+    from paper_2509_19777_b200 import Solver
+    p, s, h, _ = gpu_case("cfg1")
+    h.set_rhs(s.b)
+    xo, ito, histo, rro, convo = gmres.gmres(s.A, s.b, h.apply_M, tol=1e-8, restart=restart,
+                                             maxit=max_iter)
+    sv = Solver(p, restart=restart, max_iter=max_iter).assemble(0).setup()
+    x, rep, hist = sv.solve(s.b.copy(), tol=1e-8)
+    assert rep["converged"] == int(convo)
+    if convo:
+        assert abs(rep["iterations"] - ito) <= 1
+        assert rel(x, xo) <= 1e-8
+    else:
+        assert rep["iterations"] == ito == max_iter and len(hist) == max_iter
+        assert rel(x, xo) <= 1e-10
+        assert abs(rep["final_true_relres"] - rro) <= 1e-8 * max(rro, 1.0)
+        assert np.allclose(hist, histo, rtol=1e-8)
