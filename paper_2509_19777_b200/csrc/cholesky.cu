@@ -203,21 +203,65 @@ __device__ __forceinline__ void tile_mv(const double* __restrict__ M, double2 v,
 
 constexpr int TR_WARPS = 8;
 
+__device__ __forceinline__ void tr_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+// whole 64x64 tile -> shared memory (same col-major layout)
+__device__ __forceinline__ void tr_prefetch(double* dst, const double* src) {
+  for (int e = threadIdx.x; e < TILE / 2; e += blockDim.x) tr_cp16(dst + 2 * e, src + 2 * e);
+}
+// y(2l, 2l+1) += M v, M a col-major 64x64 tile in shared memory
+__device__ __forceinline__ void tile_mv_s(const double* M, double2 v, int lane, double& y0,
+                                          double& y1) {
+  const double2* A = reinterpret_cast<const double2*>(M) + lane;
+#pragma unroll 16
+  for (int c = 0; c < TB; ++c) {
+    const double2 a = A[c * (TB / 2)];
+    const double x = __shfl_sync(0xffffffffu, (c & 1) ? v.y : v.x, c >> 1);
+    y0 = fma(a.x, x, y0);
+    y1 = fma(a.y, x, y1);
+  }
+}
+
+// The chain of the triangular sweeps runs through the diagonal: row I waits
+// for block I-1 (forward) / I+1 (backward) last.  The two tiles that step
+// needs -- the adjacent off-diagonal tile and the inverted diagonal block --
+// do not depend on the sweep, so they are copied into shared memory (cp.async)
+// before the row starts, and the wait-to-publish path reads only shared
+// memory.  The other blocks of the row are consumed by all warps as they are
+// published (farthest first).
+
 // forward: z_I = L_II^-1 (r_I - sum_{J<I} L_IJ z_J), rows ascending
 __global__ void __launch_bounds__(32 * TR_WARPS, 1)
     k_trsv_fwd(int nb, const double* __restrict__ tiles, const double* __restrict__ linv,
                const double* __restrict__ r, double* z, int* flag, int epoch) {
+  extern __shared__ __align__(16) double trs[];   // [tile (I, I-1) | L_II^-1]
   __shared__ double red[TR_WARPS][TB];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int I = blockIdx.x; I < nb; I += gridDim.x) {
+    if (I > 0) tr_prefetch(trs, tiles + ctid(I, I - 1) * TILE);
+    tr_prefetch(trs + TILE, linv + (int64_t)I * TILE);
+    asm volatile("cp.async.commit_group;" ::: "memory");
     double y0 = 0.0, y1 = 0.0;
-    for (int J = w; J < I; J += TR_WARPS) {
+    for (int J = w; J < I - 1; J += TR_WARPS) {
       if (lane == 0)
         while (ld_acquire(flag + J) < epoch) {
         }
       __syncwarp();
       const double2 zj = __ldcg(reinterpret_cast<const double2*>(z + (int64_t)J * TB) + lane);
       tile_mv(tiles + ctid(I, J) * TILE, zj, lane, y0, y1);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (w == 0 && I > 0) {   // the chain step
+      if (lane == 0)
+        while (ld_acquire(flag + I - 1) < epoch) {
+        }
+      __syncwarp();
+      const double2 zj = __ldcg(reinterpret_cast<const double2*>(z + (int64_t)(I - 1) * TB) + lane);
+      tile_mv_s(trs, zj, lane, y0, y1);
     }
     red[w][2 * lane] = y0;
     red[w][2 * lane + 1] = y1;
@@ -230,9 +274,9 @@ __global__ void __launch_bounds__(32 * TR_WARPS, 1)
         v.y -= red[q][2 * lane + 1];
       }
       double o0 = 0.0, o1 = 0.0;
-      tile_mv(linv + (int64_t)I * TILE, v, lane, o0, o1);
+      tile_mv_s(trs + TILE, v, lane, o0, o1);
       __stcg(reinterpret_cast<double2*>(z + (int64_t)I * TB) + lane, make_double2(o0, o1));
-      __threadfence();
+      // bar.warp.sync orders the lanes' stores before lane 0's (cumulative) release
       __syncwarp();
       if (lane == 0) st_release(flag + I, epoch);
     }
@@ -244,6 +288,7 @@ __global__ void __launch_bounds__(32 * TR_WARPS, 1)
 __global__ void __launch_bounds__(32 * TR_WARPS, 1)
     k_trsv_bwd(int nb, const double* __restrict__ tiles, const double* __restrict__ linvT,
                const double* __restrict__ z, double* y, int* flag, int epoch) {
+  extern __shared__ __align__(16) double trs[];   // [tile (I+1, I) | L_II^-T]
   __shared__ double red[TR_WARPS][TB];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // this CTA's rows, descending
@@ -251,11 +296,14 @@ __global__ void __launch_bounds__(32 * TR_WARPS, 1)
   if (first >= nb) return;
   const int last = first + ((nb - 1 - first) / gridDim.x) * gridDim.x;
   for (int I = last; I >= first; I -= gridDim.x) {
+    if (I + 1 < nb) tr_prefetch(trs, tiles + ctid(I + 1, I) * TILE);
+    tr_prefetch(trs + TILE, linvT + (int64_t)I * TILE);
+    asm volatile("cp.async.commit_group;" ::: "memory");
     double cp[64];
 #pragma unroll
     for (int c = 0; c < 64; ++c) cp[c] = 0.0;
-    // farthest blocks first: the last one needed (J = I + 1) is published last
-    for (int J = nb - 1 - w; J > I; J -= TR_WARPS) {
+    // farthest blocks first; the chain block J = I + 1 comes last (below)
+    for (int J = nb - 1 - w; J > I + 1; J -= TR_WARPS) {
       if (lane == 0)
         while (ld_acquire(flag + J) < epoch) {
         }
@@ -265,6 +313,21 @@ __global__ void __launch_bounds__(32 * TR_WARPS, 1)
 #pragma unroll
       for (int c = 0; c < TB; ++c) {
         const double2 a = __ldcs(A + c * (TB / 2));   // rows 2l, 2l+1 of column c
+        cp[c] = fma(a.x, yj.x, fma(a.y, yj.y, cp[c]));
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (w == 0 && I + 1 < nb) {   // the chain step
+      if (lane == 0)
+        while (ld_acquire(flag + I + 1) < epoch) {
+        }
+      __syncwarp();
+      const double2 yj = __ldcg(reinterpret_cast<const double2*>(y + (int64_t)(I + 1) * TB) + lane);
+      const double2* A = reinterpret_cast<const double2*>(trs) + lane;
+#pragma unroll
+      for (int c = 0; c < TB; ++c) {
+        const double2 a = A[c * (TB / 2)];
         cp[c] = fma(a.x, yj.x, fma(a.y, yj.y, cp[c]));
       }
     }
@@ -280,9 +343,9 @@ __global__ void __launch_bounds__(32 * TR_WARPS, 1)
         v.y -= red[q][2 * lane + 1];
       }
       double o0 = 0.0, o1 = 0.0;
-      tile_mv(linvT + (int64_t)I * TILE, v, lane, o0, o1);
+      tile_mv_s(trs + TILE, v, lane, o0, o1);
       __stcg(reinterpret_cast<double2*>(y + (int64_t)I * TB) + lane, make_double2(o0, o1));
-      __threadfence();
+      // bar.warp.sync orders the lanes' stores before lane 0's (cumulative) release
       __syncwarp();
       if (lane == 0) st_release(flag + I, epoch);
     }
@@ -304,8 +367,16 @@ void launch_chol_solve(const DevBatch& b, const double* linv, const double* linv
   }
   // one CTA per SM at most: every CTA must be resident (they wait on each other)
   const int grid = std::min(nb, g_nsm_tr);
-  k_trsv_fwd<<<grid, 32 * TR_WARPS, 0, st>>>(nb, b.tiles, linv, r, zbuf, flags_fwd, epoch);
-  k_trsv_bwd<<<grid, 32 * TR_WARPS, 0, st>>>(nb, b.tiles, linvT, zbuf, y, flags_bwd, epoch);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_trsv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    cudaFuncSetAttribute(k_trsv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
+    attr = true;
+  }
+  k_trsv_fwd<<<grid, 32 * TR_WARPS, 2 * TILE * 8, st>>>(nb, b.tiles, linv, r, zbuf, flags_fwd,
+                                                        epoch);
+  k_trsv_bwd<<<grid, 32 * TR_WARPS, 2 * TILE * 8, st>>>(nb, b.tiles, linvT, zbuf, y, flags_bwd,
+                                                        epoch);
 }
 
 }  // namespace hplmm
