@@ -173,7 +173,12 @@ __device__ __forceinline__ void poll3(const double* p, double& a, double& b, dou
   a = ld_relaxed(p);
   b = ld_relaxed(p + 1);
   c = ld_relaxed(p + 2);
+  unsigned ns = 0;
   while (is_sent(a) || is_sent(b) || is_sent(c)) {
+    // back off once the wait is long (a row far ahead of the wavefront), to
+    // keep the polling traffic of thousands of waiting rows off L2
+    if (ns) __nanosleep(ns);
+    ns = ns ? min(ns * 2, 128u) : 8u;
     if (is_sent(a)) a = ld_relaxed(p);
     if (is_sent(b)) b = ld_relaxed(p + 1);
     if (is_sent(c)) c = ld_relaxed(p + 2);
