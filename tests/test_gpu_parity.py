@@ -374,3 +374,21 @@ def test_restart_and_iteration_cap(restart, max_iter):
         assert rel(x, xo) <= 1e-10
         assert abs(rep["final_true_relres"] - rro) <= 1e-8 * max(rro, 1.0)
         assert np.allclose(hist, histo, rtol=1e-8)
+
+
+@pytest.mark.parametrize("smoother", ["cg", "ilu0"])
+def test_nonfinite_rhs_reports_error(smoother):
+    """A NaN in b^ ends the solve with ERR_NONFINITE (no hang in the
+    sentinel-flagged ILU sweeps: a computed NaN is never the sentinel)."""
+    from paper_2509_19777_b200 import HPLMMError, Solver
+    import __graft_entry__
+    __graft_entry__.build()
+    p, s, h, _ = gpu_case("cube8")
+    sv = Solver(p, smoother=smoother, n_st=2 if smoother == "ilu0" else 1).assemble(0).setup()
+    b = s.b.copy()
+    b[7] = np.nan
+    with pytest.raises(HPLMMError) as ei:
+        sv.solve(b, tol=1e-8)
+    assert ei.value.status == -6
+    x, rep, _ = sv.solve(s.b.copy(), tol=1e-8)   # the handle stays usable
+    assert rep["converged"] == 1
