@@ -185,7 +185,7 @@ __device__ __forceinline__ void poll3(const double* p, double& a, double& b, dou
   }
 }
 
-// Waiting discipline (measured at cfg3, DESIGN.md §5): ONE lane per row spins,
+// Waiting discipline (measured at cfg3, DESIGN.md §10b): ONE lane per row spins,
 // on the dependency one level down that is issued last (the largest K in the
 // forward sweep = the x-neighbour, the smallest J in the backward sweep); the
 // other lanes then load their (by then almost always published) operands
@@ -194,6 +194,9 @@ __device__ __forceinline__ void poll3(const double* p, double& a, double& b, dou
 // same-line reads delay the producer's stores in L2.  Walking whole x-lines
 // per warp (the x-neighbour in registers) does not shorten the chain either:
 // the lattice level i + 2j + 4k makes every level wait on another line.
+// Pushing each result into per-consumer inboxes (all lanes poll their own
+// inbox) is 2.6x slower: the aggregate polling saturates L2.  Long waits back
+// off 8..128 ns (-4%; longer back-offs cost latency on the chain).
 
 // forward: y_I = r_I - sum_{K<I} L_IK y_K (rows in forward level order);
 // y must hold the sentinel on entry
