@@ -68,7 +68,8 @@ class HPLMM:
         n_dof = system.n_dof
         mesh = system.mesh
         self.dec = Decomposition(system, contact_h)
-        self.mor = Mortars(self.dec, mesh.node_ijk, n_mortar, beta, kind=mortar, A=A)
+        self.mor = Mortars(self.dec, mesh.node_ijk, n_mortar, beta, kind=mortar, A=A,
+                           system=system)
         dec, mor = self.dec, self.mor
         Nm = mor.n_mortar_dofs
         self.Nm = Nm

@@ -156,6 +156,116 @@ def algebraic_block(F: np.ndarray, A, mortars) -> np.ndarray:
     return M
 
 
+# ----------------------------------------------------------------------------
+# Algebraic mortars on the interface surface (reading R29, mortar = "surface")
+# ----------------------------------------------------------------------------
+# eq:algebra is the (D-1)-dimensional elasticity problem on the
+# interface Gamma^{c} with tangential derivatives only, zero stress on the
+# interface boundary and 0/1 constraints at the mortar nodes.  Discretised on
+# the voxel faces shared by a solid voxel of each grain of the interface's pair
+# (all four face nodes in F_c): Q1 on the unit square, 2x2 Gauss, all three
+# displacement components; strain = sym(grad_t eta) with the tangential
+# gradient only:  e_aa = d_a u_a, e_bb = d_b u_b, g_ab = d_b u_a + d_a u_b,
+# g_an = d_a u_n, g_bn = d_b u_n  (a, b in-plane axes, n the face normal);
+# isotropic lambda, mu from the mean E of the two voxels and the uniform nu.
+# A translation-free tie TIE * mu_bar * sum (eta_p - eta_q)^2 over the node
+# pairs of F_c coupled in A^ (the R7 interface graph, connected) attaches
+# nodes that lie on no shared face; mu_bar = mean E over solid voxels / (2(1+nu)).
+SURFACE_TIE = 0.1
+
+
+def surface_face_matrix(E: float, nu: float) -> np.ndarray:
+    """12 x 12 stiffness of one interface face, local components (a, b, n) per
+    node, nodes in corner order (0,0), (1,0), (0,1), (1,1) of (a, b)."""
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+    mu = E / (2 * (1 + nu))
+    D = np.diag([lam + 2 * mu, lam + 2 * mu, mu, mu, mu])
+    D[0, 1] = D[1, 0] = lam
+    g = 0.5 / math.sqrt(3.0)
+    K = np.zeros((12, 12))
+    corners = [(0, 0), (1, 0), (0, 1), (1, 1)]
+    for s_ in (0.5 - g, 0.5 + g):
+        for t_ in (0.5 - g, 0.5 + g):
+            B = np.zeros((5, 12))
+            for k, (da, db) in enumerate(corners):
+                fa = s_ if da else 1.0 - s_
+                fb = t_ if db else 1.0 - t_
+                dNa = (1.0 if da else -1.0) * fb      # d/ds
+                dNb = fa * (1.0 if db else -1.0)      # d/dt
+                B[0, 3 * k + 0] = dNa
+                B[1, 3 * k + 1] = dNb
+                B[2, 3 * k + 0] = dNb
+                B[2, 3 * k + 1] = dNa
+                B[3, 3 * k + 2] = dNa
+                B[4, 3 * k + 2] = dNb
+            K += 0.25 * B.T @ D @ B
+    return K
+
+
+def surface_faces(prob, lat_id, pair, pos):
+    """Faces of interface (pair, node positions pos) as (local node indices,
+    components (a, b, n), E of the face)."""
+    solid = np.asarray(prob.solid) > 0
+    grain = np.asarray(prob.grain)
+    comp_of_axis = (2, 1, 0)          # array axes (z, y, x) -> component index
+    g1, g2 = pair
+    out = []
+    for ax in range(3):
+        o0, o1 = [a for a in range(3) if a != ax]
+        sl1 = [slice(None)] * 3
+        sl2 = [slice(None)] * 3
+        sl1[ax] = slice(0, -1)
+        sl2[ax] = slice(1, None)
+        both = solid[tuple(sl1)] & solid[tuple(sl2)]
+        ga, gb = grain[tuple(sl1)], grain[tuple(sl2)]
+        hit = both & (((ga == g1) & (gb == g2)) | ((ga == g2) & (gb == g1)))
+        for v in np.argwhere(hit):
+            v = tuple(int(t) for t in v)
+            w = list(v)
+            w[ax] += 1
+            base = list(w)
+            nodes = []
+            for da, db in ((0, 0), (1, 0), (0, 1), (1, 1)):
+                c = list(base)
+                c[o0] += da
+                c[o1] += db
+                nodes.append(int(lat_id[c[0], c[1], c[2]]))
+            if not all(q in pos for q in nodes):
+                continue
+            E = 0.5 * (float(prob.E[v]) + float(prob.E[tuple(w)]))
+            out.append(([pos[q] for q in nodes],
+                        (comp_of_axis[o0], comp_of_axis[o1], comp_of_axis[ax]), E))
+    return out
+
+
+def surface_block(F, faces, ties, nu, mu_bar, mortars) -> np.ndarray:
+    """3|F| x 3nu block: the constrained solves of the Remark on the
+    surface operator K (faces + tie) instead of A^{c}_{c} (reading R29)."""
+    F = np.asarray(F)
+    pos = {int(y): f for f, y in enumerate(F)}
+    n3 = 3 * F.size
+    K = np.zeros((n3, n3))
+    for nodes, (ca, cb, cn), E in faces:
+        Kf = surface_face_matrix(E, nu)
+        idx = np.array([3 * nodes[k] + c for k in range(4) for c in (ca, cb, cn)])
+        K[np.ix_(idx, idx)] += Kf
+    tau = SURFACE_TIE * mu_bar
+    for f, q in ties:                      # each unordered pair once
+        for c in range(3):
+            K[3 * f + c, 3 * f + c] += tau
+            K[3 * q + c, 3 * q + c] += tau
+            K[3 * f + c, 3 * q + c] -= tau
+            K[3 * q + c, 3 * f + c] -= tau
+    con = np.array([3 * pos[int(x)] + g for x in mortars for g in range(3)], dtype=np.int64)
+    free = np.setdiff1d(np.arange(n3), con)
+    M = np.zeros((n3, con.size))
+    for q in range(con.size):
+        M[con[q], q] = 1.0
+        if free.size:
+            M[free, q] = -np.linalg.solve(K[np.ix_(free, free)], K[np.ix_(free, [con[q]])][:, 0])
+    return M
+
+
 class Mortars:
     """Mortar nodes + mortar blocks for every interface; coarse column ordering
     R13: interface id -> mortar index (placement order) -> gamma in {x,y,z}.
@@ -163,8 +273,13 @@ class Mortars:
     "algebraic" (eq:algebra via the Remark; needs A)."""
 
     def __init__(self, decomp, node_ijk, n_mortar: int, beta: float, kind: str = "gaussian",
-                 A=None):
+                 A=None, system=None):
         self.kind = kind
+        if kind == "surface":
+            prob = system.mesh.prob
+            solid = np.asarray(prob.solid) > 0
+            mu_bar = float(np.asarray(prob.E)[solid].mean()) / (2.0 * (1.0 + prob.nu))
+            rp, ci = system.row_ptr, system.col_idx
         self.nodes = []
         self.weights = []       # Gaussian W[f, i] (kind == "gaussian")
         self.blocks = []        # 3|F| x 3nu per interface (both kinds)
@@ -178,6 +293,13 @@ class Mortars:
                 self.blocks.append(gaussian_block(W))
             elif kind == "algebraic":
                 self.blocks.append(algebraic_block(F, A, X))
+            elif kind == "surface":
+                ci_ = len(self.nodes) - 1
+                pos = {int(y): f for f, y in enumerate(F)}
+                faces = surface_faces(prob, system.mesh.lat_id, tuple(decomp.iface_pair[ci_]), pos)
+                ties = [(pos[int(y)], pos[int(q)]) for y in F for q in ci[rp[y]:rp[y + 1]]
+                        if int(q) in pos and int(q) > int(y)]
+                self.blocks.append(surface_block(F, faces, ties, prob.nu, mu_bar, X))
             else:
                 raise ValueError(kind)
             self.offset.append(self.offset[-1] + len(X))
