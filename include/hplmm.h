@@ -100,7 +100,12 @@ typedef struct {
   int32_t mortar_kind;   /* mortar functions: 0 = Gaussian (eq:gauss,
                             the paper's choice, default); 1 = Algebraic
                             (eq:algebra, built by the Remark's constrained
-                            interface solves; reading R25)             */
+                            interface solves on A^{c}_{c}; reading R25);
+                            2 = Algebraic on the interface surface: the same
+                            constrained solves on eq:algebra discretised over
+                            the voxel faces shared by the pair's grains
+                            (tangential strain, Q1) + a translation-free tie
+                            (reading R29; partition of unity exact)        */
   int32_t smoother;      /* base smoother M_l of eq:local_smoother:
                             0 = contact-grain M_CG (eq:local_smoother_CG, the
                                 paper's choice with n_st = 1; default);

@@ -25,6 +25,7 @@ namespace {
 thread_local std::string g_last_error;
 
 constexpr int kSnLeaf = 40;                          // ND leaf size (nodes)
+constexpr double kSurfaceTie = 0.1;                  // R29 tie (x mean shear modulus)
 static int sn_leaf() {   // HPLMM_SN_LEAF overrides (ordering experiments)
   static const int v = getenv("HPLMM_SN_LEAF") ? std::max(4, atoi(getenv("HPLMM_SN_LEAF"))) : kSnLeaf;
   return v;
@@ -1033,18 +1034,115 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         int32_t big2 = INT_MAX;
         CK(cudaMemsetAsync(ab.tiles, 0, (size_t)ab.ntiles * TILE * 8, h->st));
         CK(cudaMemcpyAsync(ab.err, &big2, 4, cudaMemcpyHostToDevice, h->st));
-        launch_extract_local(ab, free_ptr.back(), h->upload(free_ptr), h->upload(free_nodes),
-                             h->d_row_ptr, h->d_col, h->d_val, h->st);
+        int32_t* d_free_ptr = h->upload(free_ptr);
+        int32_t* d_free_pos = h->upload(free_pos);
+        int32_t* d_con_pos = h->upload(con_pos);
+        const bool surf = hs.opt.mortar_kind == 2;
+        int64_t* d_koff = nullptr;
+        double* d_Kbuf = nullptr;
+        if (surf) {
+          // Surface reading (R29): faces shared by the pair's grains with all
+          // four nodes on the interface, in the oracle's order (array axis z,
+          // y, x; voxels lexicographic), and the pattern couplings inside F_c
+          const int nx = hs.nx, ny = hs.ny, nz = hs.nz;
+          const int64_t nx1 = nx + 1, ny1 = ny + 1;
+          std::vector<std::vector<int4>> fc(C);
+          const int comp_of_axis[3] = {2, 1, 0};
+          const int dims[3] = {nz, ny, nx};
+          for (int ax = 0; ax < 3; ++ax) {
+            int o[2], oi = 0;
+            for (int a = 0; a < 3; ++a)
+              if (a != ax) o[oi++] = a;
+            for (int k = 0; k < nz; ++k)
+              for (int j = 0; j < ny; ++j)
+                for (int i = 0; i < nx; ++i) {
+                  int v1c[3] = {k, j, i};
+                  if (v1c[ax] + 1 >= dims[ax]) continue;
+                  int v2c[3] = {k, j, i};
+                  v2c[ax] += 1;
+                  const int64_t v1 = i + (int64_t)nx * (j + (int64_t)ny * k);
+                  const int64_t v2 = v2c[2] + (int64_t)nx * (v2c[1] + (int64_t)ny * v2c[0]);
+                  if (!hs.solid[v1] || !hs.solid[v2]) continue;
+                  const int ga = hs.grain[v1], gb = hs.grain[v2];
+                  if (ga == gb) continue;
+                  int nodes[4], q = 0;
+                  for (int db = 0; db < 2; ++db)
+                    for (int da = 0; da < 2; ++da) {
+                      int c3[3] = {v2c[0], v2c[1], v2c[2]};
+                      c3[o[0]] += da;
+                      c3[o[1]] += db;
+                      nodes[q++] = hs.lat_id[c3[2] + nx1 * (c3[1] + ny1 * c3[0])];
+                    }
+                  const int cf = nodes[0] >= 0 ? hs.node_iface[nodes[0]] : -1;
+                  if (cf < 0) continue;
+                  const int p1 = std::min(ga, gb), p2 = std::max(ga, gb);
+                  if (hs.iface_pair[2 * cf] != p1 || hs.iface_pair[2 * cf + 1] != p2) continue;
+                  bool all = true;
+                  int pos[4];
+                  const int* F = hs.iface_nodes.data() + hs.iface_ptr[cf];
+                  const int nF = hs.iface_ptr[cf + 1] - hs.iface_ptr[cf];
+                  for (int t = 0; t < 4 && all; ++t) {
+                    all = nodes[t] >= 0 && hs.node_iface[nodes[t]] == cf;
+                    if (all) pos[t] = (int)(std::lower_bound(F, F + nF, nodes[t]) - F);
+                  }
+                  if (!all) continue;
+                  const int code = comp_of_axis[o[0]] | (comp_of_axis[o[1]] << 2) |
+                                   (comp_of_axis[ax] << 4);
+                  fc[cf].push_back(make_int4(pos[0], pos[1], pos[2], pos[3]));
+                  fc[cf].push_back(make_int4(code, (int)v1, (int)v2, 0));
+                }
+          }
+          std::vector<int32_t> face_ptr(C + 1, 0);
+          std::vector<int4> faces;
+          for (int c = 0; c < C; ++c) {
+            faces.insert(faces.end(), fc[c].begin(), fc[c].end());
+            face_ptr[c + 1] = (int32_t)(faces.size() / 2);
+          }
+          std::vector<int32_t> tie_ptr(hs.iface_nodes.size() + 1, 0), tie_q;
+          std::vector<int64_t> koff(C + 1, 0);
+          for (int c = 0; c < C; ++c) {
+            const int* F = hs.iface_nodes.data() + hs.iface_ptr[c];
+            const int nF = hs.iface_ptr[c + 1] - hs.iface_ptr[c];
+            for (int f = 0; f < nF; ++f) {
+              const int y = F[f];
+              for (int e = hs.row_ptr[y]; e < hs.row_ptr[y + 1]; ++e) {
+                const int qn = hs.col_idx[e];
+                if (qn == y || hs.node_iface[qn] != c) continue;
+                tie_q.push_back((int32_t)(std::lower_bound(F, F + nF, qn) - F));
+              }
+              tie_ptr[hs.iface_ptr[c] + f + 1] = (int32_t)tie_q.size();
+            }
+            koff[c + 1] = koff[c] + (int64_t)(3 * nF) * (3 * nF);
+          }
+          d_koff = h->upload(koff, true);
+          d_Kbuf = h->dalloc<double>((size_t)std::max<int64_t>(koff[C], 1), true);
+          double* d_K1 = h->dalloc<double>(144, true);
+          double* d_tau = h->dalloc<double>(1, true);
+          launch_surf_operator(C, co.iface_ptr, h->upload(face_ptr, true),
+                               reinterpret_cast<const int4*>(h->upload(
+                                   std::vector<int32_t>(reinterpret_cast<int32_t*>(faces.data()),
+                                                        reinterpret_cast<int32_t*>(faces.data()) +
+                                                            4 * faces.size()),
+                                   true)),
+                               h->d_E, h->d_solid, (int64_t)hs.nx * hs.ny * hs.nz, hs.nu,
+                               kSurfaceTie, h->upload(tie_ptr, true), h->upload(tie_q, true),
+                               d_koff, d_K1, d_tau, d_Kbuf, h->st);
+          launch_surf_extract(ab, co.iface_ptr, d_free_ptr, d_free_pos, d_koff, d_Kbuf, h->st);
+        } else {
+          launch_extract_local(ab, free_ptr.back(), d_free_ptr, h->upload(free_nodes),
+                               h->d_row_ptr, h->d_col, h->d_val, h->st);
+        }
         launch_pad_identity(ab, h->st);
         launch_sweep_invert(ab, h->st);
         CK(cudaGetLastError());
         check_batch_err(h, ab, 0, false);
-        int32_t* d_free_ptr = h->upload(free_ptr);
-        int32_t* d_free_pos = h->upload(free_pos);
-        int32_t* d_con_pos = h->upload(con_pos);
         for (int q = 0; q < maxq; ++q) {
-          launch_alg_rhs(q, ab, co.mortar_ptr, d_mortar_nodes, h->d_row_ptr, h->d_col, h->d_val,
-                         h->st);
+          if (surf)
+            launch_surf_rhs(q, ab, co.iface_ptr, co.mortar_ptr, d_free_ptr, d_free_pos, d_con_pos,
+                            d_koff, d_Kbuf, h->st);
+          else
+            launch_alg_rhs(q, ab, co.mortar_ptr, d_mortar_nodes, h->d_row_ptr, h->d_col,
+                           h->d_val, h->st);
           launch_symv(ab, h->st);
           launch_alg_store(q, C, ab, co.mortar_ptr, d_free_ptr, d_free_pos, d_con_pos, co.wt_off,
                            co.W, h->st);

@@ -271,6 +271,178 @@ __global__ void k_alg_store(int q, int C, const int32_t* mortar_ptr, const int32
   }
 }
 
+// ---------------------------------------------------------------------------
+// Surface Algebraic mortars (mortar_kind = 2, reading R29): eq:algebra
+// discretised on the voxel faces shared by the interface's two grains (Q1,
+// 2x2 Gauss, tangential strain of all 3 components) plus a translation-free
+// tie tau (eta_p - eta_q)^2 over the pattern couplings inside F_c.  Each
+// interface's operator K_c (3|F| x 3|F|, dense, transient) is assembled by one
+// CTA in a fixed order (faces one after the other, then the tie row by row),
+// copied into the free-node packed tiles of the interface batch, and its
+// constrained columns give the right-hand sides of the constrained solves.
+// ---------------------------------------------------------------------------
+// face stiffness for E = 1: local components (a, b, n) per node, corners
+// (0,0), (1,0), (0,1), (1,1) of (a, b); K = sum_gp 1/4 B^T D B
+__device__ __forceinline__ void surf_B(int col, double s, double t, double (&b)[5]) {
+  const int k = col / 3, cmp = col % 3;
+  const int da = k & 1, db = k >> 1;
+  const double fa = da ? s : 1.0 - s, fb = db ? t : 1.0 - t;
+  const double dA = (da ? 1.0 : -1.0) * fb, dB = fa * (db ? 1.0 : -1.0);
+  for (int i = 0; i < 5; ++i) b[i] = 0.0;
+  if (cmp == 0) { b[0] = dA; b[2] = dB; }
+  else if (cmp == 1) { b[1] = dB; b[2] = dA; }
+  else { b[3] = dA; b[4] = dB; }
+}
+__global__ void k_surf_K1(double nu, double* K1) {
+  const int e = threadIdx.x;
+  if (e >= 144) return;
+  const int r = e / 12, c = e % 12;
+  const double lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = 1.0 / (2.0 * (1.0 + nu));
+  const double D[5][5] = {{lam + 2 * mu, lam, 0, 0, 0}, {lam, lam + 2 * mu, 0, 0, 0},
+                          {0, 0, mu, 0, 0}, {0, 0, 0, mu, 0}, {0, 0, 0, 0, mu}};
+  const double g = 0.5 / sqrt(3.0);
+  const double gp[2] = {0.5 - g, 0.5 + g};
+  double acc = 0.0;
+  for (int is = 0; is < 2; ++is)
+    for (int it = 0; it < 2; ++it) {
+      double br[5], bc[5];
+      surf_B(r, gp[is], gp[it], br);
+      surf_B(c, gp[is], gp[it], bc);
+      double v = 0.0;
+      for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) v += br[i] * D[i][j] * bc[j];
+      acc += 0.25 * v;
+    }
+  K1[e] = acc;
+}
+// tau = TIE * mean(E over solid voxels) / (2 (1 + nu)); one block, fixed order
+__global__ void k_surf_tau(int64_t nvox, const double* __restrict__ E,
+                           const uint8_t* __restrict__ solid, double nu, double tie,
+                           double* tau) {
+  __shared__ double ss[256], sc[256];
+  double a = 0.0, c = 0.0;
+  for (int64_t v = threadIdx.x; v < nvox; v += blockDim.x)
+    if (solid[v]) { a += E[v]; c += 1.0; }
+  ss[threadIdx.x] = a;
+  sc[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      ss[threadIdx.x] += ss[threadIdx.x + o];
+      sc[threadIdx.x] += sc[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *tau = tie * (ss[0] / sc[0]) / (2.0 * (1.0 + nu));
+}
+__global__ void __launch_bounds__(256) k_surf_assemble(
+    const int32_t* __restrict__ iface_ptr, const int32_t* __restrict__ face_ptr,
+    const int4* __restrict__ faces, const double* __restrict__ E, const double* __restrict__ K1,
+    const int32_t* __restrict__ tie_ptr, const int32_t* __restrict__ tie_q,
+    const double* __restrict__ tau_p, const int64_t* __restrict__ koff, double* Kbuf) {
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const int e0 = iface_ptr[c], nF = iface_ptr[c + 1] - e0, n3 = 3 * nF;
+  double* K = Kbuf + koff[c];
+  for (int64_t e = tid; e < (int64_t)n3 * n3; e += blockDim.x) K[e] = 0.0;
+  __syncthreads();
+  for (int f = face_ptr[c]; f < face_ptr[c + 1]; ++f) {
+    if (tid < 144) {
+      const int4 nd = faces[2 * f], meta = faces[2 * f + 1];
+      const int r = tid / 12, q = tid % 12;
+      const int node[4] = {nd.x, nd.y, nd.z, nd.w};
+      const int cm[3] = {meta.x & 3, (meta.x >> 2) & 3, (meta.x >> 4) & 3};
+      const int row = 3 * node[r / 3] + cm[r % 3], col = 3 * node[q / 3] + cm[q % 3];
+      const double Ef = 0.5 * (E[meta.y] + E[meta.z]);
+      K[(int64_t)row * n3 + col] += Ef * K1[tid];
+    }
+    __syncthreads();
+  }
+  const double tau = *tau_p;
+  for (int f = tid; f < nF; f += blockDim.x)
+    for (int t = tie_ptr[e0 + f]; t < tie_ptr[e0 + f + 1]; ++t) {
+      const int q = tie_q[t];
+      for (int cc = 0; cc < 3; ++cc) {
+        K[(int64_t)(3 * f + cc) * n3 + 3 * f + cc] += tau;
+        K[(int64_t)(3 * f + cc) * n3 + 3 * q + cc] -= tau;
+      }
+    }
+}
+// free/free block of K_c -> the interface batch's packed tiles
+__global__ void __launch_bounds__(256) k_surf_extract(
+    int64_t ntiles, const int32_t* __restrict__ tile_s, const int32_t* __restrict__ tile_ij,
+    const int32_t* __restrict__ iface_ptr, const int32_t* __restrict__ free_ptr,
+    const int32_t* __restrict__ free_pos, const int64_t* __restrict__ koff,
+    const double* __restrict__ Kbuf, double* tiles) {
+  const int64_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  const int c = tile_s[t], I = tile_ij[t] >> 16, J = tile_ij[t] & 0xffff;
+  const int n3 = 3 * (iface_ptr[c + 1] - iface_ptr[c]);
+  const int f0 = free_ptr[c], m3 = 3 * (free_ptr[c + 1] - f0);
+  const double* K = Kbuf + koff[c];
+  for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+    const int lr = TB * I + (e & 63), lc = TB * J + (e >> 6);
+    if (lr < m3 && lc < m3) {
+      const int row = 3 * free_pos[f0 + lr / 3] + lr % 3;
+      const int col = 3 * free_pos[f0 + lc / 3] + lc % 3;
+      tiles[t * TILE + e] = K[(int64_t)row * n3 + col];
+    }
+  }
+}
+// right-hand side of constrained column q: -K_c[free, (mortar q/3, component q%3)]
+__global__ void k_surf_rhs(int q, int64_t nloc, const int32_t* __restrict__ row_s,
+                           const int64_t* __restrict__ row_base,
+                           const int32_t* __restrict__ iface_ptr,
+                           const int32_t* __restrict__ mortar_ptr,
+                           const int32_t* __restrict__ free_ptr,
+                           const int32_t* __restrict__ free_pos,
+                           const int32_t* __restrict__ con_pos, const int64_t* __restrict__ koff,
+                           const double* __restrict__ Kbuf, double* xloc) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nloc) return;
+  const int c = row_s[t >> 6];
+  const int64_t l = t - TB * row_base[c];
+  const int f0 = free_ptr[c], m3 = 3 * (free_ptr[c + 1] - f0);
+  const int nu3 = 3 * (mortar_ptr[c + 1] - mortar_ptr[c]);
+  double v = 0.0;
+  if (l < m3 && q < nu3) {
+    const int n3 = 3 * (iface_ptr[c + 1] - iface_ptr[c]);
+    const int row = 3 * free_pos[f0 + l / 3] + (int)(l % 3);
+    const int col = 3 * con_pos[mortar_ptr[c] + q / 3] + q % 3;
+    v = -Kbuf[koff[c] + (int64_t)row * n3 + col];
+  }
+  xloc[t] = v;
+}
+
+void launch_surf_operator(int C, const int32_t* iface_ptr, const int32_t* face_ptr,
+                          const int4* faces, const double* E, const uint8_t* solid,
+                          int64_t nvox, double nu, double tie, const int32_t* tie_ptr,
+                          const int32_t* tie_q, const int64_t* koff, double* K1, double* tau,
+                          double* Kbuf, cudaStream_t st) {
+  if (C <= 0) return;
+  k_surf_K1<<<1, 160, 0, st>>>(nu, K1);
+  k_surf_tau<<<1, 256, 0, st>>>(nvox, E, solid, nu, tie, tau);
+  k_surf_assemble<<<C, 256, 0, st>>>(iface_ptr, face_ptr, faces, E, K1, tie_ptr, tie_q, tau,
+                                     koff, Kbuf);
+}
+
+void launch_surf_extract(const DevBatch& ab, const int32_t* iface_ptr, const int32_t* free_ptr,
+                         const int32_t* free_pos, const int64_t* koff, const double* Kbuf,
+                         cudaStream_t st) {
+  if (ab.ntiles <= 0) return;
+  k_surf_extract<<<(unsigned)ab.ntiles, 256, 0, st>>>(ab.ntiles, ab.tile_s, ab.tile_ij, iface_ptr,
+                                                      free_ptr, free_pos, koff, Kbuf, ab.tiles);
+}
+
+void launch_surf_rhs(int q, const DevBatch& ab, const int32_t* iface_ptr,
+                     const int32_t* mortar_ptr, const int32_t* free_ptr, const int32_t* free_pos,
+                     const int32_t* con_pos, const int64_t* koff, const double* Kbuf,
+                     cudaStream_t st) {
+  if (ab.nloc <= 0) return;
+  k_surf_rhs<<<(unsigned)((ab.nloc + 255) / 256), 256, 0, st>>>(
+      q, ab.nloc, ab.row_s, ab.row_base, iface_ptr, mortar_ptr, free_ptr, free_pos, con_pos,
+      koff, Kbuf, ab.xloc);
+}
+
 void launch_alg_rhs(int q, const DevBatch& ab, const int32_t* mortar_ptr,
                     const int32_t* mortar_nodes, const int32_t* rp, const int32_t* col,
                     const double* val, cudaStream_t st) {

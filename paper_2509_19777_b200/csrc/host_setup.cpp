@@ -118,9 +118,9 @@ bool host_setup(const hplmm_problem* p, const hplmm_options* opt, HostSetup& hs,
       (opt->smoother != 0 && opt->smoother != 1) ||
       (opt->local_factor != 0 && opt->local_factor != 1) ||
       (opt->coarse_solver != 0 && opt->coarse_solver != 1) ||
-      (opt->mortar_kind != 0 && opt->mortar_kind != 1)) {
+      (opt->mortar_kind < 0 || opt->mortar_kind > 2)) {
     err = "hplmm_create: invalid options (n_mortar>=1, contact_h>=0, 1<=restart<=512, 1<=n_st<=64, "
-          "smoother/local_factor/coarse_solver/mortar_kind in {0,1})";
+          "smoother/local_factor/coarse_solver in {0,1}, mortar_kind in {0,1,2})";
     return false;
   }
   hs.opt = *opt;

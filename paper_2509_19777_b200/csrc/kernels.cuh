@@ -140,6 +140,21 @@ void launch_S_grain(const DevCoarse& c, double* S, int64_t lds, cudaStream_t st)
 void launch_alg_rhs(int q, const DevBatch& ab, const int32_t* mortar_ptr,
                     const int32_t* mortar_nodes, const int32_t* rp, const int32_t* col,
                     const double* val, cudaStream_t st);
+// surface Algebraic mortars (mortar_kind = 2): dense interface operators K_c
+// (faces: 2 int4 per face = 4 local node positions | comps a,b,n (2 bits
+// each), voxel ids of the two sides), their free/free tiles, constrained RHS
+void launch_surf_operator(int C, const int32_t* iface_ptr, const int32_t* face_ptr,
+                          const int4* faces, const double* E, const uint8_t* solid,
+                          int64_t nvox, double nu, double tie, const int32_t* tie_ptr,
+                          const int32_t* tie_q, const int64_t* koff, double* K1, double* tau,
+                          double* Kbuf, cudaStream_t st);
+void launch_surf_extract(const DevBatch& ab, const int32_t* iface_ptr, const int32_t* free_ptr,
+                         const int32_t* free_pos, const int64_t* koff, const double* Kbuf,
+                         cudaStream_t st);
+void launch_surf_rhs(int q, const DevBatch& ab, const int32_t* iface_ptr,
+                     const int32_t* mortar_ptr, const int32_t* free_ptr, const int32_t* free_pos,
+                     const int32_t* con_pos, const int64_t* koff, const double* Kbuf,
+                     cudaStream_t st);
 void launch_alg_store(int q, int C, const DevBatch& ab, const int32_t* mortar_ptr,
                       const int32_t* free_ptr, const int32_t* free_pos, const int32_t* con_pos,
                       const int64_t* wt_off, double* W, cudaStream_t st);

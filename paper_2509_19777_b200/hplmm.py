@@ -185,7 +185,7 @@ class Solver:
         if coarse_solver is not None:
             o.coarse_solver = int(coarse_solver)
         mk = mortar if mortar is not None else getattr(prob, "mortar", "gaussian")
-        o.mortar_kind = {"gaussian": 0, "algebraic": 1}[mk]
+        o.mortar_kind = {"gaussian": 0, "algebraic": 1, "surface": 2}[mk]
         if smoother is not None:
             o.smoother = SMOOTHER[smoother] if isinstance(smoother, str) else int(smoother)
         if n_st is not None:

@@ -13,9 +13,9 @@ from workloads import make_problem
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 p = make_problem(cfg)
 print(f"{cfg}: mortar n | N_m | iterations | T_ML s | T_MG s | T_sol s | T_tot s")
-for mortar in ("gaussian", "algebraic"):
+for mortar in ("gaussian", "algebraic", "surface"):
     for n in (1, 2, 4, 8):
-        if mortar == "algebraic" and n == 1:
+        if mortar != "gaussian" and n == 1:
             continue
         sv = Solver(p, n_mortar=n, mortar=mortar).assemble(0).setup()
         b = torch.from_numpy(sv.export("RHS")).cuda()
