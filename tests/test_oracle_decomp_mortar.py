@@ -13,18 +13,24 @@ import pytest
 from oracle import decomp, mortar
 
 
+def _golden(name):
+    import json, os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", name)))
+
+
 def test_cfg1_decomposition_closed_form(cfg1):
     _, s, h = cfg1
     d = h.dec
-    assert d.n_grains == 8
-    assert d.n_interfaces == 12
+    g = _golden("cfg1_counts.json")
+    assert d.n_grains == g["grains"]
+    assert d.n_interfaces == g["interfaces"]
     sizes = sorted(F.size for F in d.interfaces)
-    assert sizes == [64] * 10 + [72] * 2
-    big = [tuple(d.iface_pair[c]) for c, F in enumerate(d.interfaces) if F.size == 72]
-    assert big == [(0, 1), (4, 5)]
-    assert sum(F.size for F in d.interfaces) == 784
-    assert int((d.node_class == decomp.CLASS_D).sum()) == 289
-    assert max(g.size for g in d.grain_nodes) == 529
+    assert sizes == g["interface_sizes_sorted"]
+    big = [list(map(int, d.iface_pair[c])) for c, F in enumerate(d.interfaces) if F.size == 72]
+    assert big == g["big_interface_pairs"]
+    assert sum(F.size for F in d.interfaces) == g["interface_nodes"]
+    assert int((d.node_class == decomp.CLASS_D).sum()) == g["dirichlet_nodes"]
+    assert max(gn.size for gn in d.grain_nodes) == g["max_grain_interior_nodes"]
     # every node is in exactly one of: some I_g, some interface
     cover = np.zeros(s.mesh.n_nodes, int)
     for g in d.grain_nodes:
@@ -127,10 +133,12 @@ def test_rectangle_placement_is_global_minimum(shape):
 
 def test_gaussian_two_node_closed_form():
     # own-node weight with two mortars = 1/(1+e^{-1/4})
-    ijk = np.array([[0, 0, 0], [5, 0, 0], [2, 0, 0]])
-    W = mortar.gaussian_weights(np.array([0, 1, 2]), ijk, [0, 1], 4.0)
+    # (tests/golden/gauss_two_node.json)
+    g = _golden("gauss_two_node.json")
+    ijk = np.array(g["mortars_ijk"] + [g["probe_ijk"]])
+    W = mortar.gaussian_weights(np.array([0, 1, 2]), ijk, [0, 1], g["beta"])
     assert abs(W[0, 0] - 1.0 / (1.0 + math.exp(-0.25))) <= 1e-15
-    assert abs(W[0, 0] - 0.5621765008857981) <= 1e-15
+    assert abs(W[0, 0] - g["w_own"]) <= 1e-15
 
 
 def test_mortar_partition_of_unity_and_nu1(porous20):

@@ -14,12 +14,15 @@ from workloads import Problem, make_problem
 
 def test_cfg1_counts():
     # BASELINE.json configs[0]: 14,739 DOF = 17^3 * 3; nnzb closed form
-    # (3*17-2)^3 = 117,649 before and 110,735 after Dirichlet removal.
+    # (3*17-2)^3 = 117,649 before and 110,735 after Dirichlet removal
+    # (tests/golden/cfg1_counts.json).
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg1_counts.json")))
     s = fem.build_system(make_problem("cfg1"))
-    assert s.n_dof == 14739 == 17 ** 3 * 3
-    assert s.full.nnz // 9 == (3 * 17 - 2) ** 3 == 117649
-    assert s.nnzb == 110735
-    assert int(s.mesh.dirichlet.sum()) == 17 * 17
+    assert s.n_dof == g["n_dof"] == 17 ** 3 * 3
+    assert s.full.nnz // 9 == g["nnzb_full"] == (3 * 17 - 2) ** 3
+    assert s.nnzb == g["nnzb_constrained"]
+    assert int(s.mesh.dirichlet.sum()) == g["dirichlet_nodes"] == 17 * 17
 
 
 @pytest.mark.parametrize("nu", [0.25, 0.3, 0.45])
