@@ -419,3 +419,29 @@ def test_surface_mortars(case, lf):
     x, rep, _ = sv.solve(s.b.copy(), tol=1e-8)
     assert convo and rep["converged"] == 1 and abs(rep["iterations"] - ito) <= 1, (rep["iterations"], ito)
     assert rel(x, xo) <= 1e-8
+
+
+@pytest.mark.parametrize("mortar", ["gaussian", "algebraic", "surface"])
+@pytest.mark.parametrize("smoother", ["cg", "ilu0"])
+@pytest.mark.parametrize("coarse", [0, 1])
+@pytest.mark.parametrize("lf", LF)
+def test_option_matrix_cube8(lf, coarse, smoother, mortar):
+    """Every combination of local solver x coarse solver x smoother x mortar
+    kind on cube8: GMRES iterations within +-1 of the oracle with the same
+    operator, x within 1e-8."""
+    from oracle import gmres, hplmm
+    from paper_2509_19777_b200 import Solver
+    from workloads import make_problem
+    import __graft_entry__
+    __graft_entry__.build()
+    n_st = 3 if smoother == "ilu0" else 1
+    p = make_problem("cube8", mortar=mortar)
+    s, h = hplmm.setup(p, smoother=smoother, n_st=n_st)
+    h.set_rhs(s.b)
+    xo, ito, _, _, convo = gmres.gmres(s.A, s.b, h.apply_M, tol=1e-8)
+    sv = Solver(p, local_factor=lf, coarse_solver=coarse, smoother=smoother,
+                n_st=n_st).assemble(0).setup()
+    x, rep, _ = sv.solve(s.b.copy(), tol=1e-8)
+    assert convo and rep["converged"] == 1
+    assert abs(rep["iterations"] - ito) <= 1, (rep["iterations"], ito)
+    assert rel(x, xo) <= 1e-8
