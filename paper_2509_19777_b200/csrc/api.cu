@@ -88,6 +88,8 @@ struct hplmm_handle {
          *d_t = nullptr, *d_rm = nullptr, *d_rc = nullptr, *d_yc = nullptr, *d_x = nullptr,
          *d_u = nullptr, *d_bb = nullptr;
   double *d_V = nullptr, *d_partial = nullptr, *d_hbuf = nullptr;
+  double* h_hh = nullptr;   // pinned host copy of the Arnoldi step's dots
+  int hh_cap = 0;
   int64_t ldv = 0;
   int Vcap = 0;
 
@@ -163,6 +165,7 @@ struct hplmm_handle {
       cudaDeviceSynchronize();
       for (void* p : allocs) cudaFree(p);
       free_setup();
+      if (h_hh) cudaFreeHost(h_hh);
       for (auto e : ev_pool) cudaEventDestroy(e);
       for (auto& e : ev_pending) {
         cudaEventDestroy(e.second.first);
@@ -1377,7 +1380,14 @@ hplmm_status hplmm_solve(hplmm_handle* h, const double* b, double tol, double* x
       do_set_rhs(h, dB);   // correction columns for this RHS (R15)
       // r = b (x0 = 0)
       CK(cudaMemcpyAsync(h->d_r1, dB, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
-      std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), hh(2 * (m + 1) + 1);
+      std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1);
+      // the per-step Hessenberg column comes back through pinned memory
+      if (h->hh_cap < 2 * (m + 1) + 1) {
+        if (h->h_hh) cudaFreeHost(h->h_hh);
+        CK(cudaMallocHost(&h->h_hh, (size_t)(2 * (m + 1) + 1) * 8));
+        h->hh_cap = 2 * (m + 1) + 1;
+      }
+      double* hh = h->h_hh;
       double beta2 = bn2;
       while (true) {
         double beta = std::sqrt(beta2);
@@ -1401,7 +1411,7 @@ hplmm_status hplmm_solve(hplmm_handle* h, const double* b, double tol, double* x
           launch_multidot(n, j + 1, V, h->ldv, w, h->d_partial, hb + (m + 1), st);
           launch_update(n, j + 1, V, h->ldv, hb + (m + 1), w, h->d_partial, hb + 2 * (m + 1), st);
           h->launches += 7;
-          CK(cudaMemcpyAsync(hh.data(), hb, (2 * (m + 1) + 1) * 8, cudaMemcpyDeviceToHost, st));
+          CK(cudaMemcpyAsync(hh, hb, (2 * (m + 1) + 1) * 8, cudaMemcpyDeviceToHost, st));
           CK(cudaStreamSynchronize(st));
           double hn = std::sqrt(hh[2 * (m + 1)]);
           std::vector<double> col(j + 2);
