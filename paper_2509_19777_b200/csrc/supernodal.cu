@@ -533,6 +533,10 @@ int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r) {
   if (getenv("HPLMM_SN_CHUNK")) return sn_chunk_doubles();
   const int base = sn_chunk_doubles();
   if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base) == 8) return base;
+  // enough subdomains for 8 x 2 but x_S leaves no room for two 32-KiB stages:
+  // smaller chunks keep the 8 x 2 shape (far cheaper per byte than 16 x 1)
+  for (int c : {3072, 2048})
+    if (c < base && sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c) == 8) return c;
   for (int c : {SN_CHUNK_DOUBLES_MAX, 6144})
     if (c > base && sn_solve_stages(max_n, max_r, 1, c, 16) >= 2) return c;
   return base;
