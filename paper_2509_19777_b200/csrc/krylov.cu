@@ -1,7 +1,12 @@
 // Arnoldi / GMRES vector kernels (sm_100a, fp64): fused multi-dot, multi-axpy
 // with an optional fused norm, all with deterministic two-stage reductions
 // (fixed block->range mapping, fixed-order final sums).  CGS2 (R22) uses
-// multidot + update twice per Arnoldi step.
+// multidot + update twice per Arnoldi step.  Measured and dropped: fusing the
+// first update with the second multidot (one DRAM pass over V fewer; the
+// element's V values re-read from L1/L2 for the dots) was 0.04 ms per
+// iteration SLOWER at cfg3 -- the 2 x 50 per-thread accumulators / operands
+// take 255 registers, one CTA per SM, and the per-element FMA chain then
+// stalls the stream.
 #include "kernels.cuh"
 
 namespace hplmm {
