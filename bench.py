@@ -369,7 +369,15 @@ def main():
     # per-iteration algorithmic bytes (whole hot path)
     nnzb = rep0["nnzb"]
     n = 3 * rep0["n_nodes"]
-    spmv_bytes = 76 * nnzb + 4 * rep0["n_nodes"] + 24 * n
+    ebe = rep0.get("fine_operator", 1) == 0
+    if ebe:   # element-by-element A^: x, v, y + node coordinates and Dirichlet flag,
+        # lattice map (4 B / lattice point) and voxel moduli (8 B / voxel)
+        nxyz = (p.nx, p.ny, p.nz)
+        spmv_bytes = (24 * n + 13 * rep0["n_nodes"]
+                      + 4 * (nxyz[0] + 1) * (nxyz[1] + 1) * (nxyz[2] + 1)
+                      + 8 * nxyz[0] * nxyz[1] * nxyz[2])
+    else:     # stored BSR blocks: 72 B values + 4 B column per block, row pointers
+        spmv_bytes = 76 * nnzb + 4 * rep0["n_nodes"] + 24 * n
     pb = 12 * rep0["prolong_nnz"]
     if ilu:   # n_st ILU applies + their n_st - 1 stage residuals; y and w SpMVs
         per_iter_bytes = (n_st * alg[5] + alg[2] + (2 + n_st - 1) * spmv_bytes + 2 * pb
@@ -399,6 +407,7 @@ def main():
                    "parallelism": f"replicas{world}",
                    "local_factor": "supernodal" if sparse else "dense-inverse",
                    "smoother": smoother, "n_st": n_st,
+                   "fine_operator": "element-by-element" if ebe else "bsr",
                    "l2": "no flush: working set (local factors) >> 126 MB L2"},
         "iterations": iters, "iterations_per_s": iters_per_s * world,
         "solves_per_s_aggregate": world / t_s,

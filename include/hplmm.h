@@ -114,6 +114,15 @@ typedef struct {
                                 pattern of every stored 3x3 block (R26), held
                                 as block ILU(0) factors in A^'s BSR layout;
                                 contact-grid factors are not built        */
+  int32_t operator_kind; /* how the solve applies A^ (GMRES, eq:multi_precond,
+                            eq:local_smoother_CG):
+                            0 = element-by-element from the voxel data,
+                                sum_e E_e K0 x_e over each node's voxels with
+                                R4's identity Dirichlet rows (default; used
+                                only when A^ is the library's own assembly --
+                                after hplmm_set_matrix the stored blocks are
+                                used);
+                            1 = the stored BSR blocks (TMA-streamed SpMV)    */
 } hplmm_options;
 
 typedef struct {
@@ -142,6 +151,7 @@ typedef struct {
   double t_rhs_s;         /* per-RHS correction columns (set_rhs)                   */
   double t_solve_s;       /* GMRES (T_sol)                                          */
   int64_t kernel_launches;/* kernels launched by the last solve                      */
+  int32_t fine_operator;  /* A^ applied by the solve: 0 element-by-element, 1 BSR   */
 } hplmm_report;
 
 typedef struct hplmm_handle hplmm_handle;
@@ -209,8 +219,11 @@ typedef enum {
   HPLMM_OP_PROLONG = 7, /* out[n_dof] = P^ in, in has n_coarse entries          */
   HPLMM_OP_COARSE = 8,  /* out[N_m] = S^-1 in[N_m]: the coarse mortar-block solve  */
   HPLMM_OP_MILU = 9,    /* out = U^-1 L^-1 in: one ILU(0) apply (smoother = 1)     */
-  HPLMM_OP_ML = 10      /* out = M_L^-1 in: n_st stages of the base smoother
+  HPLMM_OP_ML = 10,     /* out = M_L^-1 in: n_st stages of the base smoother
                            (eq:local_smoother)                                   */
+  HPLMM_OP_SPMV_BSR = 11 /* out = A^ in from the stored BSR blocks, whatever
+                           operator_kind (HPLMM_OP_SPMV uses the solve's
+                           operator); for operator parity                      */
 } hplmm_op;
 
 /* One application of an operator (parity entry point).  in/out: host or

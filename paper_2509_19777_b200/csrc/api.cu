@@ -128,6 +128,12 @@ struct hplmm_handle {
   double *d_ls_u = nullptr, *d_ls_t0 = nullptr, *d_ls_t1 = nullptr, *d_ls_acc = nullptr;
   bool ilu_smoother() const { return hs.opt.smoother == 1; }
 
+  // element-by-element A^ (operator_kind = 0, own assembly only)
+  bool ebe = false, matrix_external = false;
+  int32_t* d_lat_ebe = nullptr;
+  double* d_Es = nullptr;
+  double K0h[576];
+
   size_t alloc_bytes = 0, alloc_peak = 0;
   template <class T>
   T* dalloc(size_t n, bool setup_only = false) {
@@ -435,7 +441,11 @@ void setup_ilu(hplmm_handle* h) {
 // operator applications (all on device vectors of length n_dof)
 // ---------------------------------------------------------------------------
 void op_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
-  launch_spmv(h->n_nodes, h->d_row_ptr, h->d_col, h->d_val, x, v, y, h->st, h->max_row_blocks);
+  if (h->ebe)
+    launch_ebe(h->n_nodes, h->d_ijk, h->d_dir, h->d_lat_ebe, h->d_Es, h->hs.nx, h->hs.ny,
+               h->hs.nz, h->K0h, x, v, y, h->st);
+  else
+    launch_spmv(h->n_nodes, h->d_row_ptr, h->d_col, h->d_val, x, v, y, h->st, h->max_row_blocks);
   h->launches++;
 }
 
@@ -608,6 +618,7 @@ void hplmm_default_options(hplmm_options* o) {
   o->coarse_solver = 0;
   o->mortar_kind = 0;
   o->smoother = 0;
+  o->operator_kind = 0;
 }
 
 const char* hplmm_last_error(void) { return g_last_error.c_str(); }
@@ -706,6 +717,7 @@ hplmm_status hplmm_set_matrix(hplmm_handle* h, const double* val, void* stream) 
     require_device(h);
     h->st = (cudaStream_t)stream;
     to_device(h, h->d_val, val, h->nnzb * 9);
+    h->matrix_external = true;   // A^ no longer the voxel assembly: stored blocks only
     CK(cudaStreamSynchronize(h->st));
     return HPLMM_OK;
   } catch (const HError& e) {
@@ -723,6 +735,27 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     HostSetup& hs = h->hs;
     const int G = hs.n_grains, C = hs.n_ifaces(), N = h->n_nodes;
     const int Nm = 3 * hs.n_mortar_nodes();
+
+    // ---------------- fine operator (operator_kind) ------------------------
+    {
+      const char* e = getenv("HPLMM_EBE");   // HPLMM_EBE=0: stored blocks (A/B)
+      h->ebe = hs.opt.operator_kind == 0 && !h->matrix_external && !(e && e[0] == '0');
+      h->rep.fine_operator = h->ebe ? 0 : 1;
+      if (h->ebe) {
+        const int64_t nvox = (int64_t)hs.nx * hs.ny * hs.nz;
+        std::vector<double> Es(nvox);
+        for (int64_t v = 0; v < nvox; ++v) Es[v] = hs.solid[v] ? hs.E[v] : 0.0;
+        std::vector<int32_t> lat(hs.lat_id.size());
+        for (size_t k = 0; k < lat.size(); ++k) {
+          const int32_t q = hs.lat_id[k];
+          lat[k] = (q < 0 || hs.dir[q]) ? -1 : q;
+        }
+        h->d_Es = h->upload(Es);
+        h->d_lat_ebe = h->upload(lat);
+        CK(cudaMemcpyAsync(h->K0h, h->d_K0, sizeof(h->K0h), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+      }
+    }
 
     // ---------------- host bookkeeping -----------------------------------
     std::vector<int32_t> node_local(N, -1);
@@ -1259,7 +1292,7 @@ hplmm_status hplmm_apply(hplmm_handle* h, int32_t op, const double* in, double* 
   try {
     require_device(h);
     h->st = (cudaStream_t)stream;
-    if (op == HPLMM_OP_SPMV) {
+    if (op == HPLMM_OP_SPMV || op == HPLMM_OP_SPMV_BSR) {
       if (!h->assembled) throw HError{HPLMM_ERR_STATE, "apply(SPMV) before assemble"};
     } else if (!h->setup_done) {
       throw HError{HPLMM_ERR_STATE, "apply before hplmm_setup"};
@@ -1270,7 +1303,7 @@ hplmm_status hplmm_apply(hplmm_handle* h, int32_t op, const double* in, double* 
     int nd = h->n_dof;
     double* din = h->d_in;
     double* dout = h->d_out;
-    if (op == HPLMM_OP_SPMV && !din) {  // before setup: temporary buffers
+    if ((op == HPLMM_OP_SPMV || op == HPLMM_OP_SPMV_BSR) && !din) {  // before setup: temporary buffers
       din = h->dalloc<double>(nd);
       dout = h->dalloc<double>(nd);
       h->d_in = din;
@@ -1299,6 +1332,11 @@ hplmm_status hplmm_apply(hplmm_handle* h, int32_t op, const double* in, double* 
       to_device(h, din, in, nin);
       switch (op) {
         case HPLMM_OP_SPMV: op_spmv(h, din, nullptr, dout); break;
+        case HPLMM_OP_SPMV_BSR:
+          launch_spmv(h->n_nodes, h->d_row_ptr, h->d_col, h->d_val, din, nullptr, dout, h->st,
+                      h->max_row_blocks);
+          h->launches++;
+          break;
         case HPLMM_OP_MG: op_mg(h, din, dout); break;
         case HPLMM_OP_MZETA: op_mzeta(h, din, dout); break;
         case HPLMM_OP_MGRAIN: op_mgrain(h, din, nullptr, nullptr, dout); break;

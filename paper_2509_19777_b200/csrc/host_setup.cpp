@@ -116,11 +116,12 @@ bool host_setup(const hplmm_problem* p, const hplmm_options* opt, HostSetup& hs,
   if (opt->n_mortar < 1 || opt->contact_h < 0 || opt->restart < 1 || opt->restart > 512 ||
       opt->max_iter < 1 || opt->n_st < 1 || opt->n_st > 64 || !(opt->beta > 0) ||
       (opt->smoother != 0 && opt->smoother != 1) ||
+      (opt->operator_kind != 0 && opt->operator_kind != 1) ||
       (opt->local_factor != 0 && opt->local_factor != 1) ||
       (opt->coarse_solver != 0 && opt->coarse_solver != 1) ||
       (opt->mortar_kind < 0 || opt->mortar_kind > 2)) {
     err = "hplmm_create: invalid options (n_mortar>=1, contact_h>=0, 1<=restart<=512, 1<=n_st<=64, "
-          "smoother/local_factor/coarse_solver in {0,1}, mortar_kind in {0,1,2})";
+          "smoother/local_factor/coarse_solver/operator_kind in {0,1}, mortar_kind in {0,1,2})";
     return false;
   }
   hs.opt = *opt;

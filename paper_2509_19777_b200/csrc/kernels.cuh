@@ -54,6 +54,12 @@ void launch_assemble_rhs(int n_nodes, const int32_t* drow_ptr, const int32_t* dc
 void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const double* val,
                  const double* x, const double* v, double* y, cudaStream_t st,
                  int max_row_blocks);
+// Element-by-element A^ (operator_kind = 0; same y = A^ x / y = v - A^ x as
+// launch_spmv).  lat: lattice point -> free node id, -1 for no node or a
+// Dirichlet node; Es: E per voxel, 0 where void; K0_host: 576 doubles (host)
+void launch_ebe(int n_nodes, const int32_t* node_ijk, const uint8_t* dir, const int32_t* lat,
+                const double* Es, int nx, int ny, int nz, const double* K0_host, const double* x,
+                const double* v, double* y, cudaStream_t st);
 void launch_mortar_weights(int n_iface_nodes, const int32_t* iface_of, const int32_t* iface_ptr,
                            const int32_t* iface_nodes, const int32_t* mortar_ptr,
                            const int32_t* mortar_nodes, const int64_t* wt_off,

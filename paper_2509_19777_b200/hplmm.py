@@ -21,7 +21,7 @@ OK, NOT_CONVERGED = 0, 1
 ERR_NAMES = {-1: "ERR_ARG", -2: "ERR_CUDA", -3: "ERR_OOM", -4: "ERR_SINGULAR_LOCAL",
              -5: "ERR_SINGULAR_COARSE", -6: "ERR_NONFINITE", -7: "ERR_STATE"}
 OP = dict(SPMV=0, MG=1, MZETA=2, MGRAIN=3, MCG=4, MINV=5, RESTRICT=6, PROLONG=7, COARSE=8,
-          MILU=9, ML=10)
+          MILU=9, ML=10, SPMV_BSR=11)
 ART = dict(NODE_KEY=0, ROW_PTR=1, COL_IDX=2, NODE_CLASS=3, NODE_IFACE=4, NODE_OWNER=5,
            IFACE_PTR=6, IFACE_NODES=7, CONTACT_PTR=8, CONTACT_NODES=9, MORTAR_PTR=10,
            MORTAR_NODES=11, GRAIN_COLS_PTR=12, GRAIN_COLS=13, VAL=14, RHS=15, S=16,
@@ -49,7 +49,7 @@ class Options(C.Structure):
                 ("restart", C.c_int32), ("max_iter", C.c_int32), ("n_st", C.c_int32),
                 ("coarse_refine", C.c_int32), ("local_factor", C.c_int32),
                 ("coarse_solver", C.c_int32), ("mortar_kind", C.c_int32),
-                ("smoother", C.c_int32)]
+                ("smoother", C.c_int32), ("operator_kind", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -62,7 +62,7 @@ class Report(C.Structure):
                 ("t_host_setup_s", C.c_double), ("t_assemble_s", C.c_double),
                 ("t_setup_local_s", C.c_double), ("t_setup_coarse_s", C.c_double),
                 ("t_rhs_s", C.c_double), ("t_solve_s", C.c_double),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("fine_operator", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -151,12 +151,15 @@ def default_options(**kw) -> Options:
     return o
 
 
+OPERATOR = {"ebe": 0, "bsr": 1}   # hplmm_options.operator_kind
+
+
 class Solver:
     """Handle over one voxel problem (a ``workloads.Problem``-like object)."""
 
     def __init__(self, prob, n_mortar=None, beta=None, contact_h=None, restart=None,
                  max_iter=None, coarse_refine=0, local_factor=None, coarse_solver=None,
-                 mortar=None, smoother=None, n_st=None):
+                 mortar=None, smoother=None, n_st=None, operator=None):
         lib = load()
         self._lib = lib
         self._keep = []
@@ -190,6 +193,8 @@ class Solver:
             o.smoother = SMOOTHER[smoother] if isinstance(smoother, str) else int(smoother)
         if n_st is not None:
             o.n_st = int(n_st)
+        if operator is not None:
+            o.operator_kind = OPERATOR[operator] if isinstance(operator, str) else int(operator)
         self.options = o
         h = C.c_void_p()
         _check(lib.hplmm_create(C.byref(p), C.byref(o), C.byref(h)))

@@ -89,6 +89,13 @@ def test_cfg3_spmv(cfg3):
     p, s, d, sv = cfg3
     v = np.random.default_rng(12345).standard_normal(s.n_dof)
     assert rel(sv.apply("SPMV", dev(v)).cpu().numpy(), s.A @ v) <= 1e-12
+    # the solve's element-by-element operator vs the stored blocks and the
+    # oracle's A^, row by row (summation order only)
+    scale = abs(s.A) @ np.abs(v)
+    ye = sv.apply("SPMV", dev(v)).cpu().numpy()
+    assert sv.report()["fine_operator"] == 0
+    assert np.all(np.abs(ye - sv.apply("SPMV_BSR", dev(v)).cpu().numpy()) <= 1e-13 * scale)
+    assert np.all(np.abs(ye - s.A @ v) <= 1e-13 * scale)
     b = sv.export("RHS")
     assert np.abs(b - s.b).max() <= 1e-13 * np.abs(s.b).max()
 
