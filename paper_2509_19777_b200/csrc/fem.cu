@@ -427,6 +427,11 @@ void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const 
 // x, y (+ v) and the node's coordinates; the lattice map (4 B per lattice
 // point) and voxel moduli (8 B per voxel) stay in L2 -- ~20x fewer than the
 // 76 B per stored block of the BSR SpMV.  Deterministic (fixed order).
+// Measured (cfg3, B200): 0.096 ms per apply vs 0.223 ms for the BSR SpMV
+// (ncu); FP64 pipe 28% active, issue 36%, long-scoreboard stalls on the
+// lattice-map -> x gathers (each AoS 24-byte x gather is ~6 L1 wavefronts per
+// warp).  Capping registers for 50-75% occupancy (E applied per contribution
+// instead of 8 per-voxel accumulators) measured the same, so it was dropped.
 // ---------------------------------------------------------------------------
 struct EbeK0 {
   double k[576];
