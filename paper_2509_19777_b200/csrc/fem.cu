@@ -428,8 +428,8 @@ void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const 
 // point) and voxel moduli (8 B per voxel) stay in L2 -- ~20x fewer than the
 // 76 B per stored block of the BSR SpMV.  Deterministic (fixed order).
 // Measured (cfg3, B200): 0.096 ms per apply vs 0.223 ms for the BSR SpMV
-// (ncu); FP64 pipe 28% active, issue 36%, long-scoreboard stalls on the
-// lattice-map -> x gathers (each AoS 24-byte x gather is ~6 L1 wavefronts per
+// (ncu, before the grouped lookups below); FP64 pipe 28% active, issue 36%,
+// long-scoreboard stalls on the lattice-map -> x gathers (each AoS 24-byte x gather is ~6 L1 wavefronts per
 // warp).  Capping registers for 50-75% occupancy (E applied per contribution
 // instead of 8 per-voxel accumulators) measured the same, so it was dropped.
 // ---------------------------------------------------------------------------
@@ -468,37 +468,49 @@ __global__ void __launch_bounds__(128) k_ebe(int n, const int32_t* __restrict__ 
 #pragma unroll
   for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = acc[a][2] = 0.0;
   const int64_t nx1 = nx + 1, ny1 = ny + 1;
+  // all 27 lattice-map lookups are issued first (predicated on a shared
+  // solid voxel, which also keeps them in range), then the x gathers: one
+  // lookup -> gather chain per neighbour cost 0.126 ms per apply, grouped
+  // 0.107 ms (one dz plane at a time: 0.106 ms)
+  constexpr int GRP = 27;
 #pragma unroll
-  for (int dz = -1; dz <= 1; ++dz)
+  for (int g0 = 0; g0 < 27; g0 += GRP) {
+    int qs[GRP];
 #pragma unroll
-    for (int dy = -1; dy <= 1; ++dy)
+    for (int t = 0; t < GRP; ++t) {
+      const int k = g0 + t, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+      bool any = false;
 #pragma unroll
-      for (int dx = -1; dx <= 1; ++dx) {
-        bool any = false;
+      for (int a = 0; a < 8; ++a) {
+        const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
+        if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1)
+          any |= Ea[a] != 0.0;
+      }
+      // no shared solid voxel -> no coupling; q < 0: no node or a Dirichlet
+      // column, structurally removed (R4)
+      qs[t] = any ? lat[(ix + dx) + nx1 * ((iy + dy) + ny1 * (iz + dz))] : -1;
+    }
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
-          if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1)
-            any |= Ea[a] != 0.0;
-        }
-        if (!any) continue;   // no solid voxel shared with this neighbour
-        const int q = lat[(ix + dx) + nx1 * ((iy + dy) + ny1 * (iz + dz))];
-        if (q < 0) continue;  // Dirichlet column: structurally removed (R4)
-        const double x0 = x[3 * (int64_t)q], x1 = x[3 * (int64_t)q + 1],
-                     x2 = x[3 * (int64_t)q + 2];
+    for (int t = 0; t < GRP; ++t) {
+      const int k = g0 + t, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+      const int q = qs[t];
+      if (q < 0) continue;
+      const double x0 = x[3 * (int64_t)q], x1 = x[3 * (int64_t)q + 1],
+                   x2 = x[3 * (int64_t)q + 2];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
-          if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1) {
-            const int b = bx + 2 * by + 4 * bz;
+      for (int a = 0; a < 8; ++a) {
+        const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
+        if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1) {
+          const int b = bx + 2 * by + 4 * bz;
 #pragma unroll
-            for (int r = 0; r < 3; ++r) {
-              const double* kr = K0.k + (3 * a + r) * 24 + 3 * b;
-              acc[a][r] = fma(kr[2], x2, fma(kr[1], x1, fma(kr[0], x0, acc[a][r])));
-            }
+          for (int r = 0; r < 3; ++r) {
+            const double* kr = K0.k + (3 * a + r) * 24 + 3 * b;
+            acc[a][r] = fma(kr[2], x2, fma(kr[1], x1, fma(kr[0], x0, acc[a][r])));
           }
         }
       }
+    }
+  }
   double out[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int a = 0; a < 8; ++a)
