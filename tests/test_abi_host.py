@@ -96,3 +96,42 @@ def test_mortar_placement_other_n_bit_exact(lib, n):
     ptr, nodes = _csr(m.nodes)
     assert np.array_equal(sv.export("MORTAR_PTR"), ptr)
     assert np.array_equal(sv.export("MORTAR_NODES"), nodes)
+
+
+def test_binding_struct_layout_matches_header(tmp_path):
+    """The ctypes structs of the binding have the C layout of include/hplmm.h
+    (size and every field offset, compiled with the system C compiler) and
+    the enums' values agree."""
+    import shutil
+    import subprocess
+    from paper_2509_19777_b200 import hplmm
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = {"hplmm_problem": hplmm.Problem, "hplmm_options": hplmm.Options,
+               "hplmm_report": hplmm.Report}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "hplmm.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    for op, v in hplmm.OP.items():
+        lines.append(f'printf("op {op} %d\\n", (int)HPLMM_OP_{op});')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {}
+    for ln in out:
+        if ln:
+            a, b, c = ln.split()
+            got[(a, b)] = int(c)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
+    for op, v in hplmm.OP.items():
+        assert got[("op", op)] == v, op
