@@ -432,6 +432,11 @@ void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const 
 // long-scoreboard stalls on the lattice-map -> x gathers (each AoS 24-byte x gather is ~6 L1 wavefronts per
 // warp).  Capping registers for 50-75% occupancy (E applied per contribution
 // instead of 8 per-voxel accumulators) measured the same, so it was dropped.
+// A lattice-tiled variant (CTA = 2 full x lines of one z plane; x of the
+// 3 x 4 x (nx+3) lattice halo and the voxel moduli staged in shared memory,
+// then every row computed from shared memory) measured 0.175 ms: the staging
+// phase does not overlap the compute at 3 CTAs per SM and a quarter of the
+// threads sit on padding / void lattice points.
 // ---------------------------------------------------------------------------
 struct EbeK0 {
   double k[576];
