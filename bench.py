@@ -378,7 +378,9 @@ def main():
                       + 8 * nxyz[0] * nxyz[1] * nxyz[2])
     else:     # stored BSR blocks: 72 B values + 4 B column per block, row pointers
         spmv_bytes = 76 * nnzb + 4 * rep0["n_nodes"] + 24 * n
-    pb = 12 * rep0["prolong_nnz"]
+    # P^ values only: the per-grain blocks are dense over their column sets,
+    # so no column indices stream (SURVEY §8(d)'s 12 B/entry assumes CSR)
+    pb = 8 * rep0["prolong_nnz"]
     if ilu:   # n_st ILU applies + their n_st - 1 stage residuals; y and w SpMVs
         per_iter_bytes = (n_st * alg[5] + alg[2] + (2 + n_st - 1) * spmv_bytes + 2 * pb
                           + (4 * 11 + 6) * 8 * n)
