@@ -209,7 +209,8 @@ hplmm_status hplmm_solve_many(hplmm_handle *h, int32_t nrhs, const double *B, do
                               double *X, hplmm_report *reports, void *stream);
 
 typedef enum {
-  HPLMM_OP_SPMV = 0,   /* out = A^ in                                           */
+  HPLMM_OP_SPMV = 0,   /* out = A^ in, by the solve's operator (operator_kind;
+                          before hplmm_setup: the stored blocks)               */
   HPLMM_OP_MG = 1,     /* out = M_G^-1 in        (needs set_rhs)                */
   HPLMM_OP_MZETA = 2,  /* out = M_zeta^-1 in     (eq:Mg_Mz)                      */
   HPLMM_OP_MGRAIN = 3, /* out = M_g^-1 in        (eq:Mg_Mz, R18)                 */
