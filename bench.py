@@ -322,6 +322,29 @@ def main():
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / k2
 
+    # SpMV HBM GB/s (the metric's third part): the solve's fine operator from
+    # the timed region (class 6, plain and residual forms mixed), and the
+    # stored-block BSR SpMV y = A^ x timed alone (class 7, 20 applies, CUDA
+    # events on the library stream around each launch)
+    fo_ms, fo_n, fo_bytes = sv.kernel_stats(6)
+    vd = torch.from_numpy(np.random.default_rng(5).standard_normal(sv.n_dof)).cuda()
+    od = torch.empty_like(vd)
+    for _ in range(3):
+        sv.apply("SPMV_BSR", vd, od)
+    sv.profile(True, True)
+    for _ in range(20):
+        sv.apply("SPMV_BSR", vd, od)
+    sv.profile(False, False)
+    bs_ms, bs_n, bs_bytes = sv.kernel_stats(7)
+    spmv = {"solve_operator": "element-by-element" if rep0.get("fine_operator", 1) == 0 else "bsr",
+            "solve_operator_ms_per_apply": (fo_ms / fo_n) if fo_n else None,
+            "solve_operator_applies_per_step": fo_n / args.steps,
+            "bsr_spmv_ms": (bs_ms / bs_n) if bs_n else None,
+            "bsr_spmv_algorithmic_bytes": bs_bytes,
+            "bsr_spmv_gbs": (bs_bytes / (bs_ms / bs_n / 1e3) / 1e9) if bs_n else None}
+    if rep0.get("fine_operator", 1) == 0 and fo_n:
+        spmv["solve_operator_algorithmic_bytes"] = fo_bytes
+
     t_s, e2e_s = reduce_max([ms / 1e3, e2e_s], dist)
 
     # algorithmic bytes per launch, per kernel class
@@ -428,6 +451,7 @@ def main():
                          "share_of_step": (tot_ms / args.steps) / (t_s * 1e3)}},
         "per_iteration": {"algorithmic_bytes": per_iter_bytes, "ms": t_s * 1e3 / max(iters, 1),
                           "roofline_frac": per_iter_frac},
+        "spmv": spmv,
         "gpu_launches": int(launches_per_step * args.steps),
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n},

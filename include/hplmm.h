@@ -272,7 +272,9 @@ hplmm_status hplmm_profile(hplmm_handle *h, int32_t enable, int32_t reset);
 
 /* Statistics of kernel class `kernel` (0 = grain SYMV tiles, 1 = contact-grid
  * SYMV tiles, 2 = coarse SYMV tiles, 3 = grain supernodal solve, 4 =
- * contact-grid supernodal solve, 5 = ILU(0) apply = forward + backward sweep):
+ * contact-grid supernodal solve, 5 = ILU(0) apply = forward + backward sweep,
+ * 6 = element-by-element fine operator, 7 = stored-block BSR SpMV; for 6 / 7
+ * tile_bytes = the algorithmic bytes of one y = A^ x apply):
  * total device ms and launch count since the last reset; tile_bytes = factor
  * bytes one launch streams. */
 hplmm_status hplmm_kernel_stats(hplmm_handle *h, int32_t kernel, double *total_ms,

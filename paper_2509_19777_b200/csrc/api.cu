@@ -47,7 +47,7 @@ struct HError {
 
 enum KernelClass {
   KC_SYMV_GRAIN = 0, KC_SYMV_CONTACT = 1, KC_SYMV_COARSE = 2, KC_SN_GRAIN = 3, KC_SN_CONTACT = 4,
-  KC_ILU = 5, KC_N = 6
+  KC_ILU = 5, KC_EBE = 6, KC_BSR = 7, KC_N = 8
 };
 
 }  // namespace
@@ -97,8 +97,8 @@ struct hplmm_handle {
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
-  double kc_ms[KC_N] = {0, 0, 0, 0, 0, 0};
-  int64_t kc_launches[KC_N] = {0, 0, 0, 0, 0, 0};
+  double kc_ms[KC_N] = {};
+  int64_t kc_launches[KC_N] = {};
 
   // coarse Cholesky (coarse_solver == 1)
   double *d_linv = nullptr, *d_linvT = nullptr, *d_zc = nullptr;
@@ -440,12 +440,38 @@ void setup_ilu(hplmm_handle* h) {
 // ---------------------------------------------------------------------------
 // operator applications (all on device vectors of length n_dof)
 // ---------------------------------------------------------------------------
+// y = A^ x (v null) or v - A^ x from the stored blocks; profiled as KC_BSR
+void bsr_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->profile) {
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, h->st));
+  }
+  launch_spmv(h->n_nodes, h->d_row_ptr, h->d_col, h->d_val, x, v, y, h->st, h->max_row_blocks);
+  if (h->profile) {
+    CK(cudaEventRecord(e1, h->st));
+    h->ev_pending.push_back({KC_BSR, {e0, e1}});
+  }
+}
+
 void op_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
-  if (h->ebe)
+  if (h->ebe) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->profile) {
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, h->st));
+    }
     launch_ebe(h->n_nodes, h->d_ijk, h->d_dir, h->d_lat_ebe, h->d_Es, h->hs.nx, h->hs.ny,
                h->hs.nz, h->K0h, x, v, y, h->st);
-  else
-    launch_spmv(h->n_nodes, h->d_row_ptr, h->d_col, h->d_val, x, v, y, h->st, h->max_row_blocks);
+    if (h->profile) {
+      CK(cudaEventRecord(e1, h->st));
+      h->ev_pending.push_back({KC_EBE, {e0, e1}});
+    }
+  } else {
+    bsr_spmv(h, x, v, y);
+  }
   h->launches++;
 }
 
@@ -1333,8 +1359,7 @@ hplmm_status hplmm_apply(hplmm_handle* h, int32_t op, const double* in, double* 
       switch (op) {
         case HPLMM_OP_SPMV: op_spmv(h, din, nullptr, dout); break;
         case HPLMM_OP_SPMV_BSR:
-          launch_spmv(h->n_nodes, h->d_row_ptr, h->d_col, h->d_val, din, nullptr, dout, h->st,
-                      h->max_row_blocks);
+          bsr_spmv(h, din, nullptr, dout);
           h->launches++;
           break;
         case HPLMM_OP_MG: op_mg(h, din, dout); break;
@@ -1626,6 +1651,18 @@ hplmm_status hplmm_kernel_stats(hplmm_handle* h, int32_t kernel, double* total_m
   if (!h || kernel < 0 || kernel >= KC_N) { g_last_error = "bad argument"; return HPLMM_ERR_ARG; }
   if (total_ms) *total_ms = h->kc_ms[kernel];
   if (launches) *launches = h->kc_launches[kernel];
+  if (kernel == KC_EBE) {   // y = A^ x form: x, y, node coords + flag, lattice map, moduli
+    const HostSetup& hs = h->hs;
+    if (tile_bytes)
+      *tile_bytes = 16 * (int64_t)h->n_dof + 13 * (int64_t)h->n_nodes +
+                    4 * (int64_t)(hs.nx + 1) * (hs.ny + 1) * (hs.nz + 1) +
+                    8 * (int64_t)hs.nx * hs.ny * hs.nz;
+    return HPLMM_OK;
+  }
+  if (kernel == KC_BSR) {   // y = A^ x form: 72 B values + 4 B column per block, row_ptr, x, y
+    if (tile_bytes) *tile_bytes = 76 * h->nnzb + 4 * (int64_t)h->n_nodes + 16 * (int64_t)h->n_dof;
+    return HPLMM_OK;
+  }
   if (kernel == KC_ILU) {   // every stored block once per apply (L in fwd, U + D in bwd)
     if (tile_bytes) *tile_bytes = h->ilu.val ? h->nnzb * 72 : 0;
     return HPLMM_OK;
