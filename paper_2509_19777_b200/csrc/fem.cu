@@ -436,7 +436,10 @@ void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const 
 // 3 x 4 x (nx+3) lattice halo and the voxel moduli staged in shared memory,
 // then every row computed from shared memory) measured 0.175 ms: the staging
 // phase does not overlap the compute at 3 CTAs per SM and a quarter of the
-// threads sit on padding / void lattice points.
+// threads sit on padding / void lattice points.  Gathering each x triple with two
+// 16-byte loads from the even DOF at or below 3q (instead of three 8-byte
+// loads) measured 0.126 vs 0.107 ms: the parity selects and the wider
+// requests cost more than the saved load instructions.
 // ---------------------------------------------------------------------------
 struct EbeK0 {
   double k[576];
