@@ -4,6 +4,7 @@ SURVEY §8(c) pins O4 (closed-form cfg1 decomposition), O5 (brute-force contact
 grids), O6 (brute-force global minimum of the Coulomb energy, eq:node_init),
 O7 (partition of unity, nu=1 reduction, two-node closed form; eq:gauss).
 """
+import functools
 import itertools
 import math
 
@@ -221,3 +222,73 @@ def test_algebraic_hplmm_projection_and_gmres():
     assert np.linalg.norm(h.apply_MG(s.A @ Pz) - Pz) <= 1e-10 * np.linalg.norm(Pz)
     x, it, hist, rr, conv = gmres.gmres(s.A, s.b, h.apply_M, tol=1e-8)
     assert conv and it < 60
+
+
+# ---- mortar placement sweeps (eq:node_init + the sweep of P:142; R10) -----
+def _pot_np(P, y, others):
+    """sum over the other mortar nodes of 1/||y - x|| (numpy, any order)."""
+    d = np.sqrt(((P[others] - P[y]) ** 2).sum(-1))
+    return float(np.sum(1.0 / d))
+
+
+def _fixpoint_violations(F, ijk, X):
+    """Nodes i of placement X for which some unchosen y in F lowers the
+    potential of the other mortar nodes by more than the R10 tie band."""
+    P = ijk.astype(np.float64)
+    bad = []
+    for i in range(len(X)):
+        others = np.array([x for t, x in enumerate(X) if t != i])
+        cur = _pot_np(P, X[i], others)
+        cand = np.array([y for y in F if y not in set(others.tolist())])
+        d = np.sqrt(((P[cand][:, None, :] - P[others][None, :, :]) ** 2).sum(-1))
+        best = (1.0 / d).sum(1).min()
+        if best < cur * (1.0 - 2e-12):
+            bad.append(i)
+    return bad
+
+
+@functools.lru_cache(maxsize=None)
+def _decomp(name):
+    from oracle import fem
+    from workloads import make_problem
+    p = make_problem(name)
+    s = fem.build_system(p)
+    return s, decomp.Decomposition(s, p.contact_h)
+
+
+@pytest.mark.parametrize("name", ["porous20", "cfg2"])
+def test_placement_n2_is_farthest_pair(name):
+    """n = 2: the sweep cannot improve on the farthest pair (R10 (ii)), so the
+    result is the brute-force farthest pair by integer d^2, lowest ids."""
+    s, d = _decomp(name)
+    ijk = s.mesh.node_ijk
+    for F in d.interfaces:
+        if F.size <= 2:
+            continue
+        P = ijk[F].astype(np.int64)
+        D2 = ((P[:, None, :] - P[None, :, :]) ** 2).sum(-1)
+        m = D2.max()
+        a, b = np.argwhere(np.triu(D2 == m, 1))[0]     # row-major: lowest (a, b)
+        assert mortar.place_mortars(F, ijk, 2) == [int(F[a]), int(F[b])]
+
+
+@pytest.mark.parametrize("name", ["porous20", "cfg2"])
+@pytest.mark.parametrize("n", [3, 4, 8])
+def test_placement_is_sweep_fixpoint(name, n):
+    """the sweeps stop when no mortar node moves -- i.e. the returned
+    placement is a fixpoint: no single-node move to an unchosen interface node
+    lowers that node's potential sum_{j != i} 1/||y - x_j|| (brute force, numpy,
+    independent summation).  The greedy start alone is NOT a fixpoint on a
+    number of these interfaces (checked below), so dropping the sweeps fails."""
+    s, d = _decomp(name)
+    ijk = s.mesh.node_ijk
+    moved = 0
+    for F in d.interfaces:
+        if F.size <= n:
+            continue
+        X = mortar.place_mortars(F, ijk, n)
+        assert len(set(X)) == n and set(X) <= set(map(int, F))
+        assert _fixpoint_violations(list(map(int, F)), ijk, X) == []
+        X0 = mortar.place_mortars(F, ijk, n, max_sweeps=0)
+        moved += X0 != X
+    assert moved > 0

@@ -116,3 +116,45 @@ def test_assemble_rows_matches_system(case):
         assert np.array_equal(cols, s.col_idx[lo:hi])
         assert np.abs(blocks - s.val[lo:hi]).max() <= 1e-14 * scale
         assert np.abs(bp - s.b[3 * p:3 * p + 3]).max() <= 1e-13 * max(1.0, np.abs(s.b).max())
+
+
+def _uniaxial_problem(E, nu, sigma, L=3, M=4):
+    """L x L x M solid box (x, y, z), uniform (E, nu); top face z = M loaded by
+    a normal traction sigma (consistent nodal loads: sigma/4 per corner of each
+    top voxel face); sides traction-free; the bottom face z = 0 prescribed to
+    the exact uniaxial-stress field u = (-nu sigma x / E, -nu sigma y / E, 0)."""
+    solid = np.ones((M, L, L), np.uint8)
+    lat = (M + 1, L + 1, L + 1)
+    k, j, i = np.meshgrid(np.arange(M + 1), np.arange(L + 1), np.arange(L + 1), indexing="ij")
+    X = np.stack([i, j, k], -1).astype(float)
+    u_exact = np.stack([-nu * sigma * X[..., 0] / E, -nu * sigma * X[..., 1] / E,
+                        sigma * X[..., 2] / E], -1)
+    node_u = u_exact.copy()
+    node_u[..., 2] = np.where(k == 0, 0.0, node_u[..., 2])
+    f = np.zeros(lat + (3,))
+    for vj in range(L):
+        for vi in range(L):
+            for dy in (0, 1):
+                for dx in (0, 1):
+                    f[M, vj + dy, vi + dx, 2] += sigma / 4.0
+    p = Problem(name="uniaxial", nx=L, ny=L, nz=M, solid=solid, E=np.full((M, L, L), E),
+                nu=nu, grain=np.zeros((M, L, L), np.int32), n_grains=1,
+                node_dirichlet=(k == 0).astype(np.uint8), node_u=node_u, node_f=f, block=L)
+    return p, u_exact
+
+
+@pytest.mark.parametrize("E,nu", [(1.0, 0.3), (2.5, 0.25), (0.7, 0.45)])
+def test_uniaxial_stress_closed_form(E, nu):
+    """Pins (E, nu) -> (lambda, mu) (eq:stiff_iso P:69-71, reading R2) without
+    calling the oracle's own formula: under a uniform top traction sigma with
+    free sides, linear elasticity has the exact linear solution
+    eps_zz = sigma/E, eps_xx = eps_yy = -nu sigma/E (Hooke's law for uniaxial
+    stress, any textbook), which Q1 reproduces exactly.  The FEM solution must
+    equal it to 1e-12.  Any other (lambda, mu) pair -- e.g. plane-stress lambda
+    or mu = E/(1+nu) -- changes both strains."""
+    sigma = 0.3
+    p, u = _uniaxial_problem(E, nu, sigma)
+    s = fem.build_system(p)
+    x = spla.spsolve(s.A.tocsc(), s.b)
+    ue = u.reshape(-1, 3)[s.mesh.node_key].ravel()
+    assert np.abs(x - ue).max() <= 1e-12 * np.abs(ue).max()
