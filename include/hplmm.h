@@ -123,6 +123,25 @@ typedef struct {
                                 after hplmm_set_matrix the stored blocks are
                                 used);
                             1 = the stored BSR blocks (TMA-streamed SpMV)    */
+  int32_t sn_shape;      /* launch shape of the supernodal local solves
+                            (local_factor = 1): 0 = automatic (8 consumer warps
+                            x 2 CTAs per SM when a batch has >= 2 subdomains per
+                            CTA, else 16 x 1; default), 8 = force 8 x 2, 16 =
+                            force 16 x 1 (a shape the subdomains do not fit
+                            falls back to automatic).  Same operator A_s^-1;
+                            only the summation order of the group reductions
+                            differs (parity tests run both shapes)          */
+  int32_t host_loop;     /* how hplmm_solve drives GMRES (R22):
+                            0 = device-resident (default): the whole solve --
+                                every Arnoldi step, Givens update, stop test and
+                                restart cycle -- is one CUDA-graph launch (two
+                                nested WHILE conditional nodes) and one host
+                                synchronisation; used with smoother = 0 and
+                                coarse_solver = 0 while profiling is off (else
+                                the host loop runs);
+                            1 = host-driven loop: one pinned D2H of the
+                                Hessenberg column and one synchronisation per
+                                Arnoldi step, Givens on the host            */
 } hplmm_options;
 
 typedef struct {
@@ -152,9 +171,30 @@ typedef struct {
   double t_solve_s;       /* GMRES (T_sol)                                          */
   int64_t kernel_launches;/* kernels launched by the last solve                      */
   int32_t fine_operator;  /* A^ applied by the solve: 0 element-by-element, 1 BSR   */
+  int32_t sn_shape_grain;   /* consumer warps per CTA of the grain / contact-grid    */
+  int32_t sn_shape_contact; /* supernodal solves in use (8: 8 x 2 CTAs/SM, 16: 16 x 1;
+                               0 = not built)                                      */
 } hplmm_report;
 
 typedef struct hplmm_handle hplmm_handle;
+
+/* The fine matrix A^ of eq:ls_all in 3x3-block CSR (BSR), node-major
+ * DOFs 3 p + c (R3).  Every array is HOST or DEVICE memory (classified per
+ * pointer) and borrowed for the call.
+ *   row_ptr  int32[n_nodes + 1]  block-row offsets, row_ptr[0] = 0
+ *   col_idx  int32[nnzb]         block columns, strictly ascending in a row
+ *   val      double[9 nnzb]      each block row-major (entry (a, b) of block e at
+ *                                val[9 e + 3 a + b])
+ *   node_ijk int32[3 n_nodes]    lattice coordinates (i, j, k) of node p, or NULL
+ *                                (then the R3 numbering is assumed)           */
+typedef struct {
+  int32_t n_nodes;
+  int64_t nnzb;
+  const int32_t *row_ptr;
+  const int32_t *col_idx;
+  const double *val;
+  const int32_t *node_ijk;
+} hplmm_bsr;
 
 /* Default options: n=4, beta=4, h=1, restart=50, max_iter=300, n_st=1,
  * coarse_refine=0. */
@@ -164,13 +204,39 @@ void hplmm_default_options(hplmm_options *opt);
  * mesh numbering (R3), BSR pattern with Dirichlet couplings removed (R4),
  * node classes (R6), interfaces (R7), grain-interior sets (R18), contact grids
  * (R8), mortar placement (eq:node_init, R10), shape-vector column sets (R14).
- * Copies everything it needs from `prob`. */
+ * Copies everything it needs from `prob`.  opt = NULL: the defaults. */
 hplmm_status hplmm_create(const hplmm_problem *prob, const hplmm_options *opt,
                           hplmm_handle **out);
 
 /* GPU assembly of A^ values and b^ (R2, R4) into handle-owned device
  * memory.  Selects device `device` for the handle (cudaSetDevice). */
 hplmm_status hplmm_assemble(hplmm_handle *h, int32_t device, void *stream);
+
+/* hplmm_setup(A in 3x3-block CSR, subdomain partition, material and BC data)
+ * of the north star, in one call: the problem A^ x^ = b^ (eq:ls_all)
+ * on the voxel geometry `geom` (grain labels per voxel = the subdomain partition
+ * of §3.1; Dirichlet flags = the BC data of eq:BC P:53-61; E, nu only
+ * for mortar_kind = 2, which builds its interface operators from them) with
+ * the CALLER's matrix A.  Runs hplmm_create (integer setup from geom),
+ * checks that A's node numbering (node_ijk, if given) and block pattern are
+ * the ones the geometry defines (R3: nodes in lattice-key order; R4:
+ * Dirichlet couplings removed, identity-pattern Dirichlet rows) -- the
+ * decomposition (R6-R8, R14) is defined on that pattern --, binds `device`,
+ * uploads A's values and runs hplmm_setup with them.  The solve then applies
+ * the stored blocks (operator_kind 1).  A must be SPD on the non-Dirichlet
+ * DOFs (SINGULAR_LOCAL / SINGULAR_COARSE otherwise).  On success *out is a
+ * handle ready for hplmm_solve / hplmm_apply; on error *out = NULL and nothing
+ * is leaked.  ERR_ARG names the first mismatching row / node. */
+hplmm_status hplmm_setup_bsr(const hplmm_bsr *A, const hplmm_problem *geom,
+                             const hplmm_options *opt, int32_t device, void *stream,
+                             hplmm_handle **out);
+
+/* The library's own assembly of A^ and b^ (R2-R4) returned to the
+ * host: *A (and its arrays) and *b (n_dof doubles) are allocated by the
+ * library and released with hplmm_free_bsr.  Runs on `device`. */
+hplmm_status hplmm_assemble_bsr(const hplmm_problem *prob, int32_t device, hplmm_bsr **A,
+                                double **b);
+void hplmm_free_bsr(hplmm_bsr *A, double *b);
 
 /* Replace the values of A^ (nnzb*9 doubles, row-major 3x3 blocks in the
  * handle's pattern, host or device) -- used to parity-test later stages on an
@@ -264,10 +330,12 @@ hplmm_status hplmm_export(hplmm_handle *h, int32_t artifact, void *buf, int64_t 
 /* Sizes / timings gathered so far. */
 hplmm_status hplmm_get_report(hplmm_handle *h, hplmm_report *report);
 
-/* Profiling of the dominant kernel (the packed symmetric tile product that
- * applies every local and coarse inverse): when enabled, CUDA events are
- * recorded around each launch on the launch stream.  reset != 0 clears the
- * accumulated statistics. */
+/* Profiling of the dominant kernels (supernodal local solves, packed SYMV tiles
+ * of the local / coarse inverses, ILU(0) sweeps, fine operator; classes as in
+ * hplmm_kernel_stats): when enabled, CUDA events are recorded around each such
+ * launch on the launch stream (this adds event records to the timed path --
+ * keep it off for headline timings).  reset != 0 clears the accumulated
+ * statistics. */
 hplmm_status hplmm_profile(hplmm_handle *h, int32_t enable, int32_t reset);
 
 /* Statistics of kernel class `kernel` (0 = grain SYMV tiles, 1 = contact-grid

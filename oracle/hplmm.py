@@ -29,6 +29,8 @@ additive overlap sum, ascending interface id), R21 (M_G first; M_zeta first).
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 import scipy.linalg as sla
 import scipy.sparse as sp
@@ -63,6 +65,8 @@ class HPLMM:
             raise ValueError("smoother must be 'cg' or 'ilu0' and n_st >= 1")
         self.smoother, self.n_st = smoother, int(n_st)
         self.sys = system
+        self.timings = {}      # wall seconds of the setup phases (bench's cpu baseline)
+        t0 = time.perf_counter()
         A = system.A
         self.A = A
         n_dof = system.n_dof
@@ -88,6 +92,7 @@ class HPLMM:
         self.Qo = sp.csc_matrix((np.concatenate(v), (np.concatenate(r), np.concatenate(c))),
                                 shape=(n_dof, Nm)) if r else sp.csc_matrix((n_dof, Nm))
 
+        t1 = time.perf_counter()
         # grain-interior DOF sets and their factors (eq:permute_blk_2, R18)
         self.grain_dofs = [node_dofs(nodes) for nodes in dec.grain_nodes]
         self.grain_solve = [_Local(A, d) for d in self.grain_dofs]
@@ -99,6 +104,7 @@ class HPLMM:
         self.ilu = (ILU0(block_pattern_csr(system.row_ptr, system.col_idx, system.val,
                                            mesh.n_nodes))
                     if smoother == "ilu0" else None)
+        t2 = time.perf_counter()
 
         # cols_g (R14 option B, structural): every mortar column of an interface
         # that has a node coupled (a block of A^) to a class-G node of grain g.
@@ -127,20 +133,44 @@ class HPLMM:
             Rg = (A[dg] @ self.Qo[:, cg]).toarray()
             Bg = -self.grain_solve[g].solve(Rg)
             self.B.append(Bg)
-            rows.append(np.repeat(dg, cg.size))
-            cols.append(np.tile(cg, dg.size))
+            rows.append(np.repeat(dg.astype(np.int32), cg.size))     # int32: cfg3 has
+            cols.append(np.tile(cg.astype(np.int32), dg.size))       # 0.25 G entries
             vals.append(Bg.ravel())
-        PB = sp.csc_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
-                           shape=(n_dof, Nm)) if rows else sp.csc_matrix((n_dof, Nm))
+        if rows:
+            rows, cols, vals = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+            PB = sp.csc_matrix((vals, (rows, cols)), shape=(n_dof, Nm))
+            del rows, cols, vals
+        else:
+            PB = sp.csc_matrix((n_dof, Nm))
         self.PB = (self.Qo + PB).tocsc()
-        self.PBT = self.PB.T.tocsr()
+        del PB
+        self.PBT = self.PB.T          # CSR view of the same arrays
 
-        # coarse mortar block S = P_B^T A^ P_B (eq:mg_struct, R16), symmetrised
-        # from its lower triangle; dense Cholesky (R17)
-        S = (self.PBT @ (A @ self.PB)).toarray()
-        self.S = np.tril(S) + np.tril(S, -1).T
+        # coarse mortar block S = P_B^T A^ P_B (eq:mg_struct, R16), formed a
+        # block of columns of P_B at a time (the sparse intermediate A^ P_B of
+        # the whole P_B is ~10 GB at cfg3), symmetrised from its lower
+        # triangle; dense Cholesky (R17)
+        S = np.zeros((Nm, Nm))
+        for j0 in range(0, Nm, 2048):
+            J = slice(j0, min(Nm, j0 + 2048))
+            S[:, J] = (self.PBT @ (A @ self.PB[:, J])).toarray()
+        # S = tril(S) + tril(S, -1)^T, block by block in place: S[I, J] = S[J, I]^T, I < J
+        for i0 in range(0, Nm, 2048):
+            I = slice(i0, min(Nm, i0 + 2048))
+            for j0 in range(i0, Nm, 2048):
+                J = slice(j0, min(Nm, j0 + 2048))
+                if j0 == i0:
+                    blk = S[I, J]
+                    S[I, J] = np.tril(blk) + np.tril(blk, -1).T
+                else:
+                    S[I, J] = S[J, I].T
+        self.S = S
         self.S_chol = sla.cho_factor(self.S, lower=True) if Nm else None
         self.corr = []          # set by set_rhs
+        t3 = time.perf_counter()
+        # T_ML-like: local (grain + contact-grid) factorisations; T_MG-like:
+        # decomposition, mortars, Q^o, shape vectors, S and its factor
+        self.timings = {"T_ML": t2 - t1, "T_MG": (t1 - t0) + (t3 - t2)}
 
     # ------------------------------------------------------------------
     def set_rhs(self, b: np.ndarray):

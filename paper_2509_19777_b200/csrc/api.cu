@@ -90,6 +90,18 @@ struct hplmm_handle {
   double *d_V = nullptr, *d_partial = nullptr, *d_hbuf = nullptr;
   double* h_hh = nullptr;   // pinned host copy of the Arnoldi step's dots
   int hh_cap = 0;
+
+  // device-resident solve: one CUDA graph per handle (two nested WHILE
+  // conditional nodes: restart cycles around Arnoldi steps), gmres.cu
+  cudaGraph_t solve_graph = nullptr;
+  cudaGraphExec_t solve_exec = nullptr;
+  cudaStream_t cap_st = nullptr;
+  GmresDev gdev{};
+  GmresScalars* h_gs = nullptr;   // pinned host mirror of the solve's scalars
+  double* h_ghist = nullptr;      // pinned host copy of the history
+  double *d_vj = nullptr, *d_w = nullptr;
+  int64_t graph_launches_pre = 0, graph_launches_cycle = 0, graph_launches_step = 0;
+  bool graph_failed = false;
   int64_t ldv = 0;
   int Vcap = 0;
 
@@ -172,6 +184,11 @@ struct hplmm_handle {
       for (void* p : allocs) cudaFree(p);
       free_setup();
       if (h_hh) cudaFreeHost(h_hh);
+      if (h_gs) cudaFreeHost(h_gs);
+      if (h_ghist) cudaFreeHost(h_ghist);
+      if (solve_exec) cudaGraphExecDestroy(solve_exec);
+      if (solve_graph) cudaGraphDestroy(solve_graph);
+      if (cap_st) cudaStreamDestroy(cap_st);
       for (auto e : ev_pool) cudaEventDestroy(e);
       for (auto& e : ev_pending) {
         cudaEventDestroy(e.second.first);
@@ -366,6 +383,15 @@ void from_device(hplmm_handle* h, double* dst, const double* src, int64_t n) {
                      is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
 }
 
+// copy `n` elements of a host-or-device array to a host vector
+template <class T>
+std::vector<T> host_copy(const T* p, int64_t n) {
+  std::vector<T> v((size_t)n);
+  if (n == 0) return v;
+  if (is_device_ptr(p)) CK(cudaMemcpy(v.data(), p, (size_t)n * sizeof(T), cudaMemcpyDeviceToHost));
+  else std::memcpy(v.data(), p, (size_t)n * sizeof(T));
+  return v;
+}
 void require_device(hplmm_handle* h) {
   if (h->device < 0) throw HError{HPLMM_ERR_STATE, "no device bound: call hplmm_assemble first"};
   CK(cudaSetDevice(h->device));
@@ -626,6 +652,136 @@ void do_set_rhs(hplmm_handle* h, const double* b_dev) {
   h->rep.t_rhs_s = t.stop();
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident solve (R22 on the GPU, gmres.cu).  The graph is
+//   WHILE (outer: restart cycles) {
+//     cycle init: g = beta e1, V0 = r / beta
+//     WHILE (inner: Arnoldi steps) {
+//       u = M^-1 v_j ; w = A^ u ; CGS2 (j read on the device) ; Givens,
+//       history, stop test ; v_{j+1} = w / ||w||
+//     }
+//     y = H^-1 g ; x += M^-1 (V y) ; r = b - A^ x ; restart test
+//   }
+// captured once per handle on a private stream (every pointer is a handle
+// buffer), launched once per solve.  Used when the kernels of a step take no
+// per-call host state: M_CG smoother (ILU(0) sweeps carry a host ticket base)
+// and the explicit coarse inverse (the Cholesky sweeps carry a host epoch);
+// profiling (CUDA events around kernels) also selects the host loop.
+bool graph_eligible(hplmm_handle* h) {
+  static const bool off = [] {
+    const char* e = getenv("HPLMM_GRAPH");
+    return e && e[0] == '0';
+  }();
+  return !off && !h->hs.opt.host_loop && !h->graph_failed && !h->profile && !h->ilu_smoother() &&
+         !h->chol();
+}
+
+void build_solve_graph(hplmm_handle* h) {
+  const int n = h->n_dof;
+  const int m = h->hs.opt.restart;
+  const int maxit = h->hs.opt.max_iter;
+  if (!h->d_vj) {
+    h->d_vj = h->dalloc<double>((size_t)h->ldv);
+    h->d_w = h->dalloc<double>((size_t)h->ldv);
+    // scalars | H (m+1) x m | g m+1 | cs m | sn m | y m | hist maxit
+    const size_t nd = (size_t)(m + 1) * m + (m + 1) + 3 * (size_t)m + maxit;
+    char* base = h->dalloc<char>(256 + nd * 8);
+    GmresDev& d = h->gdev;
+    d.s = (GmresScalars*)base;
+    double* p = (double*)(base + 256);
+    d.H = p; p += (size_t)(m + 1) * m;
+    d.g = p; p += m + 1;
+    d.cs = p; p += m;
+    d.sn = p; p += m;
+    d.y = p; p += m;
+    d.hist = p;
+    d.hb = h->d_hbuf;
+    d.beta2 = h->d_hbuf + 2 * (m + 1);
+    CK(cudaMallocHost(&h->h_gs, sizeof(GmresScalars)));
+    CK(cudaMallocHost(&h->h_ghist, (size_t)maxit * 8));
+  }
+  if (!h->cap_st) CK(cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking));
+  const GmresDev& d = h->gdev;
+  cudaGraph_t G = nullptr;
+  CK(cudaGraphCreate(&G, 0));
+  cudaStream_t user = h->st;
+  const int64_t launches0 = h->launches;
+  try {
+    cudaGraphConditionalHandle outer, inner;
+    CK(cudaGraphConditionalHandleCreate(&outer, G, 1, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&inner, G, 1, 0));
+    cudaGraphNodeParams po{};
+    po.type = cudaGraphNodeTypeConditional;
+    po.conditional.handle = outer;
+    po.conditional.type = cudaGraphCondTypeWhile;
+    po.conditional.size = 1;
+    cudaGraphNode_t n_outer;
+    CK(cudaGraphAddNode(&n_outer, G, nullptr, 0, &po));
+    cudaGraph_t body1 = po.conditional.phGraph_out[0];
+    cudaStream_t cs = h->cap_st;
+    h->st = cs;
+    double* V = h->d_V;
+    // (1) cycle start, captured into the outer body
+    CK(cudaStreamBeginCaptureToGraph(cs, body1, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    launch_gmres_cycle_init(d, inner, n, h->d_r1, V, h->d_vj, cs);
+    cudaStreamCaptureStatus cst;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    CK(cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps));
+    std::vector<cudaGraphNode_t> dv(deps, deps + ndeps);
+    cudaGraph_t tmp;
+    CK(cudaStreamEndCapture(cs, &tmp));
+    // (2) the Arnoldi step loop
+    cudaGraphNodeParams pi{};
+    pi.type = cudaGraphNodeTypeConditional;
+    pi.conditional.handle = inner;
+    pi.conditional.type = cudaGraphCondTypeWhile;
+    pi.conditional.size = 1;
+    cudaGraphNode_t n_inner;
+    CK(cudaGraphAddNode(&n_inner, body1, dv.data(), dv.size(), &pi));
+    cudaGraph_t body2 = pi.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(cs, body2, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const int64_t l_step0 = h->launches;
+    op_minv(h, h->d_vj, h->d_u);
+    op_spmv(h, h->d_u, nullptr, h->d_w);
+    launch_multidot(n, m, V, h->ldv, h->d_w, h->d_partial, h->d_hbuf, cs, &d.s->j);
+    launch_update(n, m, V, h->ldv, h->d_hbuf, h->d_w, nullptr, nullptr, cs, &d.s->j);
+    launch_multidot(n, m, V, h->ldv, h->d_w, h->d_partial, h->d_hbuf + (m + 1), cs, &d.s->j);
+    launch_update(n, m, V, h->ldv, h->d_hbuf + (m + 1), h->d_w, h->d_partial, d.beta2, cs, &d.s->j);
+    launch_gmres_step_end(d, inner, n, h->d_w, V, h->ldv, h->d_vj, cs);
+    h->launches += 9;
+    h->graph_launches_step = h->launches - l_step0;
+    CK(cudaStreamEndCapture(cs, &tmp));
+    // (3) cycle end, captured into the outer body after the step loop
+    CK(cudaStreamBeginCaptureToGraph(cs, body1, &n_inner, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+    const int64_t l_cyc0 = h->launches;
+    launch_gmres_combine(d, n, V, h->ldv, h->d_in, cs);
+    op_minv(h, h->d_in, h->d_u);
+    launch_axpy(n, 1.0, h->d_u, h->d_x, cs);
+    op_spmv(h, h->d_x, h->d_bb, h->d_r1);   // r = b - A^ x
+    launch_norm2(n, h->d_r1, h->d_partial, d.beta2, cs);
+    launch_gmres_cycle_end(d, outer, cs);
+    h->launches += 7;
+    h->graph_launches_cycle = h->launches - l_cyc0 + 2;   // + the cycle start
+    CK(cudaStreamEndCapture(cs, &tmp));
+    h->st = user;
+    CK(cudaGraphInstantiate(&h->solve_exec, G, 0));
+    h->solve_graph = G;
+  } catch (...) {
+    h->st = user;
+    cudaStreamCaptureStatus cst;
+    if (cudaStreamIsCapturing(h->cap_st, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+      cudaGraph_t junk;
+      cudaStreamEndCapture(h->cap_st, &junk);
+    }
+    cudaGetLastError();
+    cudaGraphDestroy(G);
+    h->launches = launches0;
+    throw;
+  }
+  h->launches = launches0;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -645,6 +801,8 @@ void hplmm_default_options(hplmm_options* o) {
   o->mortar_kind = 0;
   o->smoother = 0;
   o->operator_kind = 0;
+  o->sn_shape = 0;
+  o->host_loop = 0;
 }
 
 const char* hplmm_last_error(void) { return g_last_error.c_str(); }
@@ -653,6 +811,11 @@ hplmm_status hplmm_create(const hplmm_problem* prob, const hplmm_options* opt,
                           hplmm_handle** out) {
   if (!out) { g_last_error = "hplmm_create: out is NULL"; return HPLMM_ERR_ARG; }
   *out = nullptr;
+  hplmm_options dflt;
+  if (!opt) {   // NULL options = the defaults
+    hplmm_default_options(&dflt);
+    opt = &dflt;
+  }
   auto t0 = std::chrono::steady_clock::now();
   hplmm_handle* h = new hplmm_handle();
   std::string err;
@@ -749,6 +912,124 @@ hplmm_status hplmm_set_matrix(hplmm_handle* h, const double* val, void* stream) 
   } catch (const HError& e) {
     return fail(e);
   }
+}
+
+hplmm_status hplmm_setup_bsr(const hplmm_bsr* A, const hplmm_problem* geom,
+                             const hplmm_options* opt, int32_t device, void* stream,
+                             hplmm_handle** out) {
+  if (!out) { g_last_error = "hplmm_setup_bsr: out is NULL"; return HPLMM_ERR_ARG; }
+  *out = nullptr;
+  if (!A || !geom || !A->row_ptr || !A->col_idx || !A->val || A->n_nodes <= 0 || A->nnzb <= 0) {
+    g_last_error = "hplmm_setup_bsr: null matrix / geometry or empty matrix";
+    return HPLMM_ERR_ARG;
+  }
+  hplmm_handle* h = nullptr;
+  hplmm_status s = hplmm_create(geom, opt, &h);
+  if (s != HPLMM_OK) return s;
+  try {
+    const HostSetup& hs = h->hs;
+    if (A->n_nodes != h->n_nodes)
+      throw HError{HPLMM_ERR_ARG, "hplmm_setup_bsr: A has " + std::to_string(A->n_nodes) +
+                                      " block rows, the geometry defines " +
+                                      std::to_string(h->n_nodes) + " nodes (R3)"};
+    if (A->nnzb != h->nnzb)
+      throw HError{HPLMM_ERR_ARG, "hplmm_setup_bsr: A has " + std::to_string(A->nnzb) +
+                                      " blocks, the geometry's pattern (R4) has " +
+                                      std::to_string(h->nnzb)};
+    if (A->node_ijk) {
+      const std::vector<int32_t> ijk = host_copy(A->node_ijk, 3 * (int64_t)A->n_nodes);
+      for (int p = 0; p < h->n_nodes; ++p)
+        for (int c = 0; c < 3; ++c)
+          if (ijk[3 * p + c] != hs.node_ijk[3 * p + c])
+            throw HError{HPLMM_ERR_ARG, "hplmm_setup_bsr: node " + std::to_string(p) +
+                                            " is not the geometry's node in lattice-key order (R3)"};
+    }
+    const std::vector<int32_t> rp = host_copy(A->row_ptr, (int64_t)A->n_nodes + 1);
+    const std::vector<int32_t> ci = host_copy(A->col_idx, A->nnzb);
+    for (int p = 0; p <= h->n_nodes; ++p)
+      if (rp[p] != hs.row_ptr[p])
+        throw HError{HPLMM_ERR_ARG, "hplmm_setup_bsr: row_ptr differs from the geometry's pattern "
+                                    "at block row " + std::to_string(p > 0 ? p - 1 : 0) + " (R4)"};
+    for (int p = 0; p < h->n_nodes; ++p)
+      for (int e = rp[p]; e < rp[p + 1]; ++e)
+        if (ci[e] != hs.col_idx[e])
+          throw HError{HPLMM_ERR_ARG, "hplmm_setup_bsr: col_idx differs from the geometry's "
+                                      "pattern in block row " + std::to_string(p) + " (R4)"};
+  } catch (const HError& e) {
+    delete h;
+    return fail(e);
+  }
+  if ((s = hplmm_assemble(h, device, stream)) != HPLMM_OK ||
+      (s = hplmm_set_matrix(h, A->val, stream)) != HPLMM_OK ||
+      (s = hplmm_setup(h, stream)) != HPLMM_OK) {
+    const std::string msg = g_last_error;
+    delete h;
+    g_last_error = msg;
+    return s;
+  }
+  *out = h;
+  return HPLMM_OK;
+}
+
+hplmm_status hplmm_assemble_bsr(const hplmm_problem* prob, int32_t device, hplmm_bsr** A,
+                                double** b) {
+  if (!A || !b) { g_last_error = "hplmm_assemble_bsr: null output"; return HPLMM_ERR_ARG; }
+  *A = nullptr;
+  *b = nullptr;
+  hplmm_handle* h = nullptr;
+  hplmm_status s = hplmm_create(prob, nullptr, &h);
+  if (s != HPLMM_OK) return s;
+  if ((s = hplmm_assemble(h, device, nullptr)) != HPLMM_OK) {
+    const std::string msg = g_last_error;
+    delete h;
+    g_last_error = msg;
+    return s;
+  }
+  hplmm_bsr* M = (hplmm_bsr*)std::calloc(1, sizeof(hplmm_bsr));
+  const int n = h->n_nodes;
+  const int64_t nb = h->nnzb;
+  int32_t* rp = (int32_t*)std::malloc((size_t)(n + 1) * 4);
+  int32_t* ci = (int32_t*)std::malloc((size_t)nb * 4);
+  int32_t* ijk = (int32_t*)std::malloc((size_t)n * 12);
+  double* val = (double*)std::malloc((size_t)nb * 72);
+  double* bb = (double*)std::malloc((size_t)n * 24);
+  if (!M || !rp || !ci || !ijk || !val || !bb) {
+    std::free(M); std::free(rp); std::free(ci); std::free(ijk); std::free(val); std::free(bb);
+    delete h;
+    g_last_error = "hplmm_assemble_bsr: host allocation failed";
+    return HPLMM_ERR_OOM;
+  }
+  std::memcpy(rp, h->hs.row_ptr.data(), (size_t)(n + 1) * 4);
+  std::memcpy(ci, h->hs.col_idx.data(), (size_t)nb * 4);
+  std::memcpy(ijk, h->hs.node_ijk.data(), (size_t)n * 12);
+  cudaError_t e1 = cudaMemcpy(val, h->d_val, (size_t)nb * 72, cudaMemcpyDeviceToHost);
+  cudaError_t e2 = cudaMemcpy(bb, h->d_b, (size_t)n * 24, cudaMemcpyDeviceToHost);
+  delete h;
+  M->n_nodes = n;
+  M->nnzb = nb;
+  M->row_ptr = rp;
+  M->col_idx = ci;
+  M->val = val;
+  M->node_ijk = ijk;
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    hplmm_free_bsr(M, bb);
+    g_last_error = "hplmm_assemble_bsr: device-to-host copy failed";
+    return HPLMM_ERR_CUDA;
+  }
+  *A = M;
+  *b = bb;
+  return HPLMM_OK;
+}
+
+void hplmm_free_bsr(hplmm_bsr* A, double* b) {
+  if (A) {
+    std::free((void*)A->row_ptr);
+    std::free((void*)A->col_idx);
+    std::free((void*)A->val);
+    std::free((void*)A->node_ijk);
+    std::free(A);
+  }
+  std::free(b);
 }
 
 hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
@@ -974,14 +1255,17 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
       };
       double t0 = wall();
-      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, sn_leaf(), h->sg.sym, err, h->nsm) ||
-          (!ilu &&
-           !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, sn_leaf(), h->sc.sym, err, h->nsm)))
+      const int shape = hs.opt.sn_shape;
+      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, sn_leaf(), h->sg.sym, err, h->nsm, shape) ||
+          (!ilu && !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, sn_leaf(), h->sc.sym, err,
+                               h->nsm, shape)))
         throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
       double t1 = wall();
       try {
         sn_upload(h->sg, halloc, h->st, h->nsm);
         if (!ilu) sn_upload(h->sc, halloc, h->st, h->nsm);
+        h->rep.sn_shape_grain = h->sg.work.cons;
+        h->rep.sn_shape_contact = ilu ? 0 : h->sc.work.cons;
         double t2 = wall();
         sn_factor(h->sg, h->d_val, halloc, h->st, kSnPoolBytes);
         double t3 = wall();
@@ -1443,6 +1727,38 @@ hplmm_status hplmm_solve(hplmm_handle* h, const double* b, double tol, double* x
       do_set_rhs(h, dB);   // correction columns for this RHS (R15)
       // r = b (x0 = 0)
       CK(cudaMemcpyAsync(h->d_r1, dB, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+      bool graph = graph_eligible(h);
+      if (graph && !h->solve_exec) {
+        try {
+          build_solve_graph(h);
+        } catch (const HError& e) {
+          h->graph_failed = true;   // fall back to the host-driven loop below
+          graph = false;
+          if (getenv("HPLMM_DEBUG")) fprintf(stderr, "hplmm: solve graph unavailable: %s\n", e.msg.c_str());
+        }
+      }
+      if (graph) {
+        GmresScalars& s0 = *h->h_gs;
+        s0 = GmresScalars{};
+        s0.m = m;
+        s0.maxit = maxit;
+        s0.bnorm = bnorm;
+        s0.tol = tol;
+        CK(cudaMemcpyAsync(h->gdev.s, &s0, sizeof(GmresScalars), cudaMemcpyHostToDevice, st));
+        CK(cudaGraphLaunch(h->solve_exec, st));
+        CK(cudaMemcpyAsync(h->h_gs, h->gdev.s, sizeof(GmresScalars), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h->h_ghist, h->gdev.hist, (size_t)maxit * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const GmresScalars& s1 = *h->h_gs;
+        if (s1.nonfinite) throw HError{HPLMM_ERR_NONFINITE, "non-finite GMRES residual"};
+        total = s1.total;
+        conv = s1.converged != 0;
+        relres = s1.relres;
+        hl = total;
+        if (hist)
+          for (int i = 0; i < std::min(total, hist_cap); ++i) hist[i] = h->h_ghist[i];
+        h->launches += h->graph_launches_cycle * s1.cycles + h->graph_launches_step * total;
+      }
       std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1);
       // the per-step Hessenberg column comes back through pinned memory
       if (h->hh_cap < 2 * (m + 1) + 1) {
@@ -1452,7 +1768,7 @@ hplmm_status hplmm_solve(hplmm_handle* h, const double* b, double tol, double* x
       }
       double* hh = h->h_hh;
       double beta2 = bn2;
-      while (true) {
+      while (!graph) {
         double beta = std::sqrt(beta2);
         // V0 = r / beta
         double* V = h->d_V;

@@ -192,11 +192,13 @@ void launch_sum_contact(int n_dof, const int32_t* cptr, const int32_t* cidx, con
 // ---- Krylov (krylov.cu) ----------------------------------------------------
 int krylov_blocks(int64_t n);
 // partial[b*m + j] = sum over block b of V[j][i] * w[i], j < m; final[j] = sum_b
+// cnt (optional, device): vector count = *cnt + 1 read by the kernels (m = its maximum)
 void launch_multidot(int64_t n, int m, const double* V, int64_t ldv, const double* w,
-                     double* partial, double* out, cudaStream_t st);
+                     double* partial, double* out, cudaStream_t st, const int* cnt = nullptr);
 // w -= sum_j V[j] h[j]; optional: partial norm^2 of the updated w -> out_norm2
 void launch_update(int64_t n, int m, const double* V, int64_t ldv, const double* h, double* w,
-                   double* partial, double* out_norm2, cudaStream_t st);
+                   double* partial, double* out_norm2, cudaStream_t st,
+                   const int* cnt = nullptr);
 void launch_norm2(int64_t n, const double* x, double* partial, double* out, cudaStream_t st);
 void launch_scale(int64_t n, const double* x, const double* s_dev, int invert, double* y,
                   cudaStream_t st);
@@ -204,6 +206,39 @@ void launch_scale(int64_t n, const double* x, const double* s_dev, int invert, d
 void launch_combine_basis(int64_t n, int m, const double* V, int64_t ldv, const double* y,
                           double* x, cudaStream_t st);
 void launch_axpy(int64_t n, double a, const double* x, double* y, cudaStream_t st);
+
+// ---- device-resident GMRES cycle (gmres.cu; graph-captured, R22) ------------
+// Scalars of one solve, in device memory next to the small dense arrays.
+struct GmresScalars {
+  int j;           // Arnoldi step within the cycle (vectors V[0..j] exist)
+  int total;       // Arnoldi steps of the solve
+  int k;           // steps of the current cycle when it stopped
+  int stop_inner;  // the cycle's step loop has ended
+  int done;        // the solve has ended (converged, cap, or non-finite)
+  int converged;
+  int nonfinite;
+  int m, maxit;
+  int cycles;      // restart cycles started
+  double bnorm, tol, relres;
+};
+struct GmresDev {
+  GmresScalars* s;
+  double *H, *g, *cs, *sn, *y, *hist;   // (m+1) x m (row-major, ld m), m+1, m, m, m, maxit
+  const double* hb;                     // CGS2 dots: [0, m] pass 1, [m+1, 2m+1] pass 2, [2m+2] ||w||^2
+  double* beta2;                        // ||r||^2 slot (= hb + 2(m+1))
+};
+// cycle start: g = beta e_1, j = 0, step loop on; V[0] = r / beta, vj = V[0]
+void launch_gmres_cycle_init(const GmresDev& d, unsigned long long inner, int64_t n, const double* r,
+                             double* V, double* vj, cudaStream_t st);
+// after CGS2 of step j: Givens update of H(:, j), g; history; stop test; then
+// V[j+1] = w / ||w|| and vj = V[j+1] unless the step loop stops
+void launch_gmres_step_end(const GmresDev& d, unsigned long long inner, int64_t n, const double* w,
+                           double* V, int64_t ldv, double* vj, cudaStream_t st);
+// cycle end, part 1: y = H(0:k, 0:k)^-1 g, out = sum_{j<k} V[j] y[j]
+void launch_gmres_combine(const GmresDev& d, int64_t n, const double* V, int64_t ldv, double* out,
+                          cudaStream_t st);
+// cycle end, part 2: relres from beta2; done / converged / non-finite; loop flag
+void launch_gmres_cycle_end(const GmresDev& d, unsigned long long outer, cudaStream_t st);
 
 // ---- ILU(0) base smoother (ilu.cu) -----------------------------------------
 // Block ILU(0) factor of A^ in its own BSR layout (row_ptr/col of A^):

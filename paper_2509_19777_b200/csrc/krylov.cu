@@ -45,10 +45,16 @@ __device__ __forceinline__ void pair_range(int64_t n, int64_t& i0, int64_t& i1) 
   i1 = min(n, i0 + chunk);
 }
 
+// cnt: if non-null, the vector count is *cnt + 1 (the Arnoldi step index j
+// read on the device, for the graph-captured GMRES cycle) instead of m
+__device__ __forceinline__ int vec_count(int m, const int* cnt) { return cnt ? *cnt + 1 : m; }
+
 __global__ void __launch_bounds__(KT) k_multidot(int64_t n, int m, const double* __restrict__ V,
                                                  int64_t ldv, const double* __restrict__ w,
-                                                 double* __restrict__ partial) {
+                                                 double* __restrict__ partial,
+                                                 const int* __restrict__ cnt) {
   __shared__ double red[MD_J][KT / 32];
+  m = vec_count(m, cnt);
   const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t i0, i1;
   pair_range(n, i0, i1);
@@ -95,7 +101,8 @@ __global__ void __launch_bounds__(KT) k_multidot(int64_t n, int m, const double*
 // out[j] = sum_b partial[b*m + j]: one warp per j, fixed lane assignment and
 // fixed butterfly (deterministic)
 __global__ void k_final_sum(int nb, int m, const double* __restrict__ partial,
-                            double* __restrict__ out) {
+                            double* __restrict__ out, const int* __restrict__ cnt = nullptr) {
+  m = vec_count(m, cnt);
   int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (j >= m) return;
@@ -107,19 +114,23 @@ __global__ void k_final_sum(int nb, int m, const double* __restrict__ partial,
 }
 
 void launch_multidot(int64_t n, int m, const double* V, int64_t ldv, const double* w,
-                     double* partial, double* out, cudaStream_t st) {
+                     double* partial, double* out, cudaStream_t st, const int* cnt) {
+  // with a device count, m is the largest count (grid of the final sums) and
+  // partial holds nb x (count) entries laid out with the device count
   int nb = krylov_blocks(n);
-  k_multidot<<<nb, KT, 0, st>>>(n, m, V, ldv, w, partial);
-  k_final_sum<<<(m + 3) / 4, 128, 0, st>>>(nb, m, partial, out);
+  k_multidot<<<nb, KT, 0, st>>>(n, m, V, ldv, w, partial, cnt);
+  k_final_sum<<<(m + 3) / 4, 128, 0, st>>>(nb, m, partial, out, cnt);
 }
 
 // w -= sum_j V[j] h[j]   (+ partial ||w||^2 per block); per element the
 // j-order of the update is fixed; two elements per thread (128-bit loads)
 __global__ void __launch_bounds__(KT) k_update(int64_t n, int m, const double* __restrict__ V,
                                                int64_t ldv, const double* __restrict__ h,
-                                               double* __restrict__ w, double* __restrict__ partial) {
+                                               double* __restrict__ w, double* __restrict__ partial,
+                                               const int* __restrict__ cnt) {
   __shared__ double hs[513];
   __shared__ double red[KT / 32];
+  m = vec_count(m, cnt);
   for (int j = threadIdx.x; j < m; j += KT) hs[j] = h[j];
   __syncthreads();
   int64_t i0, i1;
@@ -165,9 +176,9 @@ __global__ void __launch_bounds__(KT) k_update(int64_t n, int m, const double* _
 }
 
 void launch_update(int64_t n, int m, const double* V, int64_t ldv, const double* h, double* w,
-                   double* partial, double* out_norm2, cudaStream_t st) {
+                   double* partial, double* out_norm2, cudaStream_t st, const int* cnt) {
   int nb = krylov_blocks(n);
-  k_update<<<nb, KT, 0, st>>>(n, m, V, ldv, h, w, out_norm2 ? partial : nullptr);
+  k_update<<<nb, KT, 0, st>>>(n, m, V, ldv, h, w, out_norm2 ? partial : nullptr, cnt);
   if (out_norm2) k_final_sum<<<1, 32, 0, st>>>(nb, 1, partial, out_norm2);
 }
 

@@ -82,11 +82,12 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   }
   wk.cons = force_cons ? force_cons
                        : sn_solve_cfg((int)isub.size(), nblocks, s.max_n, s.max_r, nrhs,
-                                      s.chunk_doubles);
+                                      s.chunk_doubles, s.shape);
   if (wk.cons == 0)
     throw SnError{-1, "subdomain of " + std::to_string(s.max_n) +
                           " DOFs does not fit the supernodal solve's shared memory"};
   nblocks *= wk.cons == 16 ? 1 : 2;
+  if (const char* e = getenv("HPLMM_SN_CTAS")) nblocks = std::max(1, atoi(e));   // experiments
   nblocks = std::max(1, std::min<int>(nblocks, (int)isub.size()));
   std::vector<int32_t> ptr, ids;
   lpt(wgt, nblocks, ptr, ids);

@@ -3,6 +3,7 @@
 // applies every grain / contact-grid inverse in the hot path (eq:Mg_Mz).
 // See supernodal.h for the algebra and the layout.
 #include <algorithm>
+#include <vector>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -30,6 +31,13 @@ namespace hplmm {
 // has read it; the producer runs ahead across supernode and item boundaries.
 // ===========================================================================
 constexpr int SN_MAXST = 16;
+// per-CTA start / end %globaltimer of the last launch (flags & 16; experiments)
+__device__ unsigned long long g_sn_cta_t[2 * 4096];
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 // per-warp phase timing of k_sn_solve (printf for a few CTAs when flags & 2);
 // compiled out unless built with -DHPLMM_SN_PROF=1
 #ifndef HPLMM_SN_PROF
@@ -215,6 +223,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     if (prof) t_sync += clock64() - ts_;               \
   } while (0)
   const SnChunk* __restrict__ ch = wk.chunks;
+  if ((flags & 16) && threadIdx.x == 0 && blockIdx.x < 4096) g_sn_cta_t[2 * blockIdx.x] = globaltimer();
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
@@ -224,7 +233,14 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
   }
   __syncthreads();
   if (warp == SN_CONS) {
-    // producer warp: lanes prefetch 32 chunk descriptors, lane 0 issues
+    // producer warp: lanes prefetch 32 chunk descriptors, lane 0 issues the
+    // ring loads; the chunk PD ahead of the one being loaded is prefetched
+    // into L2 by its own lane (a bulk L2 prefetch), so that a ring slot, once
+    // released, refills from L2 instead of waiting a DRAM latency.  PD = 2
+    // (flags bit 12 set: PD = (flags >> 8) & 15, 0 = off).  Measured at cfg3
+    // (contact / grain solve): no prefetch 1.94 / 1.32 ms, PD = 1 1.81 / 1.24,
+    // PD = 2 1.82 / 1.24, 4 1.82 / 1.25, 6 1.84 / 1.26
+    const int pd = (flags & 0x1000) ? ((flags >> 8) & 15) : 1;
     const uint64_t pol = policy_evict_first();
     int s = 0;
     uint32_t ph = 0;
@@ -237,9 +253,11 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
         bytes = ch[kb + lane].bytes & 0xffffff;
       }
       const int cnt = (int)min((int64_t)32, k1 - kb);
+      if (kb > k0 && lane < pd && lane < cnt) bulk_prefetch_l2(d.factor + off, (uint32_t)bytes);
       for (int j = 0; j < cnt; ++j, ++k) {
         const int64_t o = __shfl_sync(0xffffffffu, off, j);
         const int b = __shfl_sync(0xffffffffu, bytes, j);
+        if (pd > 0 && lane == j + pd && lane < cnt) bulk_prefetch_l2(d.factor + off, (uint32_t)bytes);
         if (lane == 0) {
           if (k >= stages) {
             const long long tw = prof ? clock64() : 0;
@@ -482,6 +500,10 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       PSYNC();
     }
   }
+  if (flags & 16) {
+    cons_sync<SN_NT>();
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_sn_cta_t[2 * blockIdx.x + 1] = globaltimer();
+  }
   if (prof && lane == 0)
     printf("sn_prof cta %d warp %d: total %lld full-wait %lld sync %lld | Wf %lld/%lld Ff %lld/%lld "
            "Wb %lld/%lld Rf %lld/%lld Rb %lld/%lld\n", blockIdx.x, warp, clock64() - t_start,
@@ -500,16 +522,18 @@ static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int nt) {
 
 // Launch shape of the solve: 16 consumer warps x 1 CTA per SM, or 8 x 2 (two
 // independent item streams per SM; better latency hiding when there are at
-// least two items per CTA).  cfg: 0 = automatic from the item count,
-// HPLMM_SN_CFG=16|8 forces one.
+// least two items per CTA).  shape: 0 = automatic from the item count
+// (HPLMM_SN_CFG=16|8 forces one for experiments), 8 / 16 = the handle's
+// hplmm_options.sn_shape (falls back to automatic when it does not fit).
 int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons);
 
-int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk) {
-  static int forced = -1;
-  if (forced < 0) {
+int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk, int shape) {
+  static int env_forced = -1;
+  if (env_forced < 0) {
     const char* e = getenv("HPLMM_SN_CFG");
-    forced = e ? atoi(e) : 0;
+    env_forced = e ? atoi(e) : 0;
   }
+  const int forced = shape ? shape : env_forced;
   // the group-reduction scratch (8 x 32 x cons x nrhs doubles) must fit one stage
   const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8) >= 2 && chunk >= 8 * 256 * nrhs;
   const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16) >= 2 && chunk >= 8 * 512 * nrhs;
@@ -529,14 +553,14 @@ static int cfg_cps(int cons) { return cons == 16 ? 1 : 2; }
 // two CTAs) streams 64 KiB (else 48 KiB) chunks -- half the per-chunk
 // overhead for its 16 consumer warps (cfg5 grain / contact solves -13% / -8%).
 // HPLMM_SN_CHUNK overrides.
-int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r) {
+int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape) {
   if (getenv("HPLMM_SN_CHUNK")) return sn_chunk_doubles();
   const int base = sn_chunk_doubles();
-  if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base) == 8) return base;
+  if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base, shape) == 8) return base;
   // enough subdomains for 8 x 2 but x_S leaves no room for two 32-KiB stages:
   // smaller chunks keep the 8 x 2 shape (far cheaper per byte than 16 x 1)
   for (int c : {3072, 2048})
-    if (c < base && sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c) == 8) return c;
+    if (c < base && sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape) == 8) return c;
   for (int c : {SN_CHUNK_DOUBLES_MAX, 6144})
     if (c > base && sn_solve_stages(max_n, max_r, 1, c, 16) >= 2) return c;
   return base;
@@ -565,6 +589,24 @@ static void sn_solve_launch(const SnDev& d, const SnIO& io, const SnWork& wk, in
   }
   k_sn_solve<NRHS, CONS, CPS><<<wk.nblocks, 32 * (CONS + 1), smem, st>>>(d, io, wk, stages, chunk,
                                                                           max_n, max_r, flags);
+  if ((flags & 16) && wk.nblocks <= 4096) {   // experiment: per-CTA finish-time quantiles
+    static unsigned long long h[2 * 4096];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_sn_cta_t, sizeof(unsigned long long) * 2 * wk.nblocks);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    std::vector<double> end(wk.nblocks), dur(wk.nblocks);
+    for (int b = 0; b < wk.nblocks; ++b) { t0 = std::min(t0, h[2 * b]); t1 = std::max(t1, h[2 * b + 1]); }
+    for (int b = 0; b < wk.nblocks; ++b) {
+      end[b] = (h[2 * b + 1] - t0) * 1e-3;
+      dur[b] = (h[2 * b + 1] - h[2 * b]) * 1e-3;
+    }
+    std::sort(end.begin(), end.end());
+    std::sort(dur.begin(), dur.end());
+    auto q = [&](const std::vector<double>& v, double f) { return v[(size_t)(f * (v.size() - 1))]; };
+    fprintf(stderr, "sn_solve ctas %d span %.1f us | end q10 %.1f q50 %.1f q90 %.1f max %.1f | dur q10 %.1f q50 %.1f q90 %.1f max %.1f\n",
+            wk.nblocks, (t1 - t0) * 1e-3, q(end, .1), q(end, .5), q(end, .9), end.back(), q(dur, .1),
+            q(dur, .5), q(dur, .9), dur.back());
+  }
 }
 
 template <int CONS, int CPS>

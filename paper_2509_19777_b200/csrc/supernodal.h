@@ -65,6 +65,7 @@ struct SnSymbolic {
   int nsub = 0, nsn = 0;
   int max_n = 0, max_w = 0, max_r = 0, n_levels = 0, max_children = 0;
   int chunk_doubles = 0;                   // TMA chunk (stage) size of the schedule
+  int shape = 0;                           // launch shape asked for (0 auto, 8, 16)
   // per subdomain
   std::vector<int32_t> sub_n;              // DOFs
   std::vector<int64_t> sub_base;           // offset of its local positions
@@ -96,7 +97,9 @@ struct SnSymbolic {
 // launch shape, sn_pick_chunk)
 bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
                 const std::vector<int32_t>& nodes, int leaf, SnSymbolic& out, std::string& err,
-                int nsm = 148);
-int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r);
+                int nsm = 148, int shape = 0);
+// shape: 0 = automatic, 8 = 8 consumer warps x 2 CTAs per SM, 16 = 16 x 1
+int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape = 0);
+int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk, int shape = 0);
 
 }  // namespace hplmm

@@ -196,7 +196,7 @@ int sn_chunk_doubles() {
 }
 
 bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
-                const std::vector<int32_t>& nodes, int leaf, SnSymbolic& o, std::string& err, int nsm) {
+                const std::vector<int32_t>& nodes, int leaf, SnSymbolic& o, std::string& err, int nsm, int shape) {
   const int nsub = (int)ptr.size() - 1;
   std::vector<SubResult> res(std::max(nsub, 0));
   unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
@@ -333,7 +333,8 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
   for (int s = 0; s < nsub; ++s) o.max_n = std::max(o.max_n, o.sub_n[s]);
   const int64_t foff = o_f[nsub];
   o.factor_doubles = foff;
-  o.chunk_doubles = sn_pick_chunk(nsub, nsm, o.max_n, o.max_r);
+  o.shape = shape;
+  o.chunk_doubles = sn_pick_chunk(nsub, nsm, o.max_n, o.max_r, shape);
   const double t2 = now();
   // TMA chunk schedule: forward = (W_S, rows, F_SS^-1) per S in postorder,
   // backward = (rows, W_S) per S in reverse postorder; W/F chunks are whole

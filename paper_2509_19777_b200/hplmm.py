@@ -32,7 +32,7 @@ SMOOTHER = dict(cg=0, ilu0=1)
 
 EXPORTED = ["hplmm_default_options", "hplmm_create", "hplmm_assemble", "hplmm_set_matrix",
             "hplmm_setup", "hplmm_set_rhs", "hplmm_solve", "hplmm_solve_many", "hplmm_apply",
-            "hplmm_export",
+            "hplmm_export", "hplmm_setup_bsr", "hplmm_assemble_bsr", "hplmm_free_bsr",
             "hplmm_get_report", "hplmm_profile", "hplmm_kernel_stats", "hplmm_destroy",
             "hplmm_last_error"]
 
@@ -49,7 +49,13 @@ class Options(C.Structure):
                 ("restart", C.c_int32), ("max_iter", C.c_int32), ("n_st", C.c_int32),
                 ("coarse_refine", C.c_int32), ("local_factor", C.c_int32),
                 ("coarse_solver", C.c_int32), ("mortar_kind", C.c_int32),
-                ("smoother", C.c_int32), ("operator_kind", C.c_int32)]
+                ("smoother", C.c_int32), ("operator_kind", C.c_int32),
+                ("sn_shape", C.c_int32), ("host_loop", C.c_int32)]
+
+
+class Bsr(C.Structure):
+    _fields_ = [("n_nodes", C.c_int32), ("nnzb", C.c_int64), ("row_ptr", C.c_void_p),
+                ("col_idx", C.c_void_p), ("val", C.c_void_p), ("node_ijk", C.c_void_p)]
 
 
 class Report(C.Structure):
@@ -62,7 +68,8 @@ class Report(C.Structure):
                 ("t_host_setup_s", C.c_double), ("t_assemble_s", C.c_double),
                 ("t_setup_local_s", C.c_double), ("t_setup_coarse_s", C.c_double),
                 ("t_rhs_s", C.c_double), ("t_solve_s", C.c_double),
-                ("kernel_launches", C.c_int64), ("fine_operator", C.c_int32)]
+                ("kernel_launches", C.c_int64), ("fine_operator", C.c_int32),
+                ("sn_shape_grain", C.c_int32), ("sn_shape_contact", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -92,6 +99,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hplmm_solve_many": (C.c_int, [vp, i32, vp, dbl, vp, vp, vp]),
         "hplmm_apply": (C.c_int, [vp, i32, vp, vp, vp]),
         "hplmm_export": (C.c_int, [vp, i32, vp, C.c_int64, vp]),
+        "hplmm_setup_bsr": (C.c_int, [vp, vp, vp, i32, vp, vp]),
+        "hplmm_assemble_bsr": (C.c_int, [vp, i32, vp, vp]),
+        "hplmm_free_bsr": (None, [vp, vp]),
         "hplmm_get_report": (C.c_int, [vp, vp]),
         "hplmm_profile": (C.c_int, [vp, i32, i32]),
         "hplmm_kernel_stats": (C.c_int, [vp, i32, vp, vp, vp]),
@@ -154,26 +164,56 @@ def default_options(**kw) -> Options:
 OPERATOR = {"ebe": 0, "bsr": 1}   # hplmm_options.operator_kind
 
 
+def _problem(prob):
+    """(hplmm_problem, keepalive arrays) of a ``workloads.Problem``-like object."""
+    arr = lambda a, dt: np.ascontiguousarray(a, dtype=dt)
+    solid = arr(prob.solid, np.uint8)
+    E = arr(prob.E, np.float64)
+    grain = arr(prob.grain, np.int32)
+    ndir = arr(prob.node_dirichlet, np.uint8)
+    nu_ = arr(prob.node_u, np.float64)
+    nf = arr(prob.node_f, np.float64)
+    p = Problem(prob.nx, prob.ny, prob.nz, solid.ctypes.data, E.ctypes.data, float(prob.nu),
+                grain.ctypes.data, int(prob.n_grains), ndir.ctypes.data, nu_.ctypes.data,
+                nf.ctypes.data)
+    return p, [solid, E, grain, ndir, nu_, nf]
+
+
+def assemble_bsr(prob, device: int = 0):
+    """hplmm_assemble_bsr: the library's A^ (row_ptr, col_idx, val (nnzb,3,3),
+    node_ijk (n,3)) and b^ as host NumPy copies."""
+    lib = load()
+    p, keep = _problem(prob)
+    A = C.POINTER(Bsr)()
+    b = C.POINTER(C.c_double)()
+    _check(lib.hplmm_assemble_bsr(C.byref(p), device, C.byref(A), C.byref(b)))
+    try:
+        a = A.contents
+        n, nb = a.n_nodes, a.nnzb
+        cp = lambda ptr, ct, cnt: np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), (cnt,)).copy()
+        out = dict(row_ptr=cp(a.row_ptr, C.c_int32, n + 1), col_idx=cp(a.col_idx, C.c_int32, nb),
+                   val=cp(a.val, C.c_double, 9 * nb).reshape(nb, 3, 3),
+                   node_ijk=cp(a.node_ijk, C.c_int32, 3 * n).reshape(n, 3),
+                   b=np.ctypeslib.as_array(b, (3 * n,)).copy())
+    finally:
+        lib.hplmm_free_bsr(A, b)
+    return out
+
+
 class Solver:
     """Handle over one voxel problem (a ``workloads.Problem``-like object)."""
 
     def __init__(self, prob, n_mortar=None, beta=None, contact_h=None, restart=None,
                  max_iter=None, coarse_refine=0, local_factor=None, coarse_solver=None,
-                 mortar=None, smoother=None, n_st=None, operator=None):
+                 mortar=None, smoother=None, n_st=None, operator=None, sn_shape=None,
+                 host_loop=None, bsr=None, device=0, stream=None):
+        """bsr: optional dict(row_ptr, col_idx, val, node_ijk=None) -- the
+        caller's matrix A^ (host NumPy or torch CUDA arrays): the handle is
+        then built by hplmm_setup_bsr (create + pattern check + assemble +
+        values + setup, on `device`) and is ready to solve."""
         lib = load()
         self._lib = lib
-        self._keep = []
-        arr = lambda a, dt: np.ascontiguousarray(a, dtype=dt)
-        solid = arr(prob.solid, np.uint8)
-        E = arr(prob.E, np.float64)
-        grain = arr(prob.grain, np.int32)
-        ndir = arr(prob.node_dirichlet, np.uint8)
-        nu_ = arr(prob.node_u, np.float64)
-        nf = arr(prob.node_f, np.float64)
-        self._keep += [solid, E, grain, ndir, nu_, nf]
-        p = Problem(prob.nx, prob.ny, prob.nz, solid.ctypes.data, E.ctypes.data, float(prob.nu),
-                    grain.ctypes.data, int(prob.n_grains), ndir.ctypes.data, nu_.ctypes.data,
-                    nf.ctypes.data)
+        p, self._keep = _problem(prob)
         o = default_options()
         for k, v in dict(n_mortar=n_mortar if n_mortar is not None else getattr(prob, "n_mortar", None),
                          beta=beta if beta is not None else getattr(prob, "beta", None),
@@ -195,9 +235,24 @@ class Solver:
             o.n_st = int(n_st)
         if operator is not None:
             o.operator_kind = OPERATOR[operator] if isinstance(operator, str) else int(operator)
+        if sn_shape is not None:
+            o.sn_shape = int(sn_shape)
+        if host_loop is not None:
+            o.host_loop = int(host_loop)
         self.options = o
         h = C.c_void_p()
-        _check(lib.hplmm_create(C.byref(p), C.byref(o), C.byref(h)))
+        if bsr is None:
+            _check(lib.hplmm_create(C.byref(p), C.byref(o), C.byref(h)))
+        else:
+            dt = dict(row_ptr=np.int32, col_idx=np.int32, val=np.float64, node_ijk=np.int32)
+            conv = {k: (np.ascontiguousarray(bsr[k], dtype=t)
+                        if isinstance(bsr.get(k), np.ndarray) else bsr.get(k)) for k, t in dt.items()}
+            ptrs = {k: _ptr(v) for k, v in conv.items()}
+            n = int(conv["row_ptr"].shape[0]) - 1
+            A = Bsr(n, int(conv["col_idx"].shape[0]), ptrs["row_ptr"][0], ptrs["col_idx"][0],
+                    ptrs["val"][0], ptrs["node_ijk"][0])
+            _check(lib.hplmm_setup_bsr(C.byref(A), C.byref(p), C.byref(o), int(device),
+                                       _stream(stream), C.byref(h)))
         self._h = h
         self._keep = []
         r = self.report()

@@ -109,7 +109,7 @@ def test_binding_struct_layout_matches_header(tmp_path):
     if cc is None:
         pytest.skip("no C compiler")
     structs = {"hplmm_problem": hplmm.Problem, "hplmm_options": hplmm.Options,
-               "hplmm_report": hplmm.Report}
+               "hplmm_report": hplmm.Report, "hplmm_bsr": hplmm.Bsr}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "hplmm.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')

@@ -122,6 +122,26 @@ def test_cfg3_grain_smoother_sampled(cfg3):
         assert rel(out[dofs], ref) <= tol, (g, rel(out[dofs], ref), tol)
 
 
+def test_cfg3_contact_smoother_full(cfg3):
+    """M_zeta^-1 v in full at cfg3 -- the contact batch, the largest launch of
+    the bench step, in its bench launch shape (8 warps x 2 CTAs per SM): all
+    contact grids solved by SuperLU on the oracle's A^[zeta_c, zeta_c] and
+    summed in ascending interface order (eq:Mg_Mz, R8, R19)."""
+    import scipy.sparse.linalg as spla
+    from oracle.decomp import node_dofs
+    p, s, d, sv = cfg3
+    assert sv.report()["sn_shape_contact"] == 8
+    A = s.A.tocsr()
+    v = np.random.default_rng(12345).standard_normal(s.n_dof)
+    ref = np.zeros(s.n_dof)
+    for nodes in d.contact_nodes:
+        if nodes.size:
+            dofs = node_dofs(nodes)
+            ref[dofs] += spla.splu(A[dofs][:, dofs].tocsc()).solve(v[dofs])
+    out = sv.apply("MZETA", dev(v)).cpu().numpy()
+    assert rel(out, ref) <= 1e-12, rel(out, ref)
+
+
 def test_cfg3_grain_identity(cfg3):
     """M_g^-1 A^ z = z for z supported on the grain interiors (all grains)."""
     from oracle.decomp import node_dofs
