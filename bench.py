@@ -425,6 +425,7 @@ def main():
     ap.add_argument("--config", default=os.environ.get("HPLMM_BENCH_CONFIG", "cfg3"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bsr", action="store_true", help="skip the stored-block operator line")
+    ap.add_argument("--no-multi", action="store_true", help="skip the multi-RHS block line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -620,6 +621,43 @@ def main():
                                       "roofline_frac": (pib / (tb / rb["iterations"]) / 1e9) / peak}}
         del sb
 
+    # ---- multi-RHS reuse (NEXT #2): 4 load cases, one block -----
+    multi = None
+    if not args.no_multi and not ilu and sparse:
+        from paper_2509_19777_b200 import assemble_bsr
+        from workloads import load_cases
+        cases = load_cases(prob, 4)
+        Bh = np.stack([b_host] + [assemble_bsr(q, local)["b"] for q in cases[1:]])
+        Bd = torch.from_numpy(Bh).cuda()
+        Xd = torch.zeros_like(Bd)
+        sv.solve_many(Bd, tol=prob.tol, X=Xd)      # warm-up (work lists of the block solves)
+        ms_block = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, mreps = sv.solve_many(Bd, tol=prob.tol, X=Xd)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_block.append(e0.elapsed_time(e1))
+        ms_single = []
+        its_single = []
+        for c in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, r1, _ = sv.solve(Bd[c], tol=prob.tol, x=Xd[c])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_single.append(e0.elapsed_time(e1))
+            its_single.append(r1["iterations"])
+        multi = {"rhs": 4, "load_cases": "workloads.load_cases (shifted prescribed displacements + "
+                                         "seeded nodal forces)",
+                 "block_s": _median(ms_block) / 1e3, "single_solves_s": sum(ms_single) / 1e3,
+                 "one_solve_s": med_s,
+                 "block_over_one_solve": _median(ms_block) / 1e3 / med_s,
+                 "iterations_block": [r["iterations"] for r in mreps],
+                 "iterations_single": its_single,
+                 "converged": [r["converged"] for r in mreps]}
+
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_{'sn' if sparse else 'symv'}_{args.config}.json")
     if os.path.exists(tp) and not ilu:
@@ -668,6 +706,7 @@ def main():
                                          "P^ twice + scatter/combine vectors + CGS2 at the actual "
                                          "Arnoldi index j of every step + per-cycle update"},
         "bsr_operator": bsr_line,
+        "multi_rhs": multi,
         "spmv": spmv,
         "gpu_launches": int(launches_per_step * args.steps),
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * n,

@@ -142,6 +142,15 @@ typedef struct {
                             1 = host-driven loop: one pinned D2H of the
                                 Hessenberg column and one synchronisation per
                                 Arnoldi step, Givens on the host            */
+  int32_t rhs_block;     /* hplmm_solve_many: right-hand sides solved together,
+                            1..4 (default 4).  A block runs lockstep GMRES(m):
+                            each column keeps its own Arnoldi process,
+                            correction columns (eq:col_cg, R15) and stop test,
+                            while every operator application streams its
+                            matrix data once for the whole block (the
+                            supernodal local factors, P^_B; NEXT #2, P:743,
+                            P:819).  1 = one hplmm_solve per column.  Blocks
+                            need local_factor = 1, smoother = 0, n_st = 1   */
 } hplmm_options;
 
 typedef struct {
@@ -268,9 +277,12 @@ hplmm_status hplmm_solve(hplmm_handle *h, const double *b, double tol, double *x
 /* Multi-RHS reuse (the paper's economic argument, P:743,
  * P:819): solve A^ X = B for nrhs right-hand sides with one setup -- the
  * local factors and S^-1 are reused, only the correction columns (eq:col_cg,
- * R15) are rebuilt per column.  B, X: nrhs x n_dof doubles, column-contiguous
- * (column i at B + i n_dof), host or device.  reports: nrhs entries or NULL.
- * Returns the worst status over the columns (an error stops at that column). */
+ * R15) are built per column.  Columns are solved in blocks of
+ * hplmm_options.rhs_block (lockstep GMRES, batched operator applications:
+ * each column's iterates are those of its own hplmm_solve).  B, X: nrhs x
+ * n_dof doubles, column-contiguous (column i at B + i n_dof), host or
+ * device.  reports: nrhs entries or NULL (t_solve_s: the column's block).
+ * Returns the worst status over the columns (an error stops at that block). */
 hplmm_status hplmm_solve_many(hplmm_handle *h, int32_t nrhs, const double *B, double tol,
                               double *X, hplmm_report *reports, void *stream);
 

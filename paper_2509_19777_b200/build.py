@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libhplmm.so")
 SOURCES = ["host_setup.cpp", "supernodal_host.cpp", "fem.cu", "dense.cu", "coarse.cu", "krylov.cu",
-           "supernodal.cu", "sn_setup.cu", "cholesky.cu", "ilu.cu", "gmres.cu", "api.cu"]
+           "supernodal.cu", "sn_setup.cu", "cholesky.cu", "ilu.cu", "gmres.cu", "multirhs.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-ffp-contract=off",
          "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xptxas", "-v",

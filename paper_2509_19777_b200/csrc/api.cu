@@ -102,6 +102,18 @@ struct hplmm_handle {
   double *d_vj = nullptr, *d_w = nullptr;
   int64_t graph_launches_pre = 0, graph_launches_cycle = 0, graph_launches_step = 0;
   bool graph_failed = false;
+
+  // multi-RHS batches (hplmm_solve_many, multirhs.cu): K <= 4 columns of
+  // stride ldv; per-column Krylov bases; per-RHS correction columns Ck / Dck
+  int64_t co_ct = 0, co_yo = 0;      // sizes of the restriction partials / grain coarse values
+  struct Multi {
+    int K = 0;
+    double *B = nullptr, *X = nullptr, *vin = nullptr, *y = nullptr, *r1 = nullptr, *z1 = nullptr,
+           *t = nullptr, *u = nullptr, *w = nullptr, *V = nullptr;
+    double *Ck = nullptr, *Dck = nullptr, *tk = nullptr, *gk = nullptr, *yk = nullptr, *rm = nullptr,
+           *rc = nullptr, *ym = nullptr, *yc = nullptr, *snc = nullptr, *sng = nullptr;
+    double *hb = nullptr, *partial = nullptr, *h_hb = nullptr;
+  } mr;
   int64_t ldv = 0;
   int Vcap = 0;
 
@@ -184,6 +196,7 @@ struct hplmm_handle {
       for (void* p : allocs) cudaFree(p);
       free_setup();
       if (h_hh) cudaFreeHost(h_hh);
+      if (mr.h_hb) cudaFreeHost(mr.h_hb);
       if (h_gs) cudaFreeHost(h_gs);
       if (h_ghist) cudaFreeHost(h_ghist);
       if (solve_exec) cudaGraphExecDestroy(solve_exec);
@@ -653,6 +666,289 @@ void do_set_rhs(hplmm_handle* h, const double* b_dev) {
 }
 
 // ---------------------------------------------------------------------------
+// Multi-RHS: up to 4 right-hand sides in
+// lockstep GMRES(m); every streamed operator is applied to the whole block.
+// ---------------------------------------------------------------------------
+constexpr int kMaxBlock = 4;
+
+bool multi_eligible(hplmm_handle* h) {
+  return h->sparse() && !h->ilu_smoother() && h->hs.opt.n_st == 1 && h->hs.opt.rhs_block > 1;
+}
+
+void multi_alloc(hplmm_handle* h) {
+  auto& M = h->mr;
+  if (M.K) return;
+  const int m = h->hs.opt.restart;
+  const int64_t ld = h->ldv;
+  const int K = kMaxBlock;
+  const int G = h->co.n_grains, Nm = h->co.Nm;
+  M.K = K;
+  for (double** p : {&M.B, &M.X, &M.vin, &M.y, &M.r1, &M.z1, &M.t, &M.u, &M.w})
+    *p = h->dalloc<double>((size_t)K * ld);
+  M.V = h->dalloc<double>((size_t)K * (m + 1) * ld);
+  M.Ck = h->dalloc<double>((size_t)K * std::max<int64_t>(h->gb.nloc, 1));
+  M.Dck = h->dalloc<double>((size_t)K * std::max(G, 1));
+  M.tk = h->dalloc<double>((size_t)K * std::max<int64_t>(h->co_ct, 1));
+  M.gk = h->dalloc<double>((size_t)K * std::max<int64_t>(h->co_yo, 1));
+  M.yk = h->dalloc<double>((size_t)K * std::max<int64_t>(h->co_yo, 1));
+  M.rm = h->dalloc<double>((size_t)K * std::max(Nm, 1));
+  M.ym = h->dalloc<double>((size_t)K * std::max(Nm, 1));
+  M.rc = h->dalloc<double>((size_t)K * std::max(G, 1));
+  M.yc = h->dalloc<double>((size_t)K * std::max(G, 1));
+  M.snc = h->dalloc<double>((size_t)K * std::max<int64_t>(h->sc.n_loc, 1));
+  M.sng = h->dalloc<double>((size_t)K * std::max<int64_t>(h->sg.n_loc, 1));
+  const int hbn = 2 * (m + 1) + 8;
+  M.hb = h->dalloc<double>((size_t)K * hbn);
+  M.partial = h->dalloc<double>((size_t)K * krylov_blocks(h->n_dof) * (m + 1));
+  CK(cudaMallocHost(&M.h_hb, (size_t)K * hbn * 8));
+}
+
+// out = M_G^-1 in for ncols columns (eq:mg_struct with each column's own C)
+void op_mg_k(hplmm_handle* h, int ncols, const double* in, double* out) {
+  auto& M = h->mr;
+  const int P = ncols > 2 ? 4 : ncols;
+  const int Nm = h->co.Nm, G = h->co.n_grains;
+  const int64_t ld = h->ldv;
+  launch_restrict_k(h->co, P, in, ld, ncols, M.Ck, h->gb.nloc, M.Dck, M.tk, M.gk, M.rm, M.rc, h->st);
+  for (int c = 0; c < ncols; ++c) {
+    if (Nm <= 0) break;
+    const double* ymc = op_coarse(h, M.rm + (int64_t)c * Nm);
+    CK(cudaMemcpyAsync(M.ym + (int64_t)c * Nm, ymc, (size_t)Nm * 8, cudaMemcpyDeviceToDevice, h->st));
+  }
+  launch_coarse_diag_k(ncols * G, M.rc, M.Dck, M.yc, h->st);
+  launch_prolong_k(h->co, P, M.ym, M.yc, M.Dck, M.Ck, h->gb.nloc, ncols, M.yk, out, ld, h->st);
+  h->launches += 7;
+}
+
+// out = M_zeta^-1 in, P columns per supernodal launch (factor streamed once)
+void op_mzeta_k(hplmm_handle* h, int ncols, const double* in, double* out) {
+  HandleAlloc ha(h);
+  const int P = sn_multi_width(h->sc, ha, h->st, h->nsm, ncols);
+  if (P == 0) throw HError{HPLMM_ERR_ARG, "multi-RHS contact solve does not fit shared memory"};
+  const int64_t ld = h->ldv;
+  for (int c0 = 0; c0 < ncols; c0 += P) {
+    const int nc = std::min(P, ncols - c0);
+    sn_apply_multi(h->sc, P, in + c0 * ld, ld, nc, h->mr.snc, h->st);
+    launch_sum_contact_k(h->n_dof, P, nc, h->d_cptr_sn, h->d_cidx_sn, h->mr.snc, out + c0 * ld, ld,
+                         h->st);
+    h->launches += 2;
+  }
+}
+
+// out = a + b + M_g^-1 in (a, b optional), P columns per supernodal launch
+void op_mgrain_k(hplmm_handle* h, int ncols, const double* in, const double* a, const double* b,
+                 double* out) {
+  HandleAlloc ha(h);
+  const int P = sn_multi_width(h->sg, ha, h->st, h->nsm, ncols);
+  if (P == 0) throw HError{HPLMM_ERR_ARG, "multi-RHS grain solve does not fit shared memory"};
+  const int64_t ld = h->ldv;
+  for (int c0 = 0; c0 < ncols; c0 += P) {
+    const int nc = std::min(P, ncols - c0);
+    sn_apply_multi(h->sg, P, in + c0 * ld, ld, nc, h->mr.sng, h->st);
+    launch_combine_grain_k(h->n_dof, P, nc, h->d_gpos_sn, h->mr.sng, a ? a + c0 * ld : nullptr,
+                           b ? b + c0 * ld : nullptr, ld, out + c0 * ld, h->st);
+    h->launches += 2;
+  }
+}
+
+// out = M^-1 in for ncols columns (eq:multi_precond, M_L = M_CG, n_st = 1)
+void op_minv_k(hplmm_handle* h, int ncols, const double* in, double* out) {
+  auto& M = h->mr;
+  const int64_t ld = h->ldv;
+  op_mg_k(h, ncols, in, M.y);
+  for (int c = 0; c < ncols; ++c) op_spmv(h, M.y + c * ld, in + c * ld, M.r1 + c * ld);
+  op_mzeta_k(h, ncols, M.r1, M.z1);
+  for (int c = 0; c < ncols; ++c) op_spmv(h, M.z1 + c * ld, M.r1 + c * ld, M.t + c * ld);
+  op_mgrain_k(h, ncols, M.t, M.y, M.z1, out);
+}
+
+// correction columns of the block's right-hand sides (eq:col_cg, R15, R16)
+void set_rhs_k(hplmm_handle* h, int ncols, const double* B) {
+  auto& M = h->mr;
+  for (int c = 0; c < ncols; ++c) {
+    const double* b = B + c * h->ldv;
+    h->sn_solve(h->sg, b, KC_SN_GRAIN);
+    launch_sn_to_batch(h->gb.nloc, h->gb.lmap, h->d_gpos_sn, b, h->sg.yloc, h->gb.xloc, h->gb.yloc,
+                       h->st);
+    launch_set_correction_k(h->gb, h->co.n_grains, M.Ck + c * h->gb.nloc,
+                            M.Dck + (int64_t)c * h->co.n_grains, h->st);
+    h->launches += 2;
+  }
+}
+
+// Lockstep GMRES(m) (R22) on ncols <= 4 columns of Bd (device, stride ldv):
+// each column runs its own Arnoldi process and Givens rotations exactly as
+// hplmm_solve's host loop; the operator applications of a step are batched.
+// A cycle ends when every column still iterating has stopped (converged,
+// happy breakdown, cap) or reached m; columns that stopped earlier wait.
+void solve_block(hplmm_handle* h, int ncols, double tol, hplmm_report* reps) {
+  auto& M = h->mr;
+  cudaStream_t st = h->st;
+  const int n = h->n_dof, m = h->hs.opt.restart, maxit = h->hs.opt.max_iter;
+  const int64_t ld = h->ldv;
+  const int hbn = 2 * (m + 1) + 8;
+  // ||b_c||
+  for (int c = 0; c < ncols; ++c)
+    launch_norm2(n, M.B + c * ld, M.partial, M.hb + (int64_t)c * hbn + 2 * (m + 1), st);
+  std::vector<double> bn(ncols), bn2(ncols);
+  CK(cudaMemcpyAsync(M.h_hb, M.hb, (size_t)ncols * hbn * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int c = 0; c < ncols; ++c) {
+    bn2[c] = M.h_hb[(int64_t)c * hbn + 2 * (m + 1)];
+    bn[c] = std::sqrt(bn2[c]);
+  }
+  set_rhs_k(h, ncols, M.B);
+  CK(cudaMemsetAsync(M.X, 0, (size_t)ncols * ld * 8, st));
+  CK(cudaMemcpyAsync(M.r1, M.B, (size_t)ncols * ld * 8, cudaMemcpyDeviceToDevice, st));
+  struct Col {
+    std::vector<double> H, cs, sn, g;
+    int total = 0, k = 0;
+    bool done = false, conv = false, active = false;
+    double beta2 = 0, relres = 1.0;
+  };
+  std::vector<Col> col(ncols);
+  for (int c = 0; c < ncols; ++c) {
+    col[c].H.assign((size_t)(m + 1) * m, 0.0);
+    col[c].cs.assign(m, 0.0);
+    col[c].sn.assign(m, 0.0);
+    col[c].g.assign(m + 1, 0.0);
+    col[c].beta2 = bn2[c];
+    if (bn[c] == 0.0) {
+      col[c].done = col[c].conv = true;
+      col[c].relres = 0.0;
+    }
+  }
+  double* r = M.r1;   // residual block (the cycle start vectors), overwritten per cycle
+  std::vector<double> hbuf;
+  while (true) {
+    bool any = false;
+    for (int c = 0; c < ncols; ++c) {
+      Col& C = col[c];
+      C.active = !C.done;
+      if (!C.active) continue;
+      any = true;
+      std::fill(C.H.begin(), C.H.end(), 0.0);
+      std::fill(C.g.begin(), C.g.end(), 0.0);
+      C.g[0] = std::sqrt(C.beta2);
+      C.k = 0;
+      // V_c[0] = r_c / beta_c (norm^2 in the column's hb slot)
+      CK(cudaMemcpyAsync(M.hb + (int64_t)c * hbn + 2 * (m + 1), &C.beta2, 8, cudaMemcpyHostToDevice,
+                         st));
+      launch_scale(n, r + c * ld, M.hb + (int64_t)c * hbn + 2 * (m + 1), 1,
+                   M.V + (int64_t)c * (m + 1) * ld, st);
+    }
+    if (!any) break;
+    for (int j = 0; j < m; ++j) {
+      bool stepping = false;
+      for (int c = 0; c < ncols; ++c) stepping |= col[c].active;
+      if (!stepping) break;
+      // u_c = M^-1 v_j,c (block; columns not iterating carry zeros), w_c = A u_c
+      for (int c = 0; c < ncols; ++c) {
+        if (col[c].active)
+          CK(cudaMemcpyAsync(M.vin + c * ld, M.V + ((int64_t)c * (m + 1) + j) * ld, (size_t)n * 8,
+                             cudaMemcpyDeviceToDevice, st));
+        else
+          CK(cudaMemsetAsync(M.vin + c * ld, 0, (size_t)n * 8, st));
+      }
+      op_minv_k(h, ncols, M.vin, M.u);
+      for (int c = 0; c < ncols; ++c) {
+        if (!col[c].active) continue;
+        double* V = M.V + (int64_t)c * (m + 1) * ld;
+        double* w = V + (j + 1) * ld;
+        double* hb = M.hb + (int64_t)c * hbn;
+        op_spmv(h, M.u + c * ld, nullptr, w);
+        launch_multidot(n, j + 1, V, ld, w, M.partial, hb, st);
+        launch_update(n, j + 1, V, ld, hb, w, nullptr, nullptr, st);
+        launch_multidot(n, j + 1, V, ld, w, M.partial, hb + (m + 1), st);
+        launch_update(n, j + 1, V, ld, hb + (m + 1), w, M.partial, hb + 2 * (m + 1), st);
+        h->launches += 7;
+      }
+      CK(cudaMemcpyAsync(M.h_hb, M.hb, (size_t)ncols * hbn * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int c = 0; c < ncols; ++c) {
+        Col& C = col[c];
+        if (!C.active) continue;
+        const double* hh = M.h_hb + (int64_t)c * hbn;
+        const double hn = std::sqrt(hh[2 * (m + 1)]);
+        std::vector<double> cv(j + 2);
+        for (int i = 0; i <= j; ++i) cv[i] = hh[i] + hh[m + 1 + i];
+        cv[j + 1] = hn;
+        for (int i = 0; i < j; ++i) {
+          const double tq = C.cs[i] * cv[i] + C.sn[i] * cv[i + 1];
+          cv[i + 1] = -C.sn[i] * cv[i] + C.cs[i] * cv[i + 1];
+          cv[i] = tq;
+        }
+        const double den = std::hypot(cv[j], cv[j + 1]);
+        C.cs[j] = cv[j] / den;
+        C.sn[j] = cv[j + 1] / den;
+        cv[j] = den;
+        C.g[j + 1] = -C.sn[j] * C.g[j];
+        C.g[j] = C.cs[j] * C.g[j];
+        for (int i = 0; i <= j; ++i) C.H[(size_t)i * m + j] = cv[i];
+        C.total++;
+        C.k = j + 1;
+        const double est = std::fabs(C.g[j + 1]) / bn[c];
+        if (!std::isfinite(est)) throw HError{HPLMM_ERR_NONFINITE, "non-finite GMRES residual"};
+        if (hn == 0.0 || est < tol || C.total >= maxit) {
+          C.active = false;   // this column's cycle ends here
+        } else {
+          double* V = M.V + (int64_t)c * (m + 1) * ld;
+          launch_scale(n, V + (j + 1) * ld, M.hb + (int64_t)c * hbn + 2 * (m + 1), 1,
+                       V + (j + 1) * ld, st);
+          h->launches++;
+        }
+      }
+    }
+    // cycle end: x_c += M^-1 (V_c y_c), r_c = b_c - A x_c for every column that iterated
+    for (int c = 0; c < ncols; ++c) {
+      Col& C = col[c];
+      if (C.done) {
+        CK(cudaMemsetAsync(M.vin + c * ld, 0, (size_t)n * 8, st));
+        continue;
+      }
+      std::vector<double> y(C.k);
+      for (int i = C.k - 1; i >= 0; --i) {
+        double s = C.g[i];
+        for (int l = i + 1; l < C.k; ++l) s -= C.H[(size_t)i * m + l] * y[l];
+        y[i] = s / C.H[(size_t)i * m + i];
+      }
+      double* hb = M.hb + (int64_t)c * hbn;
+      CK(cudaMemcpyAsync(hb, y.data(), C.k * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(M.vin + c * ld, 0, (size_t)n * 8, st));
+      launch_combine_basis(n, C.k, M.V + (int64_t)c * (m + 1) * ld, ld, hb, M.vin + c * ld, st);
+      h->launches++;
+    }
+    op_minv_k(h, ncols, M.vin, M.u);
+    for (int c = 0; c < ncols; ++c) {
+      if (col[c].done) continue;
+      launch_axpy(n, 1.0, M.u + c * ld, M.X + c * ld, st);
+      op_spmv(h, M.X + c * ld, M.B + c * ld, r + c * ld);
+      launch_norm2(n, r + c * ld, M.partial, M.hb + (int64_t)c * hbn + 2 * (m + 1), st);
+      h->launches += 3;
+    }
+    CK(cudaMemcpyAsync(M.h_hb, M.hb, (size_t)ncols * hbn * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int c = 0; c < ncols; ++c) {
+      Col& C = col[c];
+      if (C.done) continue;
+      C.beta2 = M.h_hb[(int64_t)c * hbn + 2 * (m + 1)];
+      C.relres = std::sqrt(C.beta2) / bn[c];
+      if (!std::isfinite(C.relres)) throw HError{HPLMM_ERR_NONFINITE, "non-finite true residual"};
+      if (C.relres < tol) C.done = C.conv = true;
+      else if (C.total >= maxit) C.done = true;
+    }
+  }
+  for (int c = 0; c < ncols; ++c) {
+    hplmm_report& R = reps[c];
+    R = h->rep;
+    R.iterations = col[c].total;
+    R.converged = col[c].conv ? 1 : 0;
+    R.hist_len = 0;
+    R.final_true_relres = col[c].relres;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Device-resident solve (R22 on the GPU, gmres.cu).  The graph is
 //   WHILE (outer: restart cycles) {
 //     cycle init: g = beta e1, V0 = r / beta
@@ -803,6 +1099,7 @@ void hplmm_default_options(hplmm_options* o) {
   o->operator_kind = 0;
   o->sn_shape = 0;
   o->host_loop = 0;
+  o->rhs_block = 4;
 }
 
 const char* hplmm_last_error(void) { return g_last_error.c_str(); }
@@ -1210,6 +1507,8 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     co.yext = h->dalloc<double>(std::max<int64_t>(yo, 1));
     co.gpart = h->dalloc<double>(std::max<int64_t>(yo, 1));
     co.yext_off = h->upload(yext_off);
+    h->co_ct = ct;
+    h->co_yo = yo;
     co.Dc = h->dalloc<double>(std::max(G, 1));
     co.Cg = h->dalloc<double>(std::max<int64_t>(co2, 1), true);
     co.cg_off = h->upload(cg_off);
@@ -1866,6 +2165,50 @@ hplmm_status hplmm_solve_many(hplmm_handle* h, int32_t nrhs, const double* B, do
   if (!h || !B || !X || nrhs < 0) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
   const int64_t n = 3 * (int64_t)h->hs.n_nodes;
   hplmm_status worst = HPLMM_OK;
+  if (nrhs > 1 && h->setup_done && multi_eligible(h)) {
+    try {
+      if (!(tol > 0)) throw HError{HPLMM_ERR_ARG, "tol must be > 0"};
+      require_device(h);
+      h->st = (cudaStream_t)stream;
+      const int m = h->hs.opt.restart;
+      if (h->Vcap < m + 1) {
+        h->ldv = ((int64_t)n + 31) / 32 * 32;
+        h->d_V = h->dalloc<double>((size_t)(m + 1) * h->ldv);
+        h->d_partial = h->dalloc<double>((size_t)krylov_blocks(n) * (m + 1));
+        h->d_hbuf = h->dalloc<double>(2 * (m + 1) + 8);
+        h->Vcap = m + 1;
+      }
+      multi_alloc(h);
+      const int blk = std::min(kMaxBlock, (int)h->hs.opt.rhs_block);
+      const bool bdev = is_device_ptr(B), xdev = is_device_ptr(X);
+      for (int c0 = 0; c0 < nrhs; c0 += blk) {
+        const int nc = std::min(blk, nrhs - c0);
+        Timer tt(h->st);
+        h->launches = 0;
+        for (int c = 0; c < nc; ++c)
+          CK(cudaMemcpyAsync(h->mr.B + c * h->ldv, B + (c0 + c) * n, n * 8,
+                             bdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
+        std::vector<hplmm_report> reps(nc);
+        solve_block(h, nc, tol, reps.data());
+        for (int c = 0; c < nc; ++c)
+          CK(cudaMemcpyAsync(X + (c0 + c) * n, h->mr.X + c * h->ldv, n * 8,
+                             xdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+        const double ts = tt.stop();
+        CK(cudaStreamSynchronize(h->st));
+        for (int c = 0; c < nc; ++c) {
+          reps[c].t_solve_s = ts;
+          reps[c].kernel_launches = h->launches;
+          if (reports) reports[c0 + c] = reps[c];
+          const hplmm_status s = reps[c].converged ? HPLMM_OK : HPLMM_NOT_CONVERGED;
+          if (s > worst) worst = s;
+        }
+        h->rep = reps[nc - 1];
+      }
+      return worst;
+    } catch (const HError& e) {
+      return fail(e);
+    }
+  }
   for (int32_t i = 0; i < nrhs; ++i) {
     hplmm_report rep{};
     const hplmm_status st = hplmm_solve(h, B + i * n, tol, X + i * n, &rep, nullptr, 0, stream);

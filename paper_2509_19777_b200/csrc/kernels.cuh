@@ -207,6 +207,21 @@ void launch_combine_basis(int64_t n, int m, const double* V, int64_t ldv, const 
                           double* x, cudaStream_t st);
 void launch_axpy(int64_t n, double a, const double* x, double* y, cudaStream_t st);
 
+// ---- multi-RHS blocks (multirhs.cu; NEXT #2) ----------------------------------
+void launch_set_correction_k(const DevBatch& gb, int G, double* Ck, double* Dck, cudaStream_t st);
+void launch_restrict_k(const DevCoarse& c, int P, const double* r, int64_t ldr, int ncols,
+                       const double* Ck, int64_t ldc, const double* Dck, double* tk, double* gk,
+                       double* rm, double* rc, cudaStream_t st);
+void launch_prolong_k(const DevCoarse& c, int P, const double* ym, const double* yc,
+                      const double* Dck, const double* Ck, int64_t ldc, int ncols, double* yk,
+                      double* x, int64_t ldx, cudaStream_t st);
+void launch_coarse_diag_k(int n, const double* rc, const double* Dck, double* yc, cudaStream_t st);
+void launch_sum_contact_k(int n, int P, int ncols, const int32_t* cptr, const int32_t* cidx,
+                          const double* yloc, double* out, int64_t ldo, cudaStream_t st);
+void launch_combine_grain_k(int n, int P, int ncols, const int32_t* gpos, const double* yloc,
+                            const double* a, const double* b, int64_t ld, double* out,
+                            cudaStream_t st);
+
 // ---- device-resident GMRES cycle (gmres.cu; graph-captured, R22) ------------
 // Scalars of one solve, in device memory next to the small dense arrays.
 struct GmresScalars {

@@ -178,6 +178,44 @@ void sn_apply(const SnBatch& B, const double* in, cudaStream_t st) {
                   B.work.cons, st);
 }
 
+static int p_slot(int P) { return P == 4 ? 2 : (P == 2 ? 1 : 0); }
+
+// A width P > 1 is used only when its solve runs in the 8-warp x 2-CTA shape:
+// measured at cfg3 (4 load cases), the 16 x 1 shape that the larger x_S of
+// P columns forces is latency-bound (barrier and shared-load stalls) and
+// takes longer than P one-column solves (contact batch: P = 4 in 8.3 ms vs
+// 4 x 1.9 ms; grain batch: P = 2 in 2.6 ms vs 2 x 1.24 ms).
+int sn_multi_width(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm, int k) {
+  static const bool any_shape = getenv("HPLMM_MULTI_ANY_SHAPE") != nullptr;   // experiments
+  for (int P : {4, 2, 1}) {
+    if (P > k && P > 1) continue;
+    int& s = B.mstate[p_slot(P)];
+    if (s == 0) {
+      try {
+        SnWork& wk = B.mwork[p_slot(P)];
+        sn_build_work(B, A, st, nsm, P, nullptr, wk);
+        s = (P == 1 || wk.cons == 8 || any_shape) ? 1 : -1;
+      } catch (const SnError&) {
+        s = -1;
+      }
+    }
+    if (s == 1) return P;
+  }
+  return 0;
+}
+
+void sn_apply_multi(const SnBatch& B, int P, const double* in, int64_t ldin, int ncols, double* out,
+                    cudaStream_t st) {
+  SnIO io;
+  io.mode = 2;
+  io.in = in;
+  io.ldin = ldin;
+  io.ncols = ncols;
+  io.out = out;
+  const SnWork& wk = B.mwork[p_slot(P)];
+  launch_sn_solve(B.dev, io, wk, P, B.sym.max_n, B.sym.max_r, B.sym.chunk_doubles, wk.cons, st);
+}
+
 // ---------------------------------------------------------------------------
 // numeric factorisation
 // ---------------------------------------------------------------------------

@@ -94,7 +94,9 @@ template <int NQ, int NRHS, int MAXQ>
 __device__ __forceinline__ void sn_rows(const double* __restrict__ st, int ld, int nc, int h,
                                         const double* __restrict__ xcol, const RowLayout& L,
                                         double (&acc)[MAXQ][2][NRHS]) {
-  constexpr int U = NQ == 1 ? 4 : (NQ == 2 ? 2 : 1);   // columns per step (register budget)
+  // columns per step (register budget: NQ row pairs x NRHS accumulators)
+  constexpr int U0 = NQ == 1 ? 4 : (NQ == 2 ? 2 : 1);
+  constexpr int U = NRHS == 1 ? U0 : (NQ == 1 ? 2 : 1);
   double acc2[NQ][2][NRHS];
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
@@ -109,8 +111,17 @@ __device__ __forceinline__ void sn_rows(const double* __restrict__ st, int ld, i
     double2 a[U][NQ];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      if constexpr (NRHS % 2 == 0) {   // x rows are 16-byte aligned: paired loads
 #pragma unroll
-      for (int c = 0; c < NRHS; ++c) xv[u][c] = xcol[(jj + u * G) * NRHS + c];
+        for (int c = 0; c < NRHS; c += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(xcol + (jj + u * G) * NRHS + c);
+          xv[u][c] = t.x;
+          xv[u][c + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NRHS; ++c) xv[u][c] = xcol[(jj + u * G) * NRHS + c];
+      }
       const double* cu = st + (size_t)(jj + u * G) * ld;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
@@ -207,7 +218,11 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
   // x_R of the current backward part; scratch of the forward group reductions
   // x_R of a backward part (16-B aligned)
   double* xr = x + (size_t)((max_n + 1) & ~1) * NRHS;
-  constexpr int SN_NT = SnT<CONS>::NT, SN_MAXQ = SnT<CONS>::MAXQ, SN_CONS = CONS;
+  constexpr int SN_NT = SnT<CONS>::NT, SN_CONS = CONS;
+  // row pairs per thread: up to 4 for one RHS (TG >= h/8); with several RHS
+  // TG >= h/2 (sn_lg), so h <= 2048 needs at most 2 with 16 warps -- a smaller
+  // accumulator array keeps the multi-RHS solve free of register spills
+  constexpr int SN_MAXQ = (NRHS == 1 || CONS != 16) ? SnT<CONS>::MAXQ : 2;
   constexpr int SN_LGNT = SnT<CONS>::LGNT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k0 = wk.chunk_ptr[blockIdx.x], k1 = wk.chunk_ptr[blockIdx.x + 1];
@@ -307,7 +322,13 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       n = d.sub_n[sub];
       base = d.sub_base[sub];
       rc0 = wk.item_c0[item];
-      if (io.mode == 0) {
+      if (io.mode == 2) {
+        for (int p = tid; p < n; p += SN_NT) {
+          const int64_t gd = __ldg(d.gmap + base + p);
+#pragma unroll
+          for (int c = 0; c < NRHS; ++c) x[p * NRHS + c] = c < io.ncols ? io.in[c * io.ldin + gd] : 0.0;
+        }
+      } else if (io.mode == 0) {
         for (int q0 = tid; q0 < n; q0 += 4 * SN_NT) {
           double v[4];
 #pragma unroll
@@ -363,9 +384,11 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       const double* xcol = x + (size_t)(p0 + cc0) * NRHS;
       const int nq = L.nq(h);
       if (nq <= 1) sn_rows<1, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
-      else if (nq == 2) sn_rows<2, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
-      else if (nq == 3) sn_rows<3, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
-      else sn_rows<4, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
+      else if (nq == 2 || SN_MAXQ == 2) sn_rows<2, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
+      else if constexpr (SN_MAXQ >= 4) {
+        if (nq == 3) sn_rows<3, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
+        else sn_rows<4, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
+      }
       if (!(last && L.G > 1)) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[cs]);
@@ -456,9 +479,19 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
           }
           for (; i < r; i += 2 * lpc) {
             const double2 a = *reinterpret_cast<const double2*>(col + i);
+            if constexpr (NRHS % 2 == 0) {   // x_R rows i, i+1: 2 NRHS contiguous doubles
 #pragma unroll
-            for (int cr = 0; cr < NRHS; ++cr)
-              sum[cr] = fma(a.x, xr[i * NRHS + cr], fma(a.y, xr[(i + 1) * NRHS + cr], sum[cr]));
+              for (int cr = 0; cr < NRHS; cr += 2) {
+                const double2 x0 = *reinterpret_cast<const double2*>(xr + i * NRHS + cr);
+                const double2 x1 = *reinterpret_cast<const double2*>(xr + (i + 1) * NRHS + cr);
+                sum[cr] = fma(a.x, x0.x, fma(a.y, x1.x, sum[cr]));
+                sum[cr + 1] = fma(a.x, x0.y, fma(a.y, x1.y, sum[cr + 1]));
+              }
+            } else {
+#pragma unroll
+              for (int cr = 0; cr < NRHS; ++cr)
+                sum[cr] = fma(a.x, xr[i * NRHS + cr], fma(a.y, xr[(i + 1) * NRHS + cr], sum[cr]));
+            }
           }
         }
 #pragma unroll
@@ -484,7 +517,9 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     if (info & SN_INFO_LAST_ITEM) {
       PSYNC();
       // ---- write the solution
-      if (io.mode == 0) {
+      if (io.mode == 2) {
+        for (int p = tid; p < n * NRHS; p += SN_NT) io.out[base * NRHS + p] = x[p];
+      } else if (io.mode == 0) {
         for (int p = tid; p < n; p += SN_NT) io.out[base + p] = x[p];
       } else {
         const int L = io.ld[sub];
@@ -534,10 +569,13 @@ int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk,
     env_forced = e ? atoi(e) : 0;
   }
   const int forced = shape ? shape : env_forced;
-  // the group-reduction scratch (8 x 32 x cons x nrhs doubles) must fit one stage
-  const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8) >= 2 && chunk >= 8 * 256 * nrhs;
-  const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16) >= 2 && chunk >= 8 * 512 * nrhs;
-  if (forced == 4 && sn_solve_stages(max_n, max_r, nrhs, chunk, 4) >= 2 && chunk >= 8 * 128 * nrhs)
+  // the group-reduction scratch must fit one stage: (G - 1) h NRHS doubles, with
+  // TG >= h/8 for one RHS (<= 8 x consumer threads) and TG >= h/2 for several
+  // (sn_lg: <= 2 x consumer threads x NRHS)
+  auto scratch = [nrhs](int nt) { return nrhs == 1 ? 8 * nt : 2 * nt * nrhs; };
+  const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8) >= 2 && chunk >= scratch(256);
+  const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16) >= 2 && chunk >= scratch(512);
+  if (forced == 4 && sn_solve_stages(max_n, max_r, nrhs, chunk, 4) >= 2 && chunk >= scratch(128))
     return 4;
   if (forced == 8 && fit8) return 8;
   if (forced == 16 && fit16) return 16;

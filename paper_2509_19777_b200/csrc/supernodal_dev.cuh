@@ -24,8 +24,12 @@ struct SnDev {
 // mode 0: x = in[gmap], out[base+p] = x (one RHS)
 // mode 1: shape-vector columns of the grain batch: x[p][c] = in[b_off + bmap*L + c0 + c],
 //         out[same] = -x  (L = ld[sub], columns [0, L-1))
+// mode 2: several right-hand sides (multi-RHS solves): x[p][c] = in[c ldin + gmap],
+//         c < ncols (0 beyond), out[(base+p) NRHS + c] = x[p][c] (interleaved)
 struct SnIO {
   int mode = 0;
+  int ncols = 1;
+  int64_t ldin = 0;
   const double* in = nullptr;
   double* out = nullptr;
   const int32_t* bmap = nullptr;

@@ -50,7 +50,7 @@ class Options(C.Structure):
                 ("coarse_refine", C.c_int32), ("local_factor", C.c_int32),
                 ("coarse_solver", C.c_int32), ("mortar_kind", C.c_int32),
                 ("smoother", C.c_int32), ("operator_kind", C.c_int32),
-                ("sn_shape", C.c_int32), ("host_loop", C.c_int32)]
+                ("sn_shape", C.c_int32), ("host_loop", C.c_int32), ("rhs_block", C.c_int32)]
 
 
 class Bsr(C.Structure):
@@ -206,7 +206,7 @@ class Solver:
     def __init__(self, prob, n_mortar=None, beta=None, contact_h=None, restart=None,
                  max_iter=None, coarse_refine=0, local_factor=None, coarse_solver=None,
                  mortar=None, smoother=None, n_st=None, operator=None, sn_shape=None,
-                 host_loop=None, bsr=None, device=0, stream=None):
+                 host_loop=None, rhs_block=None, bsr=None, device=0, stream=None):
         """bsr: optional dict(row_ptr, col_idx, val, node_ijk=None) -- the
         caller's matrix A^ (host NumPy or torch CUDA arrays): the handle is
         then built by hplmm_setup_bsr (create + pattern check + assemble +
@@ -239,6 +239,8 @@ class Solver:
             o.sn_shape = int(sn_shape)
         if host_loop is not None:
             o.host_loop = int(host_loop)
+        if rhs_block is not None:
+            o.rhs_block = int(rhs_block)
         self.options = o
         h = C.c_void_p()
         if bsr is None:

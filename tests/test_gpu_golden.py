@@ -7,8 +7,8 @@ which calls only oracle/.  Compared (north star): GMRES iterations +-1 and the
 residual history (rtol 1e-6) at 1e-8 (R22); the solution x at 4096
 sampled DOFs (rel-L2 <= 1e-8, and ||x||); M_zeta^-1 v, M_g^-1 v, M_CG^-1 v at
 the sampled DOFs (<= 1e-12 relative); M_G^-1 v and M^-1 v within the larger of
-3x the spread of the oracle's two correct fp64 coarse solves (Cholesky vs
-explicit S^-1) and 3 kappa_2(S) u.
+10x the spread of the oracle's two correct fp64 coarse solves (Cholesky vs LU,
+tests/golden/README.md) and 3 kappa_2(S) u.
 """
 import json
 import os
@@ -78,9 +78,9 @@ def test_golden_operators(name, op):
     idx = a["idx"]
     ref = a[op]
     if op in ("MG", "MINV"):
-        # 3x the spread of the oracle's two correct coarse solves, or kappa_2(S) u
+        # 10x the spread of the oracle's two correct coarse solves, or 3 kappa_2(S) u
         # (forward error of any backward-stable fp64 coarse solve)
-        tol = max(1e-12, 3.0 * rel(a[op + "_inv"], ref), 3.0 * g.get("kappa_S", 0.0) * 2.0 ** -53)
+        tol = max(1e-12, 10.0 * rel(a[op + "_inv"], ref), 3.0 * g.get("kappa_S", 0.0) * 2.0 ** -53)
     else:
         tol = 1e-12
     assert rel(out[idx], ref) <= tol, (rel(out[idx], ref), tol)

@@ -1,0 +1,84 @@
+"""Multi-RHS blocks (the paper's reuse of one setup for
+several load cases): hplmm_solve_many solves up to 4 right-hand
+sides in lockstep GMRES(50) with every operator application batched (the
+supernodal factors and P^_B streamed once per block).  Each column must be
+exactly its own GMRES run (R22) with its own correction columns (eq:col_cg,
+R15): compared column by column with the ORACLE's GMRES on that right-hand side
+-- iterations +-1, x rel-L2 <= 1e-8, true residual < tol -- and with the
+per-column path (rhs_block = 1).
+"""
+import numpy as np
+import pytest
+
+from tests.conftest import oracle_case
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def _rhs(name, k):
+    """k right-hand sides of the oracle's system: the load cases of
+    workloads.load_cases (assembled by the oracle), one of them zero if k == 4."""
+    from oracle import fem
+    from workloads import load_cases
+    p, s, h = oracle_case(name)
+    bs = [fem.build_system(q).b for q in load_cases(p, k)]
+    if k == 4:
+        bs[2] = np.zeros_like(bs[2])          # b = 0 => x = 0, 0 iterations
+    return p, s, h, np.stack(bs)
+
+
+@pytest.mark.parametrize("case", ["cube8", "cfg1", "porous20"])
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_solve_many_block_vs_oracle(case, k):
+    from oracle import gmres
+    from paper_2509_19777_b200 import Solver
+    p, s, h, B = _rhs(case, k)
+    sv = Solver(p).assemble(0).setup()
+    X, reps = sv.solve_many(torch.from_numpy(B).cuda(), tol=1e-8)
+    X = X.cpu().numpy()
+    for c in range(k):
+        b = B[c]
+        if not np.any(b):
+            assert reps[c]["iterations"] == 0 and not np.any(X[c])
+            continue
+        h.set_rhs(b)
+        xo, ito, _, _, convo = gmres.gmres(s.A, b, h.apply_M, tol=1e-8)
+        assert convo and reps[c]["converged"] == 1
+        assert abs(reps[c]["iterations"] - ito) <= 1, (c, reps[c]["iterations"], ito)
+        assert rel(X[c], xo) <= 1e-8, (c, rel(X[c], xo))
+        assert np.linalg.norm(b - s.A @ X[c]) / np.linalg.norm(b) < 1e-8
+
+
+@pytest.mark.parametrize("case", ["cfg1", "porous20"])
+def test_solve_many_block_matches_per_column(case):
+    from paper_2509_19777_b200 import Solver
+    p, s, h, B = _rhs(case, 3)
+    a = Solver(p).assemble(0).setup()
+    b = Solver(p, rhs_block=1).assemble(0).setup()
+    Xa, ra = a.solve_many(B.copy(), tol=1e-8)          # host buffers
+    Xb, rb = b.solve_many(B.copy(), tol=1e-8)
+    for c in range(3):
+        assert ra[c]["iterations"] == rb[c]["iterations"]
+        assert rel(Xa[c], Xb[c]) <= 1e-9
+
+
+def test_solve_many_restart_and_cap():
+    """Restart cycles (m = 5) and the iteration cap inside a block: every column
+    follows its own cycle sequence, as the single-RHS path does."""
+    from paper_2509_19777_b200 import Solver
+    p, s, h, B = _rhs("cfg1", 3)
+    a = Solver(p, restart=5).assemble(0).setup()
+    b = Solver(p, restart=5, rhs_block=1).assemble(0).setup()
+    Xa, ra = a.solve_many(B.copy(), tol=1e-8)
+    Xb, rb = b.solve_many(B.copy(), tol=1e-8)
+    for c in range(3):
+        assert ra[c]["iterations"] == rb[c]["iterations"] and ra[c]["converged"] == 1
+        assert rel(Xa[c], Xb[c]) <= 1e-9
+    capped = Solver(p, max_iter=7, restart=5).assemble(0).setup()
+    Xc, rc = capped.solve_many(B.copy(), tol=1e-8)
+    assert all(r["iterations"] == 7 and r["converged"] == 0 for r in rc)

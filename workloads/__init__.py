@@ -31,7 +31,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["Problem", "make_problem", "CONFIGS", "random_vector"]
+__all__ = ["Problem", "make_problem", "CONFIGS", "random_vector", "load_cases"]
 
 
 @dataclass
@@ -255,6 +255,28 @@ def make_problem(name: str, **overrides) -> Problem:
     for k, v in overrides.items():
         setattr(p, k, v)
     return p
+
+
+def load_cases(p: Problem, k: int) -> list:
+    """k load cases on one problem (the paper's multi-RHS reuse):
+    same geometry, material, decomposition and Dirichlet node set, different
+    loads.  Case 0 is ``p`` itself; case c >= 1 cyclically shifts the
+    components of the prescribed displacement on every Dirichlet node that is
+    not clamped at the bottom (shear x -> y -> z ...) and adds seeded nodal
+    forces 1e-3 N(0,1) (seed 2000 + c) on every lattice node.  Only the
+    right-hand side b^ changes from case to case (eq:ls_all)."""
+    import copy
+    out = [p]
+    for c in range(1, k):
+        q = copy.deepcopy(p)
+        q.name = f"{p.name}_load{c}"
+        u = np.asarray(p.node_u)
+        q.node_u = np.roll(u, c, axis=-1).copy()
+        q.node_u[0] = u[0]                       # the bottom clamp keeps u = 0
+        rng = np.random.default_rng(2000 + c)
+        q.node_f = np.asarray(p.node_f) + 1e-3 * rng.standard_normal(np.shape(p.node_f))
+        out.append(q)
+    return out
 
 
 def random_vector(n: int, seed: int = 12345) -> np.ndarray:
