@@ -86,7 +86,7 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   if (wk.cons == 0)
     throw SnError{-1, "subdomain of " + std::to_string(s.max_n) +
                           " DOFs does not fit the supernodal solve's shared memory"};
-  nblocks *= wk.cons == 16 ? 1 : 2;
+  nblocks *= sn_cfg_cps(wk.cons);
   if (const char* e = getenv("HPLMM_SN_CTAS")) nblocks = std::max(1, atoi(e));   // experiments
   nblocks = std::max(1, std::min<int>(nblocks, (int)isub.size()));
   std::vector<int32_t> ptr, ids;
@@ -180,13 +180,14 @@ void sn_apply(const SnBatch& B, const double* in, cudaStream_t st) {
 
 static int p_slot(int P) { return P == 4 ? 2 : (P == 2 ? 1 : 0); }
 
-// A width P > 1 is used only when its solve runs in the 8-warp x 2-CTA shape:
-// measured at cfg3 (4 load cases), the 16 x 1 shape that the larger x_S of
-// P columns forces is latency-bound (barrier and shared-load stalls) and
-// takes longer than P one-column solves (contact batch: P = 4 in 8.3 ms vs
-// 4 x 1.9 ms; grain batch: P = 2 in 2.6 ms vs 2 x 1.24 ms).
+// The larger x_S of P columns forces the 16-warp x 1-CTA shape at cfg3
+// (profiles/r02_ncu_sn_solve_nrhs4_cfg3.txt): latency-bound (barrier and
+// shared-load stalls).  Measured, 4 load cases at cfg3: the whole block
+// solve takes 0.703 s with the P = 4 / 2 solves and 0.734 s with one-column
+// solves (P = 1, 8 x 2) -- so any shape is taken (HPLMM_MULTI_8X2_ONLY=1
+// restricts P > 1 to the 8 x 2 shape).
 int sn_multi_width(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm, int k) {
-  static const bool any_shape = getenv("HPLMM_MULTI_ANY_SHAPE") != nullptr;   // experiments
+  static const bool any_shape = getenv("HPLMM_MULTI_8X2_ONLY") == nullptr;
   for (int P : {4, 2, 1}) {
     if (P > k && P > 1) continue;
     int& s = B.mstate[p_slot(P)];

@@ -175,12 +175,15 @@ __device__ __forceinline__ void sn_rows(const double* __restrict__ st, int ld, i
 }
 
 // group partials -> group 0 (fixed order g = 0..G-1), through smem scratch
-// scratch[((g - 1) h + row) NRHS + c]: (G - 1) h NRHS <= 8 NT (TG >= h/8; NRHS > 1:
+// scratch[c (G - 1) h + (g - 1) h + row]: (G - 1) h NRHS <= 8 NT (TG >= h/8; NRHS > 1:
 // TG >= h/2) doubles, i.e. within one 32-KiB stage for NT <= 512
 template <int NRHS, int MAXQ, int NT>
 __device__ __forceinline__ void sn_group_reduce(const RowLayout& L, int h, double* scratch,
                                                 double (&acc)[MAXQ][2][NRHS]) {
+  // component-major (c, g - 1, row): consecutive rows of one RHS are adjacent
+  // doubles, so the group's row-parallel writes and reads are bank-conflict free
   const int stride = h;
+  const size_t cstride = (size_t)(L.G - 1) * h;
   if (L.g > 0) {
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q)
@@ -189,7 +192,8 @@ __device__ __forceinline__ void sn_group_reduce(const RowLayout& L, int h, doubl
         const int i = 2 * (L.t + q * L.TG) + e;
         if (i < h)
 #pragma unroll
-          for (int c = 0; c < NRHS; ++c) scratch[((size_t)(L.g - 1) * stride + i) * NRHS + c] = acc[q][e][c];
+          for (int c = 0; c < NRHS; ++c)
+            scratch[(size_t)c * cstride + (size_t)(L.g - 1) * stride + i] = acc[q][e][c];
       }
   }
   cons_sync<NT>();
@@ -202,7 +206,8 @@ __device__ __forceinline__ void sn_group_reduce(const RowLayout& L, int h, doubl
           const int i = 2 * (L.t + q * L.TG) + e;
           if (i < h)
 #pragma unroll
-            for (int c = 0; c < NRHS; ++c) acc[q][e][c] += scratch[((size_t)(gg - 1) * stride + i) * NRHS + c];
+            for (int c = 0; c < NRHS; ++c)
+              acc[q][e][c] += scratch[(size_t)c * cstride + (size_t)(gg - 1) * stride + i];
         }
   }
 }
@@ -218,6 +223,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
   // x_R of the current backward part; scratch of the forward group reductions
   // x_R of a backward part (16-B aligned)
   double* xr = x + (size_t)((max_n + 1) & ~1) * NRHS;
+  const int rpad = (max_r + 3) & ~1;   // x_R: NRHS component-major rows of rpad doubles
   constexpr int SN_NT = SnT<CONS>::NT, SN_CONS = CONS;
   // row pairs per thread: up to 4 for one RHS (TG >= h/8); with several RHS
   // TG >= h/2 (sn_lg), so h <= 2048 needs at most 2 with 16 warps -- a smaller
@@ -446,9 +452,9 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       for (int i = tid; i < r; i += SN_NT) {
         const int pr = rows[i];
 #pragma unroll
-        for (int cr = 0; cr < NRHS; ++cr) xr[i * NRHS + cr] = x[pr * NRHS + cr];
+        for (int cr = 0; cr < NRHS; ++cr) xr[cr * rpad + i] = x[pr * NRHS + cr];
       }
-      if ((r & 1) && tid < NRHS) xr[r * NRHS + tid] = 0.0;
+      if ((r & 1) && tid < NRHS) xr[tid * rpad + r] = 0.0;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[cs]);
       PSYNC();
@@ -479,18 +485,12 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
           }
           for (; i < r; i += 2 * lpc) {
             const double2 a = *reinterpret_cast<const double2*>(col + i);
-            if constexpr (NRHS % 2 == 0) {   // x_R rows i, i+1: 2 NRHS contiguous doubles
+            // x_R is component-major (xr[cr rpad + i]): lanes read consecutive
+            // rows, conflict-free (an interleaved layout was 16-way conflicted)
 #pragma unroll
-              for (int cr = 0; cr < NRHS; cr += 2) {
-                const double2 x0 = *reinterpret_cast<const double2*>(xr + i * NRHS + cr);
-                const double2 x1 = *reinterpret_cast<const double2*>(xr + (i + 1) * NRHS + cr);
-                sum[cr] = fma(a.x, x0.x, fma(a.y, x1.x, sum[cr]));
-                sum[cr + 1] = fma(a.x, x0.y, fma(a.y, x1.y, sum[cr + 1]));
-              }
-            } else {
-#pragma unroll
-              for (int cr = 0; cr < NRHS; ++cr)
-                sum[cr] = fma(a.x, xr[i * NRHS + cr], fma(a.y, xr[(i + 1) * NRHS + cr], sum[cr]));
+            for (int cr = 0; cr < NRHS; ++cr) {
+              const double2 xa = *reinterpret_cast<const double2*>(xr + cr * rpad + i);
+              sum[cr] = fma(a.x, xa.x, fma(a.y, xa.y, sum[cr]));
             }
           }
         }
@@ -584,7 +584,13 @@ int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk,
   return 0;   // does not fit
 }
 
-static int cfg_cps(int cons) { return cons == 16 ? 1 : 2; }
+// CTAs per SM of a consumer-warp count; HPLMM_SN_CPS1 (experiment): 8 warps x 1 CTA
+static bool cps1_8() {
+  static const int v = getenv("HPLMM_SN_CPS1") ? 1 : 0;
+  return v;
+}
+int sn_cfg_cps(int cons) { return cons == 16 ? 1 : (cons == 8 && cps1_8() ? 1 : 2); }
+static int cfg_cps(int cons) { return sn_cfg_cps(cons); }
 
 // Chunk size of a batch's solve stream: 32 KiB when the batch runs 8 warps x 2
 // CTAs per SM; a batch that needs 16 x 1 (few subdomains, or x_S too large for
@@ -668,6 +674,7 @@ void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs,
             wk.nblocks, cons, nrhs, max_n, max_r, chunk, stages, smem);
   }
   if (cons == 4) sn_launch_nrhs<4, 2>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
+  else if (cons == 8 && cps1_8()) sn_launch_nrhs<8, 1>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
   else if (cons == 8) sn_launch_nrhs<8, 2>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
   else sn_launch_nrhs<16, 1>(d, io, wk, nrhs, stages, chunk, max_n, max_r, smem, st);
 }

@@ -100,6 +100,7 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
                 int nsm = 148, int shape = 0);
 // shape: 0 = automatic, 8 = 8 consumer warps x 2 CTAs per SM, 16 = 16 x 1
 int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape = 0);
+int sn_cfg_cps(int cons);   // CTAs per SM of a launch shape
 int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk, int shape = 0);
 
 }  // namespace hplmm

@@ -422,8 +422,9 @@ def test_coarse_cholesky_solver(case):
 
 def test_solve_many_reuses_setup():
     """hplmm_solve_many (NEXT #2): several right-hand sides on one setup give
-    the same iterates as separate solves (the correction columns are rebuilt
-    per right-hand side, R15)."""
+    the iterates of separate solves (the correction columns are built per
+    right-hand side, R15): same iteration counts, x to 1e-9 (the block path
+    batches restriction / prolongation, a different summation order)."""
     p, s, h, sv = gpu_case("cfg1")
     rng = np.random.default_rng(4)
     B = np.stack([s.b, rng.standard_normal(s.n_dof), s.b * 2.0])
@@ -431,7 +432,7 @@ def test_solve_many_reuses_setup():
     for i in range(B.shape[0]):
         x, rep, _ = sv.solve(B[i].copy(), tol=1e-8)
         assert reps[i]["converged"] == 1 and reps[i]["iterations"] == rep["iterations"]
-        assert np.array_equal(X[i], x)
+        assert rel(X[i], x) <= 1e-9
         assert np.linalg.norm(B[i] - s.A @ X[i]) / np.linalg.norm(B[i]) < 1e-8
 
 
