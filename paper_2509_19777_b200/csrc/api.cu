@@ -155,6 +155,7 @@ struct hplmm_handle {
   // element-by-element A^ (operator_kind = 0, own assembly only)
   bool ebe = false, matrix_external = false;
   int32_t* d_lat_ebe = nullptr;
+  int32_t* d_lat_all = nullptr;   // lattice -> node id (Dirichlet included) or -1
   double* d_Es = nullptr;
   double K0h[576];
 
@@ -502,7 +503,7 @@ void op_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
       CK(cudaEventCreate(&e1));
       CK(cudaEventRecord(e0, h->st));
     }
-    launch_ebe(h->n_nodes, h->d_ijk, h->d_dir, h->d_lat_ebe, h->d_Es, h->hs.nx, h->hs.ny,
+    launch_ebe(h->n_nodes, h->d_ijk, h->d_dir, h->d_lat_ebe, h->d_lat_all, h->d_Es, h->hs.nx, h->hs.ny,
                h->hs.nz, h->K0h, x, v, y, h->st);
     if (h->profile) {
       CK(cudaEventRecord(e1, h->st));
@@ -1356,6 +1357,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         }
         h->d_Es = h->upload(Es);
         h->d_lat_ebe = h->upload(lat);
+        h->d_lat_all = h->upload(hs.lat_id);
         CK(cudaMemcpyAsync(h->K0h, h->d_K0, sizeof(h->K0h), cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
       }

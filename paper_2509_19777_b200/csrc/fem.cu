@@ -529,12 +529,152 @@ __global__ void __launch_bounds__(128) k_ebe(int n, const int32_t* __restrict__ 
     y[3 * (int64_t)p + r] = RESID ? v[3 * (int64_t)p + r] - out[r] : out[r];
 }
 
+// ---------------------------------------------------------------------------
+// Two lattice nodes per thread (r02): thread t owns the lattice x-pair
+// (2k, j, l), (2k+1, j, l) -- either may be a node, a Dirichlet node or empty.
+// The pair's 36 lattice neighbours (x = 2k-1 .. 2k+2) are looked up and
+// gathered ONCE for both nodes (two single-node threads gather 54), and the
+// 12 voxel moduli around the pair are loaded once (16 for two threads).  With
+// two nodes per thread the per-voxel accumulators of k_ebe would need 48
+// doubles, so each (voxel, neighbour) contribution is scaled by E_v at once:
+// out_r += E_v sum_c K0[3a + r][3b + c] x_c.  All K0 indices are compile-time
+// constants (constant-bank operands); fixed order, deterministic.  Same
+// operator as k_ebe / the stored blocks up to summation order (R4: Dirichlet
+// rows identity, Dirichlet columns skipped).
+// MEASURED SLOWER and therefore off by default (HPLMM_EBE_PAIR=1 selects it):
+// cfg3, one apply 0.104 ms in the solve vs 0.077 ms for k_ebe (100 registers,
+// half the threads and a third more FMAs: the saved gathers do not pay for
+// the lost parallelism).
+// ---------------------------------------------------------------------------
+template <bool RESID>
+__global__ void __launch_bounds__(128) k_ebe2(int64_t npairs, int kx, int nx, int ny, int nz,
+                                              const int32_t* __restrict__ lat_all,
+                                              const int32_t* __restrict__ lat_free,
+                                              const double* __restrict__ Es,
+                                              const __grid_constant__ EbeK0 K0,
+                                              const double* __restrict__ x,
+                                              const double* __restrict__ v,
+                                              double* __restrict__ y) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= npairs) return;
+  const int64_t nx1 = nx + 1, ny1 = ny + 1;
+  const int k = (int)(t % kx);
+  const int64_t jl = t / kx;
+  const int iy = (int)(jl % ny1), iz = (int)(jl / ny1);
+  const int ix = 2 * k;
+  const int64_t key = ix + nx1 * (iy + ny1 * (int64_t)iz);
+  const int np = lat_all[key];
+  const int nq = ix + 1 <= nx ? lat_all[key + 1] : -1;
+  if (np < 0 && nq < 0) return;
+  // free (non-Dirichlet) nodes compute; Dirichlet nodes are identity rows
+  const bool fp = np >= 0 && lat_free[key] >= 0;
+  const bool fq = nq >= 0 && lat_free[key + 1] >= 0;
+  double E[3][2][2];   // voxels vx = ix-1+ox, vy = iy-1+oy, vz = iz-1+oz
+#pragma unroll
+  for (int ox = 0; ox < 3; ++ox)
+#pragma unroll
+    for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+      for (int oz = 0; oz < 2; ++oz) {
+        const int vx = ix - 1 + ox, vy = iy - 1 + oy, vz = iz - 1 + oz;
+        E[ox][oy][oz] = (vx >= 0 && vy >= 0 && vz >= 0 && vx < nx && vy < ny && vz < nz)
+                            ? Es[vx + (int64_t)nx * (vy + (int64_t)ny * vz)]
+                            : 0.0;
+      }
+  // neighbour lookups first (36), then the gathers and the contributions
+  int qs[36];
+#pragma unroll
+  for (int s = 0; s < 36; ++s) {
+    const int kk = s % 4, dy = (s / 4) % 3 - 1, dz = s / 12 - 1;
+    bool any = false;
+#pragma unroll
+    for (int ox = 0; ox < 3; ++ox)
+#pragma unroll
+      for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+        for (int oz = 0; oz < 2; ++oz) {
+          const bool inL = (kk - ox == 0 || kk - ox == 1) && (dy + 1 - oy == 0 || dy + 1 - oy == 1) &&
+                           (dz + 1 - oz == 0 || dz + 1 - oz == 1);
+          if (inL && ((fp && ox <= 1) || (fq && ox >= 1))) any |= E[ox][oy][oz] != 0.0;
+        }
+    qs[s] = any ? lat_free[key + (kk - 1) + nx1 * (dy + ny1 * (int64_t)dz)] : -1;
+  }
+  double op[3] = {0.0, 0.0, 0.0}, oq[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int s = 0; s < 36; ++s) {
+    const int kk = s % 4, dy = (s / 4) % 3 - 1, dz = s / 12 - 1;
+    const int qn = qs[s];
+    if (qn < 0) continue;
+    const double x0 = x[3 * (int64_t)qn], x1 = x[3 * (int64_t)qn + 1], x2 = x[3 * (int64_t)qn + 2];
+#pragma unroll
+    for (int ox = 0; ox < 3; ++ox)
+#pragma unroll
+      for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+        for (int oz = 0; oz < 2; ++oz) {
+          const int bx = kk - ox, by = dy + 1 - oy, bz = dz + 1 - oz;
+          if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+          const int b = bx + 2 * by + 4 * bz;
+          const double Ev = E[ox][oy][oz];
+          if (ox <= 1) {        // node p = (ix, iy, iz): corner (1-ox, 1-oy, 1-oz)
+            const int a = (1 - ox) + 2 * (1 - oy) + 4 * (1 - oz);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              const double* kr = K0.k + (3 * a + r) * 24 + 3 * b;
+              op[r] = fma(Ev, fma(kr[2], x2, fma(kr[1], x1, kr[0] * x0)), op[r]);
+            }
+          }
+          if (ox >= 1) {        // node q = (ix+1, iy, iz): corner (2-ox, 1-oy, 1-oz)
+            const int a = (2 - ox) + 2 * (1 - oy) + 4 * (1 - oz);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              const double* kr = K0.k + (3 * a + r) * 24 + 3 * b;
+              oq[r] = fma(Ev, fma(kr[2], x2, fma(kr[1], x1, kr[0] * x0)), oq[r]);
+            }
+          }
+        }
+  }
+  if (np >= 0) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int64_t d = 3 * (int64_t)np + r;
+      const double av = fp ? op[r] : x[d];
+      y[d] = RESID ? v[d] - av : av;
+    }
+  }
+  if (nq >= 0) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int64_t d = 3 * (int64_t)nq + r;
+      const double av = fq ? oq[r] : x[d];
+      y[d] = RESID ? v[d] - av : av;
+    }
+  }
+}
+
+static int g_ebe_mode = -1;   // 1 = k_ebe (default), 2 = two nodes per thread (k_ebe2)
+
 void launch_ebe(int n_nodes, const int32_t* node_ijk, const uint8_t* dir, const int32_t* lat,
-                const double* Es, int nx, int ny, int nz, const double* K0_host, const double* x,
-                const double* v, double* y, cudaStream_t st) {
+                const int32_t* lat_all, const double* Es, int nx, int ny, int nz,
+                const double* K0_host, const double* x, const double* v, double* y,
+                cudaStream_t st) {
   if (n_nodes <= 0) return;
+  if (g_ebe_mode < 0) {
+    const char* e = getenv("HPLMM_EBE_PAIR");
+    g_ebe_mode = (e && e[0] == '1') ? 2 : 1;
+  }
   EbeK0 k;
   for (int t = 0; t < 576; ++t) k.k[t] = K0_host[t];
+  if (g_ebe_mode == 2 && lat_all) {
+    const int kx = (nx + 2) / 2;   // x-pairs per lattice line (nx + 1 points)
+    const int64_t npairs = (int64_t)kx * (ny + 1) * (nz + 1);
+    const unsigned grid = (unsigned)((npairs + 127) / 128);
+    if (v)
+      k_ebe2<true><<<grid, 128, 0, st>>>(npairs, kx, nx, ny, nz, lat_all, lat, Es, k, x, v, y);
+    else
+      k_ebe2<false><<<grid, 128, 0, st>>>(npairs, kx, nx, ny, nz, lat_all, lat, Es, k, x, v, y);
+    return;
+  }
   const int grid = (n_nodes + 127) / 128;
   if (v)
     k_ebe<true><<<grid, 128, 0, st>>>(n_nodes, node_ijk, dir, lat, Es, nx, ny, nz, k, x, v, y);

@@ -58,6 +58,7 @@ void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const 
 // launch_spmv).  lat: lattice point -> free node id, -1 for no node or a
 // Dirichlet node; Es: E per voxel, 0 where void; K0_host: 576 doubles (host)
 void launch_ebe(int n_nodes, const int32_t* node_ijk, const uint8_t* dir, const int32_t* lat,
+                const int32_t* lat_all,
                 const double* Es, int nx, int ny, int nz, const double* K0_host, const double* x,
                 const double* v, double* y, cudaStream_t st);
 void launch_mortar_weights(int n_iface_nodes, const int32_t* iface_of, const int32_t* iface_ptr,

@@ -396,6 +396,20 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     }
     fprintf(stderr, "hplmm sn_analyse: solve bytes W (fwd+bwd) %.3f GB, F_SS^-1 %.3f GB, rows %.3f GB\n",
             bw / 1e9, bf / 1e9, br / 1e9);
+    int64_t nk[5] = {0, 0, 0, 0, 0}, bk[5] = {0, 0, 0, 0, 0}, small = 0;
+    for (const SnChunk& c : o.chunks) {
+      const int kind = (c.info >> 24) & 7;
+      nk[kind]++;
+      bk[kind] += c.bytes & 0xffffff;
+      small += (c.bytes & 0xffffff) < 8192;
+    }
+    fprintf(stderr, "hplmm sn_analyse: %lld supernodes, %zu chunks (W fwd %lld / %.1f KB avg, F %lld / %.1f KB, "
+            "W bwd %lld / %.1f KB, rows fwd %lld / %.2f KB, rows bwd %lld / %.2f KB), %lld chunks < 8 KB\n",
+            (long long)NS, o.chunks.size(), (long long)nk[0], bk[0] / 1024.0 / std::max<int64_t>(nk[0], 1),
+            (long long)nk[1], bk[1] / 1024.0 / std::max<int64_t>(nk[1], 1), (long long)nk[2],
+            bk[2] / 1024.0 / std::max<int64_t>(nk[2], 1), (long long)nk[3],
+            bk[3] / 1024.0 / std::max<int64_t>(nk[3], 1), (long long)nk[4],
+            bk[4] / 1024.0 / std::max<int64_t>(nk[4], 1), (long long)small);
   }
   if (dbg)
     fprintf(stderr, "hplmm sn_analyse: %d subdomains, %u threads: per-subdomain %.3f s, concat %.3f s, "
