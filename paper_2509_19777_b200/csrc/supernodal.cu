@@ -300,6 +300,10 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
   }
   const int tid = threadIdx.x;
   double acc[SN_MAXQ][2][NRHS];
+  // row positions of a W part whose row list came in its first chunk (group-0
+  // threads keep the rows they scatter to at the part's end)
+  int prow[SN_MAXQ][2];
+  bool rows_held = false;
   int item = wk.item_ptr[blockIdx.x] - 1;
   int n = 0, rc0 = 0, sub = 0;
   int64_t base = 0;
@@ -374,11 +378,26 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     }
     const long long t_k0 = prof ? clock64() : 0;
     if (++s == stages) { s = 0; ph ^= 1; }
+    const int rd = (info & SN_INFO_ROWS) ? (int)sn_rows_doubles(r) : 0;   // row-list prefix
     if (kind == SN_W_FWD || kind == SN_F_FWD) {
       // row-parallel gemv on a column chunk: W_S, F_SS^-1
       const int h = kind == SN_W_FWD ? r : w;
       const int ld = h + (h & 1);
       const RowLayout L(sn_lg<NRHS>(lgc, h), tid, SN_LGNT);
+      if (rd) {   // W_S part with its row list in front: group 0 keeps its rows
+        const int32_t* rows = reinterpret_cast<const int32_t*>(st);
+        if (L.g == 0) {
+#pragma unroll
+          for (int q = 0; q < SN_MAXQ; ++q)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 2 * (L.t + q * L.TG) + e;
+              prow[q][e] = i < r ? rows[i] : -1;
+            }
+        }
+        rows_held = true;
+        st += rd;
+      }
       if (cc0 == 0) {
 #pragma unroll
         for (int q = 0; q < SN_MAXQ; ++q)
@@ -401,15 +420,31 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       }
       if (last) {
         if (L.G > 1) {
-          // the stage just read serves as the scratch of the group reduction;
+          // the stage just read serves as the scratch of the group reduction
+          // (from its base: a row-list prefix is already held in registers);
           // it is released once group 0 has read the partials
-          double* scratch = const_cast<double*>(st);
+          double* scratch = ring + (size_t)cs * stage_doubles;
           PSYNC();
           sn_group_reduce<NRHS, SN_MAXQ, SN_NT>(L, h, scratch, acc);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[cs]);
         }
         if (kind == SN_W_FWD) {
+          if (rows_held) {   // x_R -= W_S x_S (else a ROWS_FWD chunk follows)
+            if (L.g == 0) {
+#pragma unroll
+              for (int q = 0; q < SN_MAXQ; ++q)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int pr = prow[q][e];
+                  if (pr >= 0) {
+#pragma unroll
+                    for (int cr = 0; cr < NRHS; ++cr) x[pr * NRHS + cr] -= acc[q][e][cr];
+                  }
+                }
+            }
+            rows_held = false;
+          }
         } else {
           if (L.G == 1) PSYNC();   // every thread is done reading x_S
           if (L.g == 0) {
@@ -459,6 +494,17 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       if (lane == 0) mbar_arrive(&empty[cs]);
       PSYNC();
     } else {  // SN_W_BWD: x_S[j] -= W[:,j] . x_R, LPC lanes per column
+      if (rd) {   // the row list came first in this chunk: stage x_R as ROWS_BWD does
+        const int32_t* rows = reinterpret_cast<const int32_t*>(st);
+        for (int i = tid; i < r; i += SN_NT) {
+          const int pr = rows[i];
+#pragma unroll
+          for (int cr = 0; cr < NRHS; ++cr) xr[cr * rpad + i] = x[pr * NRHS + cr];
+        }
+        if ((r & 1) && tid < NRHS) xr[tid * rpad + r] = 0.0;
+        PSYNC();
+        st += rd;
+      }
       const int ld = r + (r & 1);
       const int lpc = r > 256 ? 32 : (r > 128 ? 16 : 8);
       const int cpw = 32 / lpc;                    // columns per warp pass

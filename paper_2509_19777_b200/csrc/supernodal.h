@@ -46,12 +46,16 @@ struct SnChunk {
   int32_t bytes;   // [0,24): bytes (multiple of 16); [24,28): log2(TG) - 5, the
                    // row-pair thread-group size of the part (see k_sn_solve)
   int32_t info;    // c0 [0,12) | (ncols-1) [12,24) | kind [24,27) | last-of-part [27]
-                   // | first-of-item [28] | last-of-item [29]
+                   // | first-of-item [28] | last-of-item [29] | rows prefix [30]
   int32_t p0;      // first local DOF of S
   int32_t w, r;    // supernode width / struct rows
   int32_t sub;     // subdomain
 };
 constexpr int SN_INFO_LAST = 1 << 27, SN_INFO_FIRST_ITEM = 1 << 28, SN_INFO_LAST_ITEM = 1 << 29;
+// [30]: the chunk starts with the supernode's row list (rows header, then the
+// first W_S columns): the first W_FWD / W_BWD chunk of a part carries the rows
+// that a separate ROWS_FWD / ROWS_BWD chunk would otherwise bring
+constexpr int SN_INFO_ROWS = 1 << 30;
 
 // rows header of a supernode in the factor array: r int32 padded to 16 bytes
 #ifdef __CUDACC__

@@ -339,7 +339,8 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
   // TMA chunk schedule: forward = (W_S, rows, F_SS^-1) per S in postorder,
   // backward = (rows, W_S) per S in reverse postorder; W/F chunks are whole
   // columns of at most SN_CHUNK_DOUBLES.
-  auto push = [&](int sn, int kind, int64_t off, int bytes, int c0, int nc, bool last) {
+  auto push = [&](int sn, int kind, int64_t off, int bytes, int c0, int nc, bool last,
+                  bool rows_prefix = false) {
     SnChunk ch;
     ch.off = off;
     // thread-group size for the rows of this part: TG = pow2 >= max(32, ceil(h/8)),
@@ -348,19 +349,38 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     int lg = 5;
     while ((1 << lg) < (h + 7) / 8 && lg < 9) ++lg;
     ch.bytes = bytes | ((lg - 5) << 24);
-    ch.info = c0 | ((nc - 1) << 12) | (kind << 24) | (last ? SN_INFO_LAST : 0);
+    ch.info = c0 | ((nc - 1) << 12) | (kind << 24) | (last ? SN_INFO_LAST : 0) |
+              (rows_prefix ? SN_INFO_ROWS : 0);
     ch.p0 = o.sn_p0[sn];
     ch.w = o.sn_w[sn];
     ch.r = o.sn_r[sn];
     ch.sub = o.sn_sub[sn];
     o.chunks.push_back(ch);
   };
-  auto cols = [&](int sn, int kind, int64_t off0, int ld, int ncols_total) {
+  // W_S / F_SS^-1 as whole-column chunks; a W part may take the supernode's row
+  // list (stored right before W_S) into its first chunk (returns true then):
+  // 21% of the chunks at cfg3 were row lists of ~0.6 KB, each a ring slot and a
+  // consumer round trip of its own (HPLMM_SN_PACK=0: separate row chunks)
+  static const bool pack_rows = !(getenv("HPLMM_SN_PACK") && getenv("HPLMM_SN_PACK")[0] == '0');
+  auto cols = [&](int sn, int kind, int64_t off0, int ld, int ncols_total, int64_t rows_at = -1,
+                  int rd = 0) {
+    int c0 = 0;
+    bool packed = false;
+    if (rows_at >= 0 && pack_rows) {
+      const int per1 = (o.chunk_doubles - rd) / ld;
+      if (per1 >= 1) {
+        const int nc = std::min(per1, ncols_total);
+        push(sn, kind, rows_at, (rd + nc * ld) * 8, 0, nc, nc == ncols_total, true);
+        c0 = nc;
+        packed = true;
+      }
+    }
     const int per = std::max(1, o.chunk_doubles / ld);
-    for (int c0 = 0; c0 < ncols_total; c0 += per) {
+    for (; c0 < ncols_total; c0 += per) {
       int nc = std::min(per, ncols_total - c0);
       push(sn, kind, off0 + (int64_t)c0 * ld, nc * ld * 8, c0, nc, c0 + nc == ncols_total);
     }
+    return packed;
   };
   for (int s = 0; s < nsub; ++s) {
     int64_t fb = 0;
@@ -370,8 +390,8 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
       const int64_t rows_at = o.sn_foff[k], w_at = rows_at + sn_rows_doubles(r);
       const int64_t f_at = w_at + (int64_t)o.sn_ldw[k] * w;
       if (r > 0) {
-        cols(k, SN_W_FWD, w_at, o.sn_ldw[k], w);
-        push(k, SN_ROWS_FWD, rows_at, (int)(8 * sn_rows_doubles(r)), 0, 1, true);
+        if (!cols(k, SN_W_FWD, w_at, o.sn_ldw[k], w, rows_at, (int)sn_rows_doubles(r)))
+          push(k, SN_ROWS_FWD, rows_at, (int)(8 * sn_rows_doubles(r)), 0, 1, true);
       }
       cols(k, SN_F_FWD, f_at, o.sn_ldf[k], w);
       fb += 8 * (2 * sn_rows_doubles(r) + 2 * (int64_t)o.sn_ldw[k] * w + (int64_t)o.sn_ldf[k] * w);
@@ -381,8 +401,13 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     for (int k = o.sub_sn1[s] - 1; k >= o.sub_sn0[s]; --k) {
       const int r = o.sn_r[k];
       if (r == 0) continue;
-      push(k, SN_ROWS_BWD, o.sn_foff[k], (int)(8 * sn_rows_doubles(r)), 0, 1, true);
-      cols(k, SN_W_BWD, o.sn_foff[k] + sn_rows_doubles(r), o.sn_ldw[k], o.sn_w[k]);
+      if (pack_rows && (o.chunk_doubles - sn_rows_doubles(r)) / o.sn_ldw[k] >= 1) {
+        cols(k, SN_W_BWD, o.sn_foff[k] + sn_rows_doubles(r), o.sn_ldw[k], o.sn_w[k], o.sn_foff[k],
+             (int)sn_rows_doubles(r));
+      } else {
+        push(k, SN_ROWS_BWD, o.sn_foff[k], (int)(8 * sn_rows_doubles(r)), 0, 1, true);
+        cols(k, SN_W_BWD, o.sn_foff[k] + sn_rows_doubles(r), o.sn_ldw[k], o.sn_w[k]);
+      }
     }
     o.sub_bc1.push_back((int64_t)o.chunks.size());
     o.sub_fbytes.push_back(fb);
