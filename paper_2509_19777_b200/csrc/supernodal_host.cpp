@@ -343,11 +343,17 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
                   bool rows_prefix = false) {
     SnChunk ch;
     ch.off = off;
-    // thread-group size for the rows of this part: TG = pow2 >= max(32, ceil(h/8)),
-    // so a thread holds up to 4 row pairs and the remaining threads take other columns
+    // thread-group size for the rows of this part: TG = pow2 >= max(64, ceil(h/8)),
+    // so a thread holds up to 4 row pairs and the remaining threads take other
+    // columns.  The floor 64 (r02; r01: 32) halves the column groups of the
+    // small parts -- fewer partial sums to reduce at each part end: cfg3
+    // contact / grain apply 1.834 / 1.270 -> 1.789 / 1.256 ms; 128 (G <= 2)
+    // 1.875 / 1.292, 256 2.25 / 1.47 (HPLMM_SN_TGMIN = log2 floor)
     const int h = (kind == SN_F_FWD) ? o.sn_w[sn] : o.sn_r[sn];
-    int lg = 5;
-    while ((1 << lg) < (h + 7) / 8 && lg < 9) ++lg;
+    static const int lg0 = getenv("HPLMM_SN_TGMIN") ? atoi(getenv("HPLMM_SN_TGMIN")) : 6;
+    static const int hdiv = getenv("HPLMM_SN_TGDIV") ? atoi(getenv("HPLMM_SN_TGDIV")) : 8;
+    int lg = lg0;
+    while ((1 << lg) < (h + hdiv - 1) / hdiv && lg < 9) ++lg;
     ch.bytes = bytes | ((lg - 5) << 24);
     ch.info = c0 | ((nc - 1) << 12) | (kind << 24) | (last ? SN_INFO_LAST : 0) |
               (rows_prefix ? SN_INFO_ROWS : 0);
