@@ -700,7 +700,8 @@ void multi_alloc(hplmm_handle* h) {
   M.sng = h->dalloc<double>((size_t)K * std::max<int64_t>(h->sg.n_loc, 1));
   const int hbn = 2 * (m + 1) + 8;
   M.hb = h->dalloc<double>((size_t)K * hbn);
-  M.partial = h->dalloc<double>((size_t)K * krylov_blocks(h->n_dof) * (m + 1));
+  M.partial = h->dalloc<double>((size_t)krylov_partial_doubles(h->n_dof));
+  CK(cudaMemsetAsync(M.partial, 0, (size_t)krylov_partial_doubles(h->n_dof) * 8, h->st));
   CK(cudaMallocHost(&M.h_hb, (size_t)K * hbn * 8));
 }
 
@@ -1999,7 +2000,8 @@ hplmm_status hplmm_solve(hplmm_handle* h, const double* b, double tol, double* x
     if (h->Vcap < m + 1) {
       h->ldv = ((int64_t)n + 31) / 32 * 32;
       h->d_V = h->dalloc<double>((size_t)(m + 1) * h->ldv);
-      h->d_partial = h->dalloc<double>((size_t)krylov_blocks(n) * (m + 1));
+      h->d_partial = h->dalloc<double>((size_t)krylov_partial_doubles(n));
+        CK(cudaMemsetAsync(h->d_partial, 0, (size_t)krylov_partial_doubles(n) * 8, h->st));
       h->d_hbuf = h->dalloc<double>(2 * (m + 1) + 8);
       h->Vcap = m + 1;
     }
@@ -2176,7 +2178,8 @@ hplmm_status hplmm_solve_many(hplmm_handle* h, int32_t nrhs, const double* B, do
       if (h->Vcap < m + 1) {
         h->ldv = ((int64_t)n + 31) / 32 * 32;
         h->d_V = h->dalloc<double>((size_t)(m + 1) * h->ldv);
-        h->d_partial = h->dalloc<double>((size_t)krylov_blocks(n) * (m + 1));
+        h->d_partial = h->dalloc<double>((size_t)krylov_partial_doubles(n));
+        CK(cudaMemsetAsync(h->d_partial, 0, (size_t)krylov_partial_doubles(n) * 8, h->st));
         h->d_hbuf = h->dalloc<double>(2 * (m + 1) + 8);
         h->Vcap = m + 1;
       }

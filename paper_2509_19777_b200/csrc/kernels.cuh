@@ -192,6 +192,9 @@ void launch_sum_contact(int n_dof, const int32_t* cptr, const int32_t* cidx, con
 
 // ---- Krylov (krylov.cu) ----------------------------------------------------
 int krylov_blocks(int64_t n);
+// doubles of a handle's Krylov partial-sum buffer (incl. its completion counter;
+// allocate zeroed)
+int64_t krylov_partial_doubles(int64_t n);
 // partial[b*m + j] = sum over block b of V[j][i] * w[i], j < m; final[j] = sum_b
 // cnt (optional, device): vector count = *cnt + 1 read by the kernels (m = its maximum)
 void launch_multidot(int64_t n, int m, const double* V, int64_t ldv, const double* w,

@@ -20,6 +20,51 @@ int krylov_blocks(int64_t n) {
   return (int)b;
 }
 
+// multi-dot blocks: half as many, each over twice the range (fewer per-group
+// block reductions per byte; cfg3 j = 20: 5.6 vs 5.5 TB/s, tools/micro)
+static int md_blocks(int64_t n) {
+  int64_t b = (n + 8 * KT - 1) / (8 * KT);
+  if (b > 148 * 4) b = 148 * 4;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// The partial-sum buffer of a handle: up to 513 (= max restart + 1) partial
+// vectors of krylov_blocks(n) entries, then a completion counter (zeroed once
+// at allocation, reset by the last block of every launch).
+int64_t krylov_partial_doubles(int64_t n) { return (int64_t)krylov_blocks(n) * 513 + 8; }
+static unsigned* krylov_counter(double* partial, int64_t n) {
+  return reinterpret_cast<unsigned*>(partial + (int64_t)krylov_blocks(n) * 513);
+}
+
+// Last-block completion: every block publishes its partials, then takes a
+// ticket; the block drawing the last ticket sums the partials in a fixed
+// order (so the result is bitwise the separate k_final_sum's) and resets the
+// counter.  Saves one launch per reduction (and its ~10-30 us of latency).
+__device__ __forceinline__ bool last_block(unsigned* counter) {
+  __shared__ unsigned ticket;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(counter, 1u);
+  __syncthreads();
+  const bool last = ticket == gridDim.x - 1;
+  if (last) __threadfence();
+  return last;
+}
+
+// out[j] = sum_b partial[j nb + b], j < m: warp per j, lane-strided partial
+// sums in b order, then a fixed butterfly
+__device__ __forceinline__ void final_sums(int nb, int m, const double* partial, double* out) {
+  const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = wp; j < m; j += blockDim.x >> 5) {
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += __ldcg(partial + (int64_t)j * nb + b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[j] = s;
+  }
+}
+
 __device__ __forceinline__ double block_sum(double v, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -52,7 +97,9 @@ __device__ __forceinline__ int vec_count(int m, const int* cnt) { return cnt ? *
 __global__ void __launch_bounds__(KT) k_multidot(int64_t n, int m, const double* __restrict__ V,
                                                  int64_t ldv, const double* __restrict__ w,
                                                  double* __restrict__ partial,
-                                                 const int* __restrict__ cnt) {
+                                                 const int* __restrict__ cnt,
+                                                 double* __restrict__ out,
+                                                 unsigned* __restrict__ counter) {
   __shared__ double red[MD_J][KT / 32];
   m = vec_count(m, cnt);
   const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -93,33 +140,21 @@ __global__ void __launch_bounds__(KT) k_multidot(int64_t n, int m, const double*
     if (threadIdx.x < nj) {
       double t = 0.0;
       for (int q = 0; q < KT / 32; ++q) t += red[threadIdx.x][q];
-      partial[(int64_t)blockIdx.x * m + j0 + threadIdx.x] = t;
+      partial[(int64_t)(j0 + threadIdx.x) * gridDim.x + blockIdx.x] = t;
     }
   }
-}
-
-// out[j] = sum_b partial[b*m + j]: one warp per j, fixed lane assignment and
-// fixed butterfly (deterministic)
-__global__ void k_final_sum(int nb, int m, const double* __restrict__ partial,
-                            double* __restrict__ out, const int* __restrict__ cnt = nullptr) {
-  m = vec_count(m, cnt);
-  int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (j >= m) return;
-  double s = 0.0;
-  for (int b = lane; b < nb; b += 32) s += partial[(int64_t)b * m + j];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[j] = s;
+  if (last_block(counter)) {
+    final_sums(gridDim.x, m, partial, out);
+    if (threadIdx.x == 0) *counter = 0u;
+  }
 }
 
 void launch_multidot(int64_t n, int m, const double* V, int64_t ldv, const double* w,
                      double* partial, double* out, cudaStream_t st, const int* cnt) {
-  // with a device count, m is the largest count (grid of the final sums) and
-  // partial holds nb x (count) entries laid out with the device count
-  int nb = krylov_blocks(n);
-  k_multidot<<<nb, KT, 0, st>>>(n, m, V, ldv, w, partial, cnt);
-  k_final_sum<<<(m + 3) / 4, 128, 0, st>>>(nb, m, partial, out, cnt);
+  // with a device count, m is the largest count; partial holds (count) x nb
+  // entries, summed by the last block
+  const int nb = md_blocks(n);
+  k_multidot<<<nb, KT, 0, st>>>(n, m, V, ldv, w, partial, cnt, out, krylov_counter(partial, n));
 }
 
 // w -= sum_j V[j] h[j]   (+ partial ||w||^2 per block); per element the
@@ -127,7 +162,9 @@ void launch_multidot(int64_t n, int m, const double* V, int64_t ldv, const doubl
 __global__ void __launch_bounds__(KT) k_update(int64_t n, int m, const double* __restrict__ V,
                                                int64_t ldv, const double* __restrict__ h,
                                                double* __restrict__ w, double* __restrict__ partial,
-                                               const int* __restrict__ cnt) {
+                                               const int* __restrict__ cnt,
+                                               double* __restrict__ out_norm2,
+                                               unsigned* __restrict__ counter) {
   __shared__ double hs[513];
   __shared__ double red[KT / 32];
   m = vec_count(m, cnt);
@@ -172,18 +209,24 @@ __global__ void __launch_bounds__(KT) k_update(int64_t n, int m, const double* _
   if (partial) {
     double t = block_sum(s, red);
     if (threadIdx.x == 0) partial[blockIdx.x] = t;
+    if (last_block(counter)) {
+      final_sums(gridDim.x, 1, partial, out_norm2);
+      if (threadIdx.x == 0) *counter = 0u;
+    }
   }
 }
 
 void launch_update(int64_t n, int m, const double* V, int64_t ldv, const double* h, double* w,
                    double* partial, double* out_norm2, cudaStream_t st, const int* cnt) {
   int nb = krylov_blocks(n);
-  k_update<<<nb, KT, 0, st>>>(n, m, V, ldv, h, w, out_norm2 ? partial : nullptr, cnt);
-  if (out_norm2) k_final_sum<<<1, 32, 0, st>>>(nb, 1, partial, out_norm2);
+  k_update<<<nb, KT, 0, st>>>(n, m, V, ldv, h, w, out_norm2 ? partial : nullptr, cnt, out_norm2,
+                              out_norm2 ? krylov_counter(partial, n) : nullptr);
 }
 
 __global__ void __launch_bounds__(KT) k_norm2(int64_t n, const double* __restrict__ x,
-                                              double* __restrict__ partial) {
+                                              double* __restrict__ partial,
+                                              double* __restrict__ out,
+                                              unsigned* __restrict__ counter) {
   __shared__ double red[KT / 32];
   int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   int64_t i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
@@ -191,12 +234,15 @@ __global__ void __launch_bounds__(KT) k_norm2(int64_t n, const double* __restric
   for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) s = fma(x[i], x[i], s);
   double t = block_sum(s, red);
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    final_sums(gridDim.x, 1, partial, out);
+    if (threadIdx.x == 0) *counter = 0u;
+  }
 }
 
 void launch_norm2(int64_t n, const double* x, double* partial, double* out, cudaStream_t st) {
   int nb = krylov_blocks(n);
-  k_norm2<<<nb, KT, 0, st>>>(n, x, partial);
-  k_final_sum<<<1, 32, 0, st>>>(nb, 1, partial, out);
+  k_norm2<<<nb, KT, 0, st>>>(n, x, partial, out, krylov_counter(partial, n));
 }
 
 // y = x * s  (invert: y = x / sqrt(s))
