@@ -646,7 +646,17 @@ static int cfg_cps(int cons) { return sn_cfg_cps(cons); }
 int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape) {
   if (getenv("HPLMM_SN_CHUNK")) return sn_chunk_doubles();
   const int base = sn_chunk_doubles();
-  if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base, shape) == 8) return base;
+  if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base, shape) == 8) {
+    // the largest chunk (2 KiB steps) that keeps two 8-warp CTAs per SM with
+    // two stages: the solve's cost is per chunk more than per byte (cfg3
+    // contact batch: 32 KiB 1.79 ms, 36 KiB 1.74 ms, 38 KiB 1.70 ms)
+    int best = base;
+    for (int c = base + 256; c <= SN_CHUNK_DOUBLES_MAX; c += 256) {
+      if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape) != 8) break;
+      best = c;
+    }
+    return best;
+  }
   // enough subdomains for 8 x 2 but x_S leaves no room for two 32-KiB stages:
   // smaller chunks keep the 8 x 2 shape (far cheaper per byte than 16 x 1)
   for (int c : {3072, 2048})
