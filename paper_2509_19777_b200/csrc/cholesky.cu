@@ -146,13 +146,9 @@ __global__ void __launch_bounds__(256) k_chol_update(int k, int nb, double* tile
 void launch_chol_factor(const DevBatch& b, double* linv, double* linvT, cudaStream_t st) {
   const int nb = b.max_nb;
   const size_t sm = 2 * TILE * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
+  set_max_dynamic_smem((const void*)k_chol_diag, sm);
+  set_max_dynamic_smem((const void*)k_chol_panel, sm);
+  set_max_dynamic_smem((const void*)k_chol_update, sm);
   for (int k = 0; k < nb; ++k) {
     k_chol_diag<<<1, 256, sm, st>>>(k, b.tiles, linv, linvT, b.err);
     if (k + 1 < nb) {
@@ -353,30 +349,27 @@ __global__ void __launch_bounds__(32 * TR_WARPS, 1)
   }
 }
 
-static int g_nsm_tr = 0;
-
 void launch_chol_solve(const DevBatch& b, const double* linv, const double* linvT,
                        const double* r, double* zbuf, double* y, int* flags_fwd, int* flags_bwd,
                        int epoch, cudaStream_t st) {
   const int nb = b.max_nb;
   if (nb <= 0) return;
-  if (!g_nsm_tr) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_nsm_tr, cudaDevAttrMultiProcessorCount, dev);
-  }
-  // one CTA per SM at most: every CTA must be resident (they wait on each other)
-  const int grid = std::min(nb, g_nsm_tr);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_trsv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    cudaFuncSetAttribute(k_trsv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    attr = true;
-  }
-  k_trsv_fwd<<<grid, 32 * TR_WARPS, 2 * TILE * 8, st>>>(nb, b.tiles, linv, r, zbuf, flags_fwd,
-                                                        epoch);
-  k_trsv_bwd<<<grid, 32 * TR_WARPS, 2 * TILE * 8, st>>>(nb, b.tiles, linvT, zbuf, y, flags_bwd,
-                                                        epoch);
+  // one CTA per SM at most, and a COOPERATIVE launch: the CTAs wait on each
+  // other's rows, so they must all be resident -- the launch fails (loudly,
+  // checked by the caller) instead of hanging when co-residency is impossible
+  // (MPS SM limits, concurrent kernels holding SMs)
+  int grid = std::min(nb, device_sm_count());
+  set_max_dynamic_smem((const void*)k_trsv_fwd, 2 * TILE * 8);
+  set_max_dynamic_smem((const void*)k_trsv_bwd, 2 * TILE * 8);
+  const double* tiles = b.tiles;
+  void* af[] = {(void*)&nb, (void*)&tiles, (void*)&linv, (void*)&r, (void*)&zbuf, (void*)&flags_fwd,
+                (void*)&epoch};
+  cudaLaunchCooperativeKernel((const void*)k_trsv_fwd, dim3(grid), dim3(32 * TR_WARPS), af,
+                              2 * TILE * 8, st);
+  void* ab[] = {(void*)&nb, (void*)&tiles, (void*)&linvT, (void*)&zbuf, (void*)&y, (void*)&flags_bwd,
+                (void*)&epoch};
+  cudaLaunchCooperativeKernel((const void*)k_trsv_bwd, dim3(grid), dim3(32 * TR_WARPS), ab,
+                              2 * TILE * 8, st);
 }
 
 }  // namespace hplmm

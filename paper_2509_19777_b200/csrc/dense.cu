@@ -16,7 +16,35 @@
 #include "dmma.cuh"
 #include "tma.cuh"
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace hplmm {
+
+void set_max_dynamic_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, func}];
+  if (bytes > have) {
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    have = bytes;
+  }
+}
+
+int device_sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  int& n = cache[dev];
+  if (n == 0) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
 
 // ---------------------------------------------------------------------------
 // 64x64x64 fp64 tile product core (256 threads, 4x4 outputs each):
@@ -323,15 +351,11 @@ static void sweep_steps(const DevBatch& b, cudaStream_t st) {
 
 void launch_sweep_invert(const DevBatch& b, cudaStream_t st) {
   if (b.nsub <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    cudaFuncSetAttribute(k_sweep_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    cudaFuncSetAttribute(k_sweep_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TB * 72 * 8);
-    cudaFuncSetAttribute(k_sweep_panel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    cudaFuncSetAttribute(k_sweep_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    attr = true;
-  }
+  set_max_dynamic_smem((const void*)k_sweep_pivot, 2 * TILE * 8);
+  set_max_dynamic_smem((const void*)k_sweep_panel<true>, 2 * TILE * 8);
+  set_max_dynamic_smem((const void*)k_sweep_update<true>, 2 * TB * 72 * 8);
+  set_max_dynamic_smem((const void*)k_sweep_panel<false>, 2 * TILE * 8);
+  set_max_dynamic_smem((const void*)k_sweep_update<false>, 2 * TILE * 8);
   if (use_dmma()) sweep_steps<true>(b, st);
   else sweep_steps<false>(b, st);
   k_negate<<<148 * 8, 256, 0, st>>>(b.ntiles * TILE, b.tiles);
@@ -596,21 +620,16 @@ void launch_gather(const DevBatch& b, const double* x, cudaStream_t st) {
 }
 
 static int g_symv_mode = -1;   // 0 = register kernel, 1 = TMA pipeline (default)
-static int g_num_sms = 0;
 
 void launch_symv_tiles(const DevBatch& b, cudaStream_t st) {
   if (b.ntiles <= 0) return;
   if (g_symv_mode < 0) {
     const char* e = getenv("HPLMM_SYMV");
     g_symv_mode = (e && e[0] == '0') ? 0 : 1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_symv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SY_STAGES * TILE * 8);
   }
   if (g_symv_mode == 1) {
-    int64_t grid = std::min<int64_t>(g_num_sms, b.ntiles);
+    set_max_dynamic_smem((const void*)k_symv_tma, SY_STAGES * TILE * 8);
+    int64_t grid = std::min<int64_t>(device_sm_count(), b.ntiles);
     k_symv_tma<<<(unsigned)grid, 32 * (SY_CONS + 1), SY_STAGES * TILE * 8, st>>>(
         b.ntiles, b.tile_s, b.tile_ij, b.row_base, b.tiles, b.xloc, b.part_row, b.part_col);
     return;
@@ -681,11 +700,7 @@ void launch_symm_neg(const DevBatch& b, const int64_t* x_off, const int32_t* ld,
                      const int32_t* kcols, int max_kchunks, const double* X, double* B,
                      cudaStream_t st) {
   if (b.nrows <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_symm_neg, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TILE * 8);
-    attr = true;
-  }
+  set_max_dynamic_smem((const void*)k_symm_neg, 2 * TILE * 8);
   // grid.y = max column chunks; CTAs beyond a grain's k exit immediately
   if (max_kchunks <= 0) return;
   dim3 grid((unsigned)b.nrows, (unsigned)max_kchunks);

@@ -365,14 +365,8 @@ template <int ROWS, int CONS, int STAGES, int CPS = 1>
 static void spmv_tma(int n, const int32_t* rp, const int32_t* col, const double* val,
                      const double* x, const double* v, double* y, cudaStream_t st, int nsm) {
   constexpr int SM = STAGES * SpCfg<ROWS>::STAGE;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_spmv_tma<true, ROWS, CONS, STAGES, CPS>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
-    cudaFuncSetAttribute(k_spmv_tma<false, ROWS, CONS, STAGES, CPS>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
-    attr = true;
-  }
+  set_max_dynamic_smem((const void*)k_spmv_tma<true, ROWS, CONS, STAGES, CPS>, SM);
+  set_max_dynamic_smem((const void*)k_spmv_tma<false, ROWS, CONS, STAGES, CPS>, SM);
   int nchunks = (n + ROWS - 1) / ROWS;
   int grid = std::min(nsm * CPS, nchunks);
   if (v)
@@ -382,7 +376,6 @@ static void spmv_tma(int n, const int32_t* rp, const int32_t* col, const double*
 }
 
 static int g_spmv_mode = -1;   // >=1 TMA streaming variants (default 1), 0 = warp-per-row staging
-static int g_num_sms_spmv = 0;
 
 // max_row_blocks: the caller's bound on blocks per row (TMA kernel needs <= 27)
 void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const double* val,
@@ -392,15 +385,12 @@ void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const 
   if (g_spmv_mode < 0) {
     const char* e = getenv("HPLMM_SPMV");
     g_spmv_mode = e ? atoi(e) : 6;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms_spmv, cudaDevAttrMultiProcessorCount, dev);
   }
   // TMA-streamed kernel (measured best of the ROWS / CONS / STAGES variants on
   // B200, profiles/r01_spmv_variants.txt: 8-row chunks, 3 consumer warps x 2
   // stages, 2 CTAs per SM); HPLMM_SPMV=0 selects the plain warp-per-row kernel
   if (g_spmv_mode != 0 && max_row_blocks <= SP_MAXB) {
-    spmv_tma<8, 3, 6, 2>(n_nodes, row_ptr, col, val, x, v, y, st, g_num_sms_spmv);
+    spmv_tma<8, 3, 6, 2>(n_nodes, row_ptr, col, val, x, v, y, st, device_sm_count());
     return;
   }
   int grid = (n_nodes + SPMV_WARPS - 1) / SPMV_WARPS;

@@ -329,14 +329,14 @@ __global__ void k_lincomb(int64_t n, const double* __restrict__ a, const double*
 }
 
 int ilu_grid(int n) {
-  static int cap = 0;
-  if (!cap) {
-    int dev = 0, nsm = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_factor, 32 * ILU_WARPS, 0);
-    cap = nsm * std::max(occ, 1);
-  }
+  // (the tickets hand rows to running warps only, so the grid need not be
+  // co-resident; sized to what fits at once on the current device)
+  static const int occ = [] {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_ilu_factor, 32 * ILU_WARPS, 0);
+    return std::max(o, 1);
+  }();
+  const int cap = device_sm_count() * occ;
   return std::max(1, std::min(cap, (n + ILU_WARPS - 1) / ILU_WARPS));
 }
 

@@ -190,6 +190,13 @@ void launch_combine_grain(int n_dof, const int32_t* gpos, const double* yloc, co
 void launch_sum_contact(int n_dof, const int32_t* cptr, const int32_t* cidx, const double* yloc,
                         double* out, cudaStream_t st);
 
+// ---- per-device launch helpers (dense.cu) --------------------------------------
+// Dynamic shared-memory opt-in of a kernel on the CURRENT device (function
+// attributes belong to a device context: cached per (device, kernel),
+// thread-safe) and the current device's SM count.
+void set_max_dynamic_smem(const void* func, size_t bytes);
+int device_sm_count();
+
 // ---- Krylov (krylov.cu) ----------------------------------------------------
 int krylov_blocks(int64_t n);
 // doubles of a handle's Krylov partial-sum buffer (incl. its completion counter;

@@ -676,12 +676,7 @@ int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons) {
 template <int NRHS, int CONS, int CPS>
 static void sn_solve_launch(const SnDev& d, const SnIO& io, const SnWork& wk, int stages,
                             int chunk, int max_n, int max_r, size_t smem, cudaStream_t st) {
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_sn_solve<NRHS, CONS, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = smem;
-  }
+  set_max_dynamic_smem((const void*)k_sn_solve<NRHS, CONS, CPS>, smem);
   static int flags = -1;
   if (flags < 0) {
     const char* e = getenv("HPLMM_SN_FLAGS");
