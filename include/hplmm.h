@@ -310,6 +310,19 @@ typedef enum {
 hplmm_status hplmm_apply(hplmm_handle *h, int32_t op, const double *in, double *out,
                          void *stream);
 
+/* Block application of a local operator to ncols (1..4) vectors at once --
+ * the batched form hplmm_solve_many uses:
+ * the supernodal factors of the contact grids / grains stream once per block
+ * (k_sn_solve with NRHS = 2 or 4 columns) instead of once per vector.
+ * op: HPLMM_OP_MZETA, HPLMM_OP_MGRAIN or HPLMM_OP_MCG (the operators that do
+ * not depend on the right-hand side; eq:Mg_Mz, eq:local_smoother_CG).  Column
+ * c of in / out is in + c ldin / out + c ldout (ldin, ldout >= n_dof), host or
+ * device; out[c] equals hplmm_apply(op, in[c]) up to the summation order of
+ * the group reductions.  Needs local_factor = 1 (supernodal) and smoother = 0
+ * (else HPLMM_ERR_STATE); ncols outside 1..4 or a bad op: HPLMM_ERR_ARG. */
+hplmm_status hplmm_apply_many(hplmm_handle *h, int32_t op, int32_t ncols, const double *in,
+                              int64_t ldin, double *out, int64_t ldout, void *stream);
+
 typedef enum {
   HPLMM_ART_NODE_KEY = 0,     /* int64[n_nodes] lattice key of each node (R3)   */
   HPLMM_ART_ROW_PTR = 1,      /* int32[n_nodes+1]                               */

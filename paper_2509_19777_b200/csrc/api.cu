@@ -113,6 +113,8 @@ struct hplmm_handle {
     double *Ck = nullptr, *Dck = nullptr, *tk = nullptr, *gk = nullptr, *yk = nullptr, *rm = nullptr,
            *rc = nullptr, *ym = nullptr, *yc = nullptr, *snc = nullptr, *sng = nullptr;
     double *hb = nullptr, *partial = nullptr, *h_hb = nullptr;
+    // block coarse solve (S^-1 streamed once for the block; null: per column)
+    double *cx = nullptr, *cy = nullptr, *cpr = nullptr, *cpc = nullptr;
   } mr;
   int64_t ldv = 0;
   int Vcap = 0;
@@ -679,6 +681,7 @@ bool multi_eligible(hplmm_handle* h) {
 void multi_alloc(hplmm_handle* h) {
   auto& M = h->mr;
   if (M.K) return;
+  if (!h->ldv) h->ldv = ((int64_t)h->n_dof + 31) / 32 * 32;   // as hplmm_solve sets it
   const int m = h->hs.opt.restart;
   const int64_t ld = h->ldv;
   const int K = kMaxBlock;
@@ -700,6 +703,19 @@ void multi_alloc(hplmm_handle* h) {
   M.sng = h->dalloc<double>((size_t)K * std::max<int64_t>(h->sg.n_loc, 1));
   const int hbn = 2 * (m + 1) + 8;
   M.hb = h->dalloc<double>((size_t)K * hbn);
+  // block SYMV buffers when the coarse solve is the plain S^-1 apply and the
+  // per-column partials take < 1/8 of the free memory (else per column)
+  if (!h->chol() && !h->hs.opt.coarse_refine && h->sb.ntiles > 0) {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const size_t need = (size_t)K * 8 * (2 * h->sb.nloc + 2 * h->sb.ntiles * 64);
+    if (need < fr / 8) {
+      M.cx = h->dalloc<double>((size_t)K * h->sb.nloc);
+      M.cy = h->dalloc<double>((size_t)K * h->sb.nloc);
+      M.cpr = h->dalloc<double>((size_t)K * h->sb.ntiles * 64);
+      M.cpc = h->dalloc<double>((size_t)K * h->sb.ntiles * 64);
+    }
+  }
   M.partial = h->dalloc<double>((size_t)krylov_partial_doubles(h->n_dof));
   CK(cudaMemsetAsync(M.partial, 0, (size_t)krylov_partial_doubles(h->n_dof) * 8, h->st));
   CK(cudaMallocHost(&M.h_hb, (size_t)K * hbn * 8));
@@ -712,10 +728,19 @@ void op_mg_k(hplmm_handle* h, int ncols, const double* in, double* out) {
   const int Nm = h->co.Nm, G = h->co.n_grains;
   const int64_t ld = h->ldv;
   launch_restrict_k(h->co, P, in, ld, ncols, M.Ck, h->gb.nloc, M.Dck, M.tk, M.gk, M.rm, M.rc, h->st);
-  for (int c = 0; c < ncols; ++c) {
-    if (Nm <= 0) break;
-    const double* ymc = op_coarse(h, M.rm + (int64_t)c * Nm);
-    CK(cudaMemcpyAsync(M.ym + (int64_t)c * Nm, ymc, (size_t)Nm * 8, cudaMemcpyDeviceToDevice, h->st));
+  if (Nm > 0 && M.cx) {   // S^-1 applied to the block in one pass over its tiles
+    launch_gather_k(h->sb, ncols, M.rm, Nm, M.cx, h->st);
+    launch_symv_k(h->sb, P, ncols, M.cx, M.cy, M.cpr, M.cpc, h->st);
+    CK(cudaMemcpy2DAsync(M.ym, (size_t)Nm * 8, M.cy, (size_t)h->sb.nloc * 8, (size_t)Nm * 8,
+                         (size_t)ncols, cudaMemcpyDeviceToDevice, h->st));
+    h->launches += 3;
+  } else {
+    for (int c = 0; c < ncols; ++c) {
+      if (Nm <= 0) break;
+      const double* ymc = op_coarse(h, M.rm + (int64_t)c * Nm);
+      CK(cudaMemcpyAsync(M.ym + (int64_t)c * Nm, ymc, (size_t)Nm * 8, cudaMemcpyDeviceToDevice,
+                         h->st));
+    }
   }
   launch_coarse_diag_k(ncols * G, M.rc, M.Dck, M.yc, h->st);
   launch_prolong_k(h->co, P, M.ym, M.yc, M.Dck, M.Ck, h->gb.nloc, ncols, M.yk, out, ld, h->st);
@@ -1978,6 +2003,42 @@ hplmm_status hplmm_apply(hplmm_handle* h, int32_t op, const double* in, double* 
     from_device(h, out, dout, nout);
     CK(cudaStreamSynchronize(h->st));
     h->flush_profile();
+    return HPLMM_OK;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
+hplmm_status hplmm_apply_many(hplmm_handle* h, int32_t op, int32_t ncols, const double* in,
+                              int64_t ldin, double* out, int64_t ldout, void* stream) {
+  if (!h || !in || !out) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
+  try {
+    if (op != HPLMM_OP_MZETA && op != HPLMM_OP_MGRAIN && op != HPLMM_OP_MCG)
+      throw HError{HPLMM_ERR_ARG, "apply_many: op must be MZETA, MGRAIN or MCG"};
+    if (ncols < 1 || ncols > kMaxBlock) throw HError{HPLMM_ERR_ARG, "apply_many: ncols must be 1..4"};
+    if (!h->setup_done) throw HError{HPLMM_ERR_STATE, "apply_many before hplmm_setup"};
+    if (!h->sparse() || h->ilu_smoother())
+      throw HError{HPLMM_ERR_STATE, "apply_many needs local_factor = 1 and smoother = 0"};
+    const int n = h->n_dof;
+    if (ldin < n || ldout < n) throw HError{HPLMM_ERR_ARG, "apply_many: ld < n_dof"};
+    require_device(h);
+    h->st = (cudaStream_t)stream;
+    multi_alloc(h);
+    auto& M = h->mr;
+    const int64_t ld = h->ldv;
+    for (int c = 0; c < ncols; ++c) to_device(h, M.vin + c * ld, in + c * ldin, n);
+    if (op == HPLMM_OP_MZETA) {
+      op_mzeta_k(h, ncols, M.vin, M.u);
+    } else if (op == HPLMM_OP_MGRAIN) {
+      op_mgrain_k(h, ncols, M.vin, nullptr, nullptr, M.u);
+    } else {   // M_CG: z1 = M_zeta^-1 v ; u = z1 + M_g^-1 (v - A z1)
+      op_mzeta_k(h, ncols, M.vin, M.z1);
+      for (int c = 0; c < ncols; ++c) op_spmv(h, M.z1 + c * ld, M.vin + c * ld, M.t + c * ld);
+      op_mgrain_k(h, ncols, M.t, M.z1, nullptr, M.u);
+    }
+    CK(cudaGetLastError());
+    for (int c = 0; c < ncols; ++c) from_device(h, out + c * ldout, M.u + c * ld, n);
+    CK(cudaStreamSynchronize(h->st));
     return HPLMM_OK;
   } catch (const HError& e) {
     return fail(e);

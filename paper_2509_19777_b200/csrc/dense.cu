@@ -459,11 +459,16 @@ constexpr int SY_CONS = 3;
 // stage it waits on, which the parity wait requires.
 static_assert(SY_STAGES % SY_CONS == 0, "each stage must belong to one consumer warp");
 
+// P columns (multi-RHS blocks): each streamed tile is applied to P vectors
+// (column c at xloc + c xstr, partials at part_row / part_col + c pstr) while
+// it sits in shared memory -- S^-1 is read from HBM once per block
+template <int P>
 __global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
     k_symv_tma(int64_t ntiles, const int32_t* __restrict__ tile_s,
                const int32_t* __restrict__ tile_ij, const int64_t* __restrict__ row_base,
                const double* __restrict__ tiles, const double* __restrict__ xloc,
-               double* __restrict__ part_row, double* __restrict__ part_col) {
+               double* __restrict__ part_row, double* __restrict__ part_col, int64_t xstr,
+               int64_t pstr) {
   extern __shared__ __align__(1024) double sm_tiles[];
   __shared__ __align__(8) uint64_t full[SY_STAGES], empty[SY_STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -496,67 +501,73 @@ __global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
     const int ij = __ldg(tile_ij + t);
     const int I = ij >> 16, J = ij & 0xffff;
     const int64_t rb = __ldg(row_base + ts);
-    const double* xJ = xloc + (rb + J) * TB;
-    const double2 xI = *reinterpret_cast<const double2*>(xloc + (rb + I) * TB + 2 * lane);
-    double xj[TB / 32 * 2];
-    // stage x_J in registers: lane l holds x_J[2l], x_J[2l+1]
-    {
-      double2 v = *reinterpret_cast<const double2*>(xJ + 2 * lane);
-      xj[0] = v.x;
-      xj[1] = v.y;
-    }
-    mbar_wait(&full[s], (uint32_t)((k / SY_STAGES) & 1));
-    const double2* A = reinterpret_cast<const double2*>(sm_tiles + (size_t)s * TILE) + lane;
-    double y0 = 0.0, y1 = 0.0;
-    double cp[64];
+#pragma unroll 1
+    for (int cc = 0; cc < P; ++cc) {
+      const double* xl = xloc + cc * xstr;
+      const double* xJ = xl + (rb + J) * TB;
+      const double2 xI = *reinterpret_cast<const double2*>(xl + (rb + I) * TB + 2 * lane);
+      double xj[TB / 32 * 2];
+      // stage x_J in registers: lane l holds x_J[2l], x_J[2l+1]
+      {
+        double2 v = *reinterpret_cast<const double2*>(xJ + 2 * lane);
+        xj[0] = v.x;
+        xj[1] = v.y;
+      }
+      if (cc == 0) mbar_wait(&full[s], (uint32_t)((k / SY_STAGES) & 1));
+      const double2* A = reinterpret_cast<const double2*>(sm_tiles + (size_t)s * TILE) + lane;
+      double y0 = 0.0, y1 = 0.0;
+      double cp[64];
 #pragma unroll
-    for (int c = 0; c < TB; ++c) {
-      double2 a = A[c * (TB / 2)];
-      double x = __shfl_sync(0xffffffffu, (c & 1) ? xj[1] : xj[0], c >> 1);
-      y0 = fma(a.x, x, y0);
-      y1 = fma(a.y, x, y1);
-      cp[c] = fma(a.x, xI.x, a.y * xI.y);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    reinterpret_cast<double2*>(part_row + t * TB)[lane] = make_double2(y0, y1);
-    if (I == J) continue;
+      for (int c = 0; c < TB; ++c) {
+        double2 a = A[c * (TB / 2)];
+        double x = __shfl_sync(0xffffffffu, (c & 1) ? xj[1] : xj[0], c >> 1);
+        y0 = fma(a.x, x, y0);
+        y1 = fma(a.y, x, y1);
+        cp[c] = fma(a.x, xI.x, a.y * xI.y);
+      }
+      if (cc == P - 1) {   // last read of the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      reinterpret_cast<double2*>(part_row + cc * pstr + t * TB)[lane] = make_double2(y0, y1);
+      if (I == J) continue;
 #pragma unroll
-    for (int k2 = 0; k2 < 32; ++k2) {
-      bool up = lane & 16;
-      double send = up ? cp[k2] : cp[32 + k2];
-      double keep = up ? cp[32 + k2] : cp[k2];
-      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
+      for (int k2 = 0; k2 < 32; ++k2) {
+        bool up = lane & 16;
+        double send = up ? cp[k2] : cp[32 + k2];
+        double keep = up ? cp[32 + k2] : cp[k2];
+        cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
 #pragma unroll
-    for (int k2 = 0; k2 < 16; ++k2) {
-      bool up = lane & 8;
-      double send = up ? cp[k2] : cp[16 + k2];
-      double keep = up ? cp[16 + k2] : cp[k2];
-      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
+      for (int k2 = 0; k2 < 16; ++k2) {
+        bool up = lane & 8;
+        double send = up ? cp[k2] : cp[16 + k2];
+        double keep = up ? cp[16 + k2] : cp[k2];
+        cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
 #pragma unroll
-    for (int k2 = 0; k2 < 8; ++k2) {
-      bool up = lane & 4;
-      double send = up ? cp[k2] : cp[8 + k2];
-      double keep = up ? cp[8 + k2] : cp[k2];
-      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
+      for (int k2 = 0; k2 < 8; ++k2) {
+        bool up = lane & 4;
+        double send = up ? cp[k2] : cp[8 + k2];
+        double keep = up ? cp[8 + k2] : cp[k2];
+        cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
 #pragma unroll
-    for (int k2 = 0; k2 < 4; ++k2) {
-      bool up = lane & 2;
-      double send = up ? cp[k2] : cp[4 + k2];
-      double keep = up ? cp[4 + k2] : cp[k2];
-      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
+      for (int k2 = 0; k2 < 4; ++k2) {
+        bool up = lane & 2;
+        double send = up ? cp[k2] : cp[4 + k2];
+        double keep = up ? cp[4 + k2] : cp[k2];
+        cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
 #pragma unroll
-    for (int k2 = 0; k2 < 2; ++k2) {
-      bool up = lane & 1;
-      double send = up ? cp[k2] : cp[2 + k2];
-      double keep = up ? cp[2 + k2] : cp[k2];
-      cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+      for (int k2 = 0; k2 < 2; ++k2) {
+        bool up = lane & 1;
+        double send = up ? cp[k2] : cp[2 + k2];
+        double keep = up ? cp[2 + k2] : cp[k2];
+        cp[k2] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+      }
+      reinterpret_cast<double2*>(part_col + cc * pstr + t * TB)[lane] = make_double2(cp[0], cp[1]);
     }
-    reinterpret_cast<double2*>(part_col + t * TB)[lane] = make_double2(cp[0], cp[1]);
   }
 }
 
@@ -571,8 +582,12 @@ __global__ void __launch_bounds__(32 * SR_WARPS)
                   const int32_t* __restrict__ row_k, const int32_t* __restrict__ nb,
                   const int64_t* __restrict__ tile_base, const int64_t* __restrict__ row_base,
                   const double* __restrict__ part_row, const double* __restrict__ part_col,
-                  double* __restrict__ yloc) {
+                  double* __restrict__ yloc, int64_t ystr, int64_t pstr) {
   __shared__ double2 red[SR_WARPS][32];
+  // column blockIdx.y of a multi-RHS block (strides ystr / pstr)
+  part_row += blockIdx.y * pstr;
+  part_col += blockIdx.y * pstr;
+  yloc += blockIdx.y * ystr;
   const int64_t rbi = blockIdx.x;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = row_s[rbi], K = row_k[rbi], n = nb[s];
@@ -607,9 +622,11 @@ __global__ void __launch_bounds__(32 * SR_WARPS)
 }
 
 __global__ void k_gather(int64_t n, const int32_t* __restrict__ lmap, const double* __restrict__ x,
-                         double* __restrict__ xloc) {
+                         double* __restrict__ xloc, int64_t xld = 0) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  x += blockIdx.y * xld;     // column blockIdx.y of a block (xloc stride n)
+  xloc += blockIdx.y * n;
   int g = lmap[i];
   xloc[i] = g >= 0 ? x[g] : 0.0;
 }
@@ -628,10 +645,10 @@ void launch_symv_tiles(const DevBatch& b, cudaStream_t st) {
     g_symv_mode = (e && e[0] == '0') ? 0 : 1;
   }
   if (g_symv_mode == 1) {
-    set_max_dynamic_smem((const void*)k_symv_tma, SY_STAGES * TILE * 8);
+    set_max_dynamic_smem((const void*)k_symv_tma<1>, SY_STAGES * TILE * 8);
     int64_t grid = std::min<int64_t>(device_sm_count(), b.ntiles);
-    k_symv_tma<<<(unsigned)grid, 32 * (SY_CONS + 1), SY_STAGES * TILE * 8, st>>>(
-        b.ntiles, b.tile_s, b.tile_ij, b.row_base, b.tiles, b.xloc, b.part_row, b.part_col);
+    k_symv_tma<1><<<(unsigned)grid, 32 * (SY_CONS + 1), SY_STAGES * TILE * 8, st>>>(
+        b.ntiles, b.tile_s, b.tile_ij, b.row_base, b.tiles, b.xloc, b.part_row, b.part_col, 0, 0);
     return;
   }
   int64_t th = 32 * b.ntiles;
@@ -644,7 +661,37 @@ void launch_symv_reduce(const DevBatch& b, cudaStream_t st) {
   if (b.nrows <= 0) return;
   k_symv_reduce<<<(unsigned)b.nrows, 32 * SR_WARPS, 0, st>>>(b.nrows, b.row_s, b.row_k, b.nb,
                                                                b.tile_base, b.row_base,
-                                                               b.part_row, b.part_col, b.yloc);
+                                                               b.part_row, b.part_col, b.yloc, 0, 0);
+}
+
+// P-column block (multi-RHS): y_c = A x_c for c < ncols, with column c of the
+// block at xk / yk + c nloc and its partials at prk / pck + c ntiles TB; the
+// packed tiles stream once (k_symv_tma<P>)
+template <int P>
+static void symv_k(const DevBatch& b, int ncols, const double* xk, double* yk, double* prk,
+                   double* pck, cudaStream_t st) {
+  const int64_t pstr = b.ntiles * TB;
+  set_max_dynamic_smem((const void*)k_symv_tma<P>, SY_STAGES * TILE * 8);
+  const int64_t grid = std::min<int64_t>(device_sm_count(), b.ntiles);
+  k_symv_tma<P><<<(unsigned)grid, 32 * (SY_CONS + 1), SY_STAGES * TILE * 8, st>>>(
+      b.ntiles, b.tile_s, b.tile_ij, b.row_base, b.tiles, xk, prk, pck, b.nloc, pstr);
+  k_symv_reduce<<<dim3((unsigned)b.nrows, (unsigned)ncols), 32 * SR_WARPS, 0, st>>>(
+      b.nrows, b.row_s, b.row_k, b.nb, b.tile_base, b.row_base, prk, pck, yk, b.nloc, pstr);
+}
+
+void launch_symv_k(const DevBatch& b, int P, int ncols, const double* xk, double* yk, double* prk,
+                   double* pck, cudaStream_t st) {
+  if (b.ntiles <= 0 || ncols <= 0) return;
+  if (P == 4) symv_k<4>(b, ncols, xk, yk, prk, pck, st);
+  else if (P == 2) symv_k<2>(b, ncols, xk, yk, prk, pck, st);
+  else symv_k<1>(b, ncols, xk, yk, prk, pck, st);
+}
+
+void launch_gather_k(const DevBatch& b, int ncols, const double* x, int64_t xld, double* xk,
+                     cudaStream_t st) {
+  if (b.nloc <= 0 || ncols <= 0) return;
+  k_gather<<<dim3((unsigned)((b.nloc + 255) / 256), (unsigned)ncols), 256, 0, st>>>(b.nloc, b.lmap,
+                                                                                    x, xk, xld);
 }
 
 void launch_symv(const DevBatch& b, cudaStream_t st) {

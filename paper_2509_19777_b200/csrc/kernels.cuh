@@ -79,6 +79,12 @@ void launch_gather(const DevBatch& b, const double* x, cudaStream_t st);
 void launch_symv(const DevBatch& b, cudaStream_t st);
 void launch_symv_tiles(const DevBatch& b, cudaStream_t st);
 void launch_symv_reduce(const DevBatch& b, cudaStream_t st);
+// multi-RHS blocks: P-column SYMV (tiles streamed once; k_symv_tma<P>) and
+// gather; column c at xk / yk + c nloc, partials at prk / pck + c ntiles 64
+void launch_symv_k(const DevBatch& b, int P, int ncols, const double* xk, double* yk, double* prk,
+                   double* pck, cudaStream_t st);
+void launch_gather_k(const DevBatch& b, int ncols, const double* x, int64_t xld, double* xk,
+                     cudaStream_t st);
 // C = -(A^-1 X) for grain batch:  X row-major [64 nb x ld], cols [0,k)
 void launch_symm_neg(const DevBatch& b, const int64_t* x_off, const int32_t* ld,
                      const int32_t* kcols, int max_kchunks, const double* X, double* B,

@@ -58,12 +58,12 @@ void launch_set_correction_k(const DevBatch& gb, int G, double* Ck, double* Dck,
 // tk[(chunk_t + j) NRHS + c].  Warp w: rows 8w .. 8w+7; lane: columns.
 // ---------------------------------------------------------------------------
 template <int NRHS>
-__global__ void __launch_bounds__(256) k_restrict_chunks_k(DevCoarse c, const int32_t* lmap,
-                                                           const int64_t* row_base,
-                                                           const double* __restrict__ r,
-                                                           int64_t ldr, int ncols,
-                                                           const double* __restrict__ Ck,
-                                                           int64_t ldc, double* __restrict__ tk) {
+__global__ void __launch_bounds__(256, NRHS == 4 ? 3 : 4) k_restrict_chunks_k(DevCoarse c, const int32_t* lmap,
+                                                              const int64_t* row_base,
+                                                              const double* __restrict__ r,
+                                                              int64_t ldr, int ncols,
+                                                              const double* __restrict__ Ck,
+                                                              int64_t ldc, double* __restrict__ tk) {
   constexpr int MAXL = 640 / NRHS;
   const int64_t ch = blockIdx.x;
   if (ch >= c.n_chunks) return;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_restrict_chunks_k(DevCoarse c, const in
   const double* Bg = c.B + c.b_off[g] + (int64_t)(r0 + 8 * w) * L;
   const int64_t lrow0 = 64 * row_base[g] + r0;       // grain-batch local row of the chunk
   const int32_t* lm = lmap + lrow0;
-  __shared__ double rv[64][NRHS];
+  __shared__ __align__(16) double rv[64][NRHS];
   __shared__ double part[8][MAXL + 1][NRHS];
   if (threadIdx.x < 64) {
     const int d = lm[threadIdx.x];
@@ -82,11 +82,10 @@ __global__ void __launch_bounds__(256) k_restrict_chunks_k(DevCoarse c, const in
     for (int q = 0; q < NRHS; ++q) rv[threadIdx.x][q] = (d >= 0 && q < ncols) ? r[q * ldr + d] : 0.0;
   }
   __syncthreads();
-  double rr[8][NRHS];
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-#pragma unroll
-    for (int k = 0; k < NRHS; ++k) rr[q][k] = rv[8 * w + q][k];
+  // the warp's 8 rows of r stay in shared memory (broadcast reads in the FMA
+  // loop): an 8 x NRHS register block cost the occupancy that keeps enough
+  // B_g loads in flight (NRHS = 4: 2.3 TB/s with it)
+  const double* rw = &rv[8 * w][0];
   double* out = tk + c.chunk_t[ch] * NRHS;
   for (int j0 = 0; j0 < L; j0 += MAXL) {
     const int jn = min(MAXL, L - j0);
@@ -103,13 +102,13 @@ __global__ void __launch_bounds__(256) k_restrict_chunks_k(DevCoarse c, const in
 #pragma unroll
         for (int q = 0; q < 8; ++q)
 #pragma unroll
-          for (int k = 0; k < NRHS; ++k) a[k] = fma(v[q], rr[q][k], a[k]);
+          for (int k = 0; k < NRHS; ++k) a[k] = fma(v[q], rw[q * NRHS + k], a[k]);
       } else {   // correction column: each RHS its own c_g
 #pragma unroll
         for (int k = 0; k < NRHS; ++k) {
           const double* cc = Ck + k * ldc + lrow0 + 8 * w;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) a[k] = fma(k < ncols ? cc[q] : 0.0, rr[q][k], a[k]);
+          for (int q = 0; q < 8; ++q) a[k] = fma(k < ncols ? cc[q] : 0.0, rw[q * NRHS + k], a[k]);
         }
       }
 #pragma unroll
@@ -255,8 +254,34 @@ __global__ void k_yext_k(DevCoarse c, const double* __restrict__ ym, const doubl
   }
 }
 
-// grain rows: one CTA per 64-row block, warp = 8 rows, lanes stride the shape
-// columns (coalesced row reads of B_g, read ONCE for the NRHS vectors)
+// Sum of NV values (a power of two <= 32) of every lane over the warp, one
+// value per lane group: each halving step keeps half of the values and
+// exchanges the other half (NV - 1 + log2(32 / NV) shuffles instead of
+// 5 NV); afterwards lanes with (lane & (32 / NV - 1)) == 0 hold the sum of
+// value index idx (bits of the lane at offsets 16, 8, ...).
+template <int NV>
+__device__ __forceinline__ double warp_transpose_sum(double (&v)[NV], int lane, int& idx) {
+  idx = 0;
+  int o = 16;
+#pragma unroll
+  for (int h = NV / 2; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = lane & o;
+    if (up) idx += h;
+#pragma unroll
+    for (int t = 0; t < h; ++t) {
+      const double send = up ? v[t] : v[h + t];
+      const double keep = up ? v[h + t] : v[t];
+      v[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  return v[0];
+}
+
+// grain rows: one CTA per 64-row block (NRHS = 4: per 32-row half), warp =
+// ROWS rows, lanes stride the shape columns (coalesced row reads of B_g, read
+// ONCE for the NRHS vectors), transposing warp reduction of ROWS x NRHS sums
 template <int NRHS>
 __global__ void __launch_bounds__(256) k_prolong_rows_k(DevCoarse c, const int32_t* __restrict__ lmap,
                                                         const int32_t* __restrict__ row_s,
@@ -265,45 +290,37 @@ __global__ void __launch_bounds__(256) k_prolong_rows_k(DevCoarse c, const int32
                                                         const double* __restrict__ Ck, int64_t ldc,
                                                         int ncols, double* __restrict__ x,
                                                         int64_t ldx) {
-  constexpr int ROWS = 8;
-  const int64_t ch = blockIdx.x;
+  constexpr int ROWS = NRHS == 4 ? 4 : 8;            // ROWS x NRHS <= 32 accumulators
+  constexpr int SPLIT = 8 / ROWS;                    // CTAs per 64-row block
+  const int64_t ch = blockIdx.x / SPLIT;
+  const int half = (int)(blockIdx.x % SPLIT);
   const int g = row_s[ch];
   const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = c.ld[g];
-  const int64_t lr0 = (ch - row_base[g]) * 64 + wp * ROWS;
+  const int roff = half * 8 * ROWS + wp * ROWS;      // row of the warp in the 64-row block
+  const int64_t lr0 = (ch - row_base[g]) * 64 + roff;
   const double* Bg = c.B + c.b_off[g] + lr0 * L;
   const double* y = yk + c.yext_off[g] * NRHS;
-  const int64_t row0 = 64 * ch + wp * ROWS;          // grain-batch local row
-  double a[ROWS][NRHS];
+  const int64_t row0 = 64 * ch + roff;               // grain-batch local row
+  double a[ROWS * NRHS];
 #pragma unroll
-  for (int q = 0; q < ROWS; ++q)
-#pragma unroll
-    for (int k = 0; k < NRHS; ++k) a[q][k] = 0.0;
+  for (int q = 0; q < ROWS * NRHS; ++q) a[q] = 0.0;
   for (int j = lane; j < L - 1; j += 32) {
     double yj[NRHS];
 #pragma unroll
     for (int k = 0; k < NRHS; ++k) yj[k] = __ldg(y + (int64_t)j * NRHS + k);
+    double b[ROWS];
 #pragma unroll
-    for (int q = 0; q < ROWS; ++q) {
-      const double b = __ldcs(Bg + (int64_t)q * L + j);
+    for (int q = 0; q < ROWS; ++q) b[q] = __ldcs(Bg + (int64_t)q * L + j);
 #pragma unroll
-      for (int k = 0; k < NRHS; ++k) a[q][k] = fma(b, yj[k], a[q][k]);
-    }
+    for (int q = 0; q < ROWS; ++q)
+#pragma unroll
+      for (int k = 0; k < NRHS; ++k) a[q * NRHS + k] = fma(b[q], yj[k], a[q * NRHS + k]);
   }
-#pragma unroll
-  for (int q = 0; q < ROWS; ++q)
-#pragma unroll
-    for (int k = 0; k < NRHS; ++k)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a[q][k] += __shfl_xor_sync(0xffffffffu, a[q][k], o);
-  if (lane < ROWS * NRHS) {
-    const int q = lane / NRHS, k = lane - q * NRHS;
-    double v = 0.0;
-#pragma unroll
-    for (int qq = 0; qq < ROWS; ++qq)
-#pragma unroll
-      for (int kk = 0; kk < NRHS; ++kk)
-        if (qq == q && kk == k) v = a[qq][kk];
+  int idx;
+  const double v = warp_transpose_sum<ROWS * NRHS>(a, lane, idx);
+  if ((lane & (32 / (ROWS * NRHS) - 1)) == 0) {
+    const int q = idx / NRHS, k = idx - q * NRHS;
     const int d = lmap[row0 + q];
     if (d >= 0 && k < ncols)
       x[k * ldx + d] = v + Ck[k * ldc + row0 + q] * y[(int64_t)(L - 1) * NRHS + k];
@@ -341,7 +358,7 @@ static void prolong_k(const DevCoarse& c, const double* ym, const double* yc, co
                       cudaStream_t st) {
   if (c.n_grains > 0) k_yext_k<NRHS><<<c.n_grains, 128, 0, st>>>(c, ym, yc, Dck, ncols, yk);
   if (c.n_chunks > 0)
-    k_prolong_rows_k<NRHS><<<(unsigned)c.n_chunks, 256, 0, st>>>(c, c.g_lmap, c.g_row_s,
+    k_prolong_rows_k<NRHS><<<(unsigned)(c.n_chunks * (NRHS == 4 ? 2 : 1)), 256, 0, st>>>(c, c.g_lmap, c.g_row_s,
                                                                  c.g_row_base, yk, Ck, ldc, ncols,
                                                                  x, ldx);
   if (c.n_iface_nodes > 0)

@@ -82,7 +82,10 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   }
   wk.cons = force_cons ? force_cons
                        : sn_solve_cfg((int)isub.size(), nblocks, s.max_n, s.max_r, nrhs,
-                                      s.chunk_doubles, s.shape);
+                                      s.chunk_doubles, s.shape, s.max_w);
+  // several right-hand sides: the 8-warp CTAs hold at most 2 row pairs of
+  // every column per thread (k_sn_solve SN_MAXQ), i.e. parts of <= 1024 rows
+  if (nrhs > 1 && wk.cons == 8 && std::max(s.max_w, s.max_r) > 1024) wk.cons = 16;
   if (wk.cons == 0)
     throw SnError{-1, "subdomain of " + std::to_string(s.max_n) +
                           " DOFs does not fit the supernodal solve's shared memory"};
@@ -125,6 +128,13 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   wk.item_c0 = up(A, c0, st, setup_only);
   wk.chunk_ptr = up(A, cptr, st, setup_only);
   wk.chunks = up(A, flat, st, setup_only);
+  wk.xg = nullptr;
+  wk.xg_stride = 0;
+  wk.max_w = s.max_w;
+  if (sn_xg(nrhs) && wk.nblocks > 0) {
+    wk.xg_stride = sn_xg_stride(s.max_n, nrhs);
+    wk.xg = (double*)A.alloc((size_t)wk.nblocks * wk.xg_stride * 8, setup_only);
+  }
 }
 
 void sn_upload(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm) {

@@ -78,13 +78,16 @@ struct RowLayout {
 };
 
 // effective row-group code of a part with h rows: the host's (TG >= h/8), or
-// for NRHS > 1 TG >= h/2 so that the group-reduction scratch fits one stage
-template <int NRHS>
-__device__ __forceinline__ int sn_lg(int lgc, int h) {
+// for NRHS > 1 the smallest TG >= the host's whose row pairs fit MAXQ per
+// thread and whose group-reduction scratch (G - 1) h NRHS fits one stage
+template <int NRHS, int MAXQ>
+__device__ __forceinline__ int sn_lg(int lgc, int h, int lgnt, int stage_doubles) {
   if (NRHS == 1) return lgc;
-  int lg = 5;
-  while ((1 << lg) < (h + 1) / 2) ++lg;
-  return max(lgc, lg - 5);
+  int lg = min(lgc + 5, lgnt);
+  while (lg < lgnt && ((h + (2 << lg) - 1) >> (lg + 1) > MAXQ ||
+                       (int64_t)((1 << (lgnt - lg)) - 1) * h * NRHS > stage_doubles))
+    ++lg;
+  return lg - 5;
 }
 
 // acc[q][e][c] += sum over this group's chunk columns of col[2(t + q TG) + e] * x_S
@@ -212,23 +215,29 @@ __device__ __forceinline__ void sn_group_reduce(const RowLayout& L, int h, doubl
   }
 }
 
-template <int NRHS, int CONS, int CPS>
+template <int NRHS, int CONS, int CPS, bool XG>
 __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     k_sn_solve(SnDev d, SnIO io, SnWork wk, int stages, int stage_doubles, int max_n, int max_r,
                int flags) {
   extern __shared__ __align__(128) unsigned char sn_smem[];
   __shared__ __align__(8) uint64_t full[SN_MAXST], empty[SN_MAXST];
   double* ring = reinterpret_cast<double*>(sn_smem);
-  double* x = ring + (size_t)stages * stage_doubles;
-  // x_R of the current backward part; scratch of the forward group reductions
-  // x_R of a backward part (16-B aligned)
-  double* xr = x + (size_t)((max_n + 1) & ~1) * NRHS;
+  // x (elimination order, NRHS interleaved) and x_R of the current backward
+  // part (16-B aligned): after the ring in shared memory, or (XG) in the
+  // CTA's slice of global memory (L1/L2-resident; only the ring in smem)
+  double* x = XG ? wk.xg + (size_t)blockIdx.x * wk.xg_stride : ring + (size_t)stages * stage_doubles;
+  // XG: x_S of the current supernode staged in shared memory (forward: read by
+  // its W and F parts; backward: updated by its W part, written back at the end)
+  double* xs = ring + (size_t)stages * stage_doubles;
+  double* xr = XG ? xs + (size_t)((wk.max_w + 1) & ~1) * NRHS : x + (size_t)((max_n + 1) & ~1) * NRHS;
   const int rpad = (max_r + 3) & ~1;   // x_R: NRHS component-major rows of rpad doubles
   constexpr int SN_NT = SnT<CONS>::NT, SN_CONS = CONS;
+  static_assert(NRHS == 1 || XG, "several right-hand sides keep x in global memory");
   // row pairs per thread: up to 4 for one RHS (TG >= h/8); with several RHS
-  // TG >= h/2 (sn_lg), so h <= 2048 needs at most 2 with 16 warps -- a smaller
+  // at most 2 (sn_lg widens TG): h <= 2048 with 16 warps, h <= 1024 with 8
+  // (sn_build_work keeps taller parts off the 8-warp shape) -- a smaller
   // accumulator array keeps the multi-RHS solve free of register spills
-  constexpr int SN_MAXQ = (NRHS == 1 || CONS != 16) ? SnT<CONS>::MAXQ : 2;
+  constexpr int SN_MAXQ = (NRHS == 1 || CONS < 8) ? SnT<CONS>::MAXQ : 2;
   constexpr int SN_LGNT = SnT<CONS>::LGNT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k0 = wk.chunk_ptr[blockIdx.x], k1 = wk.chunk_ptr[blockIdx.x + 1];
@@ -383,7 +392,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       // row-parallel gemv on a column chunk: W_S, F_SS^-1
       const int h = kind == SN_W_FWD ? r : w;
       const int ld = h + (h & 1);
-      const RowLayout L(sn_lg<NRHS>(lgc, h), tid, SN_LGNT);
+      const RowLayout L(sn_lg<NRHS, SN_MAXQ>(lgc, h, SN_LGNT, stage_doubles), tid, SN_LGNT);
       if (rd) {   // W_S part with its row list in front: group 0 keeps its rows
         const int32_t* rows = reinterpret_cast<const int32_t*>(st);
         if (L.g == 0) {
@@ -405,8 +414,14 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
           for (int e = 0; e < 2; ++e)
 #pragma unroll
             for (int cr = 0; cr < NRHS; ++cr) acc[q][e][cr] = 0.0;
+        if (XG && (kind == SN_W_FWD || r == 0)) {
+          // first forward chunk of S: stage x_S (w consecutive positions from p0)
+          const double* src = x + (size_t)p0 * NRHS;
+          for (int e = tid; e < w * NRHS; e += SN_NT) xs[e] = src[e];
+          PSYNC();
+        }
       }
-      const double* xcol = x + (size_t)(p0 + cc0) * NRHS;
+      const double* xcol = XG ? xs + (size_t)cc0 * NRHS : x + (size_t)(p0 + cc0) * NRHS;
       const int nq = L.nq(h);
       if (nq <= 1) sn_rows<1, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
       else if (nq == 2 || SN_MAXQ == 2) sn_rows<2, NRHS, SN_MAXQ>(st, ld, nc, h, xcol, L, acc);
@@ -464,7 +479,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       }
     } else if (kind == SN_ROWS_FWD) {
       // x_R -= W_S x_S (summed over the W part by group 0; rows are distinct)
-      const RowLayout L(sn_lg<NRHS>(lgc, r), tid, SN_LGNT);
+      const RowLayout L(sn_lg<NRHS, SN_MAXQ>(lgc, r, SN_LGNT, stage_doubles), tid, SN_LGNT);
       const int32_t* rows = reinterpret_cast<const int32_t*>(st);
       if (L.g == 0) {
 #pragma unroll
@@ -490,6 +505,10 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
         for (int cr = 0; cr < NRHS; ++cr) xr[cr * rpad + i] = x[pr * NRHS + cr];
       }
       if ((r & 1) && tid < NRHS) xr[tid * rpad + r] = 0.0;
+      if (XG) {
+        const double* src = x + (size_t)p0 * NRHS;
+        for (int e = tid; e < w * NRHS; e += SN_NT) xs[e] = src[e];
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[cs]);
       PSYNC();
@@ -502,6 +521,10 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
           for (int cr = 0; cr < NRHS; ++cr) xr[cr * rpad + i] = x[pr * NRHS + cr];
         }
         if ((r & 1) && tid < NRHS) xr[tid * rpad + r] = 0.0;
+        if (XG) {   // and x_S of S (updated in shared memory, written back at the end)
+          const double* src = x + (size_t)p0 * NRHS;
+          for (int e = tid; e < w * NRHS; e += SN_NT) xs[e] = src[e];
+        }
         PSYNC();
         st += rd;
       }
@@ -540,21 +563,51 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
             }
           }
         }
-#pragma unroll
-        for (int cr = 0; cr < NRHS; ++cr) {
-          for (int o = lpc >> 1; o > 0; o >>= 1) sum[cr] += __shfl_xor_sync(0xffffffffu, sum[cr], o);
-        }
-        if (jj < nc && sl < NRHS) {
-          double v = sum[0];
-#pragma unroll
-          for (int cr = 1; cr < NRHS; ++cr)
-            if (sl == cr) v = sum[cr];
-          x[(p0 + cc0 + jj) * NRHS + sl] -= v;
+        if constexpr (NRHS == 1) {
+          for (int o = lpc >> 1; o > 0; o >>= 1) sum[0] += __shfl_xor_sync(0xffffffffu, sum[0], o);
+          if (jj < nc && sl == 0) {
+            if (XG) xs[cc0 + jj] -= sum[0];
+            else x[p0 + cc0 + jj] -= sum[0];
+          }
+        } else {
+          // transposing reduction of the NRHS sums over the column's lpc lanes:
+          // the first log2(NRHS) halving steps each keep half of the sums
+          // (log2(lpc) + 1 shuffles for NRHS = 4 instead of 4 log2(lpc));
+          // afterwards lane sl holds the full sum of right-hand side
+          // c = (sl & lpc/2 ? 2 : 0) + (sl & lpc/4 ? 1 : 0)
+          const int o1 = lpc >> 1;
+          const bool hi1 = sl & o1;
+          double v;
+          if constexpr (NRHS == 4) {
+            const int o2 = lpc >> 2;
+            const bool hi2 = sl & o2;
+            const double k0 = hi1 ? sum[2] : sum[0], k1 = hi1 ? sum[3] : sum[1];
+            const double s0 = hi1 ? sum[0] : sum[2], s1 = hi1 ? sum[1] : sum[3];
+            const double a0 = k0 + __shfl_xor_sync(0xffffffffu, s0, o1);
+            const double a1 = k1 + __shfl_xor_sync(0xffffffffu, s1, o1);
+            v = (hi2 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, hi2 ? a0 : a1, o2);
+            for (int o = o2 >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (jj < nc && (sl & (o2 - 1)) == 0) {
+              const int c = (hi1 ? 2 : 0) + (hi2 ? 1 : 0);
+              xs[(cc0 + jj) * NRHS + c] -= v;
+            }
+          } else {
+            v = (hi1 ? sum[1] : sum[0]) + __shfl_xor_sync(0xffffffffu, hi1 ? sum[0] : sum[1], o1);
+            for (int o = o1 >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (jj < nc && (sl & (o1 - 1)) == 0) xs[(cc0 + jj) * NRHS + (hi1 ? 1 : 0)] -= v;
+          }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[cs]);
-      if (last) PSYNC();
+      if (last) {
+        PSYNC();
+        if (XG) {   // x_S of S is final: back to x
+          double* dst = x + (size_t)p0 * NRHS;
+          for (int e = tid; e < w * NRHS; e += SN_NT) dst[e] = xs[e];
+          PSYNC();
+        }
+      }
     }
     if (prof) {
       t_kind[kind] += clock64() - t_k0;
@@ -596,8 +649,17 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
 // x_S (max_n) and x_R (max_r) after the ring; at least SN_GUARD doubles, the
 // largest row overrun of an unpredicated sn_rows read (2 TG - 1, TG <= 256)
 constexpr int SN_GUARD = 512;
-static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int nt) {
-  const size_t t = (size_t)(((max_n + 1) & ~1) + ((max_r + 3) & ~1)) * nrhs;
+// x and x_R in global memory (SnWork::xg) for several right-hand sides;
+// HPLMM_SN_XG=1 also for one (experiment)
+bool sn_xg(int nrhs) {
+  static const bool env = getenv("HPLMM_SN_XG") && atoi(getenv("HPLMM_SN_XG")) > 0;
+  return nrhs > 1 || env;
+}
+int64_t sn_xg_stride(int max_n, int nrhs) { return (int64_t)((max_n + 1) & ~1) * nrhs; }
+// shared memory after the ring: x (or, XG, x_S of one supernode) then x_R
+static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int max_w) {
+  const int xs = sn_xg(nrhs) ? max_w : max_n;
+  const size_t t = (size_t)(((xs + 1) & ~1) + ((max_r + 3) & ~1)) * nrhs;
   return t < SN_GUARD ? SN_GUARD : t;
 }
 
@@ -606,9 +668,9 @@ static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int nt) {
 // least two items per CTA).  shape: 0 = automatic from the item count
 // (HPLMM_SN_CFG=16|8 forces one for experiments), 8 / 16 = the handle's
 // hplmm_options.sn_shape (falls back to automatic when it does not fit).
-int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons);
 
-int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk, int shape) {
+int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk, int shape,
+                 int max_w) {
   static int env_forced = -1;
   if (env_forced < 0) {
     const char* e = getenv("HPLMM_SN_CFG");
@@ -619,9 +681,9 @@ int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk,
   // TG >= h/8 for one RHS (<= 8 x consumer threads) and TG >= h/2 for several
   // (sn_lg: <= 2 x consumer threads x NRHS)
   auto scratch = [nrhs](int nt) { return nrhs == 1 ? 8 * nt : 2 * nt * nrhs; };
-  const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8) >= 2 && chunk >= scratch(256);
-  const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16) >= 2 && chunk >= scratch(512);
-  if (forced == 4 && sn_solve_stages(max_n, max_r, nrhs, chunk, 4) >= 2 && chunk >= scratch(128))
+  const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8, max_w) >= 2 && chunk >= scratch(256);
+  const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16, max_w) >= 2 && chunk >= scratch(512);
+  if (forced == 4 && sn_solve_stages(max_n, max_r, nrhs, chunk, 4, max_w) >= 2 && chunk >= scratch(128))
     return 4;
   if (forced == 8 && fit8) return 8;
   if (forced == 16 && fit16) return 16;
@@ -643,16 +705,16 @@ static int cfg_cps(int cons) { return sn_cfg_cps(cons); }
 // two CTAs) streams 64 KiB (else 48 KiB) chunks -- half the per-chunk
 // overhead for its 16 consumer warps (cfg5 grain / contact solves -13% / -8%).
 // HPLMM_SN_CHUNK overrides.
-int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape) {
+int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape, int max_w) {
   if (getenv("HPLMM_SN_CHUNK")) return sn_chunk_doubles();
   const int base = sn_chunk_doubles();
-  if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base, shape) == 8) {
+  if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base, shape, max_w) == 8) {
     // the largest chunk (2 KiB steps) that keeps two 8-warp CTAs per SM with
     // two stages: the solve's cost is per chunk more than per byte (cfg3
     // contact batch: 32 KiB 1.79 ms, 36 KiB 1.74 ms, 38 KiB 1.70 ms)
     int best = base;
     for (int c = base + 256; c <= SN_CHUNK_DOUBLES_MAX; c += 256) {
-      if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape) != 8) break;
+      if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape, max_w) != 8) break;
       best = c;
     }
     return best;
@@ -660,30 +722,30 @@ int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape) {
   // enough subdomains for 8 x 2 but x_S leaves no room for two 32-KiB stages:
   // smaller chunks keep the 8 x 2 shape (far cheaper per byte than 16 x 1)
   for (int c : {3072, 2048})
-    if (c < base && sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape) == 8) return c;
+    if (c < base && sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape, max_w) == 8) return c;
   for (int c : {SN_CHUNK_DOUBLES_MAX, 6144})
-    if (c > base && sn_solve_stages(max_n, max_r, 1, c, 16) >= 2) return c;
+    if (c > base && sn_solve_stages(max_n, max_r, 1, c, 16, max_w) >= 2) return c;
   return base;
 }
 
-int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons) {
+int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons, int max_w) {
   const int p = cfg_cps(cons);
   const long avail =
-      (226L * 1024) / p - 1024 - (long)sn_tail_doubles(max_n, max_r, nrhs, 32 * cons) * 8;
+      (226L * 1024) / p - 1024 - (long)sn_tail_doubles(max_n, max_r, nrhs, max_w) * 8;
   return (int)std::min<long>(SN_MAXST, avail / ((long)chunk * 8));
 }
 
-template <int NRHS, int CONS, int CPS>
-static void sn_solve_launch(const SnDev& d, const SnIO& io, const SnWork& wk, int stages,
-                            int chunk, int max_n, int max_r, size_t smem, cudaStream_t st) {
-  set_max_dynamic_smem((const void*)k_sn_solve<NRHS, CONS, CPS>, smem);
+template <int NRHS, int CONS, int CPS, bool XG>
+static void sn_solve_launch_x(const SnDev& d, const SnIO& io, const SnWork& wk, int stages,
+                              int chunk, int max_n, int max_r, size_t smem, cudaStream_t st) {
+  set_max_dynamic_smem((const void*)k_sn_solve<NRHS, CONS, CPS, XG>, smem);
   static int flags = -1;
   if (flags < 0) {
     const char* e = getenv("HPLMM_SN_FLAGS");
     flags = e ? atoi(e) : 0;
   }
-  k_sn_solve<NRHS, CONS, CPS><<<wk.nblocks, 32 * (CONS + 1), smem, st>>>(d, io, wk, stages, chunk,
-                                                                          max_n, max_r, flags);
+  k_sn_solve<NRHS, CONS, CPS, XG><<<wk.nblocks, 32 * (CONS + 1), smem, st>>>(
+      d, io, wk, stages, chunk, max_n, max_r, flags);
   if ((flags & 16) && wk.nblocks <= 4096) {   // experiment: per-CTA finish-time quantiles
     static unsigned long long h[2 * 4096];
     cudaStreamSynchronize(st);
@@ -704,6 +766,19 @@ static void sn_solve_launch(const SnDev& d, const SnIO& io, const SnWork& wk, in
   }
 }
 
+template <int NRHS, int CONS, int CPS>
+static void sn_solve_launch(const SnDev& d, const SnIO& io, const SnWork& wk, int stages,
+                            int chunk, int max_n, int max_r, size_t smem, cudaStream_t st) {
+  // several right-hand sides always keep x in global memory (sn_build_work
+  // allocates the slices whenever sn_xg says so)
+  if constexpr (NRHS > 1) {
+    sn_solve_launch_x<NRHS, CONS, CPS, true>(d, io, wk, stages, chunk, max_n, max_r, smem, st);
+  } else {
+    if (wk.xg) sn_solve_launch_x<NRHS, CONS, CPS, true>(d, io, wk, stages, chunk, max_n, max_r, smem, st);
+    else sn_solve_launch_x<NRHS, CONS, CPS, false>(d, io, wk, stages, chunk, max_n, max_r, smem, st);
+  }
+}
+
 template <int CONS, int CPS>
 static void sn_launch_nrhs(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int stages,
                            int chunk, int max_n, int max_r, size_t smem, cudaStream_t st) {
@@ -715,8 +790,8 @@ static void sn_launch_nrhs(const SnDev& d, const SnIO& io, const SnWork& wk, int
 void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
                      int max_r, int chunk, int cons, cudaStream_t st) {
   if (wk.nblocks <= 0) return;
-  const int stages = sn_solve_stages(max_n, max_r, nrhs, chunk, cons);
-  const size_t smem = ((size_t)stages * chunk + sn_tail_doubles(max_n, max_r, nrhs, 32 * cons)) * 8;
+  const int stages = sn_solve_stages(max_n, max_r, nrhs, chunk, cons, wk.max_w);
+  const size_t smem = ((size_t)stages * chunk + sn_tail_doubles(max_n, max_r, nrhs, wk.max_w)) * 8;
   static const bool dbg = getenv("HPLMM_DEBUG") != nullptr;
   static int printed = 0;
   if (dbg && printed < 4) {

@@ -103,8 +103,14 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
                 const std::vector<int32_t>& nodes, int leaf, SnSymbolic& out, std::string& err,
                 int nsm = 148, int shape = 0);
 // shape: 0 = automatic, 8 = 8 consumer warps x 2 CTAs per SM, 16 = 16 x 1
-int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape = 0);
+int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape, int max_w);
 int sn_cfg_cps(int cons);   // CTAs per SM of a launch shape
-int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk, int shape = 0);
+// consumer warps per CTA (8: two CTAs per SM; 16: one), 0 if the subdomain
+// vectors do not fit in shared memory with >= 2 ring stages
+int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk, int shape,
+                 int max_w);
+// x of the solve in global memory (per-CTA slices of sn_xg_stride doubles)
+bool sn_xg(int nrhs);
+int64_t sn_xg_stride(int max_n, int nrhs);
 
 }  // namespace hplmm

@@ -47,6 +47,13 @@ struct SnWork {
   const int32_t* item_c0 = nullptr;
   const int64_t* chunk_ptr = nullptr;   // [nblocks+1]
   const SnChunk* chunks = nullptr;      // flat, per CTA contiguous
+  // x in global memory (xg != nullptr; used for NRHS > 1): per-CTA slice of
+  // xg_stride doubles holding x (max_n even, NRHS interleaved); shared memory
+  // then holds the factor ring, x_S of the current supernode (staged per part,
+  // max_w) and x_R, so that the 8 x 2 shape fits several columns
+  double* xg = nullptr;
+  int64_t xg_stride = 0;
+  int max_w = 0;
 };
 
 // numeric-factorisation view (device pointers)
@@ -83,11 +90,8 @@ struct GemmProb {
   int transA;     // op(A) = A^T: A stored k x m (lda >= k)
 };
 
-// consumer warps per CTA (8: two CTAs per SM; 16: one), 0 if the subdomain
-// vectors do not fit in shared memory with >= 2 ring stages
-int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk);
-int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons);
-int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r);
+// ring stages of a launch shape (cons consumer warps) for these subdomain sizes
+int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons, int max_w);
 void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
                      int max_r, int chunk, int cons, cudaStream_t st);
 void launch_front_asm(const int32_t* list, int nlist, const SnNum& nm, const double* val,

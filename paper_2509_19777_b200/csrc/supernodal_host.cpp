@@ -334,7 +334,7 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
   const int64_t foff = o_f[nsub];
   o.factor_doubles = foff;
   o.shape = shape;
-  o.chunk_doubles = sn_pick_chunk(nsub, nsm, o.max_n, o.max_r, shape);
+  o.chunk_doubles = sn_pick_chunk(nsub, nsm, o.max_n, o.max_r, shape, o.max_w);
   const double t2 = now();
   // TMA chunk schedule: forward = (W_S, rows, F_SS^-1) per S in postorder,
   // backward = (rows, W_S) per S in reverse postorder; W/F chunks are whole

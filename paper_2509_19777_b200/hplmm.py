@@ -32,6 +32,7 @@ SMOOTHER = dict(cg=0, ilu0=1)
 
 EXPORTED = ["hplmm_default_options", "hplmm_create", "hplmm_assemble", "hplmm_set_matrix",
             "hplmm_setup", "hplmm_set_rhs", "hplmm_solve", "hplmm_solve_many", "hplmm_apply",
+            "hplmm_apply_many",
             "hplmm_export", "hplmm_setup_bsr", "hplmm_assemble_bsr", "hplmm_free_bsr",
             "hplmm_get_report", "hplmm_profile", "hplmm_kernel_stats", "hplmm_destroy",
             "hplmm_last_error"]
@@ -98,6 +99,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hplmm_solve": (C.c_int, [vp, vp, dbl, vp, vp, vp, i32, vp]),
         "hplmm_solve_many": (C.c_int, [vp, i32, vp, dbl, vp, vp, vp]),
         "hplmm_apply": (C.c_int, [vp, i32, vp, vp, vp]),
+        "hplmm_apply_many": (C.c_int, [vp, i32, i32, vp, C.c_int64, vp, C.c_int64, vp]),
         "hplmm_export": (C.c_int, [vp, i32, vp, C.c_int64, vp]),
         "hplmm_setup_bsr": (C.c_int, [vp, vp, vp, i32, vp, vp]),
         "hplmm_assemble_bsr": (C.c_int, [vp, i32, vp, vp]),
@@ -314,6 +316,21 @@ class Solver:
         if isinstance(X, np.ndarray) and kx is not X:
             X[:] = kx
         return X, [reps[i].as_dict() for i in range(nrhs)]
+
+    def apply_many(self, op, V, out=None, stream=None):
+        """V: (ncols <= 4, n_dof) NumPy or torch CUDA array, rows = vectors;
+        out[c] = op applied to V[c] through one block application."""
+        opi = OP[op] if isinstance(op, str) else int(op)
+        if out is None:
+            out = np.zeros_like(V) if isinstance(V, np.ndarray) else V.new_zeros(V.shape)
+        pi, ki = _ptr(V)
+        po, ko = _ptr(out)
+        ld = int(V.shape[1])
+        _check(self._lib.hplmm_apply_many(self._h, opi, int(V.shape[0]), pi, ld, po,
+                                          int(out.shape[1]), _stream(stream)))
+        if isinstance(out, np.ndarray) and ko is not out:
+            out[:] = ko
+        return out
 
     def apply(self, op, v, out=None, stream=None):
         opi = OP[op] if isinstance(op, str) else int(op)
