@@ -215,6 +215,65 @@ __device__ __forceinline__ void sn_group_reduce(const RowLayout& L, int h, doubl
   }
 }
 
+// Backward W part chunk: x_S[j] -= W[:, j]^T x_R for the chunk's nc columns
+// (column-major, ld), LPC lanes split the rows of a column; each lane group
+// takes CB columns at once, so one x_R load serves CB columns, and the
+// CB x NRHS sums are reduced over the group by a transposing butterfly (each
+// halving step keeps half of the sums: NV - 1 + log2(LPC / NV) shuffles for
+// NV = CB NRHS sums instead of NV log2(LPC)).  xo[j NRHS + c] receives the
+// update of column j (0 <= j < nc) for right-hand side c; x_R is
+// component-major, xr[c rpad + i] (lanes read consecutive rows: conflict-free).
+template <int LPC, int NRHS, int CONS>
+__device__ __forceinline__ void sn_wbwd(const double* __restrict__ st, int ld, int r, int nc,
+                                        const double* __restrict__ xr, int rpad, double* xo,
+                                        int warp, int lane) {
+  constexpr int CB = NRHS == 1 ? 4 : (NRHS == 2 ? 4 : 2);   // NV <= 8 <= LPC
+  constexpr int NV = CB * NRHS;
+  static_assert(NV <= LPC, "one sum per lane after the halving steps");
+  constexpr int CPW = 32 / LPC;                  // lane groups per warp
+  const int sl = lane & (LPC - 1), cl = lane / LPC;
+  for (int jw = warp * CPW * CB; jw < nc; jw += CONS * CPW * CB) {
+    const int jb = jw + cl * CB;                 // first column of the lane group
+    double sum[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) sum[v] = 0.0;
+    if (jb < nc) {
+      const double* col[CB];
+#pragma unroll
+      for (int b = 0; b < CB; ++b) col[b] = st + (size_t)min(jb + b, nc - 1) * ld;   // clamped
+#pragma unroll 2
+      for (int i = 2 * sl; i < r; i += 2 * LPC) {
+        double2 xa[NRHS];
+#pragma unroll
+        for (int c = 0; c < NRHS; ++c) xa[c] = *reinterpret_cast<const double2*>(xr + c * rpad + i);
+#pragma unroll
+        for (int b = 0; b < CB; ++b) {
+          const double2 a = *reinterpret_cast<const double2*>(col[b] + i);
+#pragma unroll
+          for (int c = 0; c < NRHS; ++c)
+            sum[b * NRHS + c] = fma(a.x, xa[c].x, fma(a.y, xa[c].y, sum[b * NRHS + c]));
+        }
+      }
+    }
+    int idx = 0, o = LPC / 2;
+#pragma unroll
+    for (int h = NV / 2; h >= 1; h >>= 1, o >>= 1) {
+      const bool up = sl & o;
+      if (up) idx += h;
+#pragma unroll
+      for (int t = 0; t < h; ++t) {
+        const double send = up ? sum[t] : sum[h + t];
+        const double keep = up ? sum[h + t] : sum[t];
+        sum[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+#pragma unroll
+    for (; o > 0; o >>= 1) sum[0] += __shfl_xor_sync(0xffffffffu, sum[0], o);
+    const int b = idx / NRHS, c = idx - b * NRHS;
+    if ((sl & (LPC / NV - 1)) == 0 && jb + b < nc) xo[(jb + b) * NRHS + c] -= sum[0];
+  }
+}
+
 template <int NRHS, int CONS, int CPS, bool XG>
 __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     k_sn_solve(SnDev d, SnIO io, SnWork wk, int stages, int stage_doubles, int max_n, int max_r,
@@ -529,75 +588,10 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
         st += rd;
       }
       const int ld = r + (r & 1);
-      const int lpc = r > 256 ? 32 : (r > 128 ? 16 : 8);
-      const int cpw = 32 / lpc;                    // columns per warp pass
-      const int sl = lane & (lpc - 1), cl = lane / lpc;
-      for (int j0 = warp * cpw; j0 < nc; j0 += SN_CONS * cpw) {
-        const int jj = j0 + cl;
-        double sum[NRHS];
-#pragma unroll
-        for (int cr = 0; cr < NRHS; ++cr) sum[cr] = 0.0;
-        if (jj < nc) {
-          const double* col = st + (size_t)jj * ld;
-          int i = 2 * sl;
-          if (NRHS == 1) {
-            double s2 = 0.0;
-            for (; i + 2 * lpc < r; i += 4 * lpc) {
-              const double2 a = *reinterpret_cast<const double2*>(col + i);
-              const double2 b = *reinterpret_cast<const double2*>(col + i + 2 * lpc);
-              const double2 xa = *reinterpret_cast<const double2*>(xr + i);
-              const double2 xb = *reinterpret_cast<const double2*>(xr + i + 2 * lpc);
-              sum[0] = fma(a.x, xa.x, fma(a.y, xa.y, sum[0]));
-              s2 = fma(b.x, xb.x, fma(b.y, xb.y, s2));
-            }
-            sum[0] += s2;
-          }
-          for (; i < r; i += 2 * lpc) {
-            const double2 a = *reinterpret_cast<const double2*>(col + i);
-            // x_R is component-major (xr[cr rpad + i]): lanes read consecutive
-            // rows, conflict-free (an interleaved layout was 16-way conflicted)
-#pragma unroll
-            for (int cr = 0; cr < NRHS; ++cr) {
-              const double2 xa = *reinterpret_cast<const double2*>(xr + cr * rpad + i);
-              sum[cr] = fma(a.x, xa.x, fma(a.y, xa.y, sum[cr]));
-            }
-          }
-        }
-        if constexpr (NRHS == 1) {
-          for (int o = lpc >> 1; o > 0; o >>= 1) sum[0] += __shfl_xor_sync(0xffffffffu, sum[0], o);
-          if (jj < nc && sl == 0) {
-            if (XG) xs[cc0 + jj] -= sum[0];
-            else x[p0 + cc0 + jj] -= sum[0];
-          }
-        } else {
-          // transposing reduction of the NRHS sums over the column's lpc lanes:
-          // the first log2(NRHS) halving steps each keep half of the sums
-          // (log2(lpc) + 1 shuffles for NRHS = 4 instead of 4 log2(lpc));
-          // afterwards lane sl holds the full sum of right-hand side
-          // c = (sl & lpc/2 ? 2 : 0) + (sl & lpc/4 ? 1 : 0)
-          const int o1 = lpc >> 1;
-          const bool hi1 = sl & o1;
-          double v;
-          if constexpr (NRHS == 4) {
-            const int o2 = lpc >> 2;
-            const bool hi2 = sl & o2;
-            const double k0 = hi1 ? sum[2] : sum[0], k1 = hi1 ? sum[3] : sum[1];
-            const double s0 = hi1 ? sum[0] : sum[2], s1 = hi1 ? sum[1] : sum[3];
-            const double a0 = k0 + __shfl_xor_sync(0xffffffffu, s0, o1);
-            const double a1 = k1 + __shfl_xor_sync(0xffffffffu, s1, o1);
-            v = (hi2 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, hi2 ? a0 : a1, o2);
-            for (int o = o2 >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (jj < nc && (sl & (o2 - 1)) == 0) {
-              const int c = (hi1 ? 2 : 0) + (hi2 ? 1 : 0);
-              xs[(cc0 + jj) * NRHS + c] -= v;
-            }
-          } else {
-            v = (hi1 ? sum[1] : sum[0]) + __shfl_xor_sync(0xffffffffu, hi1 ? sum[0] : sum[1], o1);
-            for (int o = o1 >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (jj < nc && (sl & (o1 - 1)) == 0) xs[(cc0 + jj) * NRHS + (hi1 ? 1 : 0)] -= v;
-          }
-        }
-      }
+      double* xo = XG ? xs + (size_t)cc0 * NRHS : x + (size_t)(p0 + cc0) * NRHS;
+      if (r > 256) sn_wbwd<32, NRHS, SN_CONS>(st, ld, r, nc, xr, rpad, xo, warp, lane);
+      else if (r > 128) sn_wbwd<16, NRHS, SN_CONS>(st, ld, r, nc, xr, rpad, xo, warp, lane);
+      else sn_wbwd<8, NRHS, SN_CONS>(st, ld, r, nc, xr, rpad, xo, warp, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[cs]);
       if (last) {
