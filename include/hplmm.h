@@ -315,7 +315,9 @@ hplmm_status hplmm_apply(hplmm_handle *h, int32_t op, const double *in, double *
  * the supernodal factors of the contact grids / grains stream once per block
  * (k_sn_solve with NRHS = 2 or 4 columns) instead of once per vector.
  * op: HPLMM_OP_MZETA, HPLMM_OP_MGRAIN or HPLMM_OP_MCG (the operators that do
- * not depend on the right-hand side; eq:Mg_Mz, eq:local_smoother_CG).  Column
+ * not depend on the right-hand side; eq:Mg_Mz, eq:local_smoother_CG), or
+ * HPLMM_OP_SPMV (A^ by the solve's operator: the element-by-element operator
+ * applied to the block in one launch, eq:ls_all).  Column
  * c of in / out is in + c ldin / out + c ldout (ldin, ldout >= n_dof), host or
  * device; out[c] equals hplmm_apply(op, in[c]) up to the summation order of
  * the group reductions.  Needs local_factor = 1 (supernodal) and smoother = 0

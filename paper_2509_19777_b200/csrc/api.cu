@@ -517,6 +517,21 @@ void op_spmv(hplmm_handle* h, const double* x, const double* v, double* y) {
   h->launches++;
 }
 
+// y_c = A^ x_c (v == nullptr) or v_c - A^ x_c for ncols columns (x, v stride
+// ld; y stride ldy): one element-by-element launch for the block (lookups and
+// moduli shared by the columns), else the stored blocks per column
+void op_spmv_k(hplmm_handle* h, int ncols, const double* x, const double* v, double* y,
+               int64_t ld, int64_t ldy) {
+  if (h->ebe) {
+    const int P = ncols > 2 ? 4 : ncols;
+    launch_ebe_k(P, ncols, h->n_nodes, h->d_ijk, h->d_dir, h->d_lat_ebe, h->d_Es, h->hs.nx,
+                 h->hs.ny, h->hs.nz, h->K0h, x, v, y, ld, ldy, h->st);
+    h->launches++;
+    return;
+  }
+  for (int c = 0; c < ncols; ++c) op_spmv(h, x + c * ld, v ? v + c * ld : nullptr, y + c * ldy);
+}
+
 void op_mzeta(hplmm_handle* h, const double* in, double* out) {
   if (h->ilu_smoother())
     throw HError{HPLMM_ERR_STATE, "M_zeta / M_CG: contact grids are not built with smoother = 1"};
@@ -783,9 +798,9 @@ void op_minv_k(hplmm_handle* h, int ncols, const double* in, double* out) {
   auto& M = h->mr;
   const int64_t ld = h->ldv;
   op_mg_k(h, ncols, in, M.y);
-  for (int c = 0; c < ncols; ++c) op_spmv(h, M.y + c * ld, in + c * ld, M.r1 + c * ld);
+  op_spmv_k(h, ncols, M.y, in, M.r1, ld, ld);
   op_mzeta_k(h, ncols, M.r1, M.z1);
-  for (int c = 0; c < ncols; ++c) op_spmv(h, M.z1 + c * ld, M.r1 + c * ld, M.t + c * ld);
+  op_spmv_k(h, ncols, M.z1, M.r1, M.t, ld, ld);
   op_mgrain_k(h, ncols, M.t, M.y, M.z1, out);
 }
 
@@ -878,12 +893,14 @@ void solve_block(hplmm_handle* h, int ncols, double tol, hplmm_report* reps) {
           CK(cudaMemsetAsync(M.vin + c * ld, 0, (size_t)n * 8, st));
       }
       op_minv_k(h, ncols, M.vin, M.u);
+      // w_c = A u_c for the whole block into V_c[j + 1] (columns not iterating
+      // have u_c = 0: their slot j + 1 > their last step is not used)
+      op_spmv_k(h, ncols, M.u, nullptr, M.V + (int64_t)(j + 1) * ld, ld, (int64_t)(m + 1) * ld);
       for (int c = 0; c < ncols; ++c) {
         if (!col[c].active) continue;
         double* V = M.V + (int64_t)c * (m + 1) * ld;
         double* w = V + (j + 1) * ld;
         double* hb = M.hb + (int64_t)c * hbn;
-        op_spmv(h, M.u + c * ld, nullptr, w);
         launch_multidot(n, j + 1, V, ld, w, M.partial, hb, st);
         launch_update(n, j + 1, V, ld, hb, w, nullptr, nullptr, st);
         launch_multidot(n, j + 1, V, ld, w, M.partial, hb + (m + 1), st);
@@ -2013,8 +2030,8 @@ hplmm_status hplmm_apply_many(hplmm_handle* h, int32_t op, int32_t ncols, const 
                               int64_t ldin, double* out, int64_t ldout, void* stream) {
   if (!h || !in || !out) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
   try {
-    if (op != HPLMM_OP_MZETA && op != HPLMM_OP_MGRAIN && op != HPLMM_OP_MCG)
-      throw HError{HPLMM_ERR_ARG, "apply_many: op must be MZETA, MGRAIN or MCG"};
+    if (op != HPLMM_OP_MZETA && op != HPLMM_OP_MGRAIN && op != HPLMM_OP_MCG && op != HPLMM_OP_SPMV)
+      throw HError{HPLMM_ERR_ARG, "apply_many: op must be SPMV, MZETA, MGRAIN or MCG"};
     if (ncols < 1 || ncols > kMaxBlock) throw HError{HPLMM_ERR_ARG, "apply_many: ncols must be 1..4"};
     if (!h->setup_done) throw HError{HPLMM_ERR_STATE, "apply_many before hplmm_setup"};
     if (!h->sparse() || h->ilu_smoother())
@@ -2027,13 +2044,15 @@ hplmm_status hplmm_apply_many(hplmm_handle* h, int32_t op, int32_t ncols, const 
     auto& M = h->mr;
     const int64_t ld = h->ldv;
     for (int c = 0; c < ncols; ++c) to_device(h, M.vin + c * ld, in + c * ldin, n);
-    if (op == HPLMM_OP_MZETA) {
+    if (op == HPLMM_OP_SPMV) {
+      op_spmv_k(h, ncols, M.vin, nullptr, M.u, ld, ld);
+    } else if (op == HPLMM_OP_MZETA) {
       op_mzeta_k(h, ncols, M.vin, M.u);
     } else if (op == HPLMM_OP_MGRAIN) {
       op_mgrain_k(h, ncols, M.vin, nullptr, nullptr, M.u);
     } else {   // M_CG: z1 = M_zeta^-1 v ; u = z1 + M_g^-1 (v - A z1)
       op_mzeta_k(h, ncols, M.vin, M.z1);
-      for (int c = 0; c < ncols; ++c) op_spmv(h, M.z1 + c * ld, M.vin + c * ld, M.t + c * ld);
+      op_spmv_k(h, ncols, M.z1, M.vin, M.t, ld, ld);
       op_mgrain_k(h, ncols, M.t, M.z1, nullptr, M.u);
     }
     CK(cudaGetLastError());

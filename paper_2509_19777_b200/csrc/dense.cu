@@ -458,12 +458,17 @@ constexpr int SY_CONS = 3;
 // warp k % CONS).  That keeps every consumer within one mbarrier phase of the
 // stage it waits on, which the parity wait requires.
 static_assert(SY_STAGES % SY_CONS == 0, "each stage must belong to one consumer warp");
+// multi-column blocks do P times the arithmetic per streamed tile: twice the
+// consumer warps (still one stage per warp residue class)
+template <int P>
+constexpr int sy_cons() { return P == 1 ? SY_CONS : 6; }
+static_assert(SY_STAGES % sy_cons<4>() == 0, "each stage must belong to one consumer warp");
 
 // P columns (multi-RHS blocks): each streamed tile is applied to P vectors
 // (column c at xloc + c xstr, partials at part_row / part_col + c pstr) while
 // it sits in shared memory -- S^-1 is read from HBM once per block
 template <int P>
-__global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
+__global__ void __launch_bounds__(32 * (sy_cons<P>() + 1), 1)
     k_symv_tma(int64_t ntiles, const int32_t* __restrict__ tile_s,
                const int32_t* __restrict__ tile_ij, const int64_t* __restrict__ row_base,
                const double* __restrict__ tiles, const double* __restrict__ xloc,
@@ -471,6 +476,7 @@ __global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
                int64_t pstr) {
   extern __shared__ __align__(1024) double sm_tiles[];
   __shared__ __align__(8) uint64_t full[SY_STAGES], empty[SY_STAGES];
+  constexpr int CONS = sy_cons<P>();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * per;
@@ -483,7 +489,7 @@ __global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
     mbar_fence_init();
   }
   __syncthreads();
-  if (warp == SY_CONS) {                       // producer
+  if (warp == CONS) {                       // producer
     if (lane == 0) {
       for (int64_t k = 0; k < nt; ++k) {
         int s = (int)(k % SY_STAGES);
@@ -494,7 +500,7 @@ __global__ void __launch_bounds__(32 * (SY_CONS + 1), 1)
     }
     return;
   }
-  for (int64_t k = warp; k < nt; k += SY_CONS) {
+  for (int64_t k = warp; k < nt; k += CONS) {
     const int64_t t = t0 + k;
     const int s = (int)(k % SY_STAGES);
     const int ts = __ldg(tile_s + t);
@@ -673,7 +679,7 @@ static void symv_k(const DevBatch& b, int ncols, const double* xk, double* yk, d
   const int64_t pstr = b.ntiles * TB;
   set_max_dynamic_smem((const void*)k_symv_tma<P>, SY_STAGES * TILE * 8);
   const int64_t grid = std::min<int64_t>(device_sm_count(), b.ntiles);
-  k_symv_tma<P><<<(unsigned)grid, 32 * (SY_CONS + 1), SY_STAGES * TILE * 8, st>>>(
+  k_symv_tma<P><<<(unsigned)grid, 32 * (sy_cons<P>() + 1), SY_STAGES * TILE * 8, st>>>(
       b.ntiles, b.tile_s, b.tile_ij, b.row_base, b.tiles, xk, prk, pck, b.nloc, pstr);
   k_symv_reduce<<<dim3((unsigned)b.nrows, (unsigned)ncols), 32 * SR_WARPS, 0, st>>>(
       b.nrows, b.row_s, b.row_k, b.nb, b.tile_base, b.row_base, prk, pck, yk, b.nloc, pstr);

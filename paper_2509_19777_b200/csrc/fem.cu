@@ -642,6 +642,118 @@ __global__ void __launch_bounds__(128) k_ebe2(int64_t npairs, int kx, int nx, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-RHS blocks (NEXT #2): the element-by-element operator applied to P
+// columns at once (column c of x / v / y at + c ld).  The 27 lattice lookups
+// and the 8 voxel moduli of a node are shared by the P columns; per-voxel
+// accumulators for P columns would not fit the registers, so each
+// (voxel a, neighbour b) contribution is scaled by E_a at once (as k_ebe2):
+// out_c,r += E_a sum_s K0[3a + r][3b + s] x_c,s.  Same operator as k_ebe up
+// to the summation order (R4: Dirichlet rows identity, columns skipped).
+// ---------------------------------------------------------------------------
+template <int P, bool RESID>
+__global__ void __launch_bounds__(128) k_ebe_k(int n, int ncols, const int32_t* __restrict__ ijk,
+                                               const uint8_t* __restrict__ dir,
+                                               const int32_t* __restrict__ lat,
+                                               const double* __restrict__ Es, int nx, int ny,
+                                               int nz, const __grid_constant__ EbeK0 K0,
+                                               const double* __restrict__ x,
+                                               const double* __restrict__ v,
+                                               double* __restrict__ y, int64_t ld, int64_t ldy) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  if (dir[p]) {   // identity row (R4)
+    for (int c = 0; c < ncols; ++c)
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int64_t d = c * ld + 3 * (int64_t)p + r;
+        y[c * ldy + 3 * (int64_t)p + r] = RESID ? v[d] - x[d] : x[d];
+      }
+    return;
+  }
+  const int ix = ijk[3 * p], iy = ijk[3 * p + 1], iz = ijk[3 * p + 2];
+  double Ea[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int vx = ix - (a & 1), vy = iy - ((a >> 1) & 1), vz = iz - ((a >> 2) & 1);
+    Ea[a] = (vx >= 0 && vy >= 0 && vz >= 0 && vx < nx && vy < ny && vz < nz)
+                ? Es[vx + (int64_t)nx * (vy + (int64_t)ny * vz)]
+                : 0.0;
+  }
+  double out[P][3];
+#pragma unroll
+  for (int c = 0; c < P; ++c) out[c][0] = out[c][1] = out[c][2] = 0.0;
+  const int64_t nx1 = nx + 1, ny1 = ny + 1;
+  int qs[27];
+#pragma unroll
+  for (int k = 0; k < 27; ++k) {
+    const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+    bool any = false;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
+      if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1) any |= Ea[a] != 0.0;
+    }
+    qs[k] = any ? lat[(ix + dx) + nx1 * ((iy + dy) + ny1 * (iz + dz))] : -1;
+  }
+#pragma unroll
+  for (int k = 0; k < 27; ++k) {
+    const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+    const int q = qs[k];
+    if (q < 0) continue;
+    double xq[P][3];
+#pragma unroll
+    for (int c = 0; c < P; ++c)
+#pragma unroll
+      for (int s2 = 0; s2 < 3; ++s2)
+        xq[c][s2] = c < ncols ? x[c * ld + 3 * (int64_t)q + s2] : 0.0;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
+      if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1) {
+        const int b = bx + 2 * by + 4 * bz;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double* kr = K0.k + (3 * a + r) * 24 + 3 * b;
+#pragma unroll
+          for (int c = 0; c < P; ++c) {
+            const double t = fma(kr[2], xq[c][2], fma(kr[1], xq[c][1], kr[0] * xq[c][0]));
+            out[c][r] = fma(Ea[a], t, out[c][r]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    if (c >= ncols) break;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int64_t d = c * ld + 3 * (int64_t)p + r;
+      y[c * ldy + 3 * (int64_t)p + r] = RESID ? v[d] - out[c][r] : out[c][r];
+    }
+  }
+}
+
+void launch_ebe_k(int P, int ncols, int n_nodes, const int32_t* node_ijk, const uint8_t* dir,
+                  const int32_t* lat, const double* Es, int nx, int ny, int nz,
+                  const double* K0_host, const double* x, const double* v, double* y, int64_t ld,
+                  int64_t ldy, cudaStream_t st) {
+  if (n_nodes <= 0 || ncols <= 0) return;
+  EbeK0 k;
+  for (int t = 0; t < 576; ++t) k.k[t] = K0_host[t];
+  const int grid = (n_nodes + 127) / 128;
+#define EBE_K(PP)                                                                                 \
+  if (v)                                                                                          \
+    k_ebe_k<PP, true><<<grid, 128, 0, st>>>(n_nodes, ncols, node_ijk, dir, lat, Es, nx, ny, nz, k, \
+                                            x, v, y, ld, ldy);                                      \
+  else                                                                                            \
+    k_ebe_k<PP, false><<<grid, 128, 0, st>>>(n_nodes, ncols, node_ijk, dir, lat, Es, nx, ny, nz,   \
+                                             k, x, v, y, ld, ldy);
+  if (P == 4) { EBE_K(4) } else if (P == 2) { EBE_K(2) } else { EBE_K(1) }
+#undef EBE_K
+}
+
 static int g_ebe_mode = -1;   // 1 = k_ebe (default), 2 = two nodes per thread (k_ebe2)
 
 void launch_ebe(int n_nodes, const int32_t* node_ijk, const uint8_t* dir, const int32_t* lat,
@@ -651,7 +763,12 @@ void launch_ebe(int n_nodes, const int32_t* node_ijk, const uint8_t* dir, const 
   if (n_nodes <= 0) return;
   if (g_ebe_mode < 0) {
     const char* e = getenv("HPLMM_EBE_PAIR");
-    g_ebe_mode = (e && e[0] == '1') ? 2 : 1;
+    const char* e1 = getenv("HPLMM_EBE_K1");   // experiment: k_ebe_k<1> (E-scaled form)
+    g_ebe_mode = (e && e[0] == '1') ? 2 : ((e1 && e1[0] == '1') ? 3 : 1);
+  }
+  if (g_ebe_mode == 3) {
+    launch_ebe_k(1, 1, n_nodes, node_ijk, dir, lat, Es, nx, ny, nz, K0_host, x, v, y, 0, 0, st);
+    return;
   }
   EbeK0 k;
   for (int t = 0; t < 576; ++t) k.k[t] = K0_host[t];

@@ -57,6 +57,11 @@ void launch_spmv(int n_nodes, const int32_t* row_ptr, const int32_t* col, const 
 // Element-by-element A^ (operator_kind = 0; same y = A^ x / y = v - A^ x as
 // launch_spmv).  lat: lattice point -> free node id, -1 for no node or a
 // Dirichlet node; Es: E per voxel, 0 where void; K0_host: 576 doubles (host)
+// multi-RHS blocks: P (1, 2, 4) columns at once, column c at x / v + c ld, y + c ldy
+void launch_ebe_k(int P, int ncols, int n_nodes, const int32_t* node_ijk, const uint8_t* dir,
+                  const int32_t* lat, const double* Es, int nx, int ny, int nz,
+                  const double* K0_host, const double* x, const double* v, double* y, int64_t ld,
+                  int64_t ldy, cudaStream_t st);
 void launch_ebe(int n_nodes, const int32_t* node_ijk, const uint8_t* dir, const int32_t* lat,
                 const int32_t* lat_all,
                 const double* Es, int nx, int ny, int nz, const double* K0_host, const double* x,

@@ -305,7 +305,25 @@ __global__ void __launch_bounds__(256) k_prolong_rows_k(DevCoarse c, const int32
   double a[ROWS * NRHS];
 #pragma unroll
   for (int q = 0; q < ROWS * NRHS; ++q) a[q] = 0.0;
-  for (int j = lane; j < L - 1; j += 32) {
+  // two column steps per pass: 2 ROWS streaming loads in flight per lane
+  int j = lane;
+  for (; j + 32 < L - 1; j += 64) {
+    double yj[2][NRHS], b[2][ROWS];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+      for (int q = 0; q < ROWS; ++q) b[u][q] = __ldcs(Bg + (int64_t)q * L + j + 32 * u);
+#pragma unroll
+      for (int k = 0; k < NRHS; ++k) yj[u][k] = __ldg(y + (int64_t)(j + 32 * u) * NRHS + k);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int q = 0; q < ROWS; ++q)
+#pragma unroll
+        for (int k = 0; k < NRHS; ++k) a[q * NRHS + k] = fma(b[u][q], yj[u][k], a[q * NRHS + k]);
+  }
+  for (; j < L - 1; j += 32) {
     double yj[NRHS];
 #pragma unroll
     for (int k = 0; k < NRHS; ++k) yj[k] = __ldg(y + (int64_t)j * NRHS + k);

@@ -89,14 +89,15 @@ _mr_solvers = {}
 
 @pytest.mark.parametrize("shape", [8, 16])
 @pytest.mark.parametrize("case", ["cube8", "cfg1", "porous20"])
-@pytest.mark.parametrize("op", ["MZETA", "MGRAIN", "MCG"])
+@pytest.mark.parametrize("op", ["SPMV", "MZETA", "MGRAIN", "MCG"])
 @pytest.mark.parametrize("k", [2, 3, 4])
 def test_apply_many_vs_oracle(case, op, k, shape):
     """The block local solves (k_sn_solve with NRHS = 2 / 4 columns, x in
     global memory with x_S / x_R staged per supernode) in both launch shapes --
     8 consumer warps x 2 CTAs per SM, what cfg3's multi-RHS block runs, and
     16 x 1 -- column by column against the oracle's M_zeta^-1, M_g^-1 and
-    M_CG^-1 (eq:Mg_Mz, eq:local_smoother_CG) at north_star's 1e-12."""
+    M_CG^-1 (eq:Mg_Mz, eq:local_smoother_CG) at north_star's 1e-12; SPMV: the
+    block element-by-element operator (k_ebe_k) against the oracle's A^."""
     from paper_2509_19777_b200 import Solver
     if (case, shape) not in _mr_solvers:
         p, s, h = oracle_case(case)
@@ -105,7 +106,8 @@ def test_apply_many_vs_oracle(case, op, k, shape):
     p, s, h = oracle_case(case)
     V = np.random.default_rng(12345 + k).standard_normal((k, s.n_dof))
     out = sv.apply_many(op, torch.from_numpy(V).cuda()).cpu().numpy()
-    ref = {"MZETA": h.apply_Mzeta, "MGRAIN": h.apply_Mg, "MCG": h.apply_MCG}[op]
+    ref = {"MZETA": h.apply_Mzeta, "MGRAIN": h.apply_Mg, "MCG": h.apply_MCG,
+           "SPMV": lambda v: s.A @ v}[op]
     for c in range(k):
         r = ref(V[c])
         assert rel(out[c], r) <= 1e-12, (c, rel(out[c], r))
