@@ -507,19 +507,27 @@ __global__ void __launch_bounds__(32 * (sy_cons<P>() + 1), 1)
     const int ij = __ldg(tile_ij + t);
     const int I = ij >> 16, J = ij & 0xffff;
     const int64_t rb = __ldg(row_base + ts);
-#pragma unroll 1
+    // x_I and x_J of every column loaded before the tile wait (lane l holds
+    // entries 2l, 2l + 1): their L2 latency overlaps the tile's arrival
+    double2 xIc[P], xJc[P];
+#pragma unroll
     for (int cc = 0; cc < P; ++cc) {
       const double* xl = xloc + cc * xstr;
-      const double* xJ = xl + (rb + J) * TB;
-      const double2 xI = *reinterpret_cast<const double2*>(xl + (rb + I) * TB + 2 * lane);
-      double xj[TB / 32 * 2];
-      // stage x_J in registers: lane l holds x_J[2l], x_J[2l+1]
-      {
-        double2 v = *reinterpret_cast<const double2*>(xJ + 2 * lane);
-        xj[0] = v.x;
-        xj[1] = v.y;
-      }
-      if (cc == 0) mbar_wait(&full[s], (uint32_t)((k / SY_STAGES) & 1));
+      xIc[cc] = *reinterpret_cast<const double2*>(xl + (rb + I) * TB + 2 * lane);
+      xJc[cc] = *reinterpret_cast<const double2*>(xl + (rb + J) * TB + 2 * lane);
+    }
+    mbar_wait(&full[s], (uint32_t)((k / SY_STAGES) & 1));
+#pragma unroll 1
+    for (int cc = 0; cc < P; ++cc) {
+      double2 xI = xIc[0];
+      double xj[TB / 32 * 2] = {xJc[0].x, xJc[0].y};
+#pragma unroll
+      for (int c2 = 1; c2 < P; ++c2)
+        if (cc == c2) {
+          xI = xIc[c2];
+          xj[0] = xJc[c2].x;
+          xj[1] = xJc[c2].y;
+        }
       const double2* A = reinterpret_cast<const double2*>(sm_tiles + (size_t)s * TILE) + lane;
       double y0 = 0.0, y1 = 0.0;
       double cp[64];
