@@ -85,7 +85,7 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
                                       s.chunk_doubles, s.shape, s.max_w);
   // several right-hand sides: the 8-warp CTAs hold at most 2 row pairs of
   // every column per thread (k_sn_solve SN_MAXQ), i.e. parts of <= 1024 rows
-  if (nrhs > 1 && wk.cons == 8 && std::max(s.max_w, s.max_r) > 1024) wk.cons = 16;
+  if (nrhs > 1 && wk.cons == 8 && std::max(s.max_w, s.max_r) > 512) wk.cons = 16;
   if (wk.cons == 0)
     throw SnError{-1, "subdomain of " + std::to_string(s.max_n) +
                           " DOFs does not fit the supernodal solve's shared memory"};

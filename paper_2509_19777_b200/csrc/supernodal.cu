@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
   // at most 2 (sn_lg widens TG): h <= 2048 with 16 warps, h <= 1024 with 8
   // (sn_build_work keeps taller parts off the 8-warp shape) -- a smaller
   // accumulator array keeps the multi-RHS solve free of register spills
-  constexpr int SN_MAXQ = (NRHS == 1 || CONS < 8) ? SnT<CONS>::MAXQ : 2;
+  constexpr int SN_MAXQ = (NRHS == 1 || CONS < 8) ? SnT<CONS>::MAXQ : (CONS == 8 ? 1 : 2);
   constexpr int SN_LGNT = SnT<CONS>::LGNT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k0 = wk.chunk_ptr[blockIdx.x], k1 = wk.chunk_ptr[blockIdx.x + 1];
