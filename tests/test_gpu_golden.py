@@ -85,3 +85,39 @@ def test_golden_operators(name, op):
         tol = 1e-12
     assert rel(out[idx], ref) <= tol, (rel(out[idx], ref), tol)
     assert abs(np.linalg.norm(out) - g["norm_" + op]) <= max(tol, 1e-12) * 10 * g["norm_" + op]
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+@pytest.mark.parametrize("op", ["MZETA", "MGRAIN", "MCG"])
+def test_golden_block_operators(name, op):
+    """The multi-RHS block local solves (k_sn_solve<4>, x_S staged per
+    supernode; at cfg3 the 8 x 2 shape solve_many runs) against the oracle:
+    the golden vector v in each of the 4 column slots of a block (other
+    columns seeded), sampled DOFs at 1e-12 (NEXT #2)."""
+    p, sv, g, a, b, v = case(name)
+    idx = a["idx"]
+    rng = np.random.default_rng(7)
+    for slot in range(4):
+        V = torch.from_numpy(rng.standard_normal((4, g["n_dof"]))).cuda()
+        V[slot] = v
+        out = sv.apply_many(op, V).cpu().numpy()
+        assert rel(out[slot][idx], a[op]) <= 1e-12, (slot, rel(out[slot][idx], a[op]))
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_golden_solve_many(name):
+    """hplmm_solve_many on a 4-column block whose first column is the
+    workload's b: that column's iterations (+-1) and x at the sampled
+    DOFs against the oracle's full-size run (R22); the other columns
+    (workloads.load_cases) converge to 1e-8."""
+    from paper_2509_19777_b200 import assemble_bsr
+    from workloads import load_cases
+    p, sv, g, a, b, v = case(name)
+    B = torch.stack([b] + [torch.from_numpy(assemble_bsr(q, 0)["b"]).cuda()
+                           for q in load_cases(p, 4)[1:]])
+    X, reps = sv.solve_many(B, tol=p.tol)
+    assert all(r["converged"] == 1 for r in reps), reps
+    assert abs(reps[0]["iterations"] - g["iterations"]) <= 1, (reps[0]["iterations"], g["iterations"])
+    x = X[0].cpu().numpy()
+    assert rel(x[a["idx"]], a["x"]) <= 1e-8, rel(x[a["idx"]], a["x"])
+    assert abs(np.linalg.norm(x) - g["norm_x"]) <= 1e-8 * g["norm_x"]
