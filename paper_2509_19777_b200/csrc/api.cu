@@ -1600,9 +1600,12 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       };
       double t0 = wall();
       const int shape = hs.opt.sn_shape;
-      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, sn_leaf(), h->sg.sym, err, h->nsm, shape) ||
+      // experiments: per-batch launch shape (HPLMM_SN_SHAPE_G / _C = 8 | 16)
+      const int shape_g = getenv("HPLMM_SN_SHAPE_G") ? atoi(getenv("HPLMM_SN_SHAPE_G")) : shape;
+      const int shape_c = getenv("HPLMM_SN_SHAPE_C") ? atoi(getenv("HPLMM_SN_SHAPE_C")) : shape;
+      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, sn_leaf(), h->sg.sym, err, h->nsm, shape_g) ||
           (!ilu && !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, sn_leaf(), h->sc.sym, err,
-                               h->nsm, shape)))
+                               h->nsm, shape_c)))
         throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
       double t1 = wall();
       try {
