@@ -804,17 +804,24 @@ void op_minv_k(hplmm_handle* h, int ncols, const double* in, double* out) {
   op_mgrain_k(h, ncols, M.t, M.y, M.z1, out);
 }
 
-// correction columns of the block's right-hand sides (eq:col_cg, R15, R16)
+// correction columns of the block's right-hand sides (eq:col_cg, R15, R16):
+// c_g = A_g^-1 b_g for all columns by one block grain solve
 void set_rhs_k(hplmm_handle* h, int ncols, const double* B) {
   auto& M = h->mr;
-  for (int c = 0; c < ncols; ++c) {
-    const double* b = B + c * h->ldv;
-    h->sn_solve(h->sg, b, KC_SN_GRAIN);
-    launch_sn_to_batch(h->gb.nloc, h->gb.lmap, h->d_gpos_sn, b, h->sg.yloc, h->gb.xloc, h->gb.yloc,
-                       h->st);
-    launch_set_correction_k(h->gb, h->co.n_grains, M.Ck + c * h->gb.nloc,
-                            M.Dck + (int64_t)c * h->co.n_grains, h->st);
-    h->launches += 2;
+  HandleAlloc ha(h);
+  const int P = sn_multi_width(h->sg, ha, h->st, h->nsm, ncols);
+  if (P == 0) throw HError{HPLMM_ERR_ARG, "multi-RHS grain solve does not fit shared memory"};
+  for (int c0 = 0; c0 < ncols; c0 += P) {
+    const int nc = std::min(P, ncols - c0);
+    sn_apply_multi(h->sg, P, B + c0 * h->ldv, h->ldv, nc, M.sng, h->st);
+    h->launches++;
+    for (int c = c0; c < c0 + nc; ++c) {
+      launch_sn_to_batch(h->gb.nloc, h->gb.lmap, h->d_gpos_sn, B + c * h->ldv, M.sng, h->gb.xloc,
+                         h->gb.yloc, h->st, P, c - c0);
+      launch_set_correction_k(h->gb, h->co.n_grains, M.Ck + c * h->gb.nloc,
+                              M.Dck + (int64_t)c * h->co.n_grains, h->st);
+      h->launches += 2;
+    }
   }
 }
 

@@ -804,19 +804,20 @@ void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs,
 __global__ void k_sn_to_batch(int64_t nloc, const int32_t* __restrict__ lmap,
                               const int32_t* __restrict__ gpos_sn, const double* __restrict__ b,
                               const double* __restrict__ ysn, double* __restrict__ xloc,
-                              double* __restrict__ yloc) {
+                              double* __restrict__ yloc, int P, int c) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nloc) return;
   const int d = lmap[i];
   xloc[i] = d >= 0 ? b[d] : 0.0;
-  yloc[i] = d >= 0 ? ysn[gpos_sn[d]] : 0.0;
+  yloc[i] = d >= 0 ? ysn[(int64_t)gpos_sn[d] * P + c] : 0.0;
 }
 
 void launch_sn_to_batch(int64_t nloc, const int32_t* lmap, const int32_t* gpos_sn, const double* b,
-                        const double* ysn, double* xloc, double* yloc, cudaStream_t st) {
+                        const double* ysn, double* xloc, double* yloc, cudaStream_t st, int P,
+                        int c) {
   if (nloc <= 0) return;
   k_sn_to_batch<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(nloc, lmap, gpos_sn, b, ysn, xloc,
-                                                                 yloc);
+                                                                 yloc, P, c);
 }
 
 // ===========================================================================

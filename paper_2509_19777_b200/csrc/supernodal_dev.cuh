@@ -101,8 +101,11 @@ void launch_front_to_tiles(const DevBatch& b, const int32_t* list, const SnNum& 
                            cudaStream_t st);
 void launch_tiles_to_finv(const DevBatch& b, const int32_t* list, int nlist, int max_w,
                           const SnNum& nm, double* factor, cudaStream_t st);
+// xloc = b[lmap], yloc = ysn[gpos_sn[lmap] P + c] (P interleaved columns of a
+// multi-RHS solve; P = 1, c = 0: one RHS)
 void launch_sn_to_batch(int64_t nloc, const int32_t* lmap, const int32_t* gpos_sn, const double* b,
-                        const double* ysn, double* xloc, double* yloc, cudaStream_t st);
+                        const double* ysn, double* xloc, double* yloc, cudaStream_t st, int P = 1,
+                        int c = 0);
 void launch_mr_io(int nitems, const SnMrItem* it, const int32_t* lidx, const int64_t* b_off,
                   const int32_t* ld, const double* R, double* X, double* B, int to_x,
                   cudaStream_t st);
