@@ -111,3 +111,21 @@ def test_apply_many_vs_oracle(case, op, k, shape):
     for c in range(k):
         r = ref(V[c])
         assert rel(out[c], r) <= 1e-12, (c, rel(out[c], r))
+
+
+def test_apply_many_errors():
+    """hplmm_apply_many's argument and state checks (include/hplmm.h): bad op,
+    ncols outside 1..4, ld < n_dof -> ERR_ARG; the dense local solver -> ERR_STATE."""
+    from paper_2509_19777_b200 import Solver
+    from paper_2509_19777_b200.hplmm import HPLMMError
+    p, s, h = oracle_case("cube8")
+    sv = Solver(p).assemble(0).setup()
+    V = torch.zeros((5, s.n_dof), dtype=torch.float64, device="cuda")
+    for op, cols in (("MG", 2), ("MZETA", 5)):
+        with pytest.raises(HPLMMError, match="ERR_ARG"):
+            sv.apply_many(op, V[:cols])
+    with pytest.raises(HPLMMError, match="ERR_ARG"):
+        sv.apply_many("MZETA", V[:2, :-1].contiguous())   # ld = n_dof - 1
+    dense = Solver(p, local_factor=0).assemble(0).setup()
+    with pytest.raises(HPLMMError, match="ERR_STATE"):
+        dense.apply_many("MZETA", V[:2])
