@@ -1529,6 +1529,10 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     co.giface_ptr = h->upload(hs.giface_ptr);
     co.giface = h->upload(hs.giface);
     co.ld = h->upload(ld);
+    co.max_ld = ld.empty() ? 0 : *std::max_element(ld.begin(), ld.end());
+    co.max_nu3 = 0;
+    for (size_t cf = 0; cf + 1 < hs.mortar_ptr.size(); ++cf)
+      co.max_nu3 = std::max(co.max_nu3, 3 * (hs.mortar_ptr[cf + 1] - hs.mortar_ptr[cf]));
     co.b_off = h->upload(b_off);
     co.B = h->dalloc<double>(std::max<int64_t>(off, 1));
     co.R = h->dalloc<double>(std::max<int64_t>(off, 1), true);

@@ -515,36 +515,101 @@ __global__ void __launch_bounds__(256) k_restrict_chunks(DevCoarse c, const int3
   }
 }
 
-// per grain: gpart[j] = sum over its 64-row chunks of tpart (chunk order; the
-// chunks of a grain are contiguous with stride ld_g, so reads are coalesced)
-__global__ void k_restrict_grain(DevCoarse c) {
+// per grain: gpart[j] = sum over its 64-row chunks of tpart.  One CTA per (grain,
+// 32-column tile): lane = column, warp w sums the chunks w, w + 8, ... (two
+// interleaved partial sums), then warp 0 adds the 8 warp sums in order (fixed
+// order; a single thread per column walking all ~100 chunks of a grain was a
+// 26-step dependent load chain: 29 us per launch at cfg3)
+__global__ void __launch_bounds__(256) k_restrict_grain(DevCoarse c) {
   const int g = blockIdx.x;
   const int L = c.ld[g];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.y * 32 + lane;
   const int c0 = c.chunk_ptr[g], c1 = c.chunk_ptr[g + 1];
-  if (c1 <= c0) return;
+  if (blockIdx.y * 32 >= L || c1 <= c0) return;
+  __shared__ double red[8][32];
   const double* t = c.tpart + c.chunk_t[c0];
-  double* out = c.gpart + c.yext_off[g];
   const int nch = c1 - c0;
-  for (int j = threadIdx.x; j < L; j += blockDim.x) {
-    // four interleaved partial sums keep four loads in flight (fixed order)
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int ch = 0;
-    for (; ch + 3 < nch; ch += 4) {
+  double a0 = 0.0, a1 = 0.0;
+  if (j < L) {
+    int ch = w;
+    for (; ch + 8 < nch; ch += 16) {
       a0 += t[(int64_t)ch * L + j];
-      a1 += t[(int64_t)(ch + 1) * L + j];
-      a2 += t[(int64_t)(ch + 2) * L + j];
-      a3 += t[(int64_t)(ch + 3) * L + j];
+      a1 += t[(int64_t)(ch + 8) * L + j];
     }
-    for (; ch < nch; ++ch) a0 += t[(int64_t)ch * L + j];
-    out[j] = (a0 + a1) + (a2 + a3);
+    if (ch < nch) a0 += t[(int64_t)ch * L + j];
+  }
+  red[w][lane] = a0 + a1;
+  __syncthreads();
+  if (w == 0 && j < L) {
+    double a = red[0][lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) a += red[q][lane];
+    c.gpart[c.yext_off[g] + j] = a;
   }
 }
 
 // rm[k] = sum over grains of the pre-summed B_g^T r parts + the interface term
+// Q^o[:, k]^T r.  One warp per interface: lanes split its rows, each lane
+// keeps the partial sums of all the interface's 3 nu mortar columns (r read
+// once per row, not once per column), one transposing butterfly reduces them
+// (fixed order).  rc[g] = correction part.  NV = 3 nu rounded up to 16 / 32.
+template <int NV>
+__global__ void __launch_bounds__(256) k_restrict_final(DevCoarse c, const double* r, double* rm,
+                                                        double* rc) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbi = (c.n_ifaces + 7) / 8;
+  if ((int)blockIdx.x >= nbi) {   // correction parts
+    const int g = ((int)blockIdx.x - nbi) * 256 + threadIdx.x;
+    if (g < c.n_grains) rc[g] = c.Dc[g] != 0.0 ? c.gpart[c.yext_off[g] + c.ld[g] - 1] : 0.0;
+    return;
+  }
+  const int cf = blockIdx.x * 8 + w;
+  if (cf >= c.n_ifaces) return;
+  const int nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
+  const int kb = 3 * c.mortar_ptr[cf];
+  const double* W = c.W + c.wt_off[cf];
+  const int e0 = c.iface_ptr[cf], e1 = c.iface_ptr[cf + 1];
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  for (int e = e0 + lane; e < e1; e += 32) {
+    const double* ry = r + 3 * (int64_t)c.iface_nodes[e];
+    const double r0 = ry[0], r1 = ry[1], r2 = ry[2];
+    const double* wr = W + 3 * (int64_t)(e - e0) * nu3;
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+      if (q < nu3) acc[q] += wr[q] * r0 + wr[nu3 + q] * r1 + wr[2 * nu3 + q] * r2;
+  }
+  int idx = 0, o = 16;
+#pragma unroll
+  for (int h = NV / 2; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = lane & o;
+    if (up) idx += h;
+#pragma unroll
+    for (int t = 0; t < h; ++t) {
+      const double send = up ? acc[t] : acc[h + t];
+      const double keep = up ? acc[h + t] : acc[t];
+      acc[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (; o > 0; o >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
+  if ((lane & (32 / NV - 1)) == 0 && idx < nu3) {
+    const int k = kb + idx;
+    double a = acc[0];
+    for (int e = c.mcol_ptr[k]; e < c.mcol_ptr[k + 1]; ++e)
+      a += c.gpart[c.yext_off[c.mcol_g[e]] + c.mcol_j[e]];
+    rm[k] = a;
+  }
+}
+
+// generic form (any 3 nu, e.g. the full-cap case nu_c = |F_c|): RF_LPC lanes per
+// mortar column.  rm[k] = sum over grains of the pre-summed B_g^T r parts + the interface term
 // Q^o[:, k]^T r; RF_LPC lanes per column split the interface rows (fixed
 // order: lane-strided partial sums, then a butterfly), rc[g] = correction part
 constexpr int RF_LPC = 8;
-__global__ void k_restrict_final(DevCoarse c, const int32_t* mortar_iface, const double* r,
+__global__ void k_restrict_final_lpc(DevCoarse c, const int32_t* mortar_iface, const double* r,
                                  double* rm, double* rc) {
   const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int k = (int)(gt / RF_LPC), sl = (int)(gt % RF_LPC);
@@ -584,11 +649,16 @@ void launch_restrict(const DevCoarse& c, const double* r, double* rm, double* rc
                      cudaStream_t st) {
   if (c.n_chunks > 0)
     k_restrict_chunks<<<(unsigned)c.n_chunks, 256, 0, st>>>(c, c.g_lmap, c.g_row_base, r);
-  int n = c.Nm + c.n_grains;
-  if (c.n_grains > 0) k_restrict_grain<<<c.n_grains, 256, 0, st>>>(c);
-  if (n > 0)
-    k_restrict_final<<<(unsigned)(((int64_t)n * RF_LPC + 255) / 256), 256, 0, st>>>(
-        c, c.mortar_iface, r, rm, rc);
+  if (c.n_grains > 0)
+    k_restrict_grain<<<dim3((unsigned)c.n_grains, (unsigned)((c.max_ld + 31) / 32)), 256, 0, st>>>(c);
+  const int nb = (c.n_ifaces + 7) / 8 + (c.n_grains + 255) / 256;
+  if (nb > 0) {
+    if (c.max_nu3 <= 16) k_restrict_final<16><<<nb, 256, 0, st>>>(c, r, rm, rc);
+    else if (c.max_nu3 <= 32) k_restrict_final<32><<<nb, 256, 0, st>>>(c, r, rm, rc);
+    else
+      k_restrict_final_lpc<<<(unsigned)(((int64_t)(c.Nm + c.n_grains) * RF_LPC + 255) / 256), 256,
+                             0, st>>>(c, c.mortar_iface, r, rm, rc);
+  }
 }
 
 // ---------------------------------------------------------------------------

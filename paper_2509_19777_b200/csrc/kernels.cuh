@@ -107,6 +107,8 @@ struct DevCoarse {
   int32_t* giface_ptr = nullptr;       // [G+1]
   int32_t* giface = nullptr;           // interfaces per grain (sorted)
   int32_t* ld = nullptr;               // [G] k_g + 1
+  int max_ld = 0;                      // max over grains of ld
+  int max_nu3 = 0;                     // max over interfaces of 3 nu_c
   int64_t* b_off = nullptr;            // [G] offset of B_g (row-major [64 nb_g x ld_g])
   double* B = nullptr;                 // shape vectors + correction column
   double* R = nullptr;                 // scratch R_g / Y_g (setup), same layout
