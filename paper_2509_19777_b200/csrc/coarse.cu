@@ -757,9 +757,15 @@ __global__ void k_prolong_iface(DevCoarse c, const double* __restrict__ ym, doub
   const int nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
   const double* w = c.W + c.wt_off[cf] + (int64_t)(3 * (en - c.iface_ptr[cf]) + gam) * nu3;
   int kb = 3 * c.mortar_ptr[cf];
-  double acc = 0.0;
-  for (int q = 0; q < nu3; ++q) acc += w[q] * ym[kb + q];
-  x[3 * (int64_t)c.iface_nodes[en] + gam] = acc;
+  // two interleaved partial sums (fixed order): half the dependent FMA chain
+  double a0 = 0.0, a1 = 0.0;
+  int q = 0;
+  for (; q + 1 < nu3; q += 2) {
+    a0 += w[q] * ym[kb + q];
+    a1 += w[q + 1] * ym[kb + q + 1];
+  }
+  if (q < nu3) a0 += w[q] * ym[kb + q];
+  x[3 * (int64_t)c.iface_nodes[en] + gam] = a0 + a1;
 }
 
 static int g_prolong_mode = -1;

@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(32 * (sy_cons<P>() + 1), 1)
 // warps per row block; warp w sums the partials of index = w (mod SR_WARPS) in
 // ascending order (four loads in flight), then warp 0 adds the warp sums in
 // order w = 0..SR_WARPS-1 (fixed order, no atomics)
-constexpr int SR_WARPS = 8;
+constexpr int SR_WARPS = 16;
 __global__ void __launch_bounds__(32 * SR_WARPS)
     k_symv_reduce(int64_t nrows, const int32_t* __restrict__ row_s,
                   const int32_t* __restrict__ row_k, const int32_t* __restrict__ nb,
