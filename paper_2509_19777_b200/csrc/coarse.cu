@@ -550,30 +550,40 @@ __global__ void __launch_bounds__(256) k_restrict_grain(DevCoarse c) {
 }
 
 // rm[k] = sum over grains of the pre-summed B_g^T r parts + the interface term
-// Q^o[:, k]^T r.  One warp per interface: lanes split its rows, each lane
-// keeps the partial sums of all the interface's 3 nu mortar columns (r read
-// once per row, not once per column), one transposing butterfly reduces them
-// (fixed order).  rc[g] = correction part.  NV = 3 nu rounded up to 16 / 32.
+// Q^o[:, k]^T r.  RF_W warps per interface split its rows; each lane keeps the
+// partial sums of all the interface's 3 nu mortar columns (r read once per
+// row, not once per column), one transposing butterfly per warp, then the
+// RF_W warp sums in order through shared memory (fixed order).  rc[g] =
+// correction part.  NV = 3 nu rounded up to 16 / 32.
+constexpr int RF_W = 4;
 template <int NV>
 __global__ void __launch_bounds__(256) k_restrict_final(DevCoarse c, const double* r, double* rm,
                                                         double* rc) {
+  constexpr int IPB = 8 / RF_W;   // interfaces per 256-thread block
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nbi = (c.n_ifaces + 7) / 8;
+  const int wi = w / RF_W, wq = w % RF_W;
+  const int nbi = (c.n_ifaces + IPB - 1) / IPB;
+  __shared__ double red[8][NV];
   if ((int)blockIdx.x >= nbi) {   // correction parts
     const int g = ((int)blockIdx.x - nbi) * 256 + threadIdx.x;
     if (g < c.n_grains) rc[g] = c.Dc[g] != 0.0 ? c.gpart[c.yext_off[g] + c.ld[g] - 1] : 0.0;
     return;
   }
-  const int cf = blockIdx.x * 8 + w;
-  if (cf >= c.n_ifaces) return;
-  const int nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
-  const int kb = 3 * c.mortar_ptr[cf];
-  const double* W = c.W + c.wt_off[cf];
-  const int e0 = c.iface_ptr[cf], e1 = c.iface_ptr[cf + 1];
+  const int cf = blockIdx.x * IPB + wi;
+  const bool live = cf < c.n_ifaces;
+  int nu3 = 0, kb = 0, e0 = 0, e1 = 0;
+  const double* W = nullptr;
+  if (live) {
+    nu3 = 3 * (c.mortar_ptr[cf + 1] - c.mortar_ptr[cf]);
+    kb = 3 * c.mortar_ptr[cf];
+    W = c.W + c.wt_off[cf];
+    e0 = c.iface_ptr[cf];
+    e1 = c.iface_ptr[cf + 1];
+  }
   double acc[NV];
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-  for (int e = e0 + lane; e < e1; e += 32) {
+  for (int e = e0 + wq * 32 + lane; e < e1; e += 32 * RF_W) {
     const double* ry = r + 3 * (int64_t)c.iface_nodes[e];
     const double r0 = ry[0], r1 = ry[1], r2 = ry[2];
     const double* wr = W + 3 * (int64_t)(e - e0) * nu3;
@@ -595,9 +605,13 @@ __global__ void __launch_bounds__(256) k_restrict_final(DevCoarse c, const doubl
   }
 #pragma unroll
   for (; o > 0; o >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
-  if ((lane & (32 / NV - 1)) == 0 && idx < nu3) {
-    const int k = kb + idx;
-    double a = acc[0];
+  if ((lane & (32 / NV - 1)) == 0) red[w][idx] = acc[0];
+  __syncthreads();
+  if (live && wq == 0 && lane < nu3) {
+    const int k = kb + lane;
+    double a = red[wi * RF_W][lane];
+#pragma unroll
+    for (int t = 1; t < RF_W; ++t) a += red[wi * RF_W + t][lane];
     for (int e = c.mcol_ptr[k]; e < c.mcol_ptr[k + 1]; ++e)
       a += c.gpart[c.yext_off[c.mcol_g[e]] + c.mcol_j[e]];
     rm[k] = a;
@@ -651,7 +665,7 @@ void launch_restrict(const DevCoarse& c, const double* r, double* rm, double* rc
     k_restrict_chunks<<<(unsigned)c.n_chunks, 256, 0, st>>>(c, c.g_lmap, c.g_row_base, r);
   if (c.n_grains > 0)
     k_restrict_grain<<<dim3((unsigned)c.n_grains, (unsigned)((c.max_ld + 31) / 32)), 256, 0, st>>>(c);
-  const int nb = (c.n_ifaces + 7) / 8 + (c.n_grains + 255) / 256;
+  const int nb = (c.n_ifaces + 8 / RF_W - 1) / (8 / RF_W) + (c.n_grains + 255) / 256;
   if (nb > 0) {
     if (c.max_nu3 <= 16) k_restrict_final<16><<<nb, 256, 0, st>>>(c, r, rm, rc);
     else if (c.max_nu3 <= 32) k_restrict_final<32><<<nb, 256, 0, st>>>(c, r, rm, rc);
