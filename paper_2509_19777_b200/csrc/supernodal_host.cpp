@@ -36,6 +36,18 @@ struct SubResult {
   std::vector<std::vector<int32_t>> rel;            // per supernode (as child)
 };
 
+// separator choice (HPLMM_SN_SEP: 0 = median plane of the longest axis,
+// 1 = fewest-node balanced plane, default); HPLMM_SN_SEPBAL = balance bound (%)
+int sep_mode() {
+  static const int v = getenv("HPLMM_SN_SEP") ? atoi(getenv("HPLMM_SN_SEP")) : 1;
+  return v;
+}
+int sep_bal() {
+  static const int v = getenv("HPLMM_SN_SEPBAL") ? atoi(getenv("HPLMM_SN_SEPBAL")) : 42;
+  return v;
+}
+#define SEP_BAL sep_bal()
+
 class NdBuilder {
  public:
   NdBuilder(const int32_t* ijk, const std::vector<int32_t>& gnodes, int leaf)
@@ -57,12 +69,52 @@ class NdBuilder {
     for (int c = 1; c < 3; ++c)
       if (hi[c] - lo[c] > hi[ax] - lo[ax]) ax = c;
     if ((int)ids.size() <= leaf_ || hi[ax] - lo[ax] < 2) return {leaf(std::move(ids))};
+    int m = 0;
+    if (sep_mode() == 0) {   // r01: median plane of the longest axis
+      std::vector<int> vals(ids.size());
+      for (size_t i = 0; i < ids.size(); ++i) vals[i] = ijk_[3 * (int64_t)g_[ids[i]] + ax];
+      std::vector<int> sorted = vals;
+      std::nth_element(sorted.begin(), sorted.begin() + sorted.size() / 2, sorted.end());
+      m = sorted[sorted.size() / 2];
+      m = std::max(lo[ax] + 1, std::min(hi[ax] - 1, m));
+    } else {
+      // r02: over every axis whose extent is at least half the longest, the
+      // lattice plane with the fewest nodes among those leaving at least
+      // SEP_BAL of the nodes on each side (a porous subdomain's planes differ
+      // in solid fraction; a smaller separator means less fill: fewer factor
+      // bytes and smaller fronts); ties -> longer axis, then nearer the median
+      const int64_t N = (int64_t)ids.size();
+      const int ax0 = ax;
+      int64_t best = INT64_MAX, best_dev = INT64_MAX;
+      for (int c = 0; c < 3; ++c) {
+        if (hi[c] - lo[c] < 2 || 2 * (hi[c] - lo[c]) < hi[ax0] - lo[ax0]) continue;
+        std::vector<int64_t> cnt(hi[c] - lo[c] + 1, 0);
+        for (int a : ids) cnt[ijk_[3 * (int64_t)g_[a] + c] - lo[c]]++;
+        int64_t below = 0;
+        for (int v = 0; v <= hi[c] - lo[c]; ++v) {
+          const int64_t above = N - below - cnt[v];
+          if (v >= 1 && v <= hi[c] - lo[c] - 1 && below * 100 >= SEP_BAL * N && above * 100 >= SEP_BAL * N) {
+            const int64_t dev = std::llabs(2 * below + cnt[v] - N);
+            const int64_t score = cnt[v];
+            if (score < best || (score == best && c == ax0 && dev < best_dev)) {
+              best = score;
+              best_dev = dev;
+              ax = c;
+              m = lo[c] + v;
+            }
+          }
+          below += cnt[v];
+        }
+      }
+      if (best == INT64_MAX) {   // no plane meets the balance bound: median
+        std::vector<int> vals(ids.size());
+        for (size_t i = 0; i < ids.size(); ++i) vals[i] = ijk_[3 * (int64_t)g_[ids[i]] + ax];
+        std::nth_element(vals.begin(), vals.begin() + vals.size() / 2, vals.end());
+        m = std::max(lo[ax] + 1, std::min(hi[ax] - 1, vals[vals.size() / 2]));
+      }
+    }
     std::vector<int> vals(ids.size());
     for (size_t i = 0; i < ids.size(); ++i) vals[i] = ijk_[3 * (int64_t)g_[ids[i]] + ax];
-    std::vector<int> sorted = vals;
-    std::nth_element(sorted.begin(), sorted.begin() + sorted.size() / 2, sorted.end());
-    int m = sorted[sorted.size() / 2];
-    m = std::max(lo[ax] + 1, std::min(hi[ax] - 1, m));
     std::vector<int32_t> L, R, S;
     for (size_t i = 0; i < ids.size(); ++i)
       (vals[i] < m ? L : (vals[i] > m ? R : S)).push_back(ids[i]);
