@@ -24,7 +24,7 @@ namespace {
 
 thread_local std::string g_last_error;
 
-constexpr int kSnLeaf = 40;                          // ND leaf size (nodes)
+constexpr int kSnLeaf = 32;                          // ND leaf size (nodes)
 constexpr double kSurfaceTie = 0.1;                  // R29 tie (x mean shear modulus)
 static int sn_leaf() {   // HPLMM_SN_LEAF overrides (ordering experiments)
   static const int v = getenv("HPLMM_SN_LEAF") ? std::max(4, atoi(getenv("HPLMM_SN_LEAF"))) : kSnLeaf;

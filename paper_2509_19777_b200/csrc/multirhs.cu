@@ -279,7 +279,7 @@ __device__ __forceinline__ double warp_transpose_sum(double (&v)[NV], int lane, 
   return v[0];
 }
 
-// grain rows: one CTA per 64-row block (NRHS = 4: per 32-row half), warp =
+// grain rows: one CTA per 64-row block, warp =
 // ROWS rows, lanes stride the shape columns (coalesced row reads of B_g, read
 // ONCE for the NRHS vectors), transposing warp reduction of ROWS x NRHS sums
 template <int NRHS>
@@ -290,7 +290,9 @@ __global__ void __launch_bounds__(256) k_prolong_rows_k(DevCoarse c, const int32
                                                         const double* __restrict__ Ck, int64_t ldc,
                                                         int ncols, double* __restrict__ x,
                                                         int64_t ldx) {
-  constexpr int ROWS = NRHS == 4 ? 4 : 8;            // ROWS x NRHS <= 32 accumulators
+  // 8 rows per warp for every NRHS (8 NRHS <= 32 accumulators): each y load
+  // serves 8 rows (4 rows per warp with NRHS = 4: 23.9 vs 19.5 ms per cfg3 block)
+  constexpr int ROWS = 8;
   constexpr int SPLIT = 8 / ROWS;                    // CTAs per 64-row block
   const int64_t ch = blockIdx.x / SPLIT;
   const int half = (int)(blockIdx.x % SPLIT);
@@ -376,7 +378,7 @@ static void prolong_k(const DevCoarse& c, const double* ym, const double* yc, co
                       cudaStream_t st) {
   if (c.n_grains > 0) k_yext_k<NRHS><<<c.n_grains, 128, 0, st>>>(c, ym, yc, Dck, ncols, yk);
   if (c.n_chunks > 0)
-    k_prolong_rows_k<NRHS><<<(unsigned)(c.n_chunks * (NRHS == 4 ? 2 : 1)), 256, 0, st>>>(c, c.g_lmap, c.g_row_s,
+    k_prolong_rows_k<NRHS><<<(unsigned)c.n_chunks, 256, 0, st>>>(c, c.g_lmap, c.g_row_s,
                                                                  c.g_row_base, yk, Ck, ldc, ncols,
                                                                  x, ldx);
   if (c.n_iface_nodes > 0)
