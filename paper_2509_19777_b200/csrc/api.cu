@@ -331,9 +331,9 @@ void build_batch(hplmm_handle* h, DevBatch& b, const std::vector<int32_t>& ptr,
   b.part_row = h->dalloc<double>((size_t)nt * TB, transient);
   b.part_col = h->dalloc<double>((size_t)nt * TB, transient);
   if (setup_buffers) {
-    b.dinv = h->dalloc<double>((size_t)nsub * TILE, true);
-    b.cbuf = h->dalloc<double>((size_t)nr * TILE, true);
-    b.wbuf = h->dalloc<double>((size_t)nr * TILE, true);
+    b.dinv = h->dalloc<double>((size_t)nsub * TILE * SWEEP_M * SWEEP_M, true);
+    b.cbuf = h->dalloc<double>((size_t)nr * TILE * SWEEP_M, true);
+    b.wbuf = h->dalloc<double>((size_t)nr * TILE * SWEEP_M, true);
   }
 }
 

@@ -155,42 +155,6 @@ void launch_pad_identity(const DevBatch& b, cudaStream_t st) {
 //   A_pp <- -D^-1,  A_ip <- A_ip D^-1,  A_ij <- A_ij - A_ip D^-1 A_pj
 // keeps A symmetric; sweeping every block yields -A^-1 (negated at the end).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_sweep_pivot(int p, int nsub, const int32_t* nb,
-                                                     const int64_t* tile_base,
-                                                     const double* tiles, double* dinv,
-                                                     int32_t* err) {
-  int s = blockIdx.x;
-  if (s >= nsub || nb[s] <= p) return;
-  extern __shared__ double sm[];
-  double* a = sm;              // 64x64 col-major
-  double* colk = sm + TILE;    // 64
-  __shared__ double dk;
-  load_tile(a, tiles + tidx(tile_base, s, p, p) * TILE);
-  bool bad = false;
-  for (int k = 0; k < TB; ++k) {
-    __syncthreads();
-    if (threadIdx.x < TB) colk[threadIdx.x] = a[k * TB + threadIdx.x];
-    if (threadIdx.x == 0) dk = a[k * TB + k];
-    __syncthreads();
-    double d = dk;
-    if (!(d > 0.0)) bad = true;
-    double inv = 1.0 / d;
-    for (int t = threadIdx.x; t < TILE; t += blockDim.x) {
-      int c = t >> 6, r = t & 63;
-      double v;
-      if (r == k && c == k) v = -inv;
-      else if (r == k) v = colk[c] * inv;
-      else if (c == k) v = colk[r] * inv;
-      else v = a[t] - colk[r] * colk[c] * inv;
-      a[t] = v;
-    }
-  }
-  __syncthreads();
-  if (bad && threadIdx.x == 0) atomicMin(err, s);
-  double* out = dinv + (int64_t)s * TILE;
-  for (int t = threadIdx.x; t < TILE; t += blockDim.x) out[t] = -a[t];
-}
-
 // C_i = A_ip (old), W_i = C_i D^-1 for every row block i != p
 template <bool DMMA>
 __global__ void __launch_bounds__(256) k_sweep_panel(int p, int64_t nrows, const int32_t* row_s,
@@ -334,12 +298,279 @@ bool use_dmma() {
   return g_dmma == 1;
 }
 
+// ---------------------------------------------------------------------------
+// Blocked sweeps (r02): M consecutive pivot tiles P = {p .. p+mg-1} (mg =
+// min(M, nb - p) per subdomain) are swept in one pass -- sweeping the pivots
+// of P one after the other equals sweeping the (64 mg)^2 block D = A_PP:
+//   A_PP <- -D^-1,  A_iP <- A_iP D^-1,  A_ij <- A_ij - A_iP D^-1 A_Pj.
+// The update is then a 64 x 64 x 64M DMMA product per tile and every target
+// tile is read and written once per M pivots instead of once per pivot: at
+// M = 1 the update moves 64 KB of HBM per 0.5 MFLOP, about the B200's FP64
+// tensor-core balance, so it cannot be compute-bound (r01: 36.8% DMMA pipe,
+// 16 TFLOP/s on the cfg3 coarse block).  D (padded with the identity when
+// mg < M) is inverted in registers by one 1024-thread CTA; C_i = A_iP and
+// W_i = C_i D^-1 are kept k-major (k * 64 + r, k < 64M) per row block.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double tile_elem_sym(const double* tiles, const int64_t* tile_base,
+                                                int s, int I, int J, int r, int c) {
+  // element (r, c) of the symmetric block (I, J) from the packed lower tiles
+  if (I >= J) return tiles[tidx(tile_base, s, I, J) * TILE + c * TB + r];
+  return tiles[tidx(tile_base, s, J, I) * TILE + r * TB + c];
+}
+
+// D^-1 by the sweep in registers: one CTA of 1024 threads per subdomain,
+// thread i owns row r = i % 64M of the columns c = i / 64M + (1024 / 64M) j.
+// Step k updates every element by the same rank-1 formula
+//   a_rc <- a_rc - (a_rk / a_kk) a_kc
+// and then fixes row k (a_kc / a_kk), column k (a_rk / a_kk) and the pivot
+// (-1 / a_kk).  The owners of column k + 1 publish it (and 1 / a_k+1,k+1)
+// into a double-buffered shared column as they update it, so a step costs one
+// barrier and two instructions per element (r01: 256 threads, the tile in
+// shared memory, two barriers and a branchy update per element -- 0.23 ms
+// per 64-wide pivot, 12% of the cfg3 setup).  The k loop is unrolled by the
+// column stride so that the register holding column k is static.
+template <int M>
+__global__ void __launch_bounds__(1024) k_sweep_pivot_m(int p, int nsub, const int32_t* nb,
+                                                        const int64_t* tile_base,
+                                                        const double* tiles, double* dinv,
+                                                        int32_t* err) {
+  constexpr int N = TB * M, PER = N * N / 1024, CSTEP = 1024 / N;
+  const int s = blockIdx.x;
+  if (s >= nsub || nb[s] <= p) return;
+  const int mg = min(M, nb[s] - p);
+  __shared__ double colbuf[2][N];
+  __shared__ double invbuf[2];
+  const int r = threadIdx.x % N, c0 = threadIdx.x / N;
+  double v[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int c = c0 + CSTEP * j;
+    const int R = r >> 6, C = c >> 6;
+    v[j] = (R < mg && C < mg) ? tile_elem_sym(tiles, tile_base, s, p + R, p + C, r & 63, c & 63)
+                              : (r == c ? 1.0 : 0.0);
+  }
+  bool bad = false;
+  if (c0 == 0) {
+    colbuf[0][r] = v[0];
+    if (r == 0) {
+      bad = !(v[0] > 0.0);
+      invbuf[0] = 1.0 / v[0];
+    }
+  }
+  __syncthreads();
+  const int K = TB * mg;
+#pragma unroll
+  for (int jj = 0; jj < PER; ++jj) {
+#pragma unroll 1
+    for (int kk = 0; kk < CSTEP; ++kk) {
+      const int k = jj * CSTEP + kk;
+      if (k >= K) break;
+      const double* colk = colbuf[k & 1];
+      const double inv = invbuf[k & 1];
+      const double ck_r = colk[r];
+      const double f = ck_r * inv;
+      double vk = 0.0;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const double ckc = colk[c0 + CSTEP * j];
+        v[j] = r == k ? ckc * inv : fma(-f, ckc, v[j]);   // row k, else the rank-1 update
+        if (j == jj) vk = v[j];
+      }
+      if (c0 == kk) vk = r == k ? -inv : f;                // column k and the pivot
+#pragma unroll
+      for (int j = 0; j < PER; ++j)
+        if (j == jj && c0 == kk) v[j] = vk;
+      // publish column k + 1 and its pivot's reciprocal
+      const int k1 = k + 1, j1 = k1 / CSTEP;
+      if (k1 < K && c0 == k1 % CSTEP) {
+        double w = 0.0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+          if (j == j1) w = v[j];
+        colbuf[k1 & 1][r] = w;
+        if (r == k1) {
+          if (!(w > 0.0)) bad = true;
+          invbuf[k1 & 1] = 1.0 / w;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (bad) atomicMin(err, s);
+  double* out = dinv + (int64_t)s * N * N;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) out[(int64_t)(c0 + CSTEP * j) * N + r] = -v[j];
+}
+
+// C_i = A_iP (k-major, zero beyond 64 mg), W_i = C_i D^-1 for every row block i
+// outside P; one CTA per row block
+template <int M>
+__global__ void __launch_bounds__(256) k_sweep_panel_m(int p, int64_t nrows, const int32_t* row_s,
+                                                       const int32_t* row_k, const int32_t* nb,
+                                                       const int64_t* tile_base,
+                                                       const double* tiles, const double* dinv,
+                                                       double* cbuf, double* wbuf) {
+  constexpr int N = TB * M;
+  const int64_t rb = blockIdx.x;
+  if (rb >= nrows) return;
+  const int s = row_s[rb], i = row_k[rb];
+  if (nb[s] <= p) return;
+  const int mg = min(M, nb[s] - p);
+  if (i >= p && i < p + mg) return;
+  extern __shared__ double sm[];
+  double* As = sm;            // (r, k) at k*64 + r, k < N
+  double* Bs = sm + TB * N;   // D^-1, (k, c) at k*N + c (symmetric)
+  for (int e = threadIdx.x; e < TB * N; e += blockDim.x) {
+    const int k = e >> 6, r = e & 63, b = k >> 6;
+    As[e] = b < mg ? tile_elem_sym(tiles, tile_base, s, i, p + b, r, k & 63) : 0.0;
+  }
+  const double* D = dinv + (int64_t)s * N * N;
+  for (int e = threadIdx.x; e < N * N / 2; e += blockDim.x)
+    reinterpret_cast<double2*>(Bs)[e] = reinterpret_cast<const double2*>(D)[e];
+  __syncthreads();
+  double* C = cbuf + rb * (int64_t)(M * TILE);
+  double* W = wbuf + rb * (int64_t)(M * TILE);
+  for (int e = threadIdx.x; e < TB * N / 2; e += blockDim.x)
+    reinterpret_cast<double2*>(C)[e] = reinterpret_cast<const double2*>(As)[e];
+#pragma unroll 1
+  for (int cb = 0; cb < M; ++cb) {
+    double acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+    tile_dmma(As, TB, Bs + cb * TB, N, N, acc);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      int r, c;
+      dmma_rc(t, r, c);
+      W[(cb * TB + c) * TB + r] = acc[t];
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// A_IJ -= W_I C_J^T over K = 64 M for every tile outside P; the tiles of
+// row / column P are overwritten with W (and -D^-1).  The K loop streams
+// 32-deep chunks of W_I and C_J (L2-resident) through a two-stage cp.async
+// ring (rows padded to 72 doubles against bank conflicts) while the target
+// tile's values are already in registers.
+constexpr int SWU_KC = 32, SWU_LDP = 72;
+constexpr size_t SWU_SMEM = 2 * 2 * SWU_KC * SWU_LDP * sizeof(double);
+
+template <int M>
+__global__ void __launch_bounds__(256) k_sweep_update_m(int p, int64_t ntiles, const int32_t* tile_s,
+                                                        const int32_t* tile_ij, const int32_t* nb,
+                                                        const int64_t* row_base, double* tiles,
+                                                        const double* dinv, const double* cbuf,
+                                                        const double* wbuf) {
+  constexpr int N = TB * M;
+  const int64_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  const int s = tile_s[t];
+  if (nb[s] <= p) return;
+  const int mg = min(M, nb[s] - p);
+  const int I = tile_ij[t] >> 16, J = tile_ij[t] & 0xffff;
+  const bool inI = I >= p && I < p + mg, inJ = J >= p && J < p + mg;
+  double* T = tiles + t * TILE;
+  if (inI && inJ) {          // -D^-1 block (I - p, J - p)
+    const double* D = dinv + (int64_t)s * N * N;
+    const int a = I - p, b = J - p;
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+      const int c = e >> 6, r = e & 63;
+      T[e] = -D[(int64_t)(b * TB + c) * N + a * TB + r];
+    }
+    return;
+  }
+  if (inJ) {                 // I > P:  A_I,p+b <- W_I[:, b]
+    const double* W = wbuf + (row_base[s] + I) * (int64_t)(M * TILE) + (J - p) * TILE;
+    for (int e = threadIdx.x; e < TILE / 2; e += blockDim.x)
+      reinterpret_cast<double2*>(T)[e] = reinterpret_cast<const double2*>(W)[e];
+    return;
+  }
+  if (inI) {                 // J < P:  A_p+a,J <- (W_J[:, a])^T
+    const double* W = wbuf + (row_base[s] + J) * (int64_t)(M * TILE) + (I - p) * TILE;
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+      const int c = e >> 6, r = e & 63;
+      T[e] = W[r * TB + c];
+    }
+    return;
+  }
+  extern __shared__ double sm[];
+  const double* Wg = wbuf + (row_base[s] + I) * (int64_t)(M * TILE);
+  const double* Cg = cbuf + (row_base[s] + J) * (int64_t)(M * TILE);
+  const int KC = TB * mg / SWU_KC;   // K chunks (the padding k beyond 64 mg are 0)
+  auto issue = [&](int kc) {
+    double* As = sm + (kc & 1) * (2 * SWU_KC * SWU_LDP);
+    double* Bs = As + SWU_KC * SWU_LDP;
+    const double* wsrc = Wg + (int64_t)kc * SWU_KC * TB;
+    const double* csrc = Cg + (int64_t)kc * SWU_KC * TB;
+    for (int e = threadIdx.x; e < SWU_KC * TB / 2; e += blockDim.x) {
+      const int k = e >> 5, r2 = (e & 31) * 2;
+      cp_async16(As + k * SWU_LDP + r2, wsrc + 2 * e);
+      cp_async16(Bs + k * SWU_LDP + r2, csrc + 2 * e);
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  if (KC > 1) issue(1);
+  double tv[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    int r, c;
+    dmma_rc(q, r, c);
+    tv[q] = T[c * TB + r];
+  }
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  for (int kc = 0; kc < KC; ++kc) {
+    if (kc + 1 < KC) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    const double* As = sm + (kc & 1) * (2 * SWU_KC * SWU_LDP);
+    tile_dmma(As, SWU_LDP, As + SWU_KC * SWU_LDP, SWU_LDP, SWU_KC, acc);
+    __syncthreads();
+    if (kc + 2 < KC) issue(kc + 2);
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    int r, c;
+    dmma_rc(q, r, c);
+    T[c * TB + r] = tv[q] - acc[q];
+  }
+}
+
+template <int M>
+static void sweep_steps_m(const DevBatch& b, cudaStream_t st) {
+  constexpr int N = TB * M;
+  const size_t sm_panel = (size_t)(TB * N + N * N) * sizeof(double);
+  set_max_dynamic_smem((const void*)k_sweep_panel_m<M>, sm_panel);
+  set_max_dynamic_smem((const void*)k_sweep_update_m<M>, SWU_SMEM);
+  for (int p = 0; p < b.max_nb; p += M) {
+    k_sweep_pivot_m<M><<<b.nsub, 1024, 0, st>>>(p, b.nsub, b.nb, b.tile_base, b.tiles, b.dinv, b.err);
+    k_sweep_panel_m<M><<<(unsigned)b.nrows, 256, sm_panel, st>>>(p, b.nrows, b.row_s, b.row_k, b.nb,
+                                                                 b.tile_base, b.tiles, b.dinv,
+                                                                 b.cbuf, b.wbuf);
+    k_sweep_update_m<M><<<(unsigned)b.ntiles, 256, SWU_SMEM, st>>>(p, b.ntiles, b.tile_s, b.tile_ij,
+                                                                   b.nb, b.row_base, b.tiles,
+                                                                   b.dinv, b.cbuf, b.wbuf);
+  }
+}
+
 template <bool DMMA>
 static void sweep_steps(const DevBatch& b, cudaStream_t st) {
-  size_t sm1 = (TILE + TB) * sizeof(double);
   size_t sm2 = 2 * TILE * sizeof(double);
   for (int p = 0; p < b.max_nb; ++p) {
-    k_sweep_pivot<<<b.nsub, 256, sm1, st>>>(p, b.nsub, b.nb, b.tile_base, b.tiles, b.dinv, b.err);
+    k_sweep_pivot_m<1><<<b.nsub, 1024, 0, st>>>(p, b.nsub, b.nb, b.tile_base, b.tiles, b.dinv, b.err);
     k_sweep_panel<DMMA><<<(unsigned)b.nrows, 256, sm2, st>>>(p, b.nrows, b.row_s, b.row_k, b.nb,
                                                              b.tile_base, b.row_base, b.tiles,
                                                              b.dinv, b.cbuf, b.wbuf);
@@ -351,12 +582,19 @@ static void sweep_steps(const DevBatch& b, cudaStream_t st) {
 
 void launch_sweep_invert(const DevBatch& b, cudaStream_t st) {
   if (b.nsub <= 0) return;
-  set_max_dynamic_smem((const void*)k_sweep_pivot, 2 * TILE * 8);
   set_max_dynamic_smem((const void*)k_sweep_panel<true>, 2 * TILE * 8);
   set_max_dynamic_smem((const void*)k_sweep_update<true>, 2 * TB * 72 * 8);
   set_max_dynamic_smem((const void*)k_sweep_panel<false>, 2 * TILE * 8);
   set_max_dynamic_smem((const void*)k_sweep_update<false>, 2 * TILE * 8);
-  if (use_dmma()) sweep_steps<true>(b, st);
+  // M = 2 for batches of few large blocks (the coarse S: cfg3 coarse inversion
+  // 0.392 -> 0.346 s); M = 1 for the batches of many supernode fronts, whose
+  // 1024-thread pivot CTAs (one per front) then keep two CTAs per SM (M = 2:
+  // cfg3 grain + contact front inversions 0.21 -> 0.27 s)
+  static const int sweep_env = getenv("HPLMM_SWEEP_M") ? atoi(getenv("HPLMM_SWEEP_M")) : -1;
+  const int sweep_m = sweep_env >= 0 ? sweep_env : (b.nsub <= 16 && b.max_nb >= 4 ? SWEEP_M : 1);
+  if (use_dmma() && sweep_m == 2) sweep_steps_m<2>(b, st);
+  else if (use_dmma() && sweep_m == 1) sweep_steps_m<1>(b, st);
+  else if (use_dmma()) sweep_steps<true>(b, st);   // HPLMM_SWEEP_M=0: r01 rank-64 kernels
   else sweep_steps<false>(b, st);
   k_negate<<<148 * 8, 256, 0, st>>>(b.ntiles * TILE, b.tiles);
 }

@@ -7,6 +7,7 @@ namespace hplmm {
 
 constexpr int TB = 64;              // dense tile edge (packed lower-tile storage)
 constexpr int TILE = TB * TB;       // doubles per tile
+constexpr int SWEEP_M = 2;          // pivot tiles per blocked sweep pass (dense.cu); setup buffers sized for it
 
 // A batch of dense SPD subdomain matrices stored as packed lower 64x64 tiles
 // (tile (I,J), J<=I, col-major; diagonal tiles full).  Used for the grain

@@ -295,9 +295,9 @@ void sn_factor(SnBatch& B, const double* d_val, DevAlloc& A, cudaStream_t st, in
   }
   DevBatch lb;
   lb.tiles = (double*)A.alloc((size_t)max_tiles * TILE * 8, true);
-  lb.dinv = (double*)A.alloc((size_t)max_list * TILE * 8, true);
-  lb.cbuf = (double*)A.alloc((size_t)max_rows * TILE * 8, true);
-  lb.wbuf = (double*)A.alloc((size_t)max_rows * TILE * 8, true);
+  lb.dinv = (double*)A.alloc((size_t)max_list * TILE * SWEEP_M * SWEEP_M * 8, true);
+  lb.cbuf = (double*)A.alloc((size_t)max_rows * TILE * SWEEP_M * 8, true);
+  lb.wbuf = (double*)A.alloc((size_t)max_rows * TILE * SWEEP_M * 8, true);
   lb.err = (int32_t*)A.alloc(4, true);
   int32_t* d_nb = (int32_t*)A.alloc(max_list * 4, true);
   int32_t* d_ndof = (int32_t*)A.alloc(max_list * 4, true);
