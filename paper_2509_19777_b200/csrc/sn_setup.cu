@@ -65,8 +65,180 @@ static int64_t sn_chunk_cost() {
   return v;
 }
 
+// ---------------------------------------------------------------------------
+// Subtree-parallel items.  When a batch has too few subdomains to fill the
+// CTAs evenly (cfg2: 64 grains on 148 SMs), the largest ones are shared by a
+// team of 2^L consecutive CTAs: the top L levels of the nested-dissection tree
+// are cut, every team member sweeps one subtree, and the separators above the
+// cut are handled by the member that owns the rightmost subtree below them.
+// Forward: a member accumulates its updates of the common ancestors' x in
+// rows it zeroed at the start; at each tree node the left subtree's owner
+// sends those rows to the node's owner (XSEND / XRECV add), which then
+// eliminates the separator.  Backward: the node's owner sends the solved
+// ancestor rows to the left owner (XRECV assign) before both descend.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct TeamOp {
+  int member;
+  int kind;        // 0 FWD [a,b), 1 BWD [a,b), SN_XSEND / SN_XRECV / SN_XZERO
+  int a = 0, b = 0;       // supernode range (FWD / BWD)
+  int lo = 0, cnt = 0;    // x range (exchange steps)
+  int xch = 0;            // exchange index within the team (flag, buffer slot)
+  bool add = false;
+};
+
+struct Team {
+  int members = 0;
+  std::vector<TeamOp> ops;            // a valid global order (sends before their receives)
+  std::vector<int32_t> lo, hi;        // owned x range per member
+  std::vector<int64_t> finish;        // modelled finish time per member (byte equivalents)
+  std::vector<int64_t> xoff;          // exchange buffer offset per exchange (doubles)
+  int64_t xdoubles = 0;
+};
+
+struct TeamBuilder {
+  const SnSymbolic& s;
+  const std::vector<int64_t>&pf, &pb;   // prefix sums of forward / backward supernode costs
+  const std::vector<std::vector<int>>& kids;
+  const std::vector<int>& start;        // first supernode of each supernode's subtree
+  Team& T;
+  std::vector<std::pair<int, int>> anc;  // ancestor chains (supernode ranges), innermost last
+  int64_t xcost;
+
+  struct Node {
+    int ca = 0, cb = 0;   // separator chain [ca, cb)
+    int la = 0, lb = 0;   // leaf: supernode range
+    int left = -1, right = -1;
+    int owner = -1;
+  };
+  std::vector<Node> nodes;
+
+  int64_t wrange(int a, int b) const { return (pf[b] - pf[a]) + (pb[b] - pb[a]); }
+  int plo(int a) const { return s.sn_p0[a]; }
+  int phi(int b) const { return s.sn_p0[b - 1] + s.sn_w[b - 1]; }
+
+  // split tree over the forest `roots` (ascending, contiguous subtrees)
+  int build(const std::vector<int>& roots, int depth) {
+    Node nd;
+    const int ra = start[roots.front()], rb = roots.back() + 1;
+    std::vector<int> parts = roots;
+    nd.ca = nd.cb = rb;
+    if (depth > 0 && parts.size() == 1) {   // a tree: peel the separator chain
+      int v = parts[0];
+      nd.cb = v + 1;
+      while (kids[v].size() == 1) v = kids[v][0];
+      nd.ca = v;
+      parts = kids[v];
+    }
+    if (depth == 0 || parts.size() < 2) {
+      nd.ca = nd.cb = 0;
+      nd.la = ra;
+      nd.lb = rb;
+      nd.owner = T.members++;
+      nodes.push_back(nd);
+      return (int)nodes.size() - 1;
+    }
+    // balanced contiguous cut of the parts
+    int64_t tot = 0, acc = 0, best = INT64_MAX;
+    for (int c : parts) tot += wrange(start[c], c + 1);
+    size_t cut = 1;
+    for (size_t j = 1; j < parts.size(); ++j) {
+      acc += wrange(start[parts[j - 1]], parts[j - 1] + 1);
+      const int64_t dev = std::llabs(2 * acc - tot);
+      if (dev < best) { best = dev; cut = j; }
+    }
+    const std::vector<int> L(parts.begin(), parts.begin() + cut), R(parts.begin() + cut, parts.end());
+    nd.left = build(L, depth - 1);
+    nd.right = build(R, depth - 1);
+    nd.owner = nodes[nd.right].owner;
+    nodes.push_back(nd);
+    return (int)nodes.size() - 1;
+  }
+
+  void emit(TeamOp op) { T.ops.push_back(op); }
+
+  // x ranges of the chain of node v (if any) and of its ancestors
+  std::vector<std::pair<int, int>> up_ranges(const Node& nd) const {
+    std::vector<std::pair<int, int>> r;
+    if (nd.cb > nd.ca) r.push_back({plo(nd.ca), phi(nd.cb)});
+    for (size_t i = anc.size(); i-- > 0;) r.push_back({plo(anc[i].first), phi(anc[i].second)});
+    return r;
+  }
+  void exchange(int from, int to, const std::vector<std::pair<int, int>>& rg, bool add) {
+    for (auto& q : rg) {
+      const int x = (int)T.xoff.size();
+      T.xoff.push_back(T.xdoubles);
+      T.xdoubles += (q.second - q.first + 1) & ~1;
+      emit({from, SN_XSEND, 0, 0, q.first, q.second - q.first, x, false});
+      emit({to, SN_XRECV, 0, 0, q.first, q.second - q.first, x, add});
+    }
+  }
+  void fwd(int v) {
+    const Node nd = nodes[v];
+    if (nd.left < 0) {
+      // rows of the common ancestors this member does not own start at zero
+      for (auto& c : anc_owner)
+        if (c.second != nd.owner) emit({nd.owner, SN_XZERO, 0, 0, plo(c.first.first), phi(c.first.second) - plo(c.first.first), 0, false});
+      emit({nd.owner, 0, nd.la, nd.lb});
+      return;
+    }
+    const bool chain = nd.cb > nd.ca;
+    if (chain) { anc.push_back({nd.ca, nd.cb}); anc_owner.push_back({{nd.ca, nd.cb}, nd.owner}); }
+    fwd(nd.left);
+    fwd(nd.right);
+    if (chain) { anc.pop_back(); anc_owner.pop_back(); }
+    exchange(nodes[nd.left].owner, nd.owner, up_ranges(nd), true);
+    if (chain) emit({nd.owner, 0, nd.ca, nd.cb});
+  }
+  void bwd(int v) {
+    const Node nd = nodes[v];
+    if (nd.left < 0) {
+      emit({nd.owner, 1, nd.la, nd.lb});
+      return;
+    }
+    const bool chain = nd.cb > nd.ca;
+    if (chain) emit({nd.owner, 1, nd.ca, nd.cb});
+    exchange(nd.owner, nodes[nd.left].owner, up_ranges(nd), false);
+    if (chain) anc.push_back({nd.ca, nd.cb});
+    bwd(nd.right);
+    bwd(nd.left);
+    if (chain) anc.pop_back();
+  }
+  std::vector<std::pair<std::pair<int, int>, int>> anc_owner;
+
+  void owned(int v) {
+    const Node& nd = nodes[v];
+    if (nd.left < 0) {
+      T.lo[nd.owner] = plo(nd.la);
+      T.hi[nd.owner] = phi(nd.lb);
+      return;
+    }
+    owned(nd.left);
+    owned(nd.right);
+    if (nd.cb > nd.ca) T.hi[nd.owner] = phi(nd.cb);   // the chain follows the right subtree
+  }
+  void model() {
+    std::vector<int64_t> t(T.members, 0), ready(T.xoff.size(), 0);
+    for (const TeamOp& op : T.ops) {
+      if (op.kind == 0) t[op.member] += pf[op.b] - pf[op.a];
+      else if (op.kind == 1) t[op.member] += pb[op.b] - pb[op.a];
+      else if (op.kind == SN_XSEND) { t[op.member] += xcost / 4; ready[op.xch] = t[op.member]; }
+      else if (op.kind == SN_XRECV) t[op.member] = std::max(t[op.member], ready[op.xch]) + xcost;
+    }
+    T.finish = t;
+  }
+};
+
+}  // namespace
+
+static int sn_split_levels() {
+  static const int v = getenv("HPLMM_SN_SPLIT") ? atoi(getenv("HPLMM_SN_SPLIT")) : 2;
+  return std::max(0, std::min(3, v));
+}
+
 void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nrhs,
-                   const std::vector<int32_t>* ncols, SnWork& wk, int force_cons) {
+                   const std::vector<int32_t>* ncols, SnWork& wk, int force_cons, bool allow_split) {
   const SnSymbolic& s = B.sym;
   const bool setup_only = ncols != nullptr;
   std::vector<int64_t> wgt;
@@ -91,35 +263,223 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
                           " DOFs does not fit the supernodal solve's shared memory"};
   nblocks *= sn_cfg_cps(wk.cons);
   if (const char* e = getenv("HPLMM_SN_CTAS")) nblocks = std::max(1, atoi(e));   // experiments
+  const int nslots = nblocks;
   nblocks = std::max(1, std::min<int>(nblocks, (int)isub.size()));
-  std::vector<int32_t> ptr, ids;
-  lpt(wgt, nblocks, ptr, ids);
-  if (getenv("HPLMM_DEBUG")) {   // balance of the static assignment
-    double tot = 0, mx = 0, big = 0;
-    for (int b = 0; b < nblocks; ++b) {
-      double w = 0;
-      for (int e = ptr[b]; e < ptr[b + 1]; ++e) w += (double)wgt[ids[e]];
-      tot += w;
-      mx = std::max(mx, w);
+  const bool dbg = getenv("HPLMM_DEBUG") != nullptr;
+
+  // ---- subtree-parallel teams for the largest items (one RHS, main solve only)
+  const int Lmax = (allow_split && nrhs == 1 && !ncols && !sn_xg(1) && !isub.empty()) ? sn_split_levels() : 0;
+  std::vector<int32_t> ord(wgt.size());
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int32_t)i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return wgt[a] > wgt[b]; });
+  std::vector<int64_t> pf, pb;
+  std::vector<std::vector<int>> kids;
+  std::vector<int> start;
+  if (Lmax > 0) {
+    pf.assign(s.nsn + 1, 0);
+    pb.assign(s.nsn + 1, 0);
+    kids.assign(s.nsn, {});
+    start.resize(s.nsn);
+    for (int k = 0; k < s.nsn; ++k) {
+      int64_t f = 0, b = 0;
+      for (int64_t c = s.sn_fcb[k]; c < s.sn_fce[k]; ++c) f += (s.chunks[c].bytes & 0xffffff) + sn_chunk_cost();
+      for (int64_t c = s.sn_bcb[k]; c < s.sn_bce[k]; ++c) b += (s.chunks[c].bytes & 0xffffff) + sn_chunk_cost();
+      pf[k + 1] = pf[k] + f;
+      pb[k + 1] = pb[k] + b;
+      start[k] = k;
+      if (s.sn_parent[k] >= 0) kids[s.sn_parent[k]].push_back(k);
     }
-    for (int64_t w : wgt) big = std::max(big, (double)w);
-    fprintf(stderr, "hplmm sn work: %zu items on %d CTAs, max/mean CTA weight %.3f, largest item %.3f of the mean\n",
-            wgt.size(), nblocks, mx / (tot / nblocks), big / (tot / nblocks));
+    for (int k = 0; k < s.nsn; ++k)
+      for (int c : kids[k]) start[k] = std::min(start[k], start[c]);
   }
-  std::vector<int32_t> sub(ids.size()), c0(ids.size());
+  const int64_t xcost = 131072;   // an exchange step in byte equivalents (~5 us of one CTA's stream)
+  auto make_team = [&](int g, int L, Team& T) {
+    TeamBuilder tb{s, pf, pb, kids, start, T, {}, xcost};
+    std::vector<int> roots;
+    for (int k = s.sub_sn0[g]; k < s.sub_sn1[g]; ++k)
+      if (s.sn_parent[k] < 0) roots.push_back(k);
+    const int root = tb.build(roots, L);
+    T.lo.assign(T.members, 0);
+    T.hi.assign(T.members, 0);
+    tb.owned(root);
+    tb.fwd(root);
+    tb.bwd(root);
+    tb.model();
+    for (int m = 0; m < T.members; ++m) T.finish[m] += 8 * (int64_t)s.sub_n[g] * 64;
+  };
+  // level[i] = tree levels cut for item i (0: one CTA).  Teams take consecutive
+  // CTAs in item-weight order and come first in their CTAs; the other items
+  // are spread by LPT over all CTAs (teams' CTAs start with their modelled
+  // finish time).
+  const int nitems = (int)ord.size();
+  std::vector<int> level(nitems, 0);
+  std::vector<std::vector<Team>> cache(nitems);   // per item: teams by level - 1
+  auto team_of = [&](int i, int L) -> const Team& {
+    auto& c = cache[i];
+    if ((int)c.size() < L) c.resize(L);
+    if (c[L - 1].members == 0) make_team(isub[i], L, c[L - 1]);
+    return c[L - 1];
+  };
+  struct Eval { int64_t ms; int nb; int argmax; };
+  // LPT of the unsplit items (weight order) onto bins with initial loads
+  auto evaluate = [&](const std::vector<int>& lv, std::vector<std::vector<int32_t>>* bins,
+                      std::vector<int>* cta_item) -> Eval {
+    int nteam = 0, nrest = 0;
+    for (int i = 0; i < nitems; ++i) {
+      if (lv[i] > 0) nteam += team_of(i, lv[i]).members;
+      else ++nrest;
+    }
+    if (nteam > nslots) return {INT64_MAX, 0, -1};
+    const int nb = std::max(1, std::max(nteam, std::min(nslots, nteam + nrest)));
+    std::vector<int64_t> load(nb, 0);
+    if (cta_item) cta_item->assign(nb, -1);
+    int b0 = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const int i = ord[k];
+      if (lv[i] == 0) continue;
+      const Team& T = team_of(i, lv[i]);
+      for (int m = 0; m < T.members; ++m) {
+        load[b0 + m] = T.finish[m];
+        if (cta_item) (*cta_item)[b0 + m] = i;
+      }
+      b0 += T.members;
+    }
+    if (bins) bins->assign(nb, {});
+    using P = std::pair<int64_t, int>;
+    std::priority_queue<P, std::vector<P>, std::greater<P>> q;
+    for (int b = 0; b < nb; ++b) q.push({load[b], b});
+    for (int k = 0; k < nitems; ++k) {
+      const int i = ord[k];
+      if (lv[i] > 0) continue;
+      P t = q.top();
+      q.pop();
+      if (bins) (*bins)[t.second].push_back(i);
+      load[t.second] = t.first + wgt[i];
+      q.push({load[t.second], t.second});
+    }
+    const int am = (int)(std::max_element(load.begin(), load.end()) - load.begin());
+    return {load[am], nb, am};
+  };
+  const int64_t ms0 = evaluate(level, nullptr, nullptr).ms;
+  int64_t best_ms = ms0;
+  if (Lmax > 0) {
+    // (1) the S largest items at a uniform level L
+    std::vector<int> best = level;
+    for (int L = 1; L <= Lmax; ++L) {
+      std::vector<int> lv(nitems, 0);
+      for (int S = 1; S <= nitems; ++S) {
+        const int i = ord[S - 1];
+        if (team_of(i, L).members < 2) break;   // cannot be cut
+        lv[i] = L;
+        const Eval e = evaluate(lv, nullptr, nullptr);
+        if (e.ms == INT64_MAX) break;           // out of CTAs
+        if (e.ms < best_ms) { best_ms = e.ms; best = lv; }
+      }
+    }
+    level = best;
+    // (2) greedy: cut the item that sets the makespan one level deeper while it helps
+    for (int it = 0; it < 4 * nslots; ++it) {
+      std::vector<std::vector<int32_t>> bins;
+      std::vector<int> cta_item;
+      const Eval e = evaluate(level, &bins, &cta_item);
+      int i = cta_item[e.argmax];
+      if (!bins[e.argmax].empty() && (i < 0 || wgt[bins[e.argmax][0]] > team_of(i, level[i]).finish[0]))
+        i = bins[e.argmax][0];   // the largest unsplit item of that CTA
+      if (i < 0 || level[i] >= Lmax) break;
+      std::vector<int> lv = level;
+      lv[i]++;
+      if (team_of(i, lv[i]).members <= (level[i] ? team_of(i, level[i]).members : 1)) break;
+      const Eval e2 = evaluate(lv, nullptr, nullptr);
+      if (e2.ms >= best_ms) break;
+      best_ms = e2.ms;
+      level = lv;
+    }
+    if ((double)best_ms >= 0.95 * (double)ms0) {   // not worth the exchange steps
+      std::fill(level.begin(), level.end(), 0);
+      best_ms = ms0;
+    }
+  }
+  std::vector<std::vector<int32_t>> bins;
+  std::vector<int> cta_item;
+  const Eval ev = evaluate(level, &bins, &cta_item);
+  nblocks = ev.nb;
+  int nsplit = 0, max_team = 1;
+  for (int i = 0; i < nitems; ++i)
+    if (level[i] > 0) {
+      ++nsplit;
+      max_team = std::max(max_team, team_of(i, level[i]).members);
+    }
+  if (dbg) {
+    double tot = 0;
+    for (int64_t w : wgt) tot += (double)w;
+    fprintf(stderr, "hplmm sn work: %zu items on %d CTAs, max/mean CTA weight %.3f (unsplit %.3f), largest item %.3f "
+            "of the mean; %d items shared by teams of up to %d CTAs\n", wgt.size(), nblocks,
+            ev.ms / (tot / nblocks), ms0 / (tot / nblocks), nitems ? (double)wgt[ord[0]] / (tot / nblocks) : 0.0,
+            nsplit, max_team);
+  }
+  // team member index of each CTA
+  std::vector<int> cta_member(nblocks, 0);
+  for (int b = 0, m = 0; b < nblocks; ++b) {
+    m = (b > 0 && cta_item[b] >= 0 && cta_item[b] == cta_item[b - 1]) ? m + 1 : 0;
+    cta_member[b] = m;
+  }
+  std::vector<int32_t> ptr(nblocks + 1, 0), sub, c0, ilo, ihi;
   std::vector<int64_t> cptr(nblocks + 1, 0);
   std::vector<SnChunk> flat;
+  int64_t xtot = 0;
+  int nflags = 0;
+  auto xchunk = [&](int g, int kind, int lo, int cnt, int64_t off, int flag, bool add) {
+    SnChunk ch;
+    ch.off = off;
+    ch.bytes = 0;
+    ch.info = (add ? 1 : 0) | (kind << 24);
+    ch.p0 = lo;
+    ch.w = cnt;
+    ch.r = flag;
+    ch.sub = g;
+    flat.push_back(ch);
+  };
   for (int b = 0; b < nblocks; ++b) {
-    for (int t = ptr[b]; t < ptr[b + 1]; ++t) {
-      sub[t] = isub[ids[t]];
-      c0[t] = ic0[ids[t]];
-      const int g = sub[t];
+    if (cta_item[b] >= 0) {
+      const Team& T = team_of(cta_item[b], level[cta_item[b]]);
+      const int m = cta_member[b], g = isub[cta_item[b]];
+      const size_t first = flat.size();
+      for (const TeamOp& op : T.ops) {
+        if (op.member != m) continue;
+        if (op.kind == 0) {
+          flat.insert(flat.end(), s.chunks.begin() + s.sn_fcb[op.a], s.chunks.begin() + s.sn_fce[op.b - 1]);
+        } else if (op.kind == 1) {
+          flat.insert(flat.end(), s.chunks.begin() + s.sn_bcb[op.b - 1], s.chunks.begin() + s.sn_bce[op.a]);
+        } else {
+          xchunk(g, op.kind, op.lo, op.cnt, op.kind == SN_XZERO ? 0 : xtot + T.xoff[op.xch],
+                 op.kind == SN_XZERO ? 0 : nflags + op.xch, op.add);
+        }
+      }
+      flat[first].info |= SN_INFO_FIRST_ITEM;
+      flat.back().info |= SN_INFO_LAST_ITEM;
+      sub.push_back(g);
+      c0.push_back(0);
+      ilo.push_back(T.lo[m]);
+      ihi.push_back(T.hi[m]);
+      if (m == T.members - 1) {
+        xtot += T.xdoubles;
+        nflags += (int)T.xoff.size();
+      }
+    }
+    std::sort(bins[b].begin(), bins[b].end());
+    for (int id : bins[b]) {
+      const int g = isub[id];
       const size_t first = flat.size();
       flat.insert(flat.end(), s.chunks.begin() + s.sub_fc0[g], s.chunks.begin() + s.sub_fc1[g]);
       flat.insert(flat.end(), s.chunks.begin() + s.sub_bc0[g], s.chunks.begin() + s.sub_bc1[g]);
       flat[first].info |= SN_INFO_FIRST_ITEM;
       flat.back().info |= SN_INFO_LAST_ITEM;
+      sub.push_back(g);
+      c0.push_back(ic0[id]);
+      ilo.push_back(0);
+      ihi.push_back(s.sub_n[g]);
     }
+    ptr[b + 1] = (int32_t)sub.size();
     cptr[b + 1] = (int64_t)flat.size();
   }
   wk.nblocks = isub.empty() ? 0 : nblocks;
@@ -131,6 +491,15 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   wk.xg = nullptr;
   wk.xg_stride = 0;
   wk.max_w = s.max_w;
+  wk.split = nsplit > 0;
+  wk.team = max_team;
+  if (wk.split) {
+    wk.item_lo = up(A, ilo, st, setup_only);
+    wk.item_hi = up(A, ihi, st, setup_only);
+    wk.xbuf = (double*)A.alloc(std::max<int64_t>(xtot, 2) * 8, setup_only);
+    wk.xflag = (int32_t*)A.alloc(std::max(nflags, 1) * 4, setup_only);
+    SN_CK(cudaMemsetAsync(wk.xflag, 0, std::max(nflags, 1) * 4, st));
+  }
   if (sn_xg(nrhs) && wk.nblocks > 0) {
     wk.xg_stride = sn_xg_stride(s.max_n, nrhs);
     wk.xg = (double*)A.alloc((size_t)wk.nblocks * wk.xg_stride * 8, setup_only);
@@ -176,7 +545,7 @@ void sn_upload(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm) {
   B.dev.factor = B.factor;
   B.solve_bytes = 0;
   for (int64_t b : s.sub_fbytes) B.solve_bytes += b;
-  sn_build_work(B, A, st, nsm, 1, nullptr, B.work);
+  sn_build_work(B, A, st, nsm, 1, nullptr, B.work, 0, true);
 }
 
 void sn_apply(const SnBatch& B, const double* in, cudaStream_t st) {

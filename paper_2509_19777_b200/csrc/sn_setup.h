@@ -42,7 +42,8 @@ struct SnBatch {
 
 void sn_upload(SnBatch& B, DevAlloc& A, cudaStream_t st, int nsm);
 void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nrhs,
-                   const std::vector<int32_t>* ncols, SnWork& wk, int force_cons = 0);
+                   const std::vector<int32_t>* ncols, SnWork& wk, int force_cons = 0,
+                   bool allow_split = false);
 // numeric factorisation; throws SnError (status -4 + subdomain) on a
 // non-positive pivot.  pool_budget: bytes of frontal matrices per wave.
 void sn_factor(SnBatch& B, const double* d_val, DevAlloc& A, cudaStream_t st,

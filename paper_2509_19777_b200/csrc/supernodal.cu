@@ -44,6 +44,16 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #define HPLMM_SN_PROF 0
 #endif
 
+// one-shot flags of the subtree-parallel exchange steps
+__device__ __forceinline__ void flag_release(int32_t* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int flag_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <int CONS>
 struct SnT {
   static constexpr int NT = 32 * CONS;                  // consumer threads
@@ -274,7 +284,7 @@ __device__ __forceinline__ void sn_wbwd(const double* __restrict__ st, int ld, i
   }
 }
 
-template <int NRHS, int CONS, int CPS, bool XG>
+template <int NRHS, int CONS, int CPS, bool XG, bool SPLIT>
 __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     k_sn_solve(SnDev d, SnIO io, SnWork wk, int stages, int stage_doubles, int max_n, int max_r,
                int flags) {
@@ -292,6 +302,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
   const int rpad = (max_r + 3) & ~1;   // x_R: NRHS component-major rows of rpad doubles
   constexpr int SN_NT = SnT<CONS>::NT, SN_CONS = CONS;
   static_assert(NRHS == 1 || XG, "several right-hand sides keep x in global memory");
+  static_assert(!SPLIT || (NRHS == 1 && !XG), "subtree-parallel items: one RHS, x in shared memory");
   // row pairs per thread: up to 4 for one RHS (TG >= h/8); with several RHS
   // at most 2 (sn_lg widens TG): h <= 2048 with 16 warps, h <= 1024 with 8
   // (sn_build_work keeps taller parts off the 8-warp shape) -- a smaller
@@ -342,11 +353,14 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
         bytes = ch[kb + lane].bytes & 0xffffff;
       }
       const int cnt = (int)min((int64_t)32, k1 - kb);
-      if (kb > k0 && lane < pd && lane < cnt) bulk_prefetch_l2(d.factor + off, (uint32_t)bytes);
-      for (int j = 0; j < cnt; ++j, ++k) {
+      if (kb > k0 && lane < pd && lane < cnt && (!SPLIT || bytes > 0))
+        bulk_prefetch_l2(d.factor + off, (uint32_t)bytes);
+      for (int j = 0; j < cnt; ++j) {
         const int64_t o = __shfl_sync(0xffffffffu, off, j);
         const int b = __shfl_sync(0xffffffffu, bytes, j);
-        if (pd > 0 && lane == j + pd && lane < cnt) bulk_prefetch_l2(d.factor + off, (uint32_t)bytes);
+        if (pd > 0 && lane == j + pd && lane < cnt && (!SPLIT || bytes > 0))
+          bulk_prefetch_l2(d.factor + off, (uint32_t)bytes);
+        if (SPLIT && b == 0) continue;   // exchange step: no factor data, no ring slot
         if (lane == 0) {
           if (k >= stages) {
             const long long tw = prof ? clock64() : 0;
@@ -359,6 +373,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
                         pol);
         }
         if (++s == stages) { s = 0; ph ^= 1; }
+        ++k;
       }
     }
     if (prof && lane == 0)
@@ -387,6 +402,7 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     // SnChunk = {off (2 ints), bytes, info | p0, w, r, sub}
     const int info = dn0.w, p0 = dn1.x, w = dn1.y, r = dn1.z, csub = dn1.w;
     const int lgc = (dn0.z >> 24) & 15;
+    const int cur_off_lo = dn0.x, cur_off_hi = dn0.y;   // SnChunk::off (exchange steps)
     if (kk + 1 < k1) {
       dn0 = __ldg(reinterpret_cast<const int4*>(ch + kk + 1));
       dn1 = __ldg(reinterpret_cast<const int4*>(ch + kk + 1) + 1);
@@ -430,6 +446,32 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
       }
       PSYNC();
     }
+    if (SPLIT && kind >= SN_XSEND) {
+      // exchange step of a subtree-parallel item (no ring slot): p0 / w = the x
+      // range, dn0.x / dn0.y = its offset in the exchange buffer, r = flag
+      double* xb = wk.xbuf + (((int64_t)(uint32_t)cur_off_hi << 32) | (uint32_t)cur_off_lo);
+      if (kind == SN_XZERO) {
+        for (int e = tid; e < w; e += SN_NT) x[p0 + e] = 0.0;
+        PSYNC();
+      } else if (kind == SN_XSEND) {
+        for (int e = tid; e < w; e += SN_NT) __stcg(xb + e, x[p0 + e]);
+        __threadfence();
+        PSYNC();
+        if (tid == 0) flag_release(wk.xflag + r, 1);
+      } else {
+        if (tid == 0) {
+          while (flag_acquire(wk.xflag + r) == 0) {}
+          wk.xflag[r] = 0;   // one-shot: the sender sets it again in the next launch
+        }
+        PSYNC();
+        if (cc0 & 1) {
+          for (int e = tid; e < w; e += SN_NT) x[p0 + e] += __ldcg(xb + e);
+        } else {
+          for (int e = tid; e < w; e += SN_NT) x[p0 + e] = __ldcg(xb + e);
+        }
+        PSYNC();
+      }
+    } else {
     {
       const long long tw = prof ? clock64() : 0;
       if (flags & 1) mbar_wait_sleep(&full[s], ph);
@@ -603,17 +645,23 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
         }
       }
     }
-    if (prof) {
+    if (prof && kind < 6) {
       t_kind[kind] += clock64() - t_k0;
       n_kind[kind]++;
     }
+    }   // factor chunk
     if (info & SN_INFO_LAST_ITEM) {
       PSYNC();
       // ---- write the solution
       if (io.mode == 2) {
         for (int p = tid; p < n * NRHS; p += SN_NT) io.out[base * NRHS + p] = x[p];
       } else if (io.mode == 0) {
-        for (int p = tid; p < n; p += SN_NT) io.out[base + p] = x[p];
+        if (SPLIT) {   // the x positions this team member owns
+          const int hi = wk.item_hi[item];
+          for (int p = wk.item_lo[item] + tid; p < hi; p += SN_NT) io.out[base + p] = x[p];
+        } else {
+          for (int p = tid; p < n; p += SN_NT) io.out[base + p] = x[p];
+        }
       } else {
         const int L = io.ld[sub];
         const int ncr = min(NRHS, L - 1 - rc0);
@@ -732,13 +780,35 @@ int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons, int max
 template <int NRHS, int CONS, int CPS, bool XG>
 static void sn_solve_launch_x(const SnDev& d, const SnIO& io, const SnWork& wk, int stages,
                               int chunk, int max_n, int max_r, size_t smem, cudaStream_t st) {
-  set_max_dynamic_smem((const void*)k_sn_solve<NRHS, CONS, CPS, XG>, smem);
   static int flags = -1;
   if (flags < 0) {
     const char* e = getenv("HPLMM_SN_FLAGS");
     flags = e ? atoi(e) : 0;
   }
-  k_sn_solve<NRHS, CONS, CPS, XG><<<wk.nblocks, 32 * (CONS + 1), smem, st>>>(
+  if constexpr (NRHS == 1 && !XG) {
+    if (wk.split) {
+      // subtree-parallel items: a team's members wait for each other, so all
+      // CTAs must be resident together: a cooperative launch (fails loudly when
+      // they cannot be); HPLMM_SN_TEAM_LAUNCH=0: a plain launch (experiments)
+      static const int mode = getenv("HPLMM_SN_TEAM_LAUNCH") ? atoi(getenv("HPLMM_SN_TEAM_LAUNCH")) : 1;
+      set_max_dynamic_smem((const void*)k_sn_solve<1, CONS, CPS, false, true>, smem);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)wk.nblocks);
+      cfg.blockDim = dim3(32 * (CONS + 1));
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = mode == 0 ? 0 : 1;
+      cudaLaunchKernelEx(&cfg, k_sn_solve<1, CONS, CPS, false, true>, d, io, wk, stages, chunk,
+                         max_n, max_r, flags);
+      return;
+    }
+  }
+  set_max_dynamic_smem((const void*)k_sn_solve<NRHS, CONS, CPS, XG, false>, smem);
+  k_sn_solve<NRHS, CONS, CPS, XG, false><<<wk.nblocks, 32 * (CONS + 1), smem, st>>>(
       d, io, wk, stages, chunk, max_n, max_r, flags);
   if ((flags & 16) && wk.nblocks <= 4096) {   // experiment: per-CTA finish-time quantiles
     static unsigned long long h[2 * 4096];

@@ -36,7 +36,12 @@ constexpr int SN_MAX_WR = 2048;          // max w and max r (DOFs) per supernode
 // backward per S: ROWS_BWD, W_BWD..).  ROWS chunks carry the supernode's row
 // list (int32) so the scatter/gather of x_R never waits on a global load.
 enum SnChunkKind : int32_t {
-  SN_W_FWD = 0, SN_F_FWD = 1, SN_W_BWD = 2, SN_ROWS_FWD = 3, SN_ROWS_BWD = 4
+  SN_W_FWD = 0, SN_F_FWD = 1, SN_W_BWD = 2, SN_ROWS_FWD = 3, SN_ROWS_BWD = 4,
+  // subtree-parallel solves (a subdomain shared by a team of CTAs, sn_build_work):
+  // exchange steps without factor data (bytes = 0: no ring slot).  p0 / w = the
+  // x positions [p0, p0 + w), off = offset of the range in the exchange
+  // buffer, r = flag index, c0 bit 0 (XRECV) = add (else assign)
+  SN_XSEND = 5, SN_XRECV = 6, SN_XZERO = 7
 };
 
 // one TMA chunk of the solve stream, denormalised so that the consumer needs
@@ -83,6 +88,10 @@ struct SnSymbolic {
   std::vector<int32_t> sn_w, sn_r, sn_p0, sn_ldw, sn_ldf, sn_level, sn_parent, sn_sub,
       sn_child_rank;
   std::vector<int64_t> sn_rows_off, sn_foff;
+  // chunk ranges of each supernode in `chunks`: forward [sn_fcb, sn_fce),
+  // backward [sn_bcb, sn_bce) (empty for r = 0); within a subdomain the
+  // forward ranges ascend and the backward ranges descend with the supernode
+  std::vector<int64_t> sn_fcb, sn_fce, sn_bcb, sn_bce;
   std::vector<int32_t> rows;               // struct rows: local DOF positions (ascending)
   std::vector<SnChunk> chunks;             // per subdomain: [fc0,fc1) forward, [bc0,bc1) backward
   int64_t factor_doubles = 0;              // layout per S: [rows][W_S: ldw x w][F_SS^-1: ldf x w]

@@ -54,6 +54,19 @@ struct SnWork {
   double* xg = nullptr;
   int64_t xg_stride = 0;
   int max_w = 0;
+  // subtree-parallel items (split = true; one RHS, x in shared memory): a team
+  // of `team` consecutive CTAs shares one subdomain, each member sweeping its
+  // own subtree of the nested-dissection tree; x ranges of the common
+  // ancestors travel through xbuf, ordered by the one-shot flags xflag (set by
+  // the sender, cleared by the receiver).  A member writes out only the x
+  // positions [item_lo, item_hi) it owns.  The launch is cooperative: all
+  // CTAs are resident together (team = the largest team, for the report).
+  bool split = false;
+  int team = 1;
+  const int32_t* item_lo = nullptr;
+  const int32_t* item_hi = nullptr;
+  double* xbuf = nullptr;
+  int32_t* xflag = nullptr;
 };
 
 // numeric-factorisation view (device pointers)

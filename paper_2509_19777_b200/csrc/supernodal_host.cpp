@@ -440,11 +440,13 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
     }
     return packed;
   };
+  for (auto* v : {&o.sn_fcb, &o.sn_fce, &o.sn_bcb, &o.sn_bce}) v->assign(NS, 0);
   for (int s = 0; s < nsub; ++s) {
     int64_t fb = 0;
     o.sub_fc0.push_back((int64_t)o.chunks.size());
     for (int k = o.sub_sn0[s]; k < o.sub_sn1[s]; ++k) {
       const int w = o.sn_w[k], r = o.sn_r[k];
+      o.sn_fcb[k] = (int64_t)o.chunks.size();
       const int64_t rows_at = o.sn_foff[k], w_at = rows_at + sn_rows_doubles(r);
       const int64_t f_at = w_at + (int64_t)o.sn_ldw[k] * w;
       if (r > 0) {
@@ -452,12 +454,14 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
           push(k, SN_ROWS_FWD, rows_at, (int)(8 * sn_rows_doubles(r)), 0, 1, true);
       }
       cols(k, SN_F_FWD, f_at, o.sn_ldf[k], w);
+      o.sn_fce[k] = (int64_t)o.chunks.size();
       fb += 8 * (2 * sn_rows_doubles(r) + 2 * (int64_t)o.sn_ldw[k] * w + (int64_t)o.sn_ldf[k] * w);
     }
     o.sub_fc1.push_back((int64_t)o.chunks.size());
     o.sub_bc0.push_back((int64_t)o.chunks.size());
     for (int k = o.sub_sn1[s] - 1; k >= o.sub_sn0[s]; --k) {
       const int r = o.sn_r[k];
+      o.sn_bcb[k] = o.sn_bce[k] = (int64_t)o.chunks.size();
       if (r == 0) continue;
       if (pack_rows && (o.chunk_doubles - sn_rows_doubles(r)) / o.sn_ldw[k] >= 1) {
         cols(k, SN_W_BWD, o.sn_foff[k] + sn_rows_doubles(r), o.sn_ldw[k], o.sn_w[k], o.sn_foff[k],
@@ -466,6 +470,7 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
         push(k, SN_ROWS_BWD, o.sn_foff[k], (int)(8 * sn_rows_doubles(r)), 0, 1, true);
         cols(k, SN_W_BWD, o.sn_foff[k] + sn_rows_doubles(r), o.sn_ldw[k], o.sn_w[k]);
       }
+      o.sn_bce[k] = (int64_t)o.chunks.size();
     }
     o.sub_bc1.push_back((int64_t)o.chunks.size());
     o.sub_fbytes.push_back(fb);
