@@ -679,6 +679,9 @@ def main():
                          "smoother": smoother, "n_st": n_st,
                          "fine_operator": "element-by-element" if ebe else "bsr",
                          "sn_shape": [rep0.get("sn_shape_grain"), rep0.get("sn_shape_contact")],
+                         "sn_teams": {"grain": rep0.get("sn_teams_grain"),
+                                      "contact": rep0.get("sn_teams_contact"),
+                                      "max_ctas": rep0.get("sn_team_max")},
                          "solve_driver": "device-resident CUDA graph (one launch per solve)"
                          if (not ilu) else "host loop"},
         "iterations": iters, "iterations_per_s": iters / med_s * world,

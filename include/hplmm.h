@@ -131,6 +131,19 @@ typedef struct {
                             falls back to automatic).  Same operator A_s^-1;
                             only the summation order of the group reductions
                             differs (parity tests run both shapes)          */
+  int32_t sn_split;      /* subtree-parallel supernodal solves: a batch with too
+                            few subdomains to load the CTAs evenly shares its
+                            largest subdomains between teams of up to 2^L CTAs
+                            (the top L levels of the nested-dissection tree are
+                            cut; the members exchange the separators' x rows).
+                            0 = automatic, L <= 2 (default; the cuts are
+                            chosen by a modelled makespan and a batch that
+                            gains < 5% keeps one CTA per subdomain), -1 = off,
+                            1..3 = forced: every subdomain, largest first, is
+                            cut as deep as its tree allows (<= L levels) while
+                            CTAs last (tests, experiments).  Same
+                            operator A_s^-1: only the order in which the
+                            subtrees' updates of a separator are added differs */
   int32_t host_loop;     /* how hplmm_solve drives GMRES (R22):
                             0 = device-resident (default): the whole solve --
                                 every Arnoldi step, Givens update, stop test and
@@ -183,6 +196,9 @@ typedef struct {
   int32_t sn_shape_grain;   /* consumer warps per CTA of the grain / contact-grid    */
   int32_t sn_shape_contact; /* supernodal solves in use (8: 8 x 2 CTAs/SM, 16: 16 x 1;
                                0 = not built)                                      */
+  int32_t sn_teams_grain;   /* grains / contact grids shared by a team of CTAs      */
+  int32_t sn_teams_contact; /* (sn_split), and the CTAs of the largest team         */
+  int32_t sn_team_max;
 } hplmm_report;
 
 typedef struct hplmm_handle hplmm_handle;
@@ -206,7 +222,7 @@ typedef struct {
 } hplmm_bsr;
 
 /* Default options: n=4, beta=4, h=1, restart=50, max_iter=300, n_st=1,
- * coarse_refine=0. */
+ * coarse_refine=0, sn_split=0. */
 void hplmm_default_options(hplmm_options *opt);
 
 /* Host-only integer setup (no GPU work; bit-exact vs the oracle):

@@ -1149,6 +1149,7 @@ void hplmm_default_options(hplmm_options* o) {
   o->smoother = 0;
   o->operator_kind = 0;
   o->sn_shape = 0;
+  o->sn_split = 0;
   o->host_loop = 0;
   o->rhs_block = 4;
 }
@@ -1620,10 +1621,14 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
       double t1 = wall();
       try {
+        h->sg.sym.split = h->sc.sym.split = hs.opt.sn_split;
         sn_upload(h->sg, halloc, h->st, h->nsm);
         if (!ilu) sn_upload(h->sc, halloc, h->st, h->nsm);
         h->rep.sn_shape_grain = h->sg.work.cons;
         h->rep.sn_shape_contact = ilu ? 0 : h->sc.work.cons;
+        h->rep.sn_teams_grain = h->sg.work.nteams;
+        h->rep.sn_teams_contact = ilu ? 0 : h->sc.work.nteams;
+        h->rep.sn_team_max = std::max(h->sg.work.team, ilu ? 1 : h->sc.work.team);
         double t2 = wall();
         sn_factor(h->sg, h->d_val, halloc, h->st, kSnPoolBytes);
         double t3 = wall();

@@ -232,8 +232,11 @@ struct TeamBuilder {
 
 }  // namespace
 
-static int sn_split_levels() {
-  static const int v = getenv("HPLMM_SN_SPLIT") ? atoi(getenv("HPLMM_SN_SPLIT")) : 2;
+// tree levels that may be cut: hplmm_options.sn_split (0: automatic = 2, or
+// HPLMM_SN_SPLIT for experiments; -1: off)
+static int sn_split_levels(int opt) {
+  static const int env = getenv("HPLMM_SN_SPLIT") ? atoi(getenv("HPLMM_SN_SPLIT")) : 2;
+  const int v = opt < 0 ? 0 : (opt > 0 ? opt : env);
   return std::max(0, std::min(3, v));
 }
 
@@ -268,7 +271,7 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   const bool dbg = getenv("HPLMM_DEBUG") != nullptr;
 
   // ---- subtree-parallel teams for the largest items (one RHS, main solve only)
-  const int Lmax = (allow_split && nrhs == 1 && !ncols && !sn_xg(1) && !isub.empty()) ? sn_split_levels() : 0;
+  const int Lmax = (allow_split && nrhs == 1 && !ncols && !sn_xg(1) && !isub.empty()) ? sn_split_levels(s.split) : 0;
   std::vector<int32_t> ord(wgt.size());
   for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int32_t)i;
   std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return wgt[a] > wgt[b]; });
@@ -362,7 +365,23 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   };
   const int64_t ms0 = evaluate(level, nullptr, nullptr).ms;
   int64_t best_ms = ms0;
-  if (Lmax > 0) {
+  if (Lmax > 0 && s.split > 0) {
+    // forced (hplmm_options.sn_split = L > 0; tests, experiments): every item,
+    // largest first, is cut as deep as it can be (<= L levels) while CTAs last
+    int used = nitems;
+    for (int k = 0; k < nitems; ++k) {
+      const int i = ord[k];
+      for (int L = Lmax; L >= 1; --L) {
+        const int m = team_of(i, L).members;
+        if (m >= 2 && used - 1 + m <= nslots) {
+          level[i] = L;
+          used += m - 1;
+          break;
+        }
+      }
+    }
+    best_ms = evaluate(level, nullptr, nullptr).ms;
+  } else if (Lmax > 0) {
     // (1) the S largest items at a uniform level L
     std::vector<int> best = level;
     for (int L = 1; L <= Lmax; ++L) {
@@ -493,6 +512,7 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   wk.max_w = s.max_w;
   wk.split = nsplit > 0;
   wk.team = max_team;
+  wk.nteams = nsplit;
   if (wk.split) {
     wk.item_lo = up(A, ilo, st, setup_only);
     wk.item_hi = up(A, ihi, st, setup_only);

@@ -75,6 +75,7 @@ struct SnSymbolic {
   int max_n = 0, max_w = 0, max_r = 0, n_levels = 0, max_children = 0;
   int chunk_doubles = 0;                   // TMA chunk (stage) size of the schedule
   int shape = 0;                           // launch shape asked for (0 auto, 8, 16)
+  int split = 0;                           // hplmm_options.sn_split (0 auto, -1 off, 1..3 levels)
   // per subdomain
   std::vector<int32_t> sub_n;              // DOFs
   std::vector<int64_t> sub_base;           // offset of its local positions

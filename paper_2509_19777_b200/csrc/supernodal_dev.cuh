@@ -63,6 +63,7 @@ struct SnWork {
   // CTAs are resident together (team = the largest team, for the report).
   bool split = false;
   int team = 1;
+  int nteams = 0;                       // subdomains shared by a team
   const int32_t* item_lo = nullptr;
   const int32_t* item_hi = nullptr;
   double* xbuf = nullptr;

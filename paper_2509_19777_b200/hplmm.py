@@ -51,7 +51,8 @@ class Options(C.Structure):
                 ("coarse_refine", C.c_int32), ("local_factor", C.c_int32),
                 ("coarse_solver", C.c_int32), ("mortar_kind", C.c_int32),
                 ("smoother", C.c_int32), ("operator_kind", C.c_int32),
-                ("sn_shape", C.c_int32), ("host_loop", C.c_int32), ("rhs_block", C.c_int32)]
+                ("sn_shape", C.c_int32), ("sn_split", C.c_int32), ("host_loop", C.c_int32),
+                ("rhs_block", C.c_int32)]
 
 
 class Bsr(C.Structure):
@@ -70,7 +71,9 @@ class Report(C.Structure):
                 ("t_setup_local_s", C.c_double), ("t_setup_coarse_s", C.c_double),
                 ("t_rhs_s", C.c_double), ("t_solve_s", C.c_double),
                 ("kernel_launches", C.c_int64), ("fine_operator", C.c_int32),
-                ("sn_shape_grain", C.c_int32), ("sn_shape_contact", C.c_int32)]
+                ("sn_shape_grain", C.c_int32), ("sn_shape_contact", C.c_int32),
+                ("sn_teams_grain", C.c_int32), ("sn_teams_contact", C.c_int32),
+                ("sn_team_max", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -208,7 +211,7 @@ class Solver:
     def __init__(self, prob, n_mortar=None, beta=None, contact_h=None, restart=None,
                  max_iter=None, coarse_refine=0, local_factor=None, coarse_solver=None,
                  mortar=None, smoother=None, n_st=None, operator=None, sn_shape=None,
-                 host_loop=None, rhs_block=None, bsr=None, device=0, stream=None):
+                 sn_split=None, host_loop=None, rhs_block=None, bsr=None, device=0, stream=None):
         """bsr: optional dict(row_ptr, col_idx, val, node_ijk=None) -- the
         caller's matrix A^ (host NumPy or torch CUDA arrays): the handle is
         then built by hplmm_setup_bsr (create + pattern check + assemble +
@@ -239,6 +242,8 @@ class Solver:
             o.operator_kind = OPERATOR[operator] if isinstance(operator, str) else int(operator)
         if sn_shape is not None:
             o.sn_shape = int(sn_shape)
+        if sn_split is not None:
+            o.sn_split = int(sn_split)
         if host_loop is not None:
             o.host_loop = int(host_loop)
         if rhs_block is not None:
