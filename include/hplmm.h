@@ -126,7 +126,8 @@ typedef struct {
   int32_t sn_shape;      /* launch shape of the supernodal local solves
                             (local_factor = 1): 0 = automatic (8 consumer warps
                             x 2 CTAs per SM when a batch has >= 2 subdomains per
-                            CTA, else 16 x 1; default), 8 = force 8 x 2, 16 =
+                            CTA or may share subdomains between CTAs (sn_split
+                            >= 0), else 16 x 1; default), 8 = force 8 x 2, 16 =
                             force 16 x 1 (a shape the subdomains do not fit
                             falls back to automatic).  Same operator A_s^-1;
                             only the summation order of the group reductions
@@ -136,7 +137,7 @@ typedef struct {
                             largest subdomains between teams of up to 2^L CTAs
                             (the top L levels of the nested-dissection tree are
                             cut; the members exchange the separators' x rows).
-                            0 = automatic, L <= 2 (default; the cuts are
+                            0 = automatic, L <= 3 (default; the cuts are
                             chosen by a modelled makespan and a batch that
                             gains < 5% keeps one CTA per subdomain), -1 = off,
                             1..3 = forced: every subdomain, largest first, is

@@ -1611,7 +1611,8 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
       };
       double t0 = wall();
-      const int shape = hs.opt.sn_shape;
+      // 1 = automatic, teams allowed (sn_solve_cfg)
+      const int shape = hs.opt.sn_shape ? hs.opt.sn_shape : (hs.opt.sn_split >= 0 ? 1 : 0);
       // experiments: per-batch launch shape (HPLMM_SN_SHAPE_G / _C = 8 | 16)
       const int shape_g = getenv("HPLMM_SN_SHAPE_G") ? atoi(getenv("HPLMM_SN_SHAPE_G")) : shape;
       const int shape_c = getenv("HPLMM_SN_SHAPE_C") ? atoi(getenv("HPLMM_SN_SHAPE_C")) : shape;

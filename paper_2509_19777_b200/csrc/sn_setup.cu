@@ -232,10 +232,10 @@ struct TeamBuilder {
 
 }  // namespace
 
-// tree levels that may be cut: hplmm_options.sn_split (0: automatic = 2, or
+// tree levels that may be cut: hplmm_options.sn_split (0: automatic = 3, or
 // HPLMM_SN_SPLIT for experiments; -1: off)
 static int sn_split_levels(int opt) {
-  static const int env = getenv("HPLMM_SN_SPLIT") ? atoi(getenv("HPLMM_SN_SPLIT")) : 2;
+  static const int env = getenv("HPLMM_SN_SPLIT") ? atoi(getenv("HPLMM_SN_SPLIT")) : 3;
   const int v = opt < 0 ? 0 : (opt > 0 ? opt : env);
   return std::max(0, std::min(3, v));
 }
