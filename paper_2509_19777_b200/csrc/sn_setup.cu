@@ -413,7 +413,12 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
       best_ms = e2.ms;
       level = lv;
     }
-    if ((double)best_ms >= 0.95 * (double)ms0) {   // not worth the exchange steps
+    // HPLMM_SN_SPLIT_GAIN (experiments): least modelled gain in percent
+    static const double gain = getenv("HPLMM_SN_SPLIT_GAIN") ? atof(getenv("HPLMM_SN_SPLIT_GAIN")) : 5.0;
+    if (dbg)
+      fprintf(stderr, "hplmm sn work: modelled makespan with teams %.3f of the unsplit one\n",
+              (double)best_ms / (double)ms0);
+    if ((double)best_ms >= (1.0 - gain / 100.0) * (double)ms0) {   // not worth the exchange steps
       std::fill(level.begin(), level.end(), 0);
       best_ms = ms0;
     }

@@ -402,7 +402,6 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     // SnChunk = {off (2 ints), bytes, info | p0, w, r, sub}
     const int info = dn0.w, p0 = dn1.x, w = dn1.y, r = dn1.z, csub = dn1.w;
     const int lgc = (dn0.z >> 24) & 15;
-    const int cur_off_lo = dn0.x, cur_off_hi = dn0.y;   // SnChunk::off (exchange steps)
     if (kk + 1 < k1) {
       dn0 = __ldg(reinterpret_cast<const int4*>(ch + kk + 1));
       dn1 = __ldg(reinterpret_cast<const int4*>(ch + kk + 1) + 1);
@@ -448,8 +447,8 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
     }
     if (SPLIT && kind >= SN_XSEND) {
       // exchange step of a subtree-parallel item (no ring slot): p0 / w = the x
-      // range, dn0.x / dn0.y = its offset in the exchange buffer, r = flag
-      double* xb = wk.xbuf + (((int64_t)(uint32_t)cur_off_hi << 32) | (uint32_t)cur_off_lo);
+      // range, SnChunk::off = its offset in the exchange buffer, r = flag
+      double* xb = wk.xbuf + ch[kk].off;
       if (kind == SN_XZERO) {
         for (int e = tid; e < w; e += SN_NT) x[p0 + e] = 0.0;
         PSYNC();
