@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -1616,29 +1617,51 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       // experiments: per-batch launch shape (HPLMM_SN_SHAPE_G / _C = 8 | 16)
       const int shape_g = getenv("HPLMM_SN_SHAPE_G") ? atoi(getenv("HPLMM_SN_SHAPE_G")) : shape;
       const int shape_c = getenv("HPLMM_SN_SHAPE_C") ? atoi(getenv("HPLMM_SN_SHAPE_C")) : shape;
-      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, sn_leaf(), h->sg.sym, err, h->nsm, shape_g) ||
-          (!ilu && !sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, sn_leaf(), h->sc.sym, err,
-                               h->nsm, shape_c)))
+      // the contact-grid analysis (host) runs on its own thread while the grain
+      // batch is analysed, uploaded and its factorisation is queued on the GPU
+      std::string err_c;
+      bool ok_c = true;
+      std::thread th_c;
+      if (!ilu)
+        th_c = std::thread([&] {
+          ok_c = sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, sn_leaf(), h->sc.sym, err_c, h->nsm,
+                            shape_c);
+        });
+      struct Joiner {
+        std::thread& t;
+        ~Joiner() { if (t.joinable()) t.join(); }
+      } joiner{th_c};
+      if (getenv("HPLMM_SN_OVERLAP") && getenv("HPLMM_SN_OVERLAP")[0] == '0' && th_c.joinable())
+        th_c.join();   // experiments: the two analyses one after the other
+      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, sn_leaf(), h->sg.sym, err, h->nsm, shape_g))
         throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
       double t1 = wall();
       try {
-        h->sg.sym.split = h->sc.sym.split = hs.opt.sn_split;
+        h->sg.sym.split = hs.opt.sn_split;
         sn_upload(h->sg, halloc, h->st, h->nsm);
-        if (!ilu) sn_upload(h->sc, halloc, h->st, h->nsm);
+        double t2 = wall();
+        sn_factor(h->sg, h->d_val, halloc, h->st, kSnPoolBytes);
+        double t3 = wall();
+        if (dbg)
+          fprintf(stderr, "hplmm T_ML: grain analyse %.3f s, upload %.3f s, grain factor %.3f s\n", t1 - t0,
+                  t2 - t1, t3 - t2);
+        if (th_c.joinable()) th_c.join();
+        if (!ok_c) throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err_c};
+        double t4 = wall();
+        if (!ilu) {
+          h->sc.sym.split = hs.opt.sn_split;
+          sn_upload(h->sc, halloc, h->st, h->nsm);
+        }
         h->rep.sn_shape_grain = h->sg.work.cons;
         h->rep.sn_shape_contact = ilu ? 0 : h->sc.work.cons;
         h->rep.sn_teams_grain = h->sg.work.nteams;
         h->rep.sn_teams_contact = ilu ? 0 : h->sc.work.nteams;
         h->rep.sn_team_max = std::max(h->sg.work.team, ilu ? 1 : h->sc.work.team);
-        double t2 = wall();
-        sn_factor(h->sg, h->d_val, halloc, h->st, kSnPoolBytes);
-        double t3 = wall();
-        if (dbg)
-          fprintf(stderr, "hplmm T_ML: analyse %.3f s, upload %.3f s, grain factor %.3f s\n", t1 - t0,
-                  t2 - t1, t3 - t2);
         if (!ilu) try {
           sn_factor(h->sc, h->d_val, halloc, h->st, kSnPoolBytes);
-          if (dbg) fprintf(stderr, "hplmm T_ML: contact factor %.3f s\n", wall() - t3);
+          if (dbg)
+            fprintf(stderr, "hplmm T_ML: wait for the contact analysis %.3f s, contact upload + factor %.3f s\n",
+                    t4 - t3, wall() - t4);
         } catch (SnError& e) {
           e.sub += G;   // contact grids are numbered after the grains
           throw;
