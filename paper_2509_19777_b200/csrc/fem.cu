@@ -4,6 +4,7 @@
 // eq:stiff_iso, readings R2 (2x2x2 Gauss, unit voxel), R3
 // (node-major 3x3 blocks), R4 (Dirichlet identity rows, lifted RHS);
 // eq:gauss with R11 for the mortar weights.
+#include <type_traits>
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
@@ -435,7 +436,53 @@ struct EbeK0 {
   double k[576];
 };
 
-template <bool RESID>
+// Value classes of K0 (isotropic trilinear unit-cube element, eq:stiff_iso):
+// K0[3a+i][3b+j] = lam G_ij + mu (G_ji + delta_ij sum_k G_kk), G_ij = int d_i N_a d_j N_b,
+// and with s_d = (bit d of a == bit d of b) the 576 entries take only 10 values
+// up to sign: i == j: class (s_i ? 0 : 3) + #{d != i : !s_d}, sign +; i != j
+// (k the third axis): class 6 + (s_k ? 0 : 2) + (s_i == s_j ? 0 : 1), sign
+// sigma_i(a) sigma_j(b) with sigma_d(n) = +1 if bit d of n else -1.  Held in 10
+// registers, they replace the 576 constant-bank operand loads of the general
+// form (27% of k_ebe's instructions).  launch_ebe checks the classes against
+// the K0 it is given and falls back to the general kernel if they do not hold.
+__host__ __device__ constexpr int ebe_cls(int row, int col) {
+  const int a = row / 3, i = row % 3, b = col / 3, j = col % 3;
+  const bool s0 = ((a ^ b) & 1) == 0, s1 = ((a ^ b) & 2) == 0, s2 = ((a ^ b) & 4) == 0;
+  const bool si = i == 0 ? s0 : (i == 1 ? s1 : s2), sj = j == 0 ? s0 : (j == 1 ? s1 : s2);
+  if (i == j) return (si ? 0 : 3) + (s0 ? 0 : 1) + (s1 ? 0 : 1) + (s2 ? 0 : 1) - (si ? 0 : 1);
+  const int k = 3 - i - j;
+  const bool sk = k == 0 ? s0 : (k == 1 ? s1 : s2);
+  return 6 + (sk ? 0 : 2) + (si == sj ? 0 : 1);
+}
+__host__ __device__ constexpr bool ebe_neg(int row, int col) {
+  const int a = row / 3, i = row % 3, b = col / 3, j = col % 3;
+  if (i == j) return false;
+  return (((a >> i) & 1) != 0) != (((b >> j) & 1) != 0);
+}
+// a positive-sign representative of each class (all in row 0 of K0)
+__host__ __device__ constexpr int ebe_rep(int c) {
+  return c == 0 ? 0 : c == 1 ? 6 : c == 2 ? 18 : c == 3 ? 3 : c == 4 ? 9 : c == 5 ? 21
+       : c == 6 ? 1 : c == 7 ? 4 : c == 8 ? 8 : 11;
+}
+template <int B, int E, class F>
+__device__ __forceinline__ void ebe_static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    ebe_static_for<B + 1, E>(f);
+  }
+}
+static bool ebe_classes_hold(const double* K0) {
+  double mx = 0.0;
+  for (int t = 0; t < 576; ++t) mx = std::max(mx, std::fabs(K0[t]));
+  for (int r = 0; r < 24; ++r)
+    for (int c = 0; c < 24; ++c) {
+      const double ref = K0[ebe_rep(ebe_cls(r, c))] * (ebe_neg(r, c) ? -1.0 : 1.0);
+      if (!(std::fabs(K0[r * 24 + c] - ref) <= 1e-14 * mx)) return false;
+    }
+  return true;
+}
+
+template <bool RESID, bool CLS>
 __global__ void __launch_bounds__(128) k_ebe(int n, const int32_t* __restrict__ ijk,
                                              const uint8_t* __restrict__ dir,
                                              const int32_t* __restrict__ lat,
@@ -465,6 +512,9 @@ __global__ void __launch_bounds__(128) k_ebe(int n, const int32_t* __restrict__ 
   double acc[8][3];
 #pragma unroll
   for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = acc[a][2] = 0.0;
+  double C[10];   // CLS: the 10 distinct |K0| values
+#pragma unroll
+  for (int c = 0; c < 10; ++c) C[c] = CLS ? K0.k[ebe_rep(c)] : 0.0;
   const int64_t nx1 = nx + 1, ny1 = ny + 1;
   // all 27 lattice-map lookups are issued first (predicated on a shared
   // solid voxel, which also keeps them in range), then the x gathers: one
@@ -488,6 +538,33 @@ __global__ void __launch_bounds__(128) k_ebe(int n, const int32_t* __restrict__ 
       // column, structurally removed (R4)
       qs[t] = any ? lat[(ix + dx) + nx1 * ((iy + dy) + ny1 * (iz + dz))] : -1;
     }
+    if constexpr (CLS) {
+      // compile-time indices throughout (ebe_cls / ebe_neg are evaluated by
+      // the compiler: every K0 value is one of the registers C[0..9])
+      static_assert(GRP == 27, "one group");
+      ebe_static_for<0, 27>([&](auto T) {
+        constexpr int k = decltype(T)::value, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+        const int q = qs[k];
+        if (q >= 0) {
+          const double x0 = x[3 * (int64_t)q], x1 = x[3 * (int64_t)q + 1],
+                       x2 = x[3 * (int64_t)q + 2];
+          ebe_static_for<0, 8>([&](auto A) {
+            constexpr int a = decltype(A)::value;
+            constexpr int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
+            if constexpr (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1) {
+              constexpr int b = bx + 2 * by + 4 * bz;
+              ebe_static_for<0, 3>([&](auto R) {
+                constexpr int r = decltype(R)::value, row = 3 * a + r, col = 3 * b;
+                constexpr int c0 = ebe_cls(row, col), c1 = ebe_cls(row, col + 1), c2 = ebe_cls(row, col + 2);
+                constexpr bool n0 = ebe_neg(row, col), n1 = ebe_neg(row, col + 1), n2 = ebe_neg(row, col + 2);
+                acc[a][r] = fma(n2 ? -C[c2] : C[c2], x2,
+                                fma(n1 ? -C[c1] : C[c1], x1, fma(n0 ? -C[c0] : C[c0], x0, acc[a][r])));
+              });
+            }
+          });
+        }
+      });
+    } else {
 #pragma unroll
     for (int t = 0; t < GRP; ++t) {
       const int k = g0 + t, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
@@ -508,6 +585,7 @@ __global__ void __launch_bounds__(128) k_ebe(int n, const int32_t* __restrict__ 
         }
       }
     }
+  }   // general form
   }
   double out[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -783,10 +861,19 @@ void launch_ebe(int n_nodes, const int32_t* node_ijk, const uint8_t* dir, const 
     return;
   }
   const int grid = (n_nodes + 127) / 128;
+  // K0's 10 value classes in registers (HPLMM_EBE_CLS=0: the general form)
+  static const bool cls_on = !(getenv("HPLMM_EBE_CLS") && getenv("HPLMM_EBE_CLS")[0] == '0');
+  if (cls_on && ebe_classes_hold(K0_host)) {
+    if (v)
+      k_ebe<true, true><<<grid, 128, 0, st>>>(n_nodes, node_ijk, dir, lat, Es, nx, ny, nz, k, x, v, y);
+    else
+      k_ebe<false, true><<<grid, 128, 0, st>>>(n_nodes, node_ijk, dir, lat, Es, nx, ny, nz, k, x, v, y);
+    return;
+  }
   if (v)
-    k_ebe<true><<<grid, 128, 0, st>>>(n_nodes, node_ijk, dir, lat, Es, nx, ny, nz, k, x, v, y);
+    k_ebe<true, false><<<grid, 128, 0, st>>>(n_nodes, node_ijk, dir, lat, Es, nx, ny, nz, k, x, v, y);
   else
-    k_ebe<false><<<grid, 128, 0, st>>>(n_nodes, node_ijk, dir, lat, Es, nx, ny, nz, k, x, v, y);
+    k_ebe<false, false><<<grid, 128, 0, st>>>(n_nodes, node_ijk, dir, lat, Es, nx, ny, nz, k, x, v, y);
 }
 
 // ---------------------------------------------------------------------------
