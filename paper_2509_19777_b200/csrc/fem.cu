@@ -482,8 +482,8 @@ static bool ebe_classes_hold(const double* K0) {
   return true;
 }
 
-template <bool RESID, bool CLS>
-__global__ void __launch_bounds__(128) k_ebe(int n, const int32_t* __restrict__ ijk,
+template <bool RESID, bool CLS, int GRP = 27, int MINB = 5>
+__global__ void __launch_bounds__(128, MINB) k_ebe(int n, const int32_t* __restrict__ ijk,
                                              const uint8_t* __restrict__ dir,
                                              const int32_t* __restrict__ lat,
                                              const double* __restrict__ Es, int nx, int ny, int nz,
@@ -520,31 +520,30 @@ __global__ void __launch_bounds__(128) k_ebe(int n, const int32_t* __restrict__ 
   // solid voxel, which also keeps them in range), then the x gathers: one
   // lookup -> gather chain per neighbour cost 0.126 ms per apply, grouped
   // 0.107 ms (one dz plane at a time: 0.106 ms)
-  constexpr int GRP = 27;
+  static_assert(27 % GRP == 0, "whole groups");
+  // lattice-map lookup of neighbour k: no shared solid voxel -> no coupling;
+  // q < 0: no node or a Dirichlet column, structurally removed (R4)
+  auto lookup = [&](int k) -> int {
+    const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+    bool any = false;
 #pragma unroll
-  for (int g0 = 0; g0 < 27; g0 += GRP) {
-    int qs[GRP];
-#pragma unroll
-    for (int t = 0; t < GRP; ++t) {
-      const int k = g0 + t, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
-      bool any = false;
-#pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
-        if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1)
-          any |= Ea[a] != 0.0;
-      }
-      // no shared solid voxel -> no coupling; q < 0: no node or a Dirichlet
-      // column, structurally removed (R4)
-      qs[t] = any ? lat[(ix + dx) + nx1 * ((iy + dy) + ny1 * (iz + dz))] : -1;
+    for (int a = 0; a < 8; ++a) {
+      const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
+      if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1) any |= Ea[a] != 0.0;
     }
-    if constexpr (CLS) {
-      // compile-time indices throughout (ebe_cls / ebe_neg are evaluated by
-      // the compiler: every K0 value is one of the registers C[0..9])
-      static_assert(GRP == 27, "one group");
-      ebe_static_for<0, 27>([&](auto T) {
-        constexpr int k = decltype(T)::value, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
-        const int q = qs[k];
+    return any ? lat[(ix + dx) + nx1 * ((iy + dy) + ny1 * (iz + dz))] : -1;
+  };
+  if constexpr (CLS) {
+    // compile-time indices throughout (ebe_cls / ebe_neg are evaluated by the
+    // compiler: every K0 value is one of the registers C[0..9])
+    ebe_static_for<0, 27 / GRP>([&](auto GI) {
+      constexpr int g0 = decltype(GI)::value * GRP;
+      int qs[GRP];
+#pragma unroll
+      for (int t = 0; t < GRP; ++t) qs[t] = lookup(g0 + t);
+      ebe_static_for<0, GRP>([&](auto T) {
+        constexpr int k = g0 + decltype(T)::value, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+        const int q = qs[decltype(T)::value];
         if (q >= 0) {
           const double x0 = x[3 * (int64_t)q], x1 = x[3 * (int64_t)q + 1],
                        x2 = x[3 * (int64_t)q + 2];
@@ -564,28 +563,34 @@ __global__ void __launch_bounds__(128) k_ebe(int n, const int32_t* __restrict__ 
           });
         }
       });
-    } else {
+    });
+  } else {
 #pragma unroll
-    for (int t = 0; t < GRP; ++t) {
-      const int k = g0 + t, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
-      const int q = qs[t];
-      if (q < 0) continue;
-      const double x0 = x[3 * (int64_t)q], x1 = x[3 * (int64_t)q + 1],
-                   x2 = x[3 * (int64_t)q + 2];
+    for (int g0 = 0; g0 < 27; g0 += GRP) {
+      int qs[GRP];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
-        if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1) {
-          const int b = bx + 2 * by + 4 * bz;
+      for (int t = 0; t < GRP; ++t) qs[t] = lookup(g0 + t);
 #pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            const double* kr = K0.k + (3 * a + r) * 24 + 3 * b;
-            acc[a][r] = fma(kr[2], x2, fma(kr[1], x1, fma(kr[0], x0, acc[a][r])));
+      for (int t = 0; t < GRP; ++t) {
+        const int k = g0 + t, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+        const int q = qs[t];
+        if (q < 0) continue;
+        const double x0 = x[3 * (int64_t)q], x1 = x[3 * (int64_t)q + 1],
+                     x2 = x[3 * (int64_t)q + 2];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          const int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
+          if (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1) {
+            const int b = bx + 2 * by + 4 * bz;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              const double* kr = K0.k + (3 * a + r) * 24 + 3 * b;
+              acc[a][r] = fma(kr[2], x2, fma(kr[1], x1, fma(kr[0], x0, acc[a][r])));
+            }
           }
         }
       }
     }
-  }   // general form
   }
   double out[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -864,6 +869,13 @@ void launch_ebe(int n_nodes, const int32_t* node_ijk, const uint8_t* dir, const 
   // K0's 10 value classes in registers (HPLMM_EBE_CLS=0: the general form)
   static const bool cls_on = !(getenv("HPLMM_EBE_CLS") && getenv("HPLMM_EBE_CLS")[0] == '0');
   if (cls_on && ebe_classes_hold(K0_host)) {
+    // Measured variants of the classed kernel (cfg3, apply(SPMV) incl. ~0.03 ms
+    // of call overhead; default 0.091-0.094 ms): lookups in 3 groups of 9 with
+    // 80 / 72 / 64 registers (6 / 7 / 8 CTAs per SM, spills) 0.096-0.098,
+    // 27 lookups at 80 registers 0.095-0.098, 116 registers (4 CTAs) 0.100-0.103,
+    // branch-free gathers (a missing neighbour gathers the node's own x and
+    // contributes zeros) 0.089-0.093 in any grouping -- none separates from the
+    // default, which stays.
     if (v)
       k_ebe<true, true><<<grid, 128, 0, st>>>(n_nodes, node_ijk, dir, lat, Es, nx, ny, nz, k, x, v, y);
     else
