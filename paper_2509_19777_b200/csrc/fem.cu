@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(128) k_ebe2(int64_t npairs, int kx, int nx, in
 // out_c,r += E_a sum_s K0[3a + r][3b + s] x_c,s.  Same operator as k_ebe up
 // to the summation order (R4: Dirichlet rows identity, columns skipped).
 // ---------------------------------------------------------------------------
-template <int P, bool RESID>
+template <int P, bool RESID, bool CLS>
 __global__ void __launch_bounds__(128) k_ebe_k(int n, int ncols, const int32_t* __restrict__ ijk,
                                                const uint8_t* __restrict__ dir,
                                                const int32_t* __restrict__ lat,
@@ -779,6 +779,41 @@ __global__ void __launch_bounds__(128) k_ebe_k(int n, int ncols, const int32_t* 
     }
     qs[k] = any ? lat[(ix + dx) + nx1 * ((iy + dy) + ny1 * (iz + dz))] : -1;
   }
+  if constexpr (CLS) {   // K0's 10 value classes in registers (see k_ebe)
+    double C[10];
+#pragma unroll
+    for (int c = 0; c < 10; ++c) C[c] = K0.k[ebe_rep(c)];
+    ebe_static_for<0, 27>([&](auto T) {
+      constexpr int k = decltype(T)::value, dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+      const int q = qs[k];
+      if (q >= 0) {
+        double xq[P][3];
+#pragma unroll
+        for (int c = 0; c < P; ++c)
+#pragma unroll
+          for (int s2 = 0; s2 < 3; ++s2)
+            xq[c][s2] = c < ncols ? x[c * ld + 3 * (int64_t)q + s2] : 0.0;
+        ebe_static_for<0, 8>([&](auto A) {
+          constexpr int a = decltype(A)::value;
+          constexpr int bx = (a & 1) + dx, by = ((a >> 1) & 1) + dy, bz = ((a >> 2) & 1) + dz;
+          if constexpr (bx >= 0 && bx <= 1 && by >= 0 && by <= 1 && bz >= 0 && bz <= 1) {
+            constexpr int b = bx + 2 * by + 4 * bz;
+            ebe_static_for<0, 3>([&](auto R) {
+              constexpr int r = decltype(R)::value, row = 3 * a + r, col = 3 * b;
+              constexpr int c0 = ebe_cls(row, col), c1 = ebe_cls(row, col + 1), c2 = ebe_cls(row, col + 2);
+              constexpr bool n0 = ebe_neg(row, col), n1 = ebe_neg(row, col + 1), n2 = ebe_neg(row, col + 2);
+              const double k0 = n0 ? -C[c0] : C[c0], k1 = n1 ? -C[c1] : C[c1], k2 = n2 ? -C[c2] : C[c2];
+#pragma unroll
+              for (int c = 0; c < P; ++c) {
+                const double t = fma(k2, xq[c][2], fma(k1, xq[c][1], k0 * xq[c][0]));
+                out[c][r] = fma(Ea[a], t, out[c][r]);
+              }
+            });
+          }
+        });
+      }
+    });
+  } else {
 #pragma unroll
   for (int k = 0; k < 27; ++k) {
     const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
@@ -807,6 +842,7 @@ __global__ void __launch_bounds__(128) k_ebe_k(int n, int ncols, const int32_t* 
       }
     }
   }
+  }
 #pragma unroll
   for (int c = 0; c < P; ++c) {
     if (c >= ncols) break;
@@ -826,15 +862,20 @@ void launch_ebe_k(int P, int ncols, int n_nodes, const int32_t* node_ijk, const 
   EbeK0 k;
   for (int t = 0; t < 576; ++t) k.k[t] = K0_host[t];
   const int grid = (n_nodes + 127) / 128;
-#define EBE_K(PP)                                                                                 \
-  if (v)                                                                                          \
-    k_ebe_k<PP, true><<<grid, 128, 0, st>>>(n_nodes, ncols, node_ijk, dir, lat, Es, nx, ny, nz, k, \
-                                            x, v, y, ld, ldy);                                      \
+  static const bool cls_on = !(getenv("HPLMM_EBE_CLS") && getenv("HPLMM_EBE_CLS")[0] == '0');
+  const bool cls = cls_on && ebe_classes_hold(K0_host);
+#define EBE_K2(PP, RR)                                                                            \
+  if (cls)                                                                                        \
+    k_ebe_k<PP, RR, true><<<grid, 128, 0, st>>>(n_nodes, ncols, node_ijk, dir, lat, Es, nx, ny,    \
+                                                nz, k, x, v, y, ld, ldy);                          \
   else                                                                                            \
-    k_ebe_k<PP, false><<<grid, 128, 0, st>>>(n_nodes, ncols, node_ijk, dir, lat, Es, nx, ny, nz,   \
-                                             k, x, v, y, ld, ldy);
+    k_ebe_k<PP, RR, false><<<grid, 128, 0, st>>>(n_nodes, ncols, node_ijk, dir, lat, Es, nx, ny,   \
+                                                 nz, k, x, v, y, ld, ldy);
+#define EBE_K(PP)                                                                                 \
+  if (v) { EBE_K2(PP, true) } else { EBE_K2(PP, false) }
   if (P == 4) { EBE_K(4) } else if (P == 2) { EBE_K(2) } else { EBE_K(1) }
 #undef EBE_K
+#undef EBE_K2
 }
 
 static int g_ebe_mode = -1;   // 1 = k_ebe (default), 2 = two nodes per thread (k_ebe2)
