@@ -25,7 +25,8 @@ grain structurally coupled to the mortar's interface), R15 (correction columns
 only for grains with b[I_g] != 0), R16 (A^o = blockdiag(S, D_c) with
 S = P_B^T A^ P_B symmetrised from its lower triangle, D_c[g] = b_g . c_g),
 R17 (dense Cholesky of S), R18 (M_g on grain-interior DOFs I_g), R19 (plain
-additive overlap sum, ascending interface id), R21 (M_G first; M_zeta first).
+additive overlap sum, ascending interface id), R21 (M_G first; M_zeta first),
+R30 (update_matrix: M_G reused across a perturbed A^, local solves refreshed).
 """
 from __future__ import annotations
 
@@ -173,6 +174,26 @@ class HPLMM:
         self.timings = {"T_ML": t2 - t1, "T_MG": (t1 - t0) + (t3 - t2)}
 
     # ------------------------------------------------------------------
+    def update_matrix(self, system: System):
+        """Reuse of M_G for a perturbed A^ (reading R30): the
+        linear system becomes `system` (same mesh, pattern and decomposition;
+        new values, e.g. locally degraded moduli), M_G keeps the P^_B and S
+        built from the ORIGINAL matrix, and everything local follows the new
+        one: the residual operator A^, the exact grain / contact-grid solves
+        of M_g and M_zeta (eq:Mg_Mz) and, through set_rhs, the correction
+        columns c^g = (A_g)^-1 b^g (eq:col_cg).  GMRES on the new system with
+        this preconditioner still converges to the new solution; only the
+        iteration count feels the stale coarse space."""
+        if self.smoother != "cg":
+            raise ValueError("update_matrix: contact-grain smoother only")
+        if system.n_dof != self.sys.n_dof or not np.array_equal(system.col_idx, self.sys.col_idx):
+            raise ValueError("update_matrix: the block pattern must not change")
+        self.sys = system
+        self.A = system.A
+        self.grain_solve = [_Local(self.A, d) for d in self.grain_dofs]
+        self.contact_solve = [_Local(self.A, d) for d in self.contact_dofs]
+        self.corr = []
+
     def set_rhs(self, b: np.ndarray):
         """Correction vectors c^g = A_g^-1 b^g (eq:col_cg) for grains with
         b[I_g] != 0 (R15); D_c[g] = b^g . c^g (R16)."""

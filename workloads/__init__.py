@@ -31,7 +31,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["Problem", "make_problem", "CONFIGS", "random_vector", "load_cases"]
+__all__ = ["Problem", "make_problem", "CONFIGS", "random_vector", "load_cases", "perturbed_moduli"]
 
 
 @dataclass
@@ -282,3 +282,28 @@ def load_cases(p: Problem, k: int) -> list:
 def random_vector(n: int, seed: int = 12345) -> np.ndarray:
     """N(0,1) parity input (default_rng(12345))."""
     return np.random.default_rng(seed).standard_normal(n)
+
+
+def perturbed_moduli(prob: "Problem", kind: str = "crack", seed: int = 11) -> np.ndarray:
+    """New per-voxel Young's moduli for the reuse of M_G across a perturbed A^
+    (P:743): same geometry, grains and boundary data.
+
+    * ``crack``: a localised degradation -- the solid voxels of a thin slanted
+      band through the middle of the sample lose 3 decades of stiffness (the
+      "local cracks" of P:743);
+    * ``global``: a mild global perturbation, E scaled voxel by voxel by a
+      seeded factor in [0.8, 1.25] ("global but not too severe").
+    """
+    E = np.array(prob.E, dtype=np.float64, copy=True)
+    nz, ny, nx = E.shape
+    if kind == "crack":
+        z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+        band = np.abs((z - nz // 2) + (x - nx // 2) // 3) <= 0
+        band &= (y >= ny // 4) & (y < ny - ny // 4)
+        E[band] *= 1e-3
+    elif kind == "global":
+        rng = np.random.default_rng(seed)
+        E *= np.exp(rng.uniform(np.log(0.8), np.log(1.25), E.shape))
+    else:
+        raise ValueError(kind)
+    return E
