@@ -192,6 +192,7 @@ typedef struct {
   double t_setup_coarse_s;/* ~T_MG: mortars, P^_B, S, coarse inversion              */
   double t_rhs_s;         /* per-RHS correction columns (set_rhs)                   */
   double t_solve_s;       /* GMRES (T_sol)                                          */
+  double t_update_s;      /* last hplmm_update_moduli (assembly + refactorisation)  */
   int64_t kernel_launches;/* kernels launched by the last solve                      */
   int32_t fine_operator;  /* A^ applied by the solve: 0 element-by-element, 1 BSR   */
   int32_t sn_shape_grain;   /* consumer warps per CTA of the grain / contact-grid    */
@@ -277,6 +278,25 @@ hplmm_status hplmm_set_matrix(hplmm_handle *h, const double *val, void *stream);
  * R16) and its inverse (R17).  Errors: SINGULAR_LOCAL (report.err_index via
  * hplmm_get_report), SINGULAR_COARSE, OOM. */
 hplmm_status hplmm_setup(hplmm_handle *h, void *stream);
+
+/* Reuse of M_G across a perturbed A^ (reading R30):
+ * "the coefficient matrix remains unchanged (load steps) or is perturbed only
+ * slightly (local cracks), in which case the M_G of hPLMM can be reused".
+ * E: nx*ny*nz new Young's moduli (HOST, [z][y][x] as hplmm_problem.E; read
+ * where solid, must be > 0 there); geometry, grains, boundary data and nu are
+ * the handle's.  Re-assembles A^ and b^ on the GPU and refactorises every
+ * grain block and contact-grid block numerically (the symbolic analysis,
+ * factor layout, work lists and solve graph of hplmm_setup are kept), so the
+ * residual operator, M_g, M_zeta and -- at the next hplmm_set_rhs /
+ * hplmm_solve -- the correction columns (eq:col_cg) follow the new matrix,
+ * while M_G keeps the P^_B and S^-1 built by hplmm_setup from the original
+ * one.  GMRES then solves the NEW system; only its iteration count feels the
+ * older coarse space.  Cost: report.t_update_s (cfg3: ~0.35 s vs ~1.2 s for
+ * hplmm_setup).  The updated b^ is hplmm_export(RHS).  Needs local_factor = 1,
+ * smoother = 0 and the library's own assembly (not hplmm_setup_bsr /
+ * hplmm_set_matrix).  Errors: STATE, ARG (E <= 0 in a solid voxel),
+ * SINGULAR_LOCAL (report.err_index). */
+hplmm_status hplmm_update_moduli(hplmm_handle *h, const double *E, void *stream);
 
 /* Per-RHS correction columns c^g = A_g^-1 b^g (eq:col_cg) for grains with
  * b[I_g] != 0 (R15), D_c[g] = b^g . c^g (R16).  b: n_dof doubles, host or

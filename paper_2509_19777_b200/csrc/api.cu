@@ -1968,6 +1968,64 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
   }
 }
 
+hplmm_status hplmm_update_moduli(hplmm_handle* h, const double* E, void* stream) {
+  if (!h || !E) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
+  try {
+    if (!h->setup_done) throw HError{HPLMM_ERR_STATE, "hplmm_update_moduli before hplmm_setup"};
+    if (h->matrix_external)
+      throw HError{HPLMM_ERR_STATE, "hplmm_update_moduli: A^ was supplied by the caller (no voxel moduli)"};
+    if (!h->sparse() || h->ilu_smoother())
+      throw HError{HPLMM_ERR_STATE,
+                   "hplmm_update_moduli needs local_factor = 1 (supernodal) and smoother = 0 (M_CG)"};
+    require_device(h);
+    h->st = (cudaStream_t)stream;
+    HostSetup& hs = h->hs;
+    const int64_t nvox = (int64_t)hs.nx * hs.ny * hs.nz;
+    for (int64_t v = 0; v < nvox; ++v)
+      if (hs.solid[v] && !(E[v] > 0) )
+        throw HError{HPLMM_ERR_ARG, "hplmm_update_moduli: E <= 0 in solid voxel " + std::to_string(v)};
+    Timer t(h->st);
+    hs.E.assign(E, E + nvox);
+    CK(cudaMemcpyAsync(h->d_E, hs.E.data(), (size_t)nvox * 8, cudaMemcpyHostToDevice, h->st));
+    if (h->d_Es) {
+      std::vector<double> Es(nvox);
+      for (int64_t v = 0; v < nvox; ++v) Es[v] = hs.solid[v] ? hs.E[v] : 0.0;
+      CK(cudaMemcpyAsync(h->d_Es, Es.data(), (size_t)nvox * 8, cudaMemcpyHostToDevice, h->st));
+      CK(cudaStreamSynchronize(h->st));   // Es is a local
+    }
+    // A^ values and b^ from the new moduli (same pattern, R4)
+    launch_assemble((int)h->nnzb, h->d_block_row, h->d_col, h->d_ijk, h->d_dir, h->d_solid,
+                    h->d_E, hs.nx, hs.ny, hs.nz, h->d_K0, h->d_val, h->st);
+    launch_assemble_rhs(h->n_nodes, h->d_drow_ptr, h->d_dcol, h->d_ijk, h->d_dir, h->d_solid,
+                        h->d_E, hs.nx, hs.ny, hs.nz, h->d_K0, h->d_f, h->d_uD, h->d_b, h->st);
+    CK(cudaGetLastError());
+    // numeric refactorisation of every grain and contact-grid block with the
+    // symbolic analysis, factor layout and work lists of hplmm_setup
+    HandleAlloc halloc(h);
+    try {
+      sn_factor(h->sg, h->d_val, halloc, h->st, kSnPoolBytes);
+      try {
+        sn_factor(h->sc, h->d_val, halloc, h->st, kSnPoolBytes);
+      } catch (SnError& e) {
+        e.sub += hs.n_grains;
+        throw;
+      }
+    } catch (const SnError& e) {
+      h->rep.err_index = e.sub;
+      h->free_setup();
+      throw HError{(hplmm_status)e.status, e.msg + " " + std::to_string(e.sub)};
+    }
+    CK(cudaGetLastError());
+    h->rep.t_update_s = t.stop();
+    CK(cudaStreamSynchronize(h->st));
+    h->free_setup();
+    h->rhs_set = false;   // the correction columns follow the new A_g (eq:col_cg)
+    return HPLMM_OK;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
 hplmm_status hplmm_set_rhs(hplmm_handle* h, const double* b, void* stream) {
   if (!h || !b) { g_last_error = "null argument"; return HPLMM_ERR_ARG; }
   try {

@@ -1,0 +1,110 @@
+"""GPU parity of hplmm_update_moduli (reuse of M_G across a perturbed A^,
+P:743; reading R30) against oracle.hplmm.HPLMM.update_matrix: the
+re-assembled A^ and b^, the refactorised local solves (1e-12), M_G / M^-1 with
+the ORIGINAL coarse space (the coarse gate of tests/test_gpu_parity.py), and
+GMRES on the new system (iterations +-1, x <= 1e-8 -- the oracle's solution is
+pinned to the new system's direct solve in tests/test_oracle_update.py)."""
+import copy
+
+import numpy as np
+import pytest
+
+from tests.test_gpu_parity import coarse_spread_gate, dev, rel
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+_cases = {}
+
+
+def updated(name, kind):
+    if (name, kind) not in _cases:
+        import __graft_entry__
+        __graft_entry__.build()
+        from oracle import fem, hplmm
+        from paper_2509_19777_b200 import Solver
+        from workloads import make_problem, perturbed_moduli
+        p = make_problem(name)
+        s, h = hplmm.setup(p)
+        sv = Solver(p).assemble(0).setup()
+        E2 = perturbed_moduli(p, kind)
+        p2 = copy.copy(p)
+        p2.E = E2
+        s2 = fem.build_system(p2)
+        h.update_matrix(s2)
+        sv.update_moduli(E2)
+        _cases[(name, kind)] = (p2, s, s2, h, sv)
+    return _cases[(name, kind)]
+
+
+CASES = [("cube8", "global"), ("porous20", "crack"), ("porous20", "global"), ("cfg1", "crack"),
+         ("cfg1", "smooth")]
+
+
+@pytest.mark.parametrize("name,kind", CASES)
+def test_update_assembly(name, kind):
+    p2, s, s2, h, sv = updated(name, kind)
+    val = sv.export("VAL").reshape(-1, 3, 3)
+    assert np.abs(val - s2.val).max() <= 1e-13 * np.abs(s2.val).max()
+    assert np.abs(s2.val - s.val).max() > 1e-3 * np.abs(s.val).max()
+    b = sv.export("RHS")
+    assert np.abs(b - s2.b).max() <= 1e-13 * max(np.abs(s2.b).max(), 1e-300)
+    v = np.random.default_rng(12345).standard_normal(s2.n_dof)
+    assert rel(sv.apply("SPMV", dev(v)).cpu().numpy(), s2.A @ v) <= 1e-12
+    assert sv.report()["t_update_s"] > 0
+
+
+@pytest.mark.parametrize("name,kind", CASES)
+@pytest.mark.parametrize("op", ["MZETA", "MGRAIN", "MCG", "MG", "MINV"])
+def test_update_preconditioner(name, kind, op):
+    p2, s, s2, h, sv = updated(name, kind)
+    sv.set_rhs(dev(s2.b))
+    h.set_rhs(s2.b)
+    v = np.random.default_rng(12345).standard_normal(s2.n_dof)
+    ref = {"MZETA": h.apply_Mzeta, "MGRAIN": h.apply_Mg, "MCG": h.apply_MCG,
+           "MG": h.apply_MG, "MINV": h.apply_M}[op](v)
+    out = sv.apply(op, dev(v)).cpu().numpy()
+    tol = 1e-12 if op in ("MZETA", "MGRAIN", "MCG") else coarse_spread_gate(h, op, v, ref)
+    assert rel(out, ref) <= tol, (rel(out, ref), tol)
+
+
+@pytest.mark.parametrize("name,kind", CASES)
+def test_update_solve(name, kind):
+    from oracle import gmres
+    p2, s, s2, h, sv = updated(name, kind)
+    h.set_rhs(s2.b)
+    xo, ito, histo, rro, convo = gmres.gmres(s2.A, s2.b, h.apply_M, tol=1e-8)
+    x, rep, hist = sv.solve(dev(s2.b), tol=1e-8)
+    x = x.cpu().numpy()
+    assert rep["converged"] == 1 and convo
+    assert abs(rep["iterations"] - ito) <= 1, (rep["iterations"], ito)
+    assert rel(x, xo) <= 1e-8
+    k = min(len(hist), len(histo)) - 2
+    assert np.allclose(hist[:k], histo[:k], rtol=1e-6, atol=1e-14)
+    # the true residual is the NEW system's
+    assert np.linalg.norm(s2.b - s2.A @ x) <= 1e-7 * np.linalg.norm(s2.b)
+
+
+def test_update_errors():
+    from paper_2509_19777_b200 import Solver
+    from paper_2509_19777_b200.hplmm import HPLMMError
+    from workloads import make_problem
+    p = make_problem("cube8")
+    sv = Solver(p).assemble(0)
+    with pytest.raises(HPLMMError):          # before setup
+        sv.update_moduli(p.E)
+    sv.setup()
+    bad = np.array(p.E, copy=True)
+    bad.flat[0] = 0.0
+    with pytest.raises(HPLMMError):          # E <= 0 in a solid voxel
+        sv.update_moduli(bad)
+    sd = Solver(p, local_factor=0).assemble(0).setup()
+    with pytest.raises(HPLMMError):          # dense local inverses: not supported
+        sd.update_moduli(p.E)
+    # an identity update leaves the solve unchanged
+    b = dev(sv.export("RHS"))
+    x0, r0, _ = sv.solve(b, tol=1e-8)
+    sv.update_moduli(p.E)
+    x1, r1, _ = sv.solve(b, tol=1e-8)
+    assert r0["iterations"] == r1["iterations"]
+    assert rel(x1.cpu().numpy(), x0.cpu().numpy()) <= 1e-12

@@ -291,8 +291,11 @@ def perturbed_moduli(prob: "Problem", kind: str = "crack", seed: int = 11) -> np
     * ``crack``: a localised degradation -- the solid voxels of a thin slanted
       band through the middle of the sample lose 3 decades of stiffness (the
       "local cracks" of P:743);
-    * ``global``: a mild global perturbation, E scaled voxel by voxel by a
-      seeded factor in [0.8, 1.25] ("global but not too severe").
+    * ``global``: E scaled voxel by voxel by a seeded, spatially uncorrelated
+      factor in [0.8, 1.25] -- global AND rough (the case where, per P:819,
+      "M_G must be updated");
+    * ``smooth``: E scaled by a smooth field in [0.8, 1.25] (one period of a
+      sine product across the sample: "global but not too severe").
     """
     E = np.array(prob.E, dtype=np.float64, copy=True)
     nz, ny, nx = E.shape
@@ -304,6 +307,10 @@ def perturbed_moduli(prob: "Problem", kind: str = "crack", seed: int = 11) -> np
     elif kind == "global":
         rng = np.random.default_rng(seed)
         E *= np.exp(rng.uniform(np.log(0.8), np.log(1.25), E.shape))
+    elif kind == "smooth":
+        z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+        f = np.sin(2 * np.pi * x / nx) * np.cos(2 * np.pi * y / ny) * np.sin(2 * np.pi * (z + 0.25 * nz) / nz)
+        E *= np.exp(np.log(1.25) * f)
     else:
         raise ValueError(kind)
     return E
