@@ -622,3 +622,40 @@ def test_device_resident_solve_iteration_cap():
         assert rep["iterations"] == 7 and rep["converged"] == 0 and len(hist) == 7
         assert np.linalg.norm(s.b - s.A @ x) / np.linalg.norm(s.b) == pytest.approx(
             rep["final_true_relres"], rel=1e-6)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_first_pass_E2(case):
+    """First-pass solution x^_aprx = M_G^-1 b^ and its error metric
+    E_2 = ||x^_aprx - x^|| / ||x^|| (eq:err_metric):
+    hplmm_set_rhs(b) + hplmm_apply(MG, b) against the oracle's first pass,
+    both measured against the sparse direct solution.  (The oracle's first
+    pass is pinned by App. B's full-cap case, tests/test_oracle_precond.py.)"""
+    import scipy.sparse.linalg as spla
+    p, s, h, sv = gpu_case(case)
+    xs = spla.spsolve(s.A.tocsc(), s.b)
+    h.set_rhs(s.b)
+    xo = h.apply_MG(s.b)
+    sv.set_rhs(dev(s.b))
+    xg = sv.apply("MG", dev(s.b)).cpu().numpy()
+    tol = coarse_spread_gate(h, "MG", s.b, xo)
+    assert rel(xg, xo) <= tol, (rel(xg, xo), tol)
+    e2o = np.linalg.norm(xo - xs) / np.linalg.norm(xs)
+    e2g = np.linalg.norm(xg - xs) / np.linalg.norm(xs)
+    assert 0 < e2o < 1 and abs(e2g - e2o) <= 1e-9 * max(e2o, 1e-3), (e2g, e2o)
+
+
+def test_first_pass_full_cap_is_direct_solve():
+    """App. B: every interface node a mortar node => the first pass is
+    the direct solve (E_2 ~ 0) and GMRES needs one iteration."""
+    import scipy.sparse.linalg as spla
+    from paper_2509_19777_b200 import Solver
+    from oracle import fem
+    from workloads import make_problem
+    p = make_problem("cube8")
+    s = fem.build_system(p)
+    sv = Solver(p, n_mortar=10 ** 6, coarse_refine=1).assemble(0).setup()
+    sv.set_rhs(dev(s.b))
+    xg = sv.apply("MG", dev(s.b)).cpu().numpy()
+    xs = spla.spsolve(s.A.tocsc(), s.b)
+    assert rel(xg, xs) <= 1e-8, rel(xg, xs)
