@@ -104,7 +104,8 @@ struct TeamBuilder {
   const std::vector<int>& start;        // first supernode of each supernode's subtree
   Team& T;
   std::vector<std::pair<int, int>> anc;  // ancestor chains (supernode ranges), innermost last
-  int64_t xcost;
+  int64_t xcost;                         // an exchange step in byte equivalents
+  std::vector<std::pair<std::pair<int, int>, int>> anc_owner;   // the same chains with their owners
 
   struct Node {
     int ca = 0, cb = 0;   // separator chain [ca, cb)
@@ -205,8 +206,6 @@ struct TeamBuilder {
     bwd(nd.left);
     if (chain) anc.pop_back();
   }
-  std::vector<std::pair<std::pair<int, int>, int>> anc_owner;
-
   void owned(int v) {
     const Node& nd = nodes[v];
     if (nd.left < 0) {
