@@ -682,6 +682,7 @@ def main():
                          "sn_teams": {"grain": rep0.get("sn_teams_grain"),
                                       "contact": rep0.get("sn_teams_contact"),
                                       "max_ctas": rep0.get("sn_team_max")},
+                         "sn_x_in_global": [rep0.get("sn_xg_grain"), rep0.get("sn_xg_contact")],
                          "solve_driver": "device-resident CUDA graph (one launch per solve)"
                          if (not ilu) else "host loop"},
         "iterations": iters, "iterations_per_s": iters / med_s * world,

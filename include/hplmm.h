@@ -201,6 +201,10 @@ typedef struct {
   int32_t sn_teams_grain;   /* grains / contact grids shared by a team of CTAs      */
   int32_t sn_teams_contact; /* (sn_split), and the CTAs of the largest team         */
   int32_t sn_team_max;
+  int32_t sn_xg_grain;      /* 1: the batch's one-RHS solves keep x in the CTA's     */
+  int32_t sn_xg_contact;    /* global-memory slice (subdomains too large for two
+                               CTAs per SM with x in shared memory), 0: x in
+                               shared memory                                      */
 } hplmm_report;
 
 typedef struct hplmm_handle hplmm_handle;

@@ -1617,6 +1617,10 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       // experiments: per-batch launch shape (HPLMM_SN_SHAPE_G / _C = 8 | 16)
       const int shape_g = getenv("HPLMM_SN_SHAPE_G") ? atoi(getenv("HPLMM_SN_SHAPE_G")) : shape;
       const int shape_c = getenv("HPLMM_SN_SHAPE_C") ? atoi(getenv("HPLMM_SN_SHAPE_C")) : shape;
+      // experiments: x of the one-RHS solves in global memory (-1 = automatic per batch)
+      const int xg_all = getenv("HPLMM_SN_XG") ? atoi(getenv("HPLMM_SN_XG")) : -1;
+      const int xg_g = getenv("HPLMM_SN_XG_G") ? atoi(getenv("HPLMM_SN_XG_G")) : xg_all;
+      const int xg_c = getenv("HPLMM_SN_XG_C") ? atoi(getenv("HPLMM_SN_XG_C")) : xg_all;
       // the contact-grid analysis (host) runs on its own thread while the grain
       // batch is analysed, uploaded and its factorisation is queued on the GPU
       std::string err_c;
@@ -1625,7 +1629,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       if (!ilu)
         th_c = std::thread([&] {
           ok_c = sn_analyse(hs, hs.contact_ptr, hs.contact_nodes, sn_leaf(), h->sc.sym, err_c, h->nsm,
-                            shape_c);
+                            shape_c, xg_c);
         });
       struct Joiner {
         std::thread& t;
@@ -1633,7 +1637,7 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
       } joiner{th_c};
       if (getenv("HPLMM_SN_OVERLAP") && getenv("HPLMM_SN_OVERLAP")[0] == '0' && th_c.joinable())
         th_c.join();   // experiments: the two analyses one after the other
-      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, sn_leaf(), h->sg.sym, err, h->nsm, shape_g))
+      if (!sn_analyse(hs, hs.grain_ptr, hs.grain_nodes, sn_leaf(), h->sg.sym, err, h->nsm, shape_g, xg_g))
         throw HError{HPLMM_ERR_ARG, "supernodal analysis: " + err};
       double t1 = wall();
       try {
@@ -1657,6 +1661,8 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
         h->rep.sn_teams_grain = h->sg.work.nteams;
         h->rep.sn_teams_contact = ilu ? 0 : h->sc.work.nteams;
         h->rep.sn_team_max = std::max(h->sg.work.team, ilu ? 1 : h->sc.work.team);
+        h->rep.sn_xg_grain = h->sg.sym.xg1 ? 1 : 0;
+        h->rep.sn_xg_contact = (!ilu && h->sc.sym.xg1) ? 1 : 0;
         if (!ilu) try {
           sn_factor(h->sc, h->d_val, halloc, h->st, kSnPoolBytes);
           if (dbg)

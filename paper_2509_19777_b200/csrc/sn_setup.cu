@@ -243,6 +243,7 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
                    const std::vector<int32_t>* ncols, SnWork& wk, int force_cons, bool allow_split) {
   const SnSymbolic& s = B.sym;
   const bool setup_only = ncols != nullptr;
+  const bool xg = sn_xg(nrhs, s.xg1);   // x in the CTA's global slice
   std::vector<int64_t> wgt;
   std::vector<int32_t> isub, ic0;
   for (int g = 0; g < s.nsub; ++g) {
@@ -256,7 +257,7 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   }
   wk.cons = force_cons ? force_cons
                        : sn_solve_cfg((int)isub.size(), nblocks, s.max_n, s.max_r, nrhs,
-                                      s.chunk_doubles, s.shape, s.max_w);
+                                      s.chunk_doubles, s.shape, s.max_w, xg);
   // several right-hand sides: the 8-warp CTAs hold at most 2 row pairs of
   // every column per thread (k_sn_solve SN_MAXQ), i.e. parts of <= 1024 rows
   if (nrhs > 1 && wk.cons == 8 && std::max(s.max_w, s.max_r) > 512) wk.cons = 16;
@@ -270,7 +271,7 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
   const bool dbg = getenv("HPLMM_DEBUG") != nullptr;
 
   // ---- subtree-parallel teams for the largest items (one RHS, main solve only)
-  const int Lmax = (allow_split && nrhs == 1 && !ncols && !sn_xg(1) && !isub.empty()) ? sn_split_levels(s.split) : 0;
+  const int Lmax = (allow_split && nrhs == 1 && !ncols && !xg && !isub.empty()) ? sn_split_levels(s.split) : 0;
   std::vector<int32_t> ord(wgt.size());
   for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int32_t)i;
   std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return wgt[a] > wgt[b]; });
@@ -524,7 +525,7 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
     wk.xflag = (int32_t*)A.alloc(std::max(nflags, 1) * 4, setup_only);
     SN_CK(cudaMemsetAsync(wk.xflag, 0, std::max(nflags, 1) * 4, st));
   }
-  if (sn_xg(nrhs) && wk.nblocks > 0) {
+  if (xg && wk.nblocks > 0) {
     wk.xg_stride = sn_xg_stride(s.max_n, nrhs);
     wk.xg = (double*)A.alloc((size_t)wk.nblocks * wk.xg_stride * 8, setup_only);
   }

@@ -690,16 +690,31 @@ __global__ void __launch_bounds__(32 * (CONS + 1), CPS)
 // x_S (max_n) and x_R (max_r) after the ring; at least SN_GUARD doubles, the
 // largest row overrun of an unpredicated sn_rows read (2 TG - 1, TG <= 256)
 constexpr int SN_GUARD = 512;
-// x and x_R in global memory (SnWork::xg) for several right-hand sides;
-// HPLMM_SN_XG=1 also for one (experiment)
-bool sn_xg(int nrhs) {
-  static const bool env = getenv("HPLMM_SN_XG") && atoi(getenv("HPLMM_SN_XG")) > 0;
-  return nrhs > 1 || env;
+// x and x_R in global memory (SnWork::xg): always for several right-hand
+// sides; for one, per batch (SnSymbolic::xg1, sn_pick_xg)
+bool sn_xg(int nrhs, bool xg1) { return nrhs > 1 || xg1; }
+// One right-hand side: x of the whole subdomain in shared memory is what makes
+// the sweep fast while two 8-warp CTAs per SM fit next to it with chunks of
+// >= 32 KiB (cfg3: 1.70 vs 2.11 ms with x in global memory).  When x is too
+// large for that -- the batch would run 16 x 1 (cfg4 / cfg5 grains, x up to
+// 12 k DOF) or 8 x 2 on 16-24 KiB chunks (their contact grids) -- x moves to
+// the CTA's global slice (L1/L2-resident, x_S staged per supernode as for
+// several RHS) and the batch keeps 8 x 2 with ~50 KiB chunks: cfg4 solve
+// 0.697 -> 0.638 s.  mode: -1 automatic, 0 / 1 forced (HPLMM_SN_XG, _G, _C).
+bool sn_pick_xg(int nitems, int nsm, int max_n, int max_r, int shape, int max_w, int mode) {
+  if (mode >= 0) return mode > 0;
+  const int cs = sn_pick_chunk(nitems, nsm, max_n, max_r, shape, max_w, false);
+  const int cfg_s = sn_solve_cfg(nitems, nsm, max_n, max_r, 1, cs, shape, max_w, false);
+  if (cfg_s == 8 && cs >= 4096) return false;
+  if (cfg_s != 8 && nitems < 2 * nsm) return false;   // few subdomains: 16 x 1 is the shape anyway
+  const int cx = sn_pick_chunk(nitems, nsm, max_n, max_r, shape, max_w, true);
+  const int cfg_x = sn_solve_cfg(nitems, nsm, max_n, max_r, 1, cx, shape, max_w, true);
+  return cfg_x == 8 && (cfg_s != 8 || cx > cs);
 }
 int64_t sn_xg_stride(int max_n, int nrhs) { return (int64_t)((max_n + 1) & ~1) * nrhs; }
 // shared memory after the ring: x (or, XG, x_S of one supernode) then x_R
-static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int max_w) {
-  const int xs = sn_xg(nrhs) ? max_w : max_n;
+static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int max_w, bool xg) {
+  const int xs = xg ? max_w : max_n;
   const size_t t = (size_t)(((xs + 1) & ~1) + ((max_r + 3) & ~1)) * nrhs;
   return t < SN_GUARD ? SN_GUARD : t;
 }
@@ -714,7 +729,7 @@ static size_t sn_tail_doubles(int max_n, int max_r, int nrhs, int max_w) {
 // twice the CTAs let the scheduler cut deeper (cfg2: 0.0352 -> 0.0292 s).
 
 int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk, int shape,
-                 int max_w) {
+                 int max_w, bool xg) {
   static int env_forced = -1;
   if (env_forced < 0) {
     const char* e = getenv("HPLMM_SN_CFG");
@@ -727,9 +742,9 @@ int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk,
   // TG >= h/8 for one RHS (<= 8 x consumer threads) and TG >= h/2 for several
   // (sn_lg: <= 2 x consumer threads x NRHS)
   auto scratch = [nrhs](int nt) { return nrhs == 1 ? 8 * nt : 2 * nt * nrhs; };
-  const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8, max_w) >= 2 && chunk >= scratch(256);
-  const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16, max_w) >= 2 && chunk >= scratch(512);
-  if (forced == 4 && sn_solve_stages(max_n, max_r, nrhs, chunk, 4, max_w) >= 2 && chunk >= scratch(128))
+  const bool fit8 = sn_solve_stages(max_n, max_r, nrhs, chunk, 8, max_w, xg) >= 2 && chunk >= scratch(256);
+  const bool fit16 = sn_solve_stages(max_n, max_r, nrhs, chunk, 16, max_w, xg) >= 2 && chunk >= scratch(512);
+  if (forced == 4 && sn_solve_stages(max_n, max_r, nrhs, chunk, 4, max_w, xg) >= 2 && chunk >= scratch(128))
     return 4;
   if (forced == 8 && fit8) return 8;
   if (forced == 16 && fit16) return 16;
@@ -751,16 +766,16 @@ static int cfg_cps(int cons) { return sn_cfg_cps(cons); }
 // two CTAs) streams 64 KiB (else 48 KiB) chunks -- half the per-chunk
 // overhead for its 16 consumer warps (cfg5 grain / contact solves -13% / -8%).
 // HPLMM_SN_CHUNK overrides.
-int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape, int max_w) {
+int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape, int max_w, bool xg) {
   if (getenv("HPLMM_SN_CHUNK")) return sn_chunk_doubles();
   const int base = sn_chunk_doubles();
-  if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base, shape, max_w) == 8) {
+  if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, base, shape, max_w, xg) == 8) {
     // the largest chunk (2 KiB steps) that keeps two 8-warp CTAs per SM with
     // two stages: the solve's cost is per chunk more than per byte (cfg3
     // contact batch: 32 KiB 1.79 ms, 36 KiB 1.74 ms, 38 KiB 1.70 ms)
     int best = base;
     for (int c = base + 256; c <= SN_CHUNK_DOUBLES_MAX; c += 256) {
-      if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape, max_w) != 8) break;
+      if (sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape, max_w, xg) != 8) break;
       best = c;
     }
     return best;
@@ -768,16 +783,16 @@ int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape, int max_
   // enough subdomains for 8 x 2 but x_S leaves no room for two 32-KiB stages:
   // smaller chunks keep the 8 x 2 shape (far cheaper per byte than 16 x 1)
   for (int c : {3072, 2048})
-    if (c < base && sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape, max_w) == 8) return c;
+    if (c < base && sn_solve_cfg(nitems, nsm, max_n, max_r, 1, c, shape, max_w, xg) == 8) return c;
   for (int c : {SN_CHUNK_DOUBLES_MAX, 6144})
-    if (c > base && sn_solve_stages(max_n, max_r, 1, c, 16, max_w) >= 2) return c;
+    if (c > base && sn_solve_stages(max_n, max_r, 1, c, 16, max_w, xg) >= 2) return c;
   return base;
 }
 
-int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons, int max_w) {
+int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons, int max_w, bool xg) {
   const int p = cfg_cps(cons);
   const long avail =
-      (226L * 1024) / p - 1024 - (long)sn_tail_doubles(max_n, max_r, nrhs, max_w) * 8;
+      (226L * 1024) / p - 1024 - (long)sn_tail_doubles(max_n, max_r, nrhs, max_w, xg) * 8;
   return (int)std::min<long>(SN_MAXST, avail / ((long)chunk * 8));
 }
 
@@ -858,8 +873,9 @@ static void sn_launch_nrhs(const SnDev& d, const SnIO& io, const SnWork& wk, int
 void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
                      int max_r, int chunk, int cons, cudaStream_t st) {
   if (wk.nblocks <= 0) return;
-  const int stages = sn_solve_stages(max_n, max_r, nrhs, chunk, cons, wk.max_w);
-  const size_t smem = ((size_t)stages * chunk + sn_tail_doubles(max_n, max_r, nrhs, wk.max_w)) * 8;
+  const bool xg = wk.xg != nullptr;
+  const int stages = sn_solve_stages(max_n, max_r, nrhs, chunk, cons, wk.max_w, xg);
+  const size_t smem = ((size_t)stages * chunk + sn_tail_doubles(max_n, max_r, nrhs, wk.max_w, xg)) * 8;
   static const bool dbg = getenv("HPLMM_DEBUG") != nullptr;
   static int printed = 0;
   if (dbg && printed < 4) {

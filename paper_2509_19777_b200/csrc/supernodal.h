@@ -76,6 +76,7 @@ struct SnSymbolic {
   int chunk_doubles = 0;                   // TMA chunk (stage) size of the schedule
   int shape = 0;                           // launch shape asked for (0 auto, 8, 16)
   int split = 0;                           // hplmm_options.sn_split (0 auto, -1 off, 1..3 levels)
+  bool xg1 = false;                        // one-RHS solves keep x in global memory (sn_pick_xg)
   // per subdomain
   std::vector<int32_t> sub_n;              // DOFs
   std::vector<int64_t> sub_base;           // offset of its local positions
@@ -111,16 +112,18 @@ struct SnSymbolic {
 // launch shape, sn_pick_chunk)
 bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
                 const std::vector<int32_t>& nodes, int leaf, SnSymbolic& out, std::string& err,
-                int nsm = 148, int shape = 0);
+                int nsm = 148, int shape = 0, int xg_mode = -1);
 // shape: 0 = automatic, 8 = 8 consumer warps x 2 CTAs per SM, 16 = 16 x 1
-int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape, int max_w);
+int sn_pick_chunk(int nitems, int nsm, int max_n, int max_r, int shape, int max_w, bool xg);
+// x of a one-RHS solve in global memory for this batch? (mode: -1 automatic, 0 / 1 forced)
+bool sn_pick_xg(int nitems, int nsm, int max_n, int max_r, int shape, int max_w, int mode);
 int sn_cfg_cps(int cons);   // CTAs per SM of a launch shape
 // consumer warps per CTA (8: two CTAs per SM; 16: one), 0 if the subdomain
 // vectors do not fit in shared memory with >= 2 ring stages
 int sn_solve_cfg(int nitems, int nsm, int max_n, int max_r, int nrhs, int chunk, int shape,
-                 int max_w);
+                 int max_w, bool xg);
 // x of the solve in global memory (per-CTA slices of sn_xg_stride doubles)
-bool sn_xg(int nrhs);
+bool sn_xg(int nrhs, bool xg1);
 int64_t sn_xg_stride(int max_n, int nrhs);
 
 }  // namespace hplmm

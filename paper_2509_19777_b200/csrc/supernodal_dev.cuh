@@ -105,7 +105,7 @@ struct GemmProb {
 };
 
 // ring stages of a launch shape (cons consumer warps) for these subdomain sizes
-int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons, int max_w);
+int sn_solve_stages(int max_n, int max_r, int nrhs, int chunk, int cons, int max_w, bool xg);
 void launch_sn_solve(const SnDev& d, const SnIO& io, const SnWork& wk, int nrhs, int max_n,
                      int max_r, int chunk, int cons, cudaStream_t st);
 void launch_front_asm(const int32_t* list, int nlist, const SnNum& nm, const double* val,

@@ -248,7 +248,8 @@ int sn_chunk_doubles() {
 }
 
 bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
-                const std::vector<int32_t>& nodes, int leaf, SnSymbolic& o, std::string& err, int nsm, int shape) {
+                const std::vector<int32_t>& nodes, int leaf, SnSymbolic& o, std::string& err, int nsm, int shape,
+                int xg_mode) {
   const int nsub = (int)ptr.size() - 1;
   std::vector<SubResult> res(std::max(nsub, 0));
   unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
@@ -386,7 +387,8 @@ bool sn_analyse(const HostSetup& hs, const std::vector<int32_t>& ptr,
   const int64_t foff = o_f[nsub];
   o.factor_doubles = foff;
   o.shape = shape;
-  o.chunk_doubles = sn_pick_chunk(nsub, nsm, o.max_n, o.max_r, shape, o.max_w);
+  o.xg1 = sn_pick_xg(nsub, nsm, o.max_n, o.max_r, shape, o.max_w, xg_mode);
+  o.chunk_doubles = sn_pick_chunk(nsub, nsm, o.max_n, o.max_r, shape, o.max_w, o.xg1);
   const double t2 = now();
   // TMA chunk schedule: forward = (W_S, rows, F_SS^-1) per S in postorder,
   // backward = (rows, W_S) per S in reverse postorder; W/F chunks are whole

@@ -73,7 +73,8 @@ class Report(C.Structure):
                 ("kernel_launches", C.c_int64), ("fine_operator", C.c_int32),
                 ("sn_shape_grain", C.c_int32), ("sn_shape_contact", C.c_int32),
                 ("sn_teams_grain", C.c_int32), ("sn_teams_contact", C.c_int32),
-                ("sn_team_max", C.c_int32)]
+                ("sn_team_max", C.c_int32), ("sn_xg_grain", C.c_int32),
+                ("sn_xg_contact", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
