@@ -364,6 +364,17 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
     return {load[am], nb, am};
   };
   const int64_t ms0 = evaluate(level, nullptr, nullptr).ms;
+  if (dbg && nitems > nslots && nitems <= 2 * nslots) {
+    // fold bound: the nslots bins hold one or two items; the 2 (n - k) smallest
+    // are paired largest-with-smallest
+    const int k = nslots, np = nitems - k;
+    int64_t fb = wgt[ord[0]];
+    for (int t = 0; t < np; ++t) fb = std::max(fb, wgt[ord[nitems - 2 * np + t]] + wgt[ord[nitems - 1 - t]]);
+    double tot = 0;
+    for (int64_t w : wgt) tot += (double)w;
+    fprintf(stderr, "hplmm sn work: LPT makespan %.4f of the mean, fold (<= 2 per CTA) %.4f\n",
+            ms0 / (tot / k), fb / (tot / k));
+  }
   int64_t best_ms = ms0;
   if (Lmax > 0 && s.split > 0) {
     // forced (hplmm_options.sn_split = L > 0; tests, experiments): every item,
