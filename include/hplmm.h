@@ -295,8 +295,9 @@ hplmm_status hplmm_setup(hplmm_handle *h, void *stream);
  * hplmm_solve -- the correction columns (eq:col_cg) follow the new matrix,
  * while M_G keeps the P^_B and S^-1 built by hplmm_setup from the original
  * one.  GMRES then solves the NEW system; only its iteration count feels the
- * older coarse space.  Cost: report.t_update_s (cfg3: ~0.35 s vs ~1.2 s for
- * hplmm_setup).  The updated b^ is hplmm_export(RHS).  Needs local_factor = 1,
+ * older coarse space (a local perturbation costs a few iterations; a global
+ * one can stall GMRES -- then set up again).  Cost: report.t_update_s (cfg3:
+ * 0.21 s vs 1.26 s for hplmm_setup).  The updated b^ is hplmm_export(RHS).  Needs local_factor = 1,
  * smoother = 0 and the library's own assembly (not hplmm_setup_bsr /
  * hplmm_set_matrix).  Errors: STATE, ARG (E <= 0 in a solid voxel),
  * SINGULAR_LOCAL (report.err_index). */
