@@ -303,6 +303,19 @@ hplmm_status hplmm_setup(hplmm_handle *h, void *stream);
  * SINGULAR_LOCAL (report.err_index). */
 hplmm_status hplmm_update_moduli(hplmm_handle *h, const double *E, void *stream);
 
+/* "Otherwise, M_G must be updated periodically": rebuild M_G for the
+ * handle's CURRENT A^ (after hplmm_update_moduli) -- shape vectors
+ * (eq:col_pk) with the current grain factors, S = P^_B^T A^ P^_B
+ * (eq:mg_struct, R16) and S^-1 (R17) -- without repeating the integer setup,
+ * the symbolic analysis or the local factorisations.  After
+ * hplmm_update_moduli + hplmm_refresh_coarse the handle applies the same M^-1
+ * as a fresh hplmm_setup on the new moduli.  Time in report.t_setup_coarse_s
+ * (cfg3: ~0.6 s).  Needs the default configuration: local_factor = 1,
+ * smoother = 0, coarse_solver = 0, coarse_refine = 0, Gaussian mortars (their
+ * weights are geometric; the Algebraic ones depend on A^).  Errors: STATE,
+ * SINGULAR_COARSE. */
+hplmm_status hplmm_refresh_coarse(hplmm_handle *h, void *stream);
+
 /* Per-RHS correction columns c^g = A_g^-1 b^g (eq:col_cg) for grains with
  * b[I_g] != 0 (R15), D_c[g] = b^g . c^g (R16).  b: n_dof doubles, host or
  * device.  hplmm_solve calls it itself; needed before hplmm_apply(MG/MINV). */

@@ -65,6 +65,8 @@ class HPLMM:
         if smoother not in ("cg", "ilu0") or n_st < 1:
             raise ValueError("smoother must be 'cg' or 'ilu0' and n_st >= 1")
         self.smoother, self.n_st = smoother, int(n_st)
+        self._params = dict(n_mortar=n_mortar, beta=beta, contact_h=contact_h, mortar=mortar,
+                            smoother=smoother, n_st=n_st)
         self.sys = system
         self.timings = {}      # wall seconds of the setup phases (bench's cpu baseline)
         t0 = time.perf_counter()
@@ -193,6 +195,13 @@ class HPLMM:
         self.grain_solve = [_Local(self.A, d) for d in self.grain_dofs]
         self.contact_solve = [_Local(self.A, d) for d in self.contact_dofs]
         self.corr = []
+
+    def refresh_coarse(self):
+        """"Otherwise, M_G must be updated periodically": M_G rebuilt
+        for the CURRENT system -- by definition the setup of eq:mg_struct /
+        eq:col_pk on that system (same geometry, decomposition and mortar
+        nodes: they do not depend on the matrix values)."""
+        self.__init__(self.sys, **self._params)
 
     def set_rhs(self, b: np.ndarray):
         """Correction vectors c^g = A_g^-1 b^g (eq:col_cg) for grains with

@@ -107,6 +107,7 @@ struct hplmm_handle {
   // multi-RHS batches (hplmm_solve_many, multirhs.cu): K <= 4 columns of
   // stride ldv; per-column Krylov bases; per-RHS correction columns Ck / Dck
   int64_t co_ct = 0, co_yo = 0;      // sizes of the restriction partials / grain coarse values
+  int64_t co_off = 0, co_cg = 0;     // doubles of B / R and of the Cg scratch (hplmm_refresh_coarse)
   struct Multi {
     int K = 0;
     double *B = nullptr, *X = nullptr, *vin = nullptr, *y = nullptr, *r1 = nullptr, *z1 = nullptr,
@@ -1566,6 +1567,8 @@ hplmm_status hplmm_setup(hplmm_handle* h, void* stream) {
     co.gpart = h->dalloc<double>(std::max<int64_t>(yo, 1));
     co.yext_off = h->upload(yext_off);
     h->co_ct = ct;
+    h->co_off = off;
+    h->co_cg = co2;
     h->co_yo = yo;
     co.Dc = h->dalloc<double>(std::max(G, 1));
     co.Cg = h->dalloc<double>(std::max<int64_t>(co2, 1), true);
@@ -2026,6 +2029,81 @@ hplmm_status hplmm_update_moduli(hplmm_handle* h, const double* E, void* stream)
     CK(cudaStreamSynchronize(h->st));
     h->free_setup();
     h->rhs_set = false;   // the correction columns follow the new A_g (eq:col_cg)
+    return HPLMM_OK;
+  } catch (const HError& e) {
+    return fail(e);
+  }
+}
+
+hplmm_status hplmm_refresh_coarse(hplmm_handle* h, void* stream) {
+  if (!h) { g_last_error = "null handle"; return HPLMM_ERR_ARG; }
+  try {
+    if (!h->setup_done) throw HError{HPLMM_ERR_STATE, "hplmm_refresh_coarse before hplmm_setup"};
+    const HostSetup& hs = h->hs;
+    if (!h->sparse() || h->ilu_smoother() || h->chol() || hs.opt.coarse_refine ||
+        hs.opt.mortar_kind != 0)
+      throw HError{HPLMM_ERR_STATE,
+                   "hplmm_refresh_coarse needs local_factor = 1, smoother = 0, coarse_solver = 0, "
+                   "coarse_refine = 0 and Gaussian mortars (whose weights do not depend on A^)"};
+    require_device(h);
+    h->st = (cudaStream_t)stream;
+    DevCoarse& co = h->co;
+    const int G = hs.n_grains;
+    Timer t(h->st);
+    HandleAlloc halloc(h);
+    const int64_t off = std::max<int64_t>(h->co_off, 1);
+    // the setup-only scratch of the T_MG phases, again
+    co.R = h->dalloc<double>(off, true);
+    co.Cg = h->dalloc<double>(std::max<int64_t>(h->co_cg, 1), true);
+    h->sb.dinv = h->dalloc<double>((size_t)std::max(h->sb.nsub, 1) * TILE * SWEEP_M * SWEEP_M, true);
+    h->sb.cbuf = h->dalloc<double>((size_t)std::max<int64_t>(h->sb.nrows, 1) * TILE * SWEEP_M, true);
+    h->sb.wbuf = h->dalloc<double>((size_t)std::max<int64_t>(h->sb.nrows, 1) * TILE * SWEEP_M, true);
+    auto drop = [&]() {
+      h->free_setup();
+      co.R = co.Cg = nullptr;
+      h->sb.dinv = h->sb.cbuf = h->sb.wbuf = nullptr;
+    };
+    try {
+      const int32_t big = INT_MAX;
+      CK(cudaMemcpyAsync(h->sb.err, &big, 4, cudaMemcpyHostToDevice, h->st));
+      CK(cudaMemsetAsync(co.B, 0, off * 8, h->st));
+      CK(cudaMemsetAsync(co.R, 0, off * 8, h->st));
+      // shape vectors B_g = -A_g^-1 A^[I_g,:] Q^o[:, cols_g] (eq:col_pk) with the current factors
+      launch_build_R(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
+      std::vector<int32_t> kc(G);
+      for (int g = 0; g < G; ++g) kc[g] = h->h_ld[g] - 1;
+      sn_shape_vectors(h->sg, halloc, h->st, h->nsm, kc, co.b_off, co.ld, co.R, co.B, off);
+      CK(cudaMemsetAsync(co.R, 0, off * 8, h->st));
+      launch_build_R(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
+      // S = P_B^T A^ P_B (eq:mg_struct, R16) and its inverse (R17)
+      launch_grain_AB(co, h->gb, h->d_row_ptr, h->d_col, h->d_val, h->st);
+      launch_grain_BtY(co, h->gb, h->st);
+      CK(cudaMemsetAsync(h->sb.tiles, 0, (size_t)h->sb.ntiles * TILE * 8, h->st));
+      if (h->d_Sdense) {
+        const int64_t npS = h->lds;
+        CK(cudaMemsetAsync(h->d_Sdense, 0, std::max<int64_t>(npS * npS, 1) * 8, h->st));
+        launch_S_iface(co, h->d_row_ptr, h->d_col, h->d_val, h->d_Sdense, npS, h->st);
+        launch_S_grain(co, h->d_Sdense, npS, h->st);
+        launch_pack_dense(h->sb, h->d_Sdense, npS, h->st);
+      } else {
+        launch_S_iface(co, h->d_row_ptr, h->d_col, h->d_val, h->sb.tiles, 0, h->st);
+        launch_S_grain(co, h->sb.tiles, 0, h->st);
+      }
+      launch_pad_identity(h->sb, h->st);
+      launch_sweep_invert(h->sb, h->st);
+      CK(cudaGetLastError());
+      check_batch_err(h, h->sb, 0, true);
+    } catch (const SnError& e) {
+      drop();
+      throw HError{(hplmm_status)e.status, e.msg};
+    } catch (const HError&) {
+      drop();
+      throw;
+    }
+    h->rep.t_setup_coarse_s = t.stop();
+    CK(cudaStreamSynchronize(h->st));
+    drop();
+    h->rhs_set = false;   // the correction column sits in B's last column (R15)
     return HPLMM_OK;
   } catch (const HError& e) {
     return fail(e);

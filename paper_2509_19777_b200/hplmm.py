@@ -31,7 +31,7 @@ _ART_DTYPE = {0: np.int64, 14: np.float64, 15: np.float64, 16: np.float64, 17: n
 SMOOTHER = dict(cg=0, ilu0=1)
 
 EXPORTED = ["hplmm_default_options", "hplmm_create", "hplmm_assemble", "hplmm_set_matrix",
-            "hplmm_setup", "hplmm_update_moduli", "hplmm_set_rhs", "hplmm_solve", "hplmm_solve_many", "hplmm_apply",
+            "hplmm_setup", "hplmm_update_moduli", "hplmm_refresh_coarse", "hplmm_set_rhs", "hplmm_solve", "hplmm_solve_many", "hplmm_apply",
             "hplmm_apply_many",
             "hplmm_export", "hplmm_setup_bsr", "hplmm_assemble_bsr", "hplmm_free_bsr",
             "hplmm_get_report", "hplmm_profile", "hplmm_kernel_stats", "hplmm_destroy",
@@ -100,6 +100,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hplmm_set_matrix": (C.c_int, [vp, vp, vp]),
         "hplmm_setup": (C.c_int, [vp, vp]),
         "hplmm_update_moduli": (C.c_int, [vp, vp, vp]),
+        "hplmm_refresh_coarse": (C.c_int, [vp, vp]),
         "hplmm_set_rhs": (C.c_int, [vp, vp, vp]),
         "hplmm_solve": (C.c_int, [vp, vp, dbl, vp, vp, vp, i32, vp]),
         "hplmm_solve_many": (C.c_int, [vp, i32, vp, dbl, vp, vp, vp]),
@@ -294,6 +295,11 @@ class Solver:
         """Reuse M_G for perturbed voxel moduli E (host array, [z][y][x])."""
         E = np.ascontiguousarray(E, dtype=np.float64)
         _check(self._lib.hplmm_update_moduli(self._h, E.ctypes.data_as(C.c_void_p), _stream(stream)))
+        return self
+
+    def refresh_coarse(self, stream=None):
+        """Rebuild M_G (shape vectors, S, S^-1) for the current A^."""
+        _check(self._lib.hplmm_refresh_coarse(self._h, _stream(stream)))
         return self
 
     def set_rhs(self, b, stream=None):

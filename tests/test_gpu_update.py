@@ -146,3 +146,53 @@ def test_update_cfg2_golden(kind):
     else:
         assert rep["iterations"] == g["iterations"] == 300
         assert abs(rep["final_true_relres"] - g["final_true_relres"]) <= 0.05 * g["final_true_relres"]
+
+
+@pytest.mark.parametrize("name,kind", [("cube8", "global"), ("porous20", "global"), ("cfg1", "smooth")])
+def test_refresh_coarse_equals_fresh_setup(name, kind):
+    """hplmm_update_moduli + hplmm_refresh_coarse ("M_G must be updated",
+    P:819) against the oracle's setup on the new moduli and against a fresh
+    GPU handle: the same M^-1, the same GMRES run."""
+    import copy as _copy
+    from oracle import fem, gmres, hplmm
+    from paper_2509_19777_b200 import Solver
+    from workloads import make_problem, perturbed_moduli
+    p = make_problem(name)
+    p2 = _copy.copy(p)
+    p2.E = perturbed_moduli(p, kind)
+    s2, h2 = hplmm.setup(p2)
+    sv = Solver(p).assemble(0).setup()
+    sv.update_moduli(p2.E)
+    sv.refresh_coarse()
+    sf = Solver(p2).assemble(0).setup()
+    sv.set_rhs(dev(s2.b))
+    sf.set_rhs(dev(s2.b))
+    h2.set_rhs(s2.b)
+    v = np.random.default_rng(12345).standard_normal(s2.n_dof)
+    for op, ref in (("MG", h2.apply_MG), ("MINV", h2.apply_M)):
+        r = ref(v)
+        out = sv.apply(op, dev(v)).cpu().numpy()
+        tol = coarse_spread_gate(h2, op, v, r)
+        assert rel(out, r) <= tol, (op, rel(out, r), tol)
+        assert rel(out, sf.apply(op, dev(v)).cpu().numpy()) <= tol
+    xo, ito, histo, rro, convo = gmres.gmres(s2.A, s2.b, h2.apply_M, tol=1e-8)
+    x, rep, hist = sv.solve(dev(s2.b), tol=1e-8)
+    assert rep["converged"] == 1 and abs(rep["iterations"] - ito) <= 1
+    assert rel(x.cpu().numpy(), xo) <= 1e-8
+    assert sv.report()["t_setup_coarse_s"] > 0
+
+
+def test_refresh_coarse_errors():
+    from paper_2509_19777_b200 import Solver
+    from paper_2509_19777_b200.hplmm import HPLMMError
+    from workloads import make_problem
+    p = make_problem("cube8")
+    sv = Solver(p).assemble(0)
+    with pytest.raises(HPLMMError):
+        sv.refresh_coarse()
+    sa = Solver(p, mortar="algebraic").assemble(0).setup()
+    with pytest.raises(HPLMMError):          # Algebraic mortars depend on A^
+        sa.refresh_coarse()
+    sc = Solver(p, coarse_solver=1).assemble(0).setup()
+    with pytest.raises(HPLMMError):
+        sc.refresh_coarse()

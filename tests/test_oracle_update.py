@@ -120,3 +120,28 @@ def test_residual_operator_is_the_new_matrix():
     assert np.linalg.norm(h.apply_M(r) - want) <= 1e-13 * np.linalg.norm(want)
     stale = y + h.apply_MCG(r - s.A @ y)
     assert np.linalg.norm(stale - want) >= 1e-6 * np.linalg.norm(want)
+
+
+def test_refresh_coarse_restores_the_projection():
+    """After update_matrix + refresh_coarse M_G is again the A-orthogonal
+    projection onto range(P_B) for the NEW matrix (eq:mg_struct), the shape
+    vectors are A_new-harmonic in the grain interiors (eq:col_pk), and GMRES
+    needs the fresh count again."""
+    p, s, h0, p2, s2, h = _updated("porous20", "global")
+    h.refresh_coarse()
+    h.corr = []
+    e = np.zeros(h.Nm)
+    e[::5] = 1.0
+    v = h.PB @ e
+    assert np.linalg.norm(h.apply_MG(s2.A @ v) - v) <= 1e-9 * np.linalg.norm(v)
+    AP = (s2.A @ h.PB).tocsr()
+    scale = abs(s2.A).max() * abs(h.PB).max()
+    for dg in h.grain_dofs:
+        if dg.size:
+            assert abs(AP[dg]).max() <= 1e-12 * scale
+    h.set_rhs(s2.b)
+    _, it, _, _, conv = gmres.gmres(s2.A, s2.b, h.apply_M, tol=1e-8)
+    s3, h3 = hplmm.setup(p2)
+    h3.set_rhs(s3.b)
+    _, it3, _, _, conv3 = gmres.gmres(s3.A, s3.b, h3.apply_M, tol=1e-8)
+    assert conv and conv3 and it == it3

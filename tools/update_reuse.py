@@ -40,4 +40,11 @@ for kind in ("crack", "smooth", "global"):
           f"{rep3['iterations']} iterations {rep3['t_solve_s']:.4f} s; |x_reused - x_fresh| / |x| = {dx:.1e}",
           flush=True)
     del sf
+    sv.refresh_coarse()
+    tr = sv.report()["t_setup_coarse_s"]
+    x4, rep4, _ = sv.solve(b2, tol=p.tol)
+    x4, rep4, _ = sv.solve(b2, tol=p.tol)
+    print(f"{cfg} {kind}: + refresh_coarse {tr:.3f} s -> {rep4['iterations']} iterations {rep4['t_solve_s']:.4f} s "
+          f"(update + refresh {tu + tr:.3f} s)", flush=True)
     sv.update_moduli(p.E)
+    sv.refresh_coarse()
