@@ -295,7 +295,8 @@ void sn_build_work(SnBatch& B, DevAlloc& A, cudaStream_t st, int nblocks, int nr
     for (int k = 0; k < s.nsn; ++k)
       for (int c : kids[k]) start[k] = std::min(start[k], start[c]);
   }
-  const int64_t xcost = 131072;   // an exchange step in byte equivalents (~5 us of one CTA's stream)
+  // an exchange step in byte equivalents (~2.5 us of one CTA's stream); HPLMM_SN_XCOST (experiments)
+  static const int64_t xcost = getenv("HPLMM_SN_XCOST") ? atoll(getenv("HPLMM_SN_XCOST")) : 65536;
   auto make_team = [&](int g, int L, Team& T) {
     TeamBuilder tb{s, pf, pb, kids, start, T, {}, xcost};
     std::vector<int> roots;
