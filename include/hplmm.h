@@ -156,19 +156,21 @@ typedef struct {
                             1 = host-driven loop: one pinned D2H of the
                                 Hessenberg column and one synchronisation per
                                 Arnoldi step, Givens on the host            */
-  int32_t rhs_block;     /* hplmm_solve_many: right-hand sides solved together,
-                            1..4 (default 4).  A block runs lockstep GMRES(m):
-                            each column keeps its own Arnoldi process,
-                            correction columns (eq:col_cg, R15) and stop test,
-                            while every operator application streams its
-                            matrix data once for the whole block (the
-                            supernodal local factors, P^_B; NEXT #2, P:743,
-                            P:819).  1 = one hplmm_solve per column.  Blocks
-                            need local_factor = 1, smoother = 0, n_st = 1.
-                            Block local solves do not form CTA teams
-                            (sn_split): for a batch with few subdomains
-                            (cfg2: 64 grains) rhs_block = 1 is the faster
-                            choice (4 load cases: 0.109 s vs 0.127 s)       */
+  int32_t rhs_block;     /* hplmm_solve_many: right-hand sides solved together.
+                            0 = automatic (default): blocks of 4, unless the
+                            one-RHS local solves form CTA teams (sn_split: a
+                            batch with few subdomains) -- the block solves do
+                            not, and one team solve per column is then faster
+                            (cfg2, 4 load cases: 0.109 s vs 0.127 s);
+                            2..4 = blocks of that width; 1 = one hplmm_solve
+                            per column.  A block runs lockstep GMRES(m): each
+                            column keeps its own Arnoldi process, correction
+                            columns (eq:col_cg, R15) and stop test, while
+                            every operator application streams its matrix
+                            data once for the whole block (the supernodal
+                            local factors, P^_B; NEXT #2).
+                            Blocks need local_factor = 1, smoother = 0,
+                            n_st = 1                                        */
 } hplmm_options;
 
 typedef struct {
@@ -232,7 +234,7 @@ typedef struct {
 } hplmm_bsr;
 
 /* Default options: n=4, beta=4, h=1, restart=50, max_iter=300, n_st=1,
- * coarse_refine=0, sn_split=0. */
+ * coarse_refine=0, sn_split=0, rhs_block=0. */
 void hplmm_default_options(hplmm_options *opt);
 
 /* Host-only integer setup (no GPU work; bit-exact vs the oracle):

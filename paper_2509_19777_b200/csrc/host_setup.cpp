@@ -122,9 +122,9 @@ bool host_setup(const hplmm_problem* p, const hplmm_options* opt, HostSetup& hs,
       (opt->mortar_kind < 0 || opt->mortar_kind > 2) ||
       (opt->sn_shape != 0 && opt->sn_shape != 8 && opt->sn_shape != 16) ||
       opt->sn_split < -1 || opt->sn_split > 3 ||
-      (opt->host_loop != 0 && opt->host_loop != 1) || opt->rhs_block < 1 || opt->rhs_block > 4) {
+      (opt->host_loop != 0 && opt->host_loop != 1) || opt->rhs_block < 0 || opt->rhs_block > 4) {
     err = "hplmm_create: invalid options (n_mortar>=1, contact_h>=0, 1<=restart<=512, 1<=n_st<=64, "
-          "smoother/local_factor/coarse_solver/operator_kind in {0,1}, mortar_kind in {0,1,2}, sn_shape in {0,8,16}, sn_split in -1..3, host_loop in {0,1}, rhs_block in 1..4)";
+          "smoother/local_factor/coarse_solver/operator_kind in {0,1}, mortar_kind in {0,1,2}, sn_shape in {0,8,16}, sn_split in -1..3, host_loop in {0,1}, rhs_block in 0..4)";
     return false;
   }
   hs.opt = *opt;

@@ -38,7 +38,7 @@ def test_solve_many_block_vs_oracle(case, k):
     from oracle import gmres
     from paper_2509_19777_b200 import Solver
     p, s, h, B = _rhs(case, k)
-    sv = Solver(p).assemble(0).setup()
+    sv = Solver(p, rhs_block=4).assemble(0).setup()   # blocks (automatic would pick team solves here)
     X, reps = sv.solve_many(torch.from_numpy(B).cuda(), tol=1e-8)
     X = X.cpu().numpy()
     for c in range(k):
@@ -58,7 +58,7 @@ def test_solve_many_block_vs_oracle(case, k):
 def test_solve_many_block_matches_per_column(case):
     from paper_2509_19777_b200 import Solver
     p, s, h, B = _rhs(case, 3)
-    a = Solver(p).assemble(0).setup()
+    a = Solver(p, rhs_block=4).assemble(0).setup()
     b = Solver(p, rhs_block=1).assemble(0).setup()
     Xa, ra = a.solve_many(B.copy(), tol=1e-8)          # host buffers
     Xb, rb = b.solve_many(B.copy(), tol=1e-8)
@@ -72,14 +72,14 @@ def test_solve_many_restart_and_cap():
     follows its own cycle sequence, as the single-RHS path does."""
     from paper_2509_19777_b200 import Solver
     p, s, h, B = _rhs("cfg1", 3)
-    a = Solver(p, restart=5).assemble(0).setup()
+    a = Solver(p, restart=5, rhs_block=4).assemble(0).setup()
     b = Solver(p, restart=5, rhs_block=1).assemble(0).setup()
     Xa, ra = a.solve_many(B.copy(), tol=1e-8)
     Xb, rb = b.solve_many(B.copy(), tol=1e-8)
     for c in range(3):
         assert ra[c]["iterations"] == rb[c]["iterations"] and ra[c]["converged"] == 1
         assert rel(Xa[c], Xb[c]) <= 1e-9
-    capped = Solver(p, max_iter=7, restart=5).assemble(0).setup()
+    capped = Solver(p, max_iter=7, restart=5, rhs_block=4).assemble(0).setup()
     Xc, rc = capped.solve_many(B.copy(), tol=1e-8)
     assert all(r["iterations"] == 7 and r["converged"] == 0 for r in rc)
 
@@ -129,3 +129,19 @@ def test_apply_many_errors():
     dense = Solver(p, local_factor=0).assemble(0).setup()
     with pytest.raises(HPLMMError, match="ERR_STATE"):
         dense.apply_many("MZETA", V[:2])
+
+
+def test_solve_many_automatic_block_choice():
+    """rhs_block = 0 (default): a batch that forms CTA teams (these small cases)
+    solves column by column, one without teams in blocks -- same results."""
+    from paper_2509_19777_b200 import Solver
+    p, s, h, B = _rhs("cfg1", 3)
+    auto = Solver(p).assemble(0).setup()
+    assert auto.report()["sn_teams_grain"] > 0
+    blk = Solver(p, sn_split=-1).assemble(0).setup()          # no teams: automatic = blocks
+    Xa, ra = auto.solve_many(B.copy(), tol=1e-8)
+    Xb, rb = blk.solve_many(B.copy(), tol=1e-8)
+    for c in range(3):
+        assert ra[c]["converged"] == 1 and rb[c]["converged"] == 1
+        assert abs(ra[c]["iterations"] - rb[c]["iterations"]) <= 1
+        assert rel(Xa[c], Xb[c]) <= 1e-8
